@@ -1,0 +1,250 @@
+/*
+ * infmoe.h — C-ABI of the B200-native InfMoE MoE-layer hot path (libinfmoe.so).
+ *
+ * Plain C types only: pointers, sizes, POD structs.  No C++ exception crosses
+ * this boundary; every entry point returns a status code:
+ *   0 OK, 2 config / invalid argument (moesim::ConfigError, std::invalid_argument),
+ *   3 capacity (moesim::CapacityError), 4 invariant breach (moesim::InvariantError),
+ *   5 CUDA / NCCL runtime failure.
+ * (errors.hpp:8-21 and SPEC.md:382 exit-code convention.)  The message for the
+ * last failure on the calling thread is infmoe_last_error().
+ *
+ * Each declaration names the reference interface it replaces
+ * (paths relative to /root/reference/proj/include/moesim/).  Device pointers
+ * are raw CUDA addresses; `stream` is a cudaStream_t passed as void*.
+ */
+#ifndef INFMOE_H_
+#define INFMOE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  INFMOE_OK = 0,
+  INFMOE_ERR_CONFIG = 2,
+  INFMOE_ERR_CAPACITY = 3,
+  INFMOE_ERR_INVARIANT = 4,
+  INFMOE_ERR_RUNTIME = 5
+};
+
+const char* infmoe_last_error(void);
+const char* infmoe_version(void);
+
+/* ---- model_config.hpp -------------------------------------------------- */
+/* = moesim::ModelGeometry (model_config.hpp:14-22) */
+typedef struct {
+  int32_t n_layers, n_heads, d_head, d_model, d_ff, n_experts_per_layer, bytes_per_param;
+} infmoe_geometry;
+/* = moesim::HardwareProfile (model_config.hpp:27-32) */
+typedef struct {
+  double peak_flops;    /* FLOP/s */
+  double h2d_bandwidth; /* bytes/s */
+  uint64_t device_memory, reserved_memory;
+} infmoe_hardware;
+
+/* validate(ModelGeometry) model_config.hpp:37-55; *warn = 1 when d_model != n_heads*d_head */
+int infmoe_validate_geometry(const infmoe_geometry* g, int32_t* warn_dmodel);
+/* validate(HardwareProfile) model_config.hpp:57-64 */
+int infmoe_validate_hardware(const infmoe_hardware* hw);
+/* expert_param_bytes model_config.hpp:69-73 */
+uint64_t infmoe_expert_param_bytes(const infmoe_geometry* g);
+/* expert_flops model_config.hpp:77-80 */
+uint64_t infmoe_expert_flops(const infmoe_geometry* g, uint64_t n_tokens);
+/* builtin_geometry_presets model_config.hpp:85-105 ("cpm2", "cpm-small") */
+int infmoe_geometry_preset(const char* name, infmoe_geometry* out);
+
+/* ---- prng.hpp ---------------------------------------------------------- */
+uint64_t infmoe_splitmix64(uint64_t x);                 /* prng.hpp:18-23 */
+uint64_t infmoe_derive_seed(uint64_t seed, uint64_t tag); /* prng.hpp:27-29 */
+/* n consecutive draws of GaussianStream(seed).next() (prng.hpp:49-71) */
+int infmoe_gaussian_fill(uint64_t seed, double* out, uint64_t n);
+
+/* ---- gating.hpp (host side) ------------------------------------------- */
+/* gating_projection gating.hpp:47-56: bits*hidden doubles, bit-major */
+int infmoe_gating_projection(uint64_t seed, int32_t n_hash_bits, int32_t hidden_dim,
+                             double* out);
+/* synthetic_workload gating.hpp:122-165; kind 0 uniform, 1 zipf, 2 balanced */
+int infmoe_synthetic_workload(int32_t kind, uint64_t total_tokens, int32_t n_experts,
+                              uint64_t seed, double zipf_s, uint64_t* counts);
+
+/* ---- cost_model.hpp ---------------------------------------------------- */
+/* compute_costs cost_model.hpp:43-62 (counts has g->n_experts_per_layer entries) */
+int infmoe_compute_costs(const infmoe_geometry* g, const infmoe_hardware* hw,
+                         const uint64_t* counts, int32_t n_experts, double* alphas,
+                         double* beta);
+/* resident_capacity cost_model.hpp:65-78 */
+int infmoe_resident_capacity(const infmoe_geometry* g, const infmoe_hardware* hw,
+                             int32_t* K);
+/* clamp_explicit_capacity cost_model.hpp:82-91; *clamped = 1 when the warning fired */
+int infmoe_clamp_explicit_capacity(int32_t explicit_k, int32_t capacity, int32_t* K,
+                                   int32_t* clamped);
+/* with_event_overhead cost_model.hpp:96-101 (in place) */
+int infmoe_with_event_overhead(double* alphas, int32_t T, double* beta, double eps);
+
+/* ---- scheduler.hpp ----------------------------------------------------- */
+enum { INFMOE_BOUND_LOWER = 0, INFMOE_BOUND_UPPER = 1 };
+/* = moesim::ConstraintReport (scheduler.hpp:25-37); position = -1 when none */
+typedef struct {
+  int32_t feasible;
+  int32_t position;
+  int32_t bound;
+  double prefix_sum, limit;
+} infmoe_constraint_report;
+/* check_constraints scheduler.hpp:70-95; slack[T] may be NULL */
+int infmoe_check_constraints(const int32_t* order, const double* alphas, int32_t T,
+                             double beta, int32_t K, double* slack,
+                             infmoe_constraint_report* rep);
+
+enum { /* OrderPolicy simulator.hpp:17 + the direct scheduler entry points */
+  INFMOE_POLICY_AUTO = 0,   /* auto_order  scheduler.hpp:243-248 (greedy + exact fallback) */
+  INFMOE_POLICY_GREEDY = 1, /* greedy_order scheduler.hpp:143-180 */
+  INFMOE_POLICY_EXACT = 2,  /* exact_order scheduler.hpp:187-237 */
+  INFMOE_POLICY_NAIVE = 3   /* naive_order scheduler.hpp:127-132 */
+};
+enum { INFMOE_DIAG_NONE = -1, INFMOE_DIAG_FEASIBLE = 0, INFMOE_DIAG_TOO_LITTLE_COMPUTE = 1,
+       INFMOE_DIAG_IMBALANCED = 2 };
+enum { INFMOE_METHOD_GREEDY = 0, INFMOE_METHOD_EXACT_FALLBACK = 1, INFMOE_METHOD_NAIVE = 2 };
+/* = moesim::Schedule (scheduler.hpp:39-45) minus the vectors */
+typedef struct {
+  int32_t feasible;
+  int32_t diagnosis; /* INFMOE_DIAG_*, NONE when unset */
+  int32_t method;    /* INFMOE_METHOD_* */
+} infmoe_schedule_info;
+int infmoe_schedule(const double* alphas, int32_t T, double beta, int32_t K, int32_t policy,
+                    int32_t exact_max_T, int32_t* order, double* slack,
+                    infmoe_schedule_info* info);
+/* diagnose scheduler.hpp:253-258 */
+int infmoe_diagnose(const double* alphas, int32_t T, double beta, int32_t K,
+                    int32_t exact_max_T, int32_t* diagnosis);
+
+/* ---- simulator.hpp ----------------------------------------------------- */
+enum { INFMOE_STREAM_LOAD = 0, INFMOE_STREAM_COMPUTE = 1 };
+enum { INFMOE_MODE_OVERLAPPED = 0, INFMOE_MODE_SERIAL = 1 };
+/* = moesim::TimelineEvent (simulator.hpp:19-25) */
+typedef struct {
+  int32_t stream, layer_id, expert_id;
+  double start, end;
+} infmoe_event;
+/* = moesim::SimReport (simulator.hpp:40-48) without per_layer */
+typedef struct {
+  double makespan, compute_busy, load_busy, compute_stall;
+  int32_t peak_resident_experts;
+  double overlap_efficiency;
+} infmoe_sim_report;
+/* = moesim::LayerReport (simulator.hpp:27-38) without the schedule */
+typedef struct {
+  int32_t layer_id, n_experts;
+  double start, end, compute_busy, load_busy, compute_stall;
+  int32_t peak_resident;
+  double lower_bound;
+} infmoe_layer_report;
+/* simulate(order, costs, K, mode) simulator.hpp:209-220; events[2T] */
+int infmoe_simulate(const int32_t* order, const double* alphas, int32_t T, double beta,
+                    int32_t K, int32_t mode, infmoe_event* events, infmoe_sim_report* rep);
+/* simulate_model(costs, K, opt) simulator.hpp:241-255.  Layer l has T[l] experts,
+ * alphas concatenated, betas[l].  policy: INFMOE_POLICY_AUTO (= OrderPolicy::Greedy),
+ * _NAIVE or _EXACT.  orders_out[sum T], events[2 sum T], per_layer[n_layers] (may be NULL). */
+int infmoe_simulate_model(int32_t n_layers, const int32_t* T, const double* alphas,
+                          const double* betas, int32_t K, int32_t mode, int32_t policy,
+                          int32_t continuous_load_stream, int32_t exact_max_T,
+                          int32_t* orders_out, infmoe_event* events, infmoe_sim_report* rep,
+                          infmoe_layer_report* per_layer);
+/* lower_bound simulator.hpp:53-56 */
+double infmoe_lower_bound(const double* alphas, int32_t T, double beta);
+
+/* ======================================================================
+ * Device path: the MoE layer forward the paper's TensorRT plugin ran
+ * (PAPER.md:345, :396).  No reference code exists for these;
+ * the semantics are fixed by oracle/oracle.h.
+ * ==================================================================== */
+enum { INFMOE_DTYPE_BF16 = 0, INFMOE_DTYPE_F32 = 1 };
+enum { INFMOE_GATE_SOFTMAX = 0, INFMOE_GATE_LSH = 1 };
+enum { INFMOE_RESIDENT = 0, INFMOE_OFFLOADED = 1 };
+
+/* counter-hash synthetic fill (oracle.h or_fill_uniform_*): out[i] = (2u-1)*scale */
+int infmoe_fill_uniform(void* out, int32_t dtype, uint64_t n, uint64_t seed, float scale,
+                        void* stream);
+
+/* N1a softmax/top-k gate: x[N,d] (dtype), wg[E,d] f32, bias[E] f32 or NULL.
+ * Outputs topk_idx[N,k] i32, topk_w[N,k] f32, counts[E] i32 (device). */
+int infmoe_gate_softmax_topk(const void* x, int32_t dtype, int64_t N, int32_t d,
+                             const float* wg, const float* bias, int32_t E, int32_t k,
+                             int32_t* topk_idx, float* topk_w, int32_t* counts, void* stream);
+/* N1b LSH gate (gating.hpp:61-104) on the fp64 promotion of x; proj[bits,d] f64 device.
+ * Writes codes[N] u32 (may be NULL), topk_idx[N], topk_w[N]=1, counts[E]. */
+int infmoe_gate_lsh(const void* x, int32_t dtype, int64_t N, int32_t d, const double* proj,
+                    int32_t bits, int32_t E, uint32_t* codes, int32_t* topk_idx,
+                    float* topk_w, int32_t* counts, void* stream);
+/* N2 dispatch: stable counting sort of N*k assignments -> offsets[E+1], perm[N*k],
+ * inv[N*k]; workspace >= infmoe_dispatch_workspace_bytes(N*k, E) bytes (device). */
+size_t infmoe_dispatch_workspace_bytes(int64_t n_assign, int32_t E);
+int infmoe_dispatch(const int32_t* topk_idx, int64_t N, int32_t k, int32_t E,
+                    int32_t* offsets, int32_t* perm, int32_t* inv, void* workspace,
+                    void* stream);
+/* N2 gather: x_perm[p] = x[perm[p] / k] for p < N*k (row-vectorised) */
+int infmoe_gather_rows(const void* x, int32_t dtype, int64_t N, int32_t d, int32_t k,
+                       const int32_t* perm, void* x_perm, void* stream);
+/* N3+N4 grouped expert FFN on tcgen05: for each listed expert e with rows
+ * [offsets[e], offsets[e+1]) of x_perm:  h = GeLU(x_perm . w_in[slot]^T) (bf16 into h),
+ * y_perm = h . w_out[slot]^T.  w_in is [n_slots, d_ff, d_model], w_out is
+ * [n_slots, d_model, d_ff] (K-major).  experts/slots are HOST arrays of n_groups
+ * entries; experts == NULL means all E with slot == expert. */
+int infmoe_expert_ffn(const void* x_perm, int64_t n_rows, int32_t d_model, int32_t d_ff,
+                      int32_t dtype, const int32_t* offsets, int32_t E,
+                      const void* w_in, const void* w_out, int32_t n_slots,
+                      const int32_t* experts, const int32_t* slots, int32_t n_groups,
+                      void* h, void* y_perm, void* stream);
+/* N5 combine: y[t] = fmaf-chain over j<k of topk_w[t,j] * y_perm[inv[t,j]] */
+int infmoe_combine(const void* y_perm, int32_t dtype, const int32_t* inv,
+                   const float* topk_w, int64_t N, int32_t k, int32_t d, void* y,
+                   void* stream);
+
+/* ---- the layer handle (N6 offload executor + N8) ---------------------- */
+typedef struct infmoe_layer infmoe_layer;
+typedef struct {
+  int32_t d_model, d_ff, n_experts, top_k;
+  int32_t dtype;      /* INFMOE_DTYPE_* */
+  int32_t gate_kind;  /* INFMOE_GATE_* */
+  int32_t residency;  /* INFMOE_RESIDENT / INFMOE_OFFLOADED */
+  int32_t K;          /* offloaded: resident capacity K; the handle owns K+1 slots (D6) */
+  int32_t policy;     /* INFMOE_POLICY_* for the offload order */
+  int32_t max_tokens; /* upper bound on N per forward */
+  int32_t device;
+  /* gate: softmax -> gate_weight[E,d] f32 (+ optional gate_bias[E]); lsh -> seed/bits */
+  const float* gate_weight; /* host pointer, copied at create */
+  const float* gate_bias;   /* host pointer or NULL */
+  uint64_t lsh_seed;
+  int32_t lsh_bits;
+  /* expert weights: w_in [E, d_ff, d_model], w_out [E, d_model, d_ff] in dtype.
+   * RESIDENT: device pointers (borrowed).  OFFLOADED: host pointers; page-locked
+   * memory is used as is, pageable memory is registered by the handle. */
+  const void* w_in;
+  const void* w_out;
+  infmoe_hardware hw; /* cost model inputs for the scheduler (alpha, beta) */
+} infmoe_layer_desc;
+
+/* per-forward outputs (all optional; host pointers unless noted) */
+typedef struct {
+  int32_t* counts;       /* [E] routed tokens per expert */
+  int32_t* order;        /* [E] executed expert order (offloaded) */
+  int32_t* feasible;     /* scheduler verdict */
+  infmoe_event* events;  /* [2E] measured timeline (seconds from layer start) */
+  double* exposed_copy_s;/* makespan - compute_busy on the measured timeline */
+} infmoe_forward_out;
+
+int infmoe_layer_create(const infmoe_layer_desc* desc, infmoe_layer** out);
+/* x, y: device [N, d_model] in dtype; stream: cudaStream_t or NULL. */
+int infmoe_layer_forward(infmoe_layer* layer, const void* x, int64_t N, void* y,
+                         infmoe_forward_out* out, void* stream);
+/* point an offloaded layer at another host weight set of the same shape */
+int infmoe_layer_set_host_weights(infmoe_layer* layer, const void* w_in, const void* w_out);
+int infmoe_layer_destroy(infmoe_layer* layer);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* INFMOE_H_ */

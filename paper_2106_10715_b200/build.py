@@ -1,0 +1,92 @@
+"""Build libinfmoe.so in-tree (paper_2106_10715_b200/_lib/) for sm_100a.
+
+nvcc cross-compiles the CUDA translation units (no GPU needed), g++ the host
+planner; everything links into one C-ABI shared library whose exports are
+declared in include/infmoe.h.  Usage: python -m paper_2106_10715_b200.build
+"""
+from __future__ import annotations
+
+import concurrent.futures as cf
+import hashlib
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+CSRC = PKG / "csrc"
+OUT_DIR = PKG / "_lib"
+OBJ_DIR = ROOT / "build" / "obj"
+LIB = OUT_DIR / "libinfmoe.so"
+
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+HOST_CXX = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++"
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+INCLUDES = [f"-I{ROOT / 'include'}", f"-I{CSRC}"]
+
+CU_SOURCES = [
+    "kernels/fill.cu",
+    "kernels/gate.cu",
+    "kernels/dispatch.cu",
+    "kernels/expert_gemm.cu",
+    "runtime/layer.cu",
+    "runtime/capi_device.cu",
+]
+CXX_SOURCES = [
+    "host/planner.cpp",
+    "host/capi_host.cpp",
+]
+
+
+def _headers_digest() -> str:
+    h = hashlib.sha256()
+    for p in sorted(list(CSRC.rglob("*.hpp")) + list(CSRC.rglob("*.cuh")) +
+                    [ROOT / "include" / "infmoe.h"]):
+        h.update(p.read_bytes())
+    return h.hexdigest()[:16]
+
+
+def _compile(src: str, digest: str, verbose: bool) -> Path:
+    path = CSRC / src
+    obj = OBJ_DIR / (src.replace("/", "_") + ".o")
+    stamp = obj.with_suffix(".stamp")
+    key = hashlib.sha256(path.read_bytes() + digest.encode()).hexdigest()
+    if obj.exists() and stamp.exists() and stamp.read_text() == key:
+        return obj
+    if src.endswith(".cu"):
+        cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++20", "-ccbin", HOST_CXX,
+               "-Xcompiler", "-fPIC", "-Xptxas", "-v" if verbose else "-O3",
+               "--expt-relaxed-constexpr", *INCLUDES, "-c", str(path), "-o", str(obj)]
+    else:
+        cmd = [HOST_CXX, "-O2", "-std=c++20", "-fPIC", "-Wall", "-ffp-contract=off",
+               *INCLUDES, f"-I/usr/local/cuda/include", "-c", str(path), "-o", str(obj)]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"compile failed: {src}\n{' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
+    if verbose and r.stderr:
+        sys.stderr.write(r.stderr)
+    stamp.write_text(key)
+    return obj
+
+
+def build(verbose: bool = False) -> Path:
+    OBJ_DIR.mkdir(parents=True, exist_ok=True)
+    OUT_DIR.mkdir(parents=True, exist_ok=True)
+    digest = _headers_digest()
+    srcs = CU_SOURCES + CXX_SOURCES
+    with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
+        objs = list(ex.map(lambda s: _compile(s, digest, verbose), srcs))
+    newest = max(o.stat().st_mtime for o in objs)
+    if LIB.exists() and LIB.stat().st_mtime >= newest:
+        return LIB
+    cmd = [NVCC, *ARCH, "-shared", "-ccbin", HOST_CXX, "-o", str(LIB), *map(str, objs),
+           "-lcudart", "-Xlinker", "-rpath,/usr/local/cuda/lib64"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"link failed\n{' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(verbose="-v" in sys.argv))

@@ -1,0 +1,208 @@
+// dispatch.cu — N2 token dispatch (stable counting sort + row gather) and N5
+// combine (its gate-weighted inverse).
+//
+// Dispatch is a three-launch stable counting sort over the N*k (token, slot)
+// assignments, so the permutation is deterministic and equals oracle.c
+// or_dispatch bit for bit:
+//   1. per-chunk histograms               (one CTA per 2048 assignments)
+//   2. exclusive scan -> offsets[E+1] and each chunk's base per expert
+//   3. per-chunk stable scatter: warps own contiguous sub-ranges, ranks inside a
+//      warp come from __match_any_sync peer masks.
+// The row gather and the combine move 16-byte vectors, one warp per row, and
+// are HBM-bound.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace infmoe {
+namespace {
+
+constexpr int kChunkAssign = 2048;
+constexpr int kScatterWarps = 8;
+constexpr int kMaxExpertsDispatch = 1024;
+
+__global__ void chunk_histogram_kernel(const int32_t* __restrict__ idx, int64_t n, int E,
+                                       int32_t* __restrict__ chunk_hist) {
+  extern __shared__ int h[];
+  for (int e = threadIdx.x; e < E; e += blockDim.x) h[e] = 0;
+  __syncthreads();
+  const int64_t a0 = int64_t(blockIdx.x) * kChunkAssign;
+  const int64_t a1 = min(n, a0 + kChunkAssign);
+  for (int64_t a = a0 + threadIdx.x; a < a1; a += blockDim.x) atomicAdd(&h[idx[a]], 1);
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += blockDim.x) chunk_hist[size_t(blockIdx.x) * E + e] = h[e];
+}
+
+// one CTA: per expert, running sum over chunks; then exclusive scan over experts
+__global__ void dispatch_scan_kernel(int32_t* __restrict__ chunk_hist, int n_chunks, int E,
+                                     int32_t* __restrict__ offsets) {
+  extern __shared__ int tot[];
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    int run = 0;
+    for (int b = 0; b < n_chunks; ++b) {
+      const int c = chunk_hist[size_t(b) * E + e];
+      chunk_hist[size_t(b) * E + e] = run;  // becomes the chunk's base inside expert e
+      run += c;
+    }
+    tot[e] = run;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int e = 0; e < E; ++e) {
+      offsets[e] = acc;
+      acc += tot[e];
+    }
+    offsets[E] = acc;
+  }
+}
+
+__global__ void __launch_bounds__(kScatterWarps * 32)
+    dispatch_scatter_kernel(const int32_t* __restrict__ idx, int64_t n, int E,
+                            const int32_t* __restrict__ chunk_base,
+                            const int32_t* __restrict__ offsets, int32_t* __restrict__ perm,
+                            int32_t* __restrict__ inv) {
+  extern __shared__ int wb[];  // [kScatterWarps][E]
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  constexpr int kPerWarp = kChunkAssign / kScatterWarps;
+  const int64_t a0 = int64_t(blockIdx.x) * kChunkAssign + int64_t(warp) * kPerWarp;
+  const int64_t a1 = min(n, a0 + kPerWarp);
+  for (int i = threadIdx.x; i < kScatterWarps * E; i += blockDim.x) wb[i] = 0;
+  __syncthreads();
+  for (int64_t a = a0 + lane; a < a1; a += 32) atomicAdd(&wb[warp * E + idx[a]], 1);
+  __syncthreads();
+  // warp bases: offsets[e] + chunk base + counts of earlier warps in this chunk
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    int run = offsets[e] + chunk_base[size_t(blockIdx.x) * E + e];
+    for (int w = 0; w < kScatterWarps; ++w) {
+      const int c = wb[w * E + e];
+      wb[w * E + e] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+  const unsigned lt = (1u << lane) - 1u;
+  for (int64_t base = a0; base < a1; base += 32) {
+    const int64_t a = base + lane;
+    const bool live = a < a1;
+    const unsigned act = __ballot_sync(0xffffffffu, live);
+    if (live) {
+      const int e = idx[a];
+      const unsigned peers = __match_any_sync(act, e);
+      const int pos = wb[warp * E + e] + __popc(peers & lt);
+      perm[pos] = int32_t(a);
+      inv[a] = pos;
+      __syncwarp(act);
+      if ((peers & lt) == 0) wb[warp * E + e] += __popc(peers);  // group leader advances
+    }
+    __syncwarp();
+  }
+}
+
+__global__ void gather_rows_kernel(const uint4* __restrict__ x, int64_t rows_out, int vec_per_row,
+                                   int k, const int32_t* __restrict__ perm,
+                                   uint4* __restrict__ xp) {
+  const int warps = blockDim.x / 32;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  for (int64_t p = int64_t(blockIdx.x) * warps + warp; p < rows_out;
+       p += int64_t(gridDim.x) * warps) {
+    const int64_t src = perm[p] / k;
+    const uint4* s = x + src * vec_per_row;
+    uint4* d = xp + p * vec_per_row;
+    for (int v = lane; v < vec_per_row; v += 32) d[v] = __ldg(s + v);
+  }
+}
+
+template <typename T>
+__global__ void combine_kernel(const T* __restrict__ yp, const int32_t* __restrict__ inv,
+                               const float* __restrict__ w, int64_t N, int k, int d,
+                               T* __restrict__ y) {
+  constexpr int V = 16 / sizeof(T);  // elements per 16-byte vector
+  const int warps = blockDim.x / 32;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int nvec = d / V;
+  for (int64_t t = int64_t(blockIdx.x) * warps + warp; t < N; t += int64_t(gridDim.x) * warps) {
+    int32_t rows[8];
+    float ws[8];
+    for (int j = 0; j < k; ++j) {
+      rows[j] = inv[t * k + j];
+      ws[j] = w[t * k + j];
+    }
+    for (int v = lane; v < nvec; v += 32) {
+      float acc[V];
+#pragma unroll
+      for (int i = 0; i < V; ++i) acc[i] = 0.0f;
+      for (int j = 0; j < k; ++j) {
+        const uint4 raw = __ldg(reinterpret_cast<const uint4*>(yp + size_t(rows[j]) * d) + v);
+        const T* e = reinterpret_cast<const T*>(&raw);
+#pragma unroll
+        for (int i = 0; i < V; ++i) acc[i] = fmaf(ws[j], load_as_f32(e, i), acc[i]);
+      }
+      uint4 out;
+      T* o = reinterpret_cast<T*>(&out);
+#pragma unroll
+      for (int i = 0; i < V; ++i) {
+        if constexpr (sizeof(T) == 2) o[i] = __float2bfloat16_rn(acc[i]);
+        else o[i] = acc[i];
+      }
+      reinterpret_cast<uint4*>(y + size_t(t) * d)[v] = out;
+    }
+  }
+}
+
+int grid_for_rows(int64_t rows, int warps_per_block) {
+  const int64_t want = (rows + warps_per_block - 1) / warps_per_block;
+  return int(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(device_sm_count()) * 8)));
+}
+
+}  // namespace
+
+size_t dispatch_workspace_bytes(int64_t n_assign, int E) {
+  const int64_t chunks = std::max<int64_t>(1, (n_assign + kChunkAssign - 1) / kChunkAssign);
+  return size_t(chunks) * size_t(E) * sizeof(int32_t);
+}
+
+void launch_dispatch(const int32_t* idx, int64_t n, int E, int32_t* offsets, int32_t* perm,
+                     int32_t* inv, void* workspace, cudaStream_t s) {
+  require(E >= 1 && E <= kMaxExpertsDispatch, "dispatch: n_experts must be in [1, 1024]");
+  require(workspace != nullptr, "dispatch: workspace is NULL");
+  const int64_t chunks = std::max<int64_t>(1, (n + kChunkAssign - 1) / kChunkAssign);
+  int32_t* ch = reinterpret_cast<int32_t*>(workspace);
+  chunk_histogram_kernel<<<unsigned(chunks), 256, E * sizeof(int), s>>>(idx, n, E, ch);
+  INFMOE_LAUNCH_CHECK();
+  dispatch_scan_kernel<<<1, 256, E * sizeof(int), s>>>(ch, int(chunks), E, offsets);
+  INFMOE_LAUNCH_CHECK();
+  if (n == 0) return;
+  dispatch_scatter_kernel<<<unsigned(chunks), kScatterWarps * 32,
+                            kScatterWarps * E * sizeof(int), s>>>(idx, n, E, ch, offsets, perm,
+                                                                  inv);
+  INFMOE_LAUNCH_CHECK();
+}
+
+void launch_gather_rows(const void* x, int dtype, int64_t N, int d, int k, const int32_t* perm,
+                        void* x_perm, cudaStream_t s) {
+  const size_t row_bytes = size_t(d) * dtype_bytes(dtype);
+  require(row_bytes % 16 == 0, "gather: row bytes must be a multiple of 16");
+  const int64_t rows = N * k;
+  if (rows == 0) return;
+  gather_rows_kernel<<<grid_for_rows(rows, 8), 256, 0, s>>>(
+      reinterpret_cast<const uint4*>(x), rows, int(row_bytes / 16), k, perm,
+      reinterpret_cast<uint4*>(x_perm));
+  INFMOE_LAUNCH_CHECK();
+}
+
+void launch_combine(const void* yp, int dtype, const int32_t* inv, const float* w, int64_t N,
+                    int k, int d, void* y, cudaStream_t s) {
+  require(k >= 1 && k <= 8, "combine: top_k must be in [1, 8]");
+  require((size_t(d) * dtype_bytes(dtype)) % 16 == 0, "combine: row bytes must be a multiple of 16");
+  if (N == 0) return;
+  if (dtype == kDtypeBf16)
+    combine_kernel<<<grid_for_rows(N, 8), 256, 0, s>>>(
+        reinterpret_cast<const __nv_bfloat16*>(yp), inv, w, N, k, d,
+        reinterpret_cast<__nv_bfloat16*>(y));
+  else
+    combine_kernel<<<grid_for_rows(N, 8), 256, 0, s>>>(reinterpret_cast<const float*>(yp), inv,
+                                                        w, N, k, d, reinterpret_cast<float*>(y));
+  INFMOE_LAUNCH_CHECK();
+}
+
+}  // namespace infmoe

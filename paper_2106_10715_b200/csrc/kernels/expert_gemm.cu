@@ -1,0 +1,478 @@
+// expert_gemm.cu — N3/N4: per-expert FFN projections as one persistent,
+// warp-specialised tcgen05 grouped GEMM for sm_100a.
+//
+//   out[r, n] = epi( sum_k A[r, k] * B[slot(r) * N + n, k] )
+//
+// A = token rows of the dispatched activations (x_perm for W_in, H for W_out),
+// B = the expert weight in nn.Linear [out, in] (K-major) layout, one slot per
+// resident expert.  The shape of one expert follows model_config.hpp:12-13
+// (d_model x d_ff and d_ff x d_model); the FLOP count is expert_flops
+// (model_config.hpp:77-80).
+//
+// Tiling: a tile is (group, 128-column block of N, up to
+// MSUB=2 x 128 token rows).  With ~128 tokens per expert the layer is
+// weight-streaming bound (128 FLOP/B < 251 FLOP/B ridge), so every weight
+// tile is read once from HBM and reused by both 128-row sub-tiles; token
+// tiles are re-read from L2.  Roles: warp 0 TMA producer, warp 1 MMA issuer
+// (one elected thread, accumulators in TMEM, 2 accumulator stages), warps 2-5
+// epilogue (tcgen05.ld -> GeLU -> bf16 -> global).
+#include <cuda.h>
+
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+
+#include "common.cuh"
+#include "expert_gemm.cuh"
+
+namespace infmoe {
+namespace gemm {
+
+constexpr int BM = 128;          // UMMA M (token rows per sub-tile)
+constexpr int BN = 128;          // UMMA N (output columns per tile)
+constexpr int ROW_BYTES = 128;   // one SW128 row = BK elements
+constexpr int MSUB = 2;          // token sub-tiles sharing one weight tile
+constexpr int STAGES = 4;
+constexpr int ACC = 2;           // TMEM accumulator stages
+constexpr int TMEM_COLS = ACC * MSUB * BN;  // 512
+constexpr uint32_t A_TILE = BM * ROW_BYTES;  // 16 KiB
+constexpr uint32_t B_TILE = BN * ROW_BYTES;  // 16 KiB
+constexpr uint32_t STAGE_BYTES = MSUB * A_TILE + B_TILE;
+constexpr int NUM_THREADS = 192;
+constexpr uint32_t SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+static_assert(TMEM_COLS <= 512, "TMEM budget");
+
+struct Params {
+  int32_t N, K;
+  int32_t n_groups;
+  int32_t ld_out;
+  int64_t a_rows;
+  const int32_t* offsets;
+  void* out;
+  int32_t experts[kMaxGroups];
+  int32_t slots[kMaxGroups];
+};
+
+// ------------------------------------------------------------ PTX wrappers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const void* tmap, uint32_t bar,
+                                            int32_t c_inner, int32_t c_outer,
+                                            uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      ".L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c_inner), "r"(c_outer), "r"(bar), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   bar)
+               : "memory");
+}
+// K-major, 128B-swizzled operand tile: rows of 128 bytes, 8-row atoms of 1 KiB.
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= uint64_t((saddr & 0x3FFFFu) >> 4);  // start address (16 B units)
+  d |= uint64_t(1) << 16;                  // leading byte offset (unused for SW128 K-major)
+  d |= uint64_t(1024 >> 4) << 32;          // stride byte offset: 8 rows x 128 B
+  d |= uint64_t(1) << 46;                  // descriptor version (sm_100)
+  d |= uint64_t(2) << 61;                  // SWIZZLE_128B
+  return d;
+}
+template <bool kTF32>
+__device__ __forceinline__ void mma(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                    uint32_t accumulate) {
+  if constexpr (kTF32) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+  }
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%"
+      "14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+        "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+        "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ float gelu_erf(float v) {
+  return 0.5f * v * (1.0f + erff(v * 0.70710678118654752f));
+}
+
+// UMMA instruction descriptor: D f32, A/B bf16 (or tf32), both K-major.
+template <bool kTF32>
+__host__ __device__ constexpr uint32_t make_idesc() {
+  return (1u << 4) | ((kTF32 ? 2u : 1u) << 7) | ((kTF32 ? 2u : 1u) << 10) |
+         (uint32_t(BN >> 3) << 17) | (uint32_t(BM >> 4) << 24);
+}
+
+// -------------------------------------------------------------- tile table
+struct TileTable {
+  int32_t n_groups;
+  int32_t n_tiles_per_row;  // N / BN
+  int32_t tile_start[kMaxGroups + 1];
+  int32_t mgroups[kMaxGroups];
+  int32_t row0[kMaxGroups];
+  int32_t rows[kMaxGroups];
+  int32_t slot[kMaxGroups];
+};
+
+struct Tile {
+  int32_t row0;       // first A row of this tile
+  int32_t rows;       // valid rows (<= MSUB*BM)
+  int32_t nsub;       // active 128-row sub-tiles
+  int32_t b_row0;     // first B row
+  int32_t n0;         // first output column
+};
+
+__device__ __forceinline__ Tile decode(const TileTable& tt, int32_t t, int32_t& g_cursor,
+                                       int32_t N) {
+  while (t >= tt.tile_start[g_cursor + 1]) ++g_cursor;
+  const int32_t g = g_cursor;
+  const int32_t local = t - tt.tile_start[g];
+  const int32_t mg = local % tt.mgroups[g];   // sub-tile groups fastest: neighbours
+  const int32_t nt = local / tt.mgroups[g];   // share the same weight tile in L2
+  Tile r;
+  r.row0 = tt.row0[g] + mg * (MSUB * BM);
+  r.rows = min(MSUB * BM, tt.rows[g] - mg * (MSUB * BM));
+  r.nsub = (r.rows + BM - 1) / BM;
+  r.b_row0 = tt.slot[g] * N + nt * BN;
+  r.n0 = nt * BN;
+  return r;
+}
+
+// ------------------------------------------------------------------ kernel
+template <bool kTF32, bool kGelu>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
+                        const __grid_constant__ CUtensorMap tmap_b, const Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ TileTable tt;
+  __shared__ uint32_t tmem_base_slot;
+
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;  // SW128 atoms need 1 KiB alignment
+  const uint32_t bar_base = base + STAGES * STAGE_BYTES;
+  auto full_bar = [&](int s) { return bar_base + 8u * s; };
+  auto empty_bar = [&](int s) { return bar_base + 8u * (STAGES + s); };
+  auto accf_bar = [&](int a) { return bar_base + 8u * (2 * STAGES + a); };
+  auto acce_bar = [&](int a) { return bar_base + 8u * (2 * STAGES + ACC + a); };
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+
+  if (threadIdx.x == 0) {
+    tt.n_groups = p.n_groups;
+    tt.n_tiles_per_row = p.N / BN;
+    int32_t acc = 0;
+    for (int g = 0; g < p.n_groups; ++g) {
+      const int e = p.experts[g];
+      const int32_t r0 = p.offsets[e];
+      const int32_t rn = p.offsets[e + 1] - r0;
+      tt.row0[g] = r0;
+      tt.rows[g] = rn;
+      tt.slot[g] = p.slots[g];
+      tt.mgroups[g] = (rn + MSUB * BM - 1) / (MSUB * BM);
+      tt.tile_start[g] = acc;
+      acc += tt.mgroups[g] * tt.n_tiles_per_row;
+    }
+    tt.tile_start[p.n_groups] = acc;
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full_bar(s), 1);
+      mbar_init(empty_bar(s), 1);
+    }
+    for (int a = 0; a < ACC; ++a) {
+      mbar_init(accf_bar(a), 1);
+      mbar_init(acce_bar(a), 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&tmem_base_slot)),
+                 "n"(TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = tmem_base_slot;
+  const int32_t n_tiles = tt.tile_start[tt.n_groups];
+  const int32_t kblocks = p.K / (ROW_BYTES / (kTF32 ? 4 : 2));
+  const int32_t bk_elems = ROW_BYTES / (kTF32 ? 4 : 2);
+
+  if (warp == 0) {
+    // ================= TMA producer =================
+    if (lane == 0) {
+      const uint64_t pol_w = policy_evict_first();  // weights: streamed once
+      const uint64_t pol_a = policy_evict_last();   // token rows: re-read per n-tile
+      int stage = 0;
+      uint32_t phase = 0;
+      int32_t gc = 0;
+      for (int32_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+        const Tile tile = decode(tt, t, gc, p.N);
+        const uint32_t bytes = tile.nsub * A_TILE + B_TILE;
+        for (int32_t kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(empty_bar(stage), phase ^ 1);
+          const uint32_t sA = base + stage * STAGE_BYTES;
+          const uint32_t sB = sA + MSUB * A_TILE;
+          mbar_expect_tx(full_bar(stage), bytes);
+          for (int s = 0; s < tile.nsub; ++s)
+            tma_load_2d(sA + s * A_TILE, &tmap_a, full_bar(stage), kb * bk_elems,
+                        tile.row0 + s * BM, pol_a);
+          tma_load_2d(sB, &tmap_b, full_bar(stage), kb * bk_elems, tile.b_row0, pol_w);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ================= MMA issuer =================
+    constexpr uint32_t idesc = make_idesc<kTF32>();
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    int32_t gc = 0;
+    for (int32_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      const Tile tile = decode(tt, t, gc, p.N);
+      mbar_wait(acce_bar(acc), acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t d_base = tmem_base + acc * (MSUB * BN);
+      for (int32_t kb = 0; kb < kblocks; ++kb) {
+        mbar_wait(full_bar(stage), phase);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t sA = base + stage * STAGE_BYTES;
+          const uint32_t sB = sA + MSUB * A_TILE;
+          const uint64_t db = sdesc(sB);
+          for (int s = 0; s < tile.nsub; ++s) {
+            const uint64_t da = sdesc(sA + s * A_TILE);
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)  // 4 x 32 B of K per 128 B row
+              mma<kTF32>(d_base + s * BN, da + 2 * kk, db + 2 * kk, idesc,
+                         (kb | kk) != 0 ? 1u : 0u);
+          }
+          tc_commit(empty_bar(stage));  // smem slot free once these MMAs retire
+        }
+        __syncwarp();
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+      if (lane == 0) tc_commit(accf_bar(acc));  // accumulator ready for the epilogue
+      __syncwarp();
+      if (++acc == ACC) { acc = 0; acc_phase ^= 1; }
+    }
+  } else {
+    // ================= epilogue (warps 2..5) =================
+    const int quarter = warp & 3;  // TMEM lanes 32*quarter .. +31 are visible to this warp
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    int32_t gc = 0;
+    for (int32_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      const Tile tile = decode(tt, t, gc, p.N);
+      mbar_wait(accf_bar(acc), acc_phase);
+      tc_fence_after();
+      for (int s = 0; s < tile.nsub; ++s) {
+        const int r_local = s * BM + quarter * 32 + lane;
+        const bool valid = r_local < tile.rows;
+        const int64_t row = int64_t(tile.row0) + r_local;
+        const uint32_t taddr =
+            tmem_base + (uint32_t(quarter * 32) << 16) + acc * (MSUB * BN) + s * BN;
+#pragma unroll 1
+        for (int cc = 0; cc < BN / 32; ++cc) {
+          uint32_t r[32];
+          tmem_ld32(taddr + cc * 32, r);
+          if (valid) {
+            if constexpr (kTF32) {
+              float* dst = reinterpret_cast<float*>(p.out) + row * p.ld_out + tile.n0 + cc * 32;
+#pragma unroll
+              for (int q = 0; q < 8; ++q) {
+                float4 v;
+                v.x = __uint_as_float(r[4 * q + 0]);
+                v.y = __uint_as_float(r[4 * q + 1]);
+                v.z = __uint_as_float(r[4 * q + 2]);
+                v.w = __uint_as_float(r[4 * q + 3]);
+                if constexpr (kGelu) {
+                  v.x = gelu_erf(v.x); v.y = gelu_erf(v.y);
+                  v.z = gelu_erf(v.z); v.w = gelu_erf(v.w);
+                }
+                reinterpret_cast<float4*>(dst)[q] = v;
+              }
+            } else {
+              __nv_bfloat16* dst =
+                  reinterpret_cast<__nv_bfloat16*>(p.out) + row * p.ld_out + tile.n0 + cc * 32;
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                uint32_t w[4];
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                  float lo = __uint_as_float(r[8 * q + 2 * h]);
+                  float hi = __uint_as_float(r[8 * q + 2 * h + 1]);
+                  if constexpr (kGelu) { lo = gelu_erf(lo); hi = gelu_erf(hi); }
+                  __nv_bfloat162 b2 = __floats2bfloat162_rn(lo, hi);
+                  w[h] = *reinterpret_cast<uint32_t*>(&b2);
+                }
+                reinterpret_cast<uint4*>(dst)[q] = make_uint4(w[0], w[1], w[2], w[3]);
+              }
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(acce_bar(acc));
+      if (++acc == ACC) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "n"(TMEM_COLS)
+                 : "memory");
+  }
+}
+
+// ------------------------------------------------------------ host helpers
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(ptr);
+  });
+  if (!fn) fail(kRuntime, "cuTensorMapEncodeTiled unavailable from the driver");
+  return fn;
+}
+
+CUtensorMap make_tmap(const void* base, uint64_t rows, uint64_t cols, bool f32,
+                      uint32_t box_rows) {
+  CUtensorMap m;
+  std::memset(&m, 0, sizeof(m));
+  const uint64_t esz = f32 ? 4 : 2;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * esz};
+  cuuint32_t box[2] = {uint32_t(ROW_BYTES / esz), box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(&m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                           2, const_cast<void*>(base), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(kRuntime, "cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
+  return m;
+}
+
+template <bool kTF32, bool kGelu>
+void launch_impl(const GroupedGemmArgs& a, cudaStream_t stream) {
+  auto kern = grouped_gemm_kernel<kTF32, kGelu>;
+  static bool configured = false;
+  if (!configured) {
+    INFMOE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(SMEM_BYTES)));
+    configured = true;
+  }
+  const CUtensorMap ta = make_tmap(a.a, uint64_t(std::max<int64_t>(a.a_rows, 1)), uint64_t(a.K),
+                                   kTF32, BM);
+  const CUtensorMap tb = make_tmap(a.b, uint64_t(a.n_slots) * uint64_t(a.N), uint64_t(a.K),
+                                   kTF32, BN);
+  Params p;
+  std::memset(&p, 0, sizeof(p));
+  p.N = a.N;
+  p.K = a.K;
+  p.n_groups = a.n_groups;
+  p.ld_out = a.N;
+  p.a_rows = a.a_rows;
+  p.offsets = a.offsets;
+  p.out = a.out;
+  for (int g = 0; g < a.n_groups; ++g) {
+    p.experts[g] = a.experts[g];
+    p.slots[g] = a.slots[g];
+  }
+  int grid = device_sm_count();
+  if (a.max_ctas > 0) grid = std::min(grid, a.max_ctas);
+  kern<<<grid, NUM_THREADS, SMEM_BYTES, stream>>>(ta, tb, p);
+  INFMOE_LAUNCH_CHECK();
+}
+
+}  // namespace gemm
+
+void launch_grouped_gemm(const GroupedGemmArgs& a, cudaStream_t stream) {
+  require(a.n_groups >= 1 && a.n_groups <= kMaxGroups, "grouped gemm: n_groups out of range");
+  require(a.N % gemm::BN == 0, "grouped gemm: N must be a multiple of 128");
+  const int bk = a.dtype == kDtypeF32 ? 32 : 64;
+  require(a.K % bk == 0 && a.K > 0, "grouped gemm: K must be a multiple of 64 (bf16) / 32 (f32)");
+  require(a.a && a.b && a.out && a.offsets, "grouped gemm: NULL pointer");
+  const bool tf32 = a.dtype == kDtypeF32;
+  if (tf32) {
+    if (a.gelu) gemm::launch_impl<true, true>(a, stream);
+    else gemm::launch_impl<true, false>(a, stream);
+  } else {
+    if (a.gelu) gemm::launch_impl<false, true>(a, stream);
+    else gemm::launch_impl<false, false>(a, stream);
+  }
+}
+
+}  // namespace infmoe

@@ -1,0 +1,34 @@
+// kernels.cuh — launchers of the non-GEMM sm_100a kernels (gate, dispatch,
+// gather, combine, fill).  All take device pointers and a stream.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace infmoe {
+
+void launch_fill_uniform(void* out, int dtype, uint64_t n, uint64_t seed, float scale,
+                         cudaStream_t stream);
+
+// N1a: logits by a sequential fmaf chain per (token, expert), top-k by strict
+// argmax (ties -> lower index), softmax weights.  counts must be zeroed by the
+// launcher (it is: the launcher issues the memset).
+void launch_gate_softmax(const void* x, int dtype, int64_t N, int d, const float* wg,
+                         const float* bias, int E, int k, int32_t* topk_idx, float* topk_w,
+                         int32_t* counts, cudaStream_t stream);
+// N1b: LSH sign-bit code over the fp64 promotion of x (gating.hpp:61-104).
+void launch_gate_lsh(const void* x, int dtype, int64_t N, int d, const double* proj, int bits,
+                     int E, uint32_t* codes, int32_t* topk_idx, float* topk_w, int32_t* counts,
+                     cudaStream_t stream);
+
+// N2: stable counting sort.  workspace bytes from dispatch_workspace_bytes.
+size_t dispatch_workspace_bytes(int64_t n_assign, int E);
+void launch_dispatch(const int32_t* topk_idx, int64_t n_assign, int E, int32_t* offsets,
+                     int32_t* perm, int32_t* inv, void* workspace, cudaStream_t stream);
+void launch_gather_rows(const void* x, int dtype, int64_t N, int d, int k, const int32_t* perm,
+                        void* x_perm, cudaStream_t stream);
+// N5
+void launch_combine(const void* y_perm, int dtype, const int32_t* inv, const float* topk_w,
+                    int64_t N, int k, int d, void* y, cudaStream_t stream);
+
+}  // namespace infmoe

@@ -1,0 +1,276 @@
+// layer.cu — the MoE layer handle: N1 gate -> N2 dispatch -> N3/N4 expert FFN
+// -> N5 combine, resident or offloaded (N6 executor).
+//
+// Offloaded execution realises the two-lane recurrence of simulator.hpp:87-194
+// (and PAPER.md:366, "by using different CUDA streams, parameter-loading and
+// computation of different experts can be easily overlapped"):
+//   * the order comes from the InfMoE scheduler on the routed counts
+//     (cost_model.hpp:43-62 -> scheduler.hpp:243-248), identical to the
+//     reference's order for the same counts / geometry / hardware / K;
+//   * a copy stream streams expert j's W_in+W_out from pinned host memory into
+//     device slot j mod (K+1) with cudaMemcpyAsync, after the expert that last
+//     used that slot (position j-K-1) finished computing.  K+1 physical slots
+//     are what the simulator's "K completed residents + one copy in flight"
+//     semantics needs;
+//   * the compute stream runs expert j's grouped-GEMM pair once load j landed.
+// The per-layer counts read-back is the one device->host sync of the path.
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <vector>
+
+#include "../host/planner.hpp"
+#include "../kernels/common.cuh"
+#include "../kernels/expert_gemm.cuh"
+#include "../kernels/kernels.cuh"
+#include "infmoe.h"
+#include "layer.hpp"
+
+namespace infmoe {
+
+namespace {
+template <class T>
+T* dalloc(size_t n, std::vector<void*>& owned) {
+  void* p = nullptr;
+  if (n == 0) n = 1;
+  INFMOE_CUDA(cudaMalloc(&p, n * sizeof(T)));
+  owned.push_back(p);
+  return reinterpret_cast<T*>(p);
+}
+}  // namespace
+
+Layer::Layer(const infmoe_layer_desc& d) : desc(d) {
+  require(d.d_model > 0 && d.d_ff > 0 && d.n_experts > 0, "layer: dimensions must be > 0");
+  require(d.n_experts <= kMaxGroups, "layer: at most 128 experts per layer");
+  require(d.top_k >= 1 && d.top_k <= 8 && d.top_k <= d.n_experts, "layer: bad top_k");
+  require(d.dtype == INFMOE_DTYPE_BF16 || d.dtype == INFMOE_DTYPE_F32, "layer: bad dtype");
+  require(d.max_tokens >= 1, "layer: max_tokens must be >= 1");
+  require(d.w_in && d.w_out, "layer: expert weights are NULL");
+  if (d.gate_kind == INFMOE_GATE_LSH) require(d.top_k == 1, "layer: the LSH gate is top-1");
+  INFMOE_CUDA(cudaSetDevice(d.device));
+  esz = dtype_bytes(d.dtype);
+  const int64_t A = int64_t(d.max_tokens) * d.top_k;
+  idx = dalloc<int32_t>(size_t(A), owned);
+  wts = dalloc<float>(size_t(A), owned);
+  counts = dalloc<int32_t>(size_t(d.n_experts), owned);
+  offsets = dalloc<int32_t>(size_t(d.n_experts) + 1, owned);
+  perm = dalloc<int32_t>(size_t(A), owned);
+  inv = dalloc<int32_t>(size_t(A), owned);
+  dws = dalloc<uint8_t>(dispatch_workspace_bytes(A, d.n_experts), owned);
+  xp = dalloc<uint8_t>(size_t(A) * d.d_model * esz, owned);
+  hbuf = dalloc<uint8_t>(size_t(A) * d.d_ff * esz, owned);
+  yp = dalloc<uint8_t>(size_t(A) * d.d_model * esz, owned);
+
+  if (d.gate_kind == INFMOE_GATE_LSH) {
+    std::vector<double> p = lsh_hyperplanes(d.lsh_seed, d.lsh_bits, d.d_model);
+    proj = dalloc<double>(p.size(), owned);
+    INFMOE_CUDA(cudaMemcpy(proj, p.data(), p.size() * sizeof(double), cudaMemcpyHostToDevice));
+  } else {
+    require(d.gate_weight != nullptr, "layer: softmax gate needs gate_weight [E, d]");
+    const size_t n = size_t(d.n_experts) * d.d_model;
+    gate_w = dalloc<float>(n, owned);
+    INFMOE_CUDA(cudaMemcpy(gate_w, d.gate_weight, n * sizeof(float), cudaMemcpyHostToDevice));
+    if (d.gate_bias) {
+      gate_b = dalloc<float>(size_t(d.n_experts), owned);
+      INFMOE_CUDA(cudaMemcpy(gate_b, d.gate_bias, sizeof(float) * d.n_experts,
+                             cudaMemcpyHostToDevice));
+    }
+  }
+  INFMOE_CUDA(cudaMallocHost(&counts_host, sizeof(int32_t) * d.n_experts));
+
+  expert_in_bytes = size_t(d.d_ff) * d.d_model * esz;
+  if (d.residency == INFMOE_OFFLOADED) {
+    require(d.K >= 1, "layer: offloaded mode needs K >= 1");
+    n_slots = std::min(d.K + 1, d.n_experts + 1);
+    slot_in = dalloc<uint8_t>(size_t(n_slots) * expert_in_bytes, owned);
+    slot_out = dalloc<uint8_t>(size_t(n_slots) * expert_in_bytes, owned);
+    INFMOE_CUDA(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
+    const int E = d.n_experts;
+    load_done.resize(size_t(E));
+    compute_done.resize(size_t(E));
+    t_load0.resize(size_t(E));
+    t_load1.resize(size_t(E));
+    t_comp0.resize(size_t(E));
+    t_comp1.resize(size_t(E));
+    for (int j = 0; j < E; ++j) {
+      INFMOE_CUDA(cudaEventCreateWithFlags(&load_done[size_t(j)], cudaEventDisableTiming));
+      INFMOE_CUDA(cudaEventCreateWithFlags(&compute_done[size_t(j)], cudaEventDisableTiming));
+      INFMOE_CUDA(cudaEventCreate(&t_load0[size_t(j)]));
+      INFMOE_CUDA(cudaEventCreate(&t_load1[size_t(j)]));
+      INFMOE_CUDA(cudaEventCreate(&t_comp0[size_t(j)]));
+      INFMOE_CUDA(cudaEventCreate(&t_comp1[size_t(j)]));
+    }
+    INFMOE_CUDA(cudaEventCreate(&t_start));
+    set_host_weights(d.w_in, d.w_out);
+  }
+}
+
+void Layer::set_host_weights(const void* w_in, const void* w_out) {
+  require(desc.residency == INFMOE_OFFLOADED, "set_host_weights: layer is resident");
+  require(w_in && w_out, "set_host_weights: NULL weights");
+  const size_t bytes = expert_in_bytes * size_t(desc.n_experts);
+  for (const void* p : {w_in, w_out}) {
+    cudaPointerAttributes at;
+    INFMOE_CUDA(cudaPointerGetAttributes(&at, p));
+    if (at.type == cudaMemoryTypeUnregistered) {
+      INFMOE_CUDA(cudaHostRegister(const_cast<void*>(p), bytes, cudaHostRegisterDefault));
+      registered.push_back(const_cast<void*>(p));
+    } else {
+      require(at.type == cudaMemoryTypeHost,
+              "offloaded layer: expert weights must live in host memory");
+    }
+  }
+  host_in = reinterpret_cast<const uint8_t*>(w_in);
+  host_out = reinterpret_cast<const uint8_t*>(w_out);
+}
+
+Layer::~Layer() {
+  cudaSetDevice(desc.device);
+  if (copy_stream) cudaStreamSynchronize(copy_stream);
+  for (auto* v : {&load_done, &compute_done, &t_load0, &t_load1, &t_comp0, &t_comp1})
+    for (cudaEvent_t e : *v) cudaEventDestroy(e);
+  if (t_start) cudaEventDestroy(t_start);
+  if (copy_stream) cudaStreamDestroy(copy_stream);
+  for (void* p : registered) cudaHostUnregister(p);
+  if (counts_host) cudaFreeHost(counts_host);
+  for (void* p : owned) cudaFree(p);
+}
+
+void Layer::route(const void* x, int64_t N, cudaStream_t s) {
+  const int E = desc.n_experts, k = desc.top_k;
+  if (desc.gate_kind == INFMOE_GATE_LSH)
+    launch_gate_lsh(x, desc.dtype, N, desc.d_model, proj, desc.lsh_bits, E, nullptr, idx, wts,
+                    counts, s);
+  else
+    launch_gate_softmax(x, desc.dtype, N, desc.d_model, gate_w, gate_b, E, k, idx, wts, counts,
+                        s);
+  launch_dispatch(idx, N * k, E, offsets, perm, inv, dws, s);
+  launch_gather_rows(x, desc.dtype, N, desc.d_model, k, perm, xp, s);
+}
+
+void Layer::ffn(const int32_t* experts, const int32_t* slots, int n, const void* w_in,
+                const void* w_out, int n_w_slots, int64_t rows, int max_ctas, cudaStream_t s) {
+  GroupedGemmArgs g;
+  std::memset(&g, 0, sizeof(g));
+  g.a = xp;
+  g.a_rows = rows;
+  g.b = w_in;
+  g.n_slots = n_w_slots;
+  g.N = desc.d_ff;
+  g.K = desc.d_model;
+  g.dtype = desc.dtype;
+  g.offsets = offsets;
+  g.n_groups = n;
+  for (int i = 0; i < n; ++i) {
+    g.experts[i] = experts[i];
+    g.slots[i] = slots[i];
+  }
+  g.out = hbuf;
+  g.gelu = 1;
+  g.max_ctas = max_ctas;
+  launch_grouped_gemm(g, s);
+  g.a = hbuf;
+  g.b = w_out;
+  g.N = desc.d_model;
+  g.K = desc.d_ff;
+  g.out = yp;
+  g.gelu = 0;
+  launch_grouped_gemm(g, s);
+}
+
+void Layer::forward(const void* x, int64_t N, void* y, infmoe_forward_out* out, cudaStream_t s) {
+  require(N >= 0 && N <= desc.max_tokens, "forward: N exceeds max_tokens");
+  INFMOE_CUDA(cudaSetDevice(desc.device));
+  const int E = desc.n_experts, k = desc.top_k;
+  const int64_t rows = N * k;
+  if (desc.residency == INFMOE_OFFLOADED) INFMOE_CUDA(cudaEventRecord(t_start, s));
+  route(x, N, s);
+
+  std::vector<int32_t> all(static_cast<size_t>(E));
+  for (int e = 0; e < E; ++e) all[size_t(e)] = e;
+
+  if (desc.residency == INFMOE_RESIDENT) {
+    if (rows > 0) ffn(all.data(), all.data(), E, desc.w_in, desc.w_out, E, rows, 0, s);
+    launch_combine(yp, desc.dtype, inv, wts, N, k, desc.d_model, y, s);
+    if (out && out->counts) {
+      INFMOE_CUDA(cudaMemcpyAsync(out->counts, counts, sizeof(int32_t) * E,
+                                  cudaMemcpyDeviceToHost, s));
+      INFMOE_CUDA(cudaStreamSynchronize(s));
+    }
+    return;
+  }
+
+  // ---- offloaded: counts -> schedule (host) ----
+  INFMOE_CUDA(cudaMemcpyAsync(counts_host, counts, sizeof(int32_t) * E, cudaMemcpyDeviceToHost, s));
+  INFMOE_CUDA(cudaStreamSynchronize(s));
+  std::vector<uint64_t> cnt(static_cast<size_t>(E));
+  for (int e = 0; e < E; ++e) cnt[size_t(e)] = uint64_t(counts_host[e]);
+  Geometry geo{1, 1, 1, desc.d_model, desc.d_ff, E, int(esz)};
+  Hardware hw{desc.hw.peak_flops, desc.hw.h2d_bandwidth, desc.hw.device_memory,
+              desc.hw.reserved_memory};
+  Costs c = derive_costs(cnt.data(), E, geo, hw);
+  Plan plan;
+  switch (desc.policy) {
+    case INFMOE_POLICY_NAIVE: plan = plan_identity(c, desc.K); break;
+    case INFMOE_POLICY_GREEDY: plan = plan_greedy(c, desc.K); break;
+    case INFMOE_POLICY_EXACT: plan = plan_exact(c, desc.K, 12); break;
+    default: plan = plan_auto(c, desc.K, 12); break;
+  }
+  const bool timed = out && (out->events || out->exposed_copy_s);
+
+  // ---- copy lane / compute lane ----
+  INFMOE_CUDA(cudaStreamWaitEvent(copy_stream, t_start, 0));  // drain: after previous layer
+  for (int j = 0; j < E; ++j) {
+    const int e = plan.order[size_t(j)];
+    const int slot = j % n_slots;
+    if (j >= n_slots) INFMOE_CUDA(cudaStreamWaitEvent(copy_stream, compute_done[size_t(j - n_slots)], 0));
+    if (timed) INFMOE_CUDA(cudaEventRecord(t_load0[size_t(j)], copy_stream));
+    INFMOE_CUDA(cudaMemcpyAsync(slot_in + size_t(slot) * expert_in_bytes,
+                                host_in + size_t(e) * expert_in_bytes, expert_in_bytes,
+                                cudaMemcpyHostToDevice, copy_stream));
+    INFMOE_CUDA(cudaMemcpyAsync(slot_out + size_t(slot) * expert_in_bytes,
+                                host_out + size_t(e) * expert_in_bytes, expert_in_bytes,
+                                cudaMemcpyHostToDevice, copy_stream));
+    if (timed) INFMOE_CUDA(cudaEventRecord(t_load1[size_t(j)], copy_stream));
+    INFMOE_CUDA(cudaEventRecord(load_done[size_t(j)], copy_stream));
+
+    INFMOE_CUDA(cudaStreamWaitEvent(s, load_done[size_t(j)], 0));
+    if (timed) INFMOE_CUDA(cudaEventRecord(t_comp0[size_t(j)], s));
+    const int32_t ex = e, sl = slot;
+    const int64_t n_e = int64_t(cnt[size_t(e)]);
+    if (n_e > 0) {
+      const int tiles = int((n_e + 255) / 256) * (desc.d_ff / 128);
+      ffn(&ex, &sl, 1, slot_in, slot_out, n_slots, rows, tiles, s);
+    }
+    if (timed) INFMOE_CUDA(cudaEventRecord(t_comp1[size_t(j)], s));
+    INFMOE_CUDA(cudaEventRecord(compute_done[size_t(j)], s));
+  }
+  launch_combine(yp, desc.dtype, inv, wts, N, k, desc.d_model, y, s);
+
+  if (out) {
+    if (out->counts) std::memcpy(out->counts, counts_host, sizeof(int32_t) * E);
+    if (out->order) std::memcpy(out->order, plan.order.data(), sizeof(int32_t) * E);
+    if (out->feasible) *out->feasible = plan.feasible ? 1 : 0;
+    if (timed) {
+      INFMOE_CUDA(cudaStreamSynchronize(s));
+      double busy = 0.0, makespan = 0.0;
+      for (int j = 0; j < E; ++j) {
+        float a = 0, b = 0, c0 = 0, c1 = 0;
+        INFMOE_CUDA(cudaEventElapsedTime(&a, t_start, t_load0[size_t(j)]));
+        INFMOE_CUDA(cudaEventElapsedTime(&b, t_start, t_load1[size_t(j)]));
+        INFMOE_CUDA(cudaEventElapsedTime(&c0, t_start, t_comp0[size_t(j)]));
+        INFMOE_CUDA(cudaEventElapsedTime(&c1, t_start, t_comp1[size_t(j)]));
+        const int e = plan.order[size_t(j)];
+        if (out->events) {
+          out->events[2 * j] = {INFMOE_STREAM_LOAD, 0, e, a * 1e-3, b * 1e-3};
+          out->events[2 * j + 1] = {INFMOE_STREAM_COMPUTE, 0, e, c0 * 1e-3, c1 * 1e-3};
+        }
+        busy += (c1 - c0) * 1e-3;
+        makespan = std::max(makespan, double(c1) * 1e-3);
+      }
+      if (out->exposed_copy_s) *out->exposed_copy_s = makespan - busy;
+    }
+  }
+}
+
+}  // namespace infmoe

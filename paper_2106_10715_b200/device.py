@@ -1,0 +1,211 @@
+"""Device-path wrappers: call the C-ABI kernels on torch-allocated device memory.
+
+torch is plumbing here (allocation, streams); every computation runs in
+libinfmoe.so.  Functions take/return torch tensors and launch on the current
+torch CUDA stream.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import (DTYPE_BF16, DTYPE_F32, GATE_LSH, GATE_SOFTMAX, OFFLOADED, POLICY_AUTO, RESIDENT,
+               Event, ForwardOut, Hardware, LayerDesc, _check, _lib)
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _dtype_code(t) -> int:
+    torch = _torch()
+    if t.dtype == torch.bfloat16:
+        return DTYPE_BF16
+    if t.dtype == torch.float32:
+        return DTYPE_F32
+    raise TypeError(f"unsupported dtype {t.dtype}")
+
+
+def _stream_ptr():
+    torch = _torch()
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _p(t) -> C.c_void_p:
+    return C.c_void_p(0 if t is None else t.data_ptr())
+
+
+def _need_cuda(*ts):
+    for t in ts:
+        if t is not None and not t.is_cuda:
+            raise ValueError("device-path call needs CUDA tensors")
+
+
+def fill_uniform(t, seed: int, scale: float) -> None:
+    """Counter-hash uniform fill (same bits as oracle or_fill_uniform_*)."""
+    _need_cuda(t)
+    _check(_lib.infmoe_fill_uniform(_p(t), _dtype_code(t), t.numel(), seed, scale,
+                                    _stream_ptr()))
+
+
+def gate_softmax_topk(x, wg, k: int, bias=None):
+    torch = _torch()
+    _need_cuda(x, wg, bias)
+    N, d = x.shape
+    E = wg.shape[0]
+    idx = torch.empty((N, k), dtype=torch.int32, device=x.device)
+    w = torch.empty((N, k), dtype=torch.float32, device=x.device)
+    counts = torch.empty(E, dtype=torch.int32, device=x.device)
+    _check(_lib.infmoe_gate_softmax_topk(_p(x), _dtype_code(x), N, d, _p(wg), _p(bias), E, k,
+                                         _p(idx), _p(w), _p(counts), _stream_ptr()))
+    return idx, w, counts
+
+
+def gate_lsh(x, proj, n_experts: int):
+    torch = _torch()
+    _need_cuda(x, proj)
+    N, d = x.shape
+    bits = proj.shape[0]
+    codes = torch.empty(N, dtype=torch.int32, device=x.device)
+    idx = torch.empty((N, 1), dtype=torch.int32, device=x.device)
+    w = torch.empty((N, 1), dtype=torch.float32, device=x.device)
+    counts = torch.empty(n_experts, dtype=torch.int32, device=x.device)
+    _check(_lib.infmoe_gate_lsh(_p(x), _dtype_code(x), N, d, _p(proj), bits, n_experts,
+                                _p(codes), _p(idx), _p(w), _p(counts), _stream_ptr()))
+    return codes, idx, w, counts
+
+
+def dispatch(topk_idx, n_experts: int):
+    torch = _torch()
+    _need_cuda(topk_idx)
+    N, k = topk_idx.shape
+    A = N * k
+    offsets = torch.empty(n_experts + 1, dtype=torch.int32, device=topk_idx.device)
+    perm = torch.empty(max(A, 1), dtype=torch.int32, device=topk_idx.device)
+    inv = torch.empty(max(A, 1), dtype=torch.int32, device=topk_idx.device)
+    ws = torch.empty(int(_lib.infmoe_dispatch_workspace_bytes(A, n_experts)), dtype=torch.uint8,
+                     device=topk_idx.device)
+    _check(_lib.infmoe_dispatch(_p(topk_idx), N, k, n_experts, _p(offsets), _p(perm), _p(inv),
+                                _p(ws), _stream_ptr()))
+    return offsets, perm[:A], inv[:A]
+
+
+def gather_rows(x, perm, k: int):
+    torch = _torch()
+    N, d = x.shape
+    xp = torch.empty((N * k, d), dtype=x.dtype, device=x.device)
+    _check(_lib.infmoe_gather_rows(_p(x), _dtype_code(x), N, d, k, _p(perm), _p(xp),
+                                   _stream_ptr()))
+    return xp
+
+
+def expert_ffn(x_perm, offsets, w_in, w_out, experts: Optional[Sequence[int]] = None,
+               slots: Optional[Sequence[int]] = None, h=None, y_perm=None):
+    """h = GeLU(x_perm . w_in[slot]^T), y = h . w_out[slot]^T per expert segment.
+
+    w_in: [n_slots, d_ff, d_model], w_out: [n_slots, d_model, d_ff]."""
+    torch = _torch()
+    _need_cuda(x_perm, offsets, w_in, w_out)
+    R, d = x_perm.shape
+    n_slots, f, _ = w_in.shape
+    E = offsets.numel() - 1
+    if h is None:
+        h = torch.empty((R, f), dtype=x_perm.dtype, device=x_perm.device)
+    if y_perm is None:
+        y_perm = torch.empty((R, d), dtype=x_perm.dtype, device=x_perm.device)
+    if experts is None:
+        ex = sl = None
+        n = E
+    else:
+        ex = np.ascontiguousarray(np.asarray(experts, dtype=np.int32))
+        sl = np.ascontiguousarray(np.asarray(slots if slots is not None else experts,
+                                             dtype=np.int32))
+        n = len(ex)
+    _check(_lib.infmoe_expert_ffn(_p(x_perm), R, d, f, _dtype_code(x_perm), _p(offsets), E,
+                                  _p(w_in), _p(w_out), n_slots,
+                                  None if ex is None else ex.ctypes.data_as(C.c_void_p),
+                                  None if sl is None else sl.ctypes.data_as(C.c_void_p), n,
+                                  _p(h), _p(y_perm), _stream_ptr()))
+    return h, y_perm
+
+
+def combine(y_perm, inv, topk_w, N: int, k: int):
+    torch = _torch()
+    d = y_perm.shape[1]
+    y = torch.empty((N, d), dtype=y_perm.dtype, device=y_perm.device)
+    _check(_lib.infmoe_combine(_p(y_perm), _dtype_code(y_perm), _p(inv), _p(topk_w), N, k, d,
+                               _p(y), _stream_ptr()))
+    return y
+
+
+class MoELayer:
+    """Owning wrapper of an infmoe_layer handle (the paper's MoE plugin)."""
+
+    def __init__(self, d_model: int, d_ff: int, n_experts: int, top_k: int, w_in, w_out, *,
+                 dtype: str = "bf16", gate: str = "lsh", gate_weight=None, gate_bias=None,
+                 lsh_seed: int = 0, lsh_bits: int = 5, offloaded: bool = False, K: int = 4,
+                 policy: int = POLICY_AUTO, max_tokens: int = 4096, device: int = 0,
+                 hw: Optional[Hardware] = None):
+        d = LayerDesc()
+        d.d_model, d.d_ff, d.n_experts, d.top_k = d_model, d_ff, n_experts, top_k
+        d.dtype = DTYPE_BF16 if dtype == "bf16" else DTYPE_F32
+        d.gate_kind = GATE_LSH if gate == "lsh" else GATE_SOFTMAX
+        d.residency = OFFLOADED if offloaded else RESIDENT
+        d.K, d.policy, d.max_tokens, d.device = K, policy, max_tokens, device
+        self._keep = []
+        if gate_weight is not None:
+            gw = np.ascontiguousarray(np.asarray(gate_weight, dtype=np.float32))
+            self._keep.append(gw)
+            d.gate_weight = gw.ctypes.data
+        if gate_bias is not None:
+            gb = np.ascontiguousarray(np.asarray(gate_bias, dtype=np.float32))
+            self._keep.append(gb)
+            d.gate_bias = gb.ctypes.data
+        d.lsh_seed, d.lsh_bits = lsh_seed, lsh_bits
+        d.w_in, d.w_out = w_in.data_ptr(), w_out.data_ptr()
+        self._keep += [w_in, w_out]
+        d.hw = hw if hw is not None else Hardware(1643.6e12, 55.5e9, 180 << 30, 8 << 30)
+        self.desc = d
+        self.n_experts = n_experts
+        self._h = C.c_void_p()
+        _check(_lib.infmoe_layer_create(C.byref(d), C.byref(self._h)))
+
+    def set_host_weights(self, w_in, w_out) -> None:
+        self._keep += [w_in, w_out]
+        _check(_lib.infmoe_layer_set_host_weights(self._h, C.c_void_p(w_in.data_ptr()),
+                                                  C.c_void_p(w_out.data_ptr())))
+
+    def forward(self, x, y=None, *, want_timeline: bool = False):
+        torch = _torch()
+        N = x.shape[0]
+        if y is None:
+            y = torch.empty_like(x)
+        E = self.n_experts
+        counts = np.zeros(E, dtype=np.int32)
+        order = np.zeros(E, dtype=np.int32)
+        feas = C.c_int32(0)
+        exposed = C.c_double(0.0)
+        events = (Event * (2 * E))()
+        out = ForwardOut(counts.ctypes.data, order.ctypes.data, C.addressof(feas),
+                         C.addressof(events) if want_timeline else None,
+                         C.addressof(exposed) if want_timeline else None)
+        _check(_lib.infmoe_layer_forward(self._h, _p(x), N, _p(y), C.byref(out), _stream_ptr()))
+        info = {"counts": counts, "order": order, "feasible": bool(feas.value)}
+        if want_timeline:
+            info["events"] = [(e.stream, e.layer_id, e.expert_id, e.start, e.end) for e in events]
+            info["exposed_copy_s"] = exposed.value
+        return y, info
+
+    def close(self) -> None:
+        if self._h:
+            _lib.infmoe_layer_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
