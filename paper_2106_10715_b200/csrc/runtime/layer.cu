@@ -100,9 +100,14 @@ Layer::Layer(const infmoe_layer_desc& d) : desc(d) {
       INFMOE_CUDA(cudaEventCreate(&t_comp0[size_t(j)]));
       INFMOE_CUDA(cudaEventCreate(&t_comp1[size_t(j)]));
     }
-    INFMOE_CUDA(cudaEventCreate(&t_start));
     set_host_weights(d.w_in, d.w_out);
+  } else {
+    t_comp0.resize(1);
+    t_comp1.resize(1);
+    INFMOE_CUDA(cudaEventCreate(&t_comp0[0]));
+    INFMOE_CUDA(cudaEventCreate(&t_comp1[0]));
   }
+  INFMOE_CUDA(cudaEventCreate(&t_start));
 }
 
 void Layer::set_host_weights(const void* w_in, const void* w_out) {
@@ -183,19 +188,31 @@ void Layer::forward(const void* x, int64_t N, void* y, infmoe_forward_out* out, 
   INFMOE_CUDA(cudaSetDevice(desc.device));
   const int E = desc.n_experts, k = desc.top_k;
   const int64_t rows = N * k;
-  if (desc.residency == INFMOE_OFFLOADED) INFMOE_CUDA(cudaEventRecord(t_start, s));
+  const bool timed = out && (out->events || out->exposed_copy_s);
+  INFMOE_CUDA(cudaEventRecord(t_start, s));
   route(x, N, s);
 
   std::vector<int32_t> all(static_cast<size_t>(E));
   for (int e = 0; e < E; ++e) all[size_t(e)] = e;
 
   if (desc.residency == INFMOE_RESIDENT) {
+    // one grouped launch per projection over all experts; no host round trip
+    if (timed) INFMOE_CUDA(cudaEventRecord(t_comp0[0], s));
     if (rows > 0) ffn(all.data(), all.data(), E, desc.w_in, desc.w_out, E, rows, 0, s);
+    if (timed) INFMOE_CUDA(cudaEventRecord(t_comp1[0], s));
     launch_combine(yp, desc.dtype, inv, wts, N, k, desc.d_model, y, s);
     if (out && out->counts) {
-      INFMOE_CUDA(cudaMemcpyAsync(out->counts, counts, sizeof(int32_t) * E,
+      INFMOE_CUDA(cudaMemcpyAsync(counts_host, counts, sizeof(int32_t) * E,
                                   cudaMemcpyDeviceToHost, s));
-      INFMOE_CUDA(cudaStreamSynchronize(s));
+    }
+    if (out && (out->counts || timed)) INFMOE_CUDA(cudaStreamSynchronize(s));
+    if (out && out->counts) std::memcpy(out->counts, counts_host, sizeof(int32_t) * E);
+    if (timed) {
+      float a = 0, b = 0;
+      INFMOE_CUDA(cudaEventElapsedTime(&a, t_start, t_comp0[0]));
+      INFMOE_CUDA(cudaEventElapsedTime(&b, t_start, t_comp1[0]));
+      if (out->events) out->events[0] = {INFMOE_STREAM_COMPUTE, 0, -1, a * 1e-3, b * 1e-3};
+      if (out->exposed_copy_s) *out->exposed_copy_s = 0.0;
     }
     return;
   }
@@ -216,7 +233,6 @@ void Layer::forward(const void* x, int64_t N, void* y, infmoe_forward_out* out, 
     case INFMOE_POLICY_EXACT: plan = plan_exact(c, desc.K, 12); break;
     default: plan = plan_auto(c, desc.K, 12); break;
   }
-  const bool timed = out && (out->events || out->exposed_copy_s);
 
   // ---- copy lane / compute lane ----
   INFMOE_CUDA(cudaStreamWaitEvent(copy_stream, t_start, 0));  // drain: after previous layer

@@ -1,0 +1,146 @@
+"""End-to-end MoE layer (the C-ABI handle) on the GPU against the oracle
+chain, resident and offloaded; the offloaded order against the reference
+scheduler; the measured timeline against replay_check's rules."""
+import ctypes as C
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2106_10715_b200 as im
+from paper_2106_10715_b200 import device as dv
+from oracle_lib import (O, REF, EventRec, bf16_bits_to_f32, f32_to_bf16_bits, fill_bf16, ptr,
+                        f64a, i32a, schedule)
+
+pytestmark = pytest.mark.gpu
+
+ATOL, RTOL = 3e-2, 2e-2  # bf16 layer output vs fp64 oracle chain
+
+
+def _setup(cuda, N, d, f, E, seed=11):
+    xb = fill_bf16(im.derive_seed(seed, 0), N * d, 1.7320508)
+    wib = fill_bf16(im.derive_seed(seed, 1000), E * f * d, 1.7320508 / np.sqrt(d))
+    wob = fill_bf16(im.derive_seed(seed, 1001), E * d * f, 1.5340 * 1.7320508 / np.sqrt(f))
+    t = lambda b, sh: torch.from_numpy(b.view(np.int16).reshape(sh)).view(torch.bfloat16)
+    return (xb, wib, wob), (t(xb, (N, d)).to(cuda), t(wib, (E, f, d)), t(wob, (E, d, f)))
+
+
+def _oracle_layer(xb, wib, wob, N, d, f, E, k, idx, w):
+    xf = bf16_bits_to_f32(xb).reshape(N, d)
+    wif, wof = bf16_bits_to_f32(wib), bf16_bits_to_f32(wob)
+    off = np.zeros(E + 1, np.int32)
+    perm = np.zeros(N * k, np.int32)
+    inv = np.zeros(N * k, np.int32)
+    O.or_dispatch(ptr(idx), N, k, E, ptr(off), ptr(perm), ptr(inv))
+    xp = np.ascontiguousarray(xf[perm // k])
+    yp = np.zeros((N * k, d), np.float32)
+    for e in range(E):
+        a, b = off[e], off[e + 1]
+        if b > a:
+            O.or_expert_ffn(ptr(np.ascontiguousarray(xp[a:b])), b - a, d, f,
+                            ptr(np.ascontiguousarray(wif[e * f * d:(e + 1) * f * d])),
+                            ptr(np.ascontiguousarray(wof[e * d * f:(e + 1) * d * f])), 1,
+                            ptr(yp[a:b]))
+    yp = bf16_bits_to_f32(f32_to_bf16_bits(yp)).reshape(N * k, d)  # device stores y_perm bf16
+    y = np.zeros((N, d), np.float32)
+    O.or_combine(ptr(yp), ptr(inv), ptr(np.ascontiguousarray(w)), N, k, d, ptr(y))
+    return y
+
+
+@pytest.mark.parametrize("gate", ["lsh", "softmax"])
+def test_resident_layer_vs_oracle(cuda, gate):
+    N, d, f, E = 600, 256, 512, 8
+    k = 1 if gate == "lsh" else 2
+    (xb, wib, wob), (x, wi, wo) = _setup(cuda, N, d, f, E)
+    gw = (np.random.default_rng(0).standard_normal((E, d)) / np.sqrt(d)).astype(np.float32)
+    layer = dv.MoELayer(d, f, E, k, wi.to(cuda), wo.to(cuda), gate=gate, gate_weight=gw,
+                        lsh_seed=77, lsh_bits=3, max_tokens=N)
+    y, info = layer.forward(x)
+    torch.cuda.synchronize()
+    xf = bf16_bits_to_f32(xb).reshape(N, d)
+    idx = np.zeros((N, k), np.int32)
+    w = np.zeros((N, k), np.float32)
+    cnt = np.zeros(E, np.int32)
+    if gate == "lsh":
+        proj = im.gating_projection(77, 3, d)
+        O.or_gate_lsh(ptr(xf), N, d, ptr(np.ascontiguousarray(proj)), 3, E, ptr(idx), ptr(w),
+                      ptr(cnt))
+    else:
+        O.or_gate_softmax(ptr(xf), N, d, ptr(gw), None, E, k, ptr(idx), ptr(w), ptr(cnt))
+    assert np.array_equal(info["counts"], cnt)
+    ref = _oracle_layer(xb, wib, wob, N, d, f, E, k, idx, w)
+    got = y.float().cpu().numpy()
+    err = np.abs(got - ref)
+    assert np.all(err <= ATOL + RTOL * np.abs(ref)), err.max()
+    layer.close()
+
+
+@pytest.mark.parametrize("K,policy", [(1, im.POLICY_AUTO), (3, im.POLICY_AUTO),
+                                      (2, im.POLICY_NAIVE)])
+def test_offloaded_layer_equals_resident_and_reference_order(cuda, K, policy):
+    N, d, f, E = 1000, 256, 384, 12
+    (xb, wib, wob), (x, wi, wo) = _setup(cuda, N, d, f, E, seed=3)
+    res = dv.MoELayer(d, f, E, 1, wi.to(cuda), wo.to(cuda), gate="lsh", lsh_seed=5, lsh_bits=4,
+                      max_tokens=N)
+    y_res, info_r = res.forward(x)
+    hw = im.Hardware(1e12, 2e10, 80 << 30, 8 << 30)
+    off = dv.MoELayer(d, f, E, 1, wi.pin_memory(), wo.pin_memory(), gate="lsh", lsh_seed=5,
+                      lsh_bits=4, offloaded=True, K=K, policy=policy, max_tokens=N, hw=hw)
+    y_off, info = off.forward(x, want_timeline=True)
+    torch.cuda.synchronize()
+    # same kernels, same tiles -> bit-identical output whatever the expert order
+    assert torch.equal(y_res.view(torch.int16), y_off.view(torch.int16))
+    assert np.array_equal(info["counts"], info_r["counts"])
+    # the executed order is the reference scheduler's order for these counts
+    g = im.make_geometry(d, f, E, 2)
+    cv = im.compute_costs(info["counts"].astype(np.uint64), g, hw)
+    if policy == im.POLICY_AUTO:
+        want = schedule("ref" if REF is not None else "or", cv.alphas, cv.beta, K, "auto")[1]
+    else:
+        want = list(range(E))
+    assert info["order"].tolist() == want
+    # measured timeline: one lane each, causality, <= K+1 simultaneous residents (D6)
+    ev = info["events"]
+    loads = sorted([e for e in ev if e[0] == 0], key=lambda e: e[3])
+    comps = sorted([e for e in ev if e[0] == 1], key=lambda e: e[3])
+    for lane in (loads, comps):
+        for a, b in zip(lane, lane[1:]):
+            assert a[4] <= b[3] + 1e-6
+    le = {e[2]: e[4] for e in loads}
+    for c in comps:
+        assert c[3] >= le[c[2]] - 1e-6
+    marks = sorted([(le[c[2]], 1) for c in comps] + [(c[4], -1) for c in comps])
+    cur = peak = 0
+    for _, dlt in sorted(marks, key=lambda m: (m[0], m[1])):
+        cur += dlt
+        peak = max(peak, cur)
+    assert peak <= K + 1
+    assert info["exposed_copy_s"] > 0
+    off.close()
+    res.close()
+
+
+def test_offloaded_layer_host_weight_swap(cuda):
+    N, d, f, E = 256, 128, 256, 4
+    (_, _, _), (x, wi, wo) = _setup(cuda, N, d, f, E, seed=8)
+    (_, _, _), (_, wi2, wo2) = _setup(cuda, N, d, f, E, seed=9)
+    off = dv.MoELayer(d, f, E, 1, wi.pin_memory(), wo.pin_memory(), gate="lsh", lsh_seed=1,
+                      lsh_bits=2, offloaded=True, K=1, max_tokens=N)
+    res2 = dv.MoELayer(d, f, E, 1, wi2.to(cuda), wo2.to(cuda), gate="lsh", lsh_seed=1,
+                       lsh_bits=2, max_tokens=N)
+    off.set_host_weights(wi2.clone(), wo2.clone())  # pageable: registered by the handle
+    y1, _ = off.forward(x)
+    y2, _ = res2.forward(x)
+    torch.cuda.synchronize()
+    assert torch.equal(y1.view(torch.int16), y2.view(torch.int16))
+    off.close()
+    res2.close()
+
+
+def test_layer_rejects_bad_config(cuda):
+    wi = torch.zeros(2, 128, 128, dtype=torch.bfloat16, device=cuda)
+    with pytest.raises(im.ConfigError):
+        dv.MoELayer(128, 128, 2, 2, wi, wi, gate="lsh", lsh_bits=1)  # LSH is top-1
+    with pytest.raises(im.ConfigError):
+        dv.MoELayer(128, 100, 2, 1, wi, wi, gate="lsh", lsh_bits=1).forward(
+            torch.zeros(4, 128, dtype=torch.bfloat16, device=cuda))  # d_ff % 128
