@@ -3,9 +3,10 @@
  *
  * Plain C types only: pointers, sizes, POD structs.  No C++ exception crosses
  * this boundary; every entry point returns a status code:
- *   0 OK, 2 config / invalid argument (moesim::ConfigError, std::invalid_argument),
- *   3 capacity (moesim::CapacityError), 4 invariant breach (moesim::InvariantError),
- *   5 CUDA / NCCL runtime failure.
+ *   0 OK, 2 config (moesim::ConfigError), 3 capacity (moesim::CapacityError),
+ *   4 invariant breach (moesim::InvariantError), 5 CUDA / NCCL runtime failure,
+ *   6 invalid argument (std::invalid_argument: malformed call, NULL pointer,
+ *     non-permutation order, K < 1, T > max_T).
  * (errors.hpp:8-21 and SPEC.md:382 exit-code convention.)  The message for the
  * last failure on the calling thread is infmoe_last_error().
  *
@@ -28,7 +29,8 @@ enum {
   INFMOE_ERR_CONFIG = 2,
   INFMOE_ERR_CAPACITY = 3,
   INFMOE_ERR_INVARIANT = 4,
-  INFMOE_ERR_RUNTIME = 5
+  INFMOE_ERR_RUNTIME = 5,
+  INFMOE_ERR_ARGUMENT = 6
 };
 
 const char* infmoe_last_error(void);

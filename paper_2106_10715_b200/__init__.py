@@ -46,6 +46,10 @@ class CudaError(RuntimeError):
     """CUDA / NCCL runtime failure, status 5."""
 
 
+class InvalidArgument(ValueError):
+    """std::invalid_argument (e.g. scheduler.hpp:49-62, :74), status 6."""
+
+
 _lib.infmoe_last_error.restype = C.c_char_p
 _lib.infmoe_version.restype = C.c_char_p
 
@@ -54,7 +58,8 @@ def _check(rc: int) -> None:
     if rc == 0:
         return
     msg = (_lib.infmoe_last_error() or b"").decode()
-    raise {2: ConfigError, 3: CapacityError, 4: InvariantError, 5: CudaError}.get(
+    raise {2: ConfigError, 3: CapacityError, 4: InvariantError, 5: CudaError,
+                6: InvalidArgument}.get(
         rc, RuntimeError)(msg)
 
 

@@ -205,7 +205,7 @@ int infmoe_simulate_model(int32_t n_layers, const int32_t* T, const double* alph
                           infmoe_event* events, infmoe_sim_report* rep,
                           infmoe_layer_report* per_layer) {
   return guarded([&] {
-    if (n_layers < 1) fail(kConfig, "simulate_model: no layers");
+    if (n_layers < 1) fail(kArgument, "simulate_model: no layers");
     require(T && alphas && betas, "NULL argument");
     std::vector<Costs> cs;
     std::vector<std::vector<int>> orders;

@@ -186,12 +186,12 @@ int capacity_slots(const Geometry& g, const Hardware& hw) {  // cost_model.hpp:6
 namespace {
 void require_order(std::span<const int> order, int T) {
   if (int(order.size()) != T)
-    fail(kConfig, "order size " + std::to_string(order.size()) + " != expert count " +
+    fail(kArgument, "order size " + std::to_string(order.size()) + " != expert count " +
                       std::to_string(T));
   std::vector<char> hit(std::size_t(T), 0);
   for (int e : order) {
     if (e < 0 || e >= T || hit[std::size_t(e)])
-      fail(kConfig, "order is not a permutation of 0.." + std::to_string(T - 1));
+      fail(kArgument, "order is not a permutation of 0.." + std::to_string(T - 1));
     hit[std::size_t(e)] = 1;
   }
 }
@@ -219,7 +219,7 @@ Plan finish(std::vector<int> order, const Costs& c, int K, Method m, bool diagno
 BandCheck band_check(std::span<const int> order, const Costs& c, int K) {
   const int T = c.size();
   require_order(order, T);
-  if (K < 1) fail(kConfig, "K must be >= 1");
+  if (K < 1) fail(kArgument, "K must be >= 1");
   BandCheck r;
   r.slack.resize(std::size_t(T));
   double P = 0.0;
@@ -248,7 +248,7 @@ BandCheck band_check(std::span<const int> order, const Costs& c, int K) {
 // go to the lower index.
 Plan plan_greedy(const Costs& c, int K) {
   check_costs(c);
-  if (K < 1) fail(kConfig, "K must be >= 1");
+  if (K < 1) fail(kArgument, "K must be >= 1");
   const int T = c.size();
   const auto& a = c.alpha;
   std::vector<char> taken(std::size_t(T), 0);
@@ -284,11 +284,11 @@ Plan plan_greedy(const Costs& c, int K) {
 // smallest feasible order.
 Plan plan_exact(const Costs& c, int K, int max_T) {
   check_costs(c);
-  if (K < 1) fail(kConfig, "K must be >= 1");
+  if (K < 1) fail(kArgument, "K must be >= 1");
   const int T = c.size();
   max_T = std::min(max_T, 24);
   if (T > max_T)
-    fail(kConfig, "exact_order: T = " + std::to_string(T) + " exceeds max_T = " +
+    fail(kArgument, "exact_order: T = " + std::to_string(T) + " exceeds max_T = " +
                       std::to_string(max_T));
   std::vector<char> dead(std::size_t(1) << T, 0);
   std::vector<int> path;
@@ -365,7 +365,7 @@ int max_resident(std::vector<std::pair<double, int>>& marks) {
 TimelineStats run_timeline(std::span<const std::vector<int>> orders,
                            std::span<const Costs> costs, int K, bool serial,
                            bool continuous_loads, std::vector<Event>* events) {
-  if (K < 1) fail(kConfig, "K must be >= 1");
+  if (K < 1) fail(kArgument, "K must be >= 1");
   TimelineStats st;
   double load_lane = 0.0, compute_lane = 0.0, last_ce = -1.0;
   for (std::size_t l = 0; l < costs.size(); ++l) {

@@ -11,10 +11,11 @@ namespace infmoe {
 
 enum Status : int {
   kOk = 0,
-  kConfig = 2,     // moesim::ConfigError / std::invalid_argument
+  kConfig = 2,     // moesim::ConfigError
   kCapacity = 3,   // moesim::CapacityError
   kInvariant = 4,  // moesim::InvariantError
   kRuntime = 5,    // CUDA / NCCL failure
+  kArgument = 6,   // std::invalid_argument (malformed call, e.g. not a permutation)
 };
 
 struct Error : std::runtime_error {
@@ -24,7 +25,7 @@ struct Error : std::runtime_error {
 
 [[noreturn]] inline void fail(Status c, const std::string& m) { throw Error(c, m); }
 inline void require(bool ok, const std::string& m) {
-  if (!ok) fail(kConfig, m);
+  if (!ok) fail(kArgument, m);
 }
 
 void set_last_error(const std::string& m);
@@ -39,7 +40,7 @@ int guarded(F&& f) noexcept {
     return e.code;
   } catch (const std::invalid_argument& e) {
     set_last_error(e.what());
-    return kConfig;
+    return kArgument;
   } catch (const std::bad_alloc&) {
     set_last_error("out of host memory");
     return kRuntime;
