@@ -9,13 +9,17 @@
 // (d_model x d_ff and d_ff x d_model); the FLOP count is expert_flops
 // (model_config.hpp:77-80).
 //
-// Tiling: a tile is (group, 128-column block of N, up to
-// MSUB=2 x 128 token rows).  With ~128 tokens per expert the layer is
-// weight-streaming bound (128 FLOP/B < 251 FLOP/B ridge), so every weight
-// tile is read once from HBM and reused by both 128-row sub-tiles; token
-// tiles are re-read from L2.  Roles: warp 0 TMA producer, warp 1 MMA issuer
-// (one elected thread, accumulators in TMEM, 2 accumulator stages), warps 2-5
-// epilogue (tcgen05.ld -> GeLU -> bf16 -> global).
+// Tiling: a tile is (group, 128 weight rows = output features,
+// up to TOK token rows).  The weight tile is the MMA's M operand (M = 128) and
+// the ragged token set is N (a multiple of 16, <= 256), so an expert with
+// ~128-150 tokens is ONE tile column: every weight byte is read from HBM once
+// and the token rows (x_perm or H) are re-read from L2 in 32-row boxes.  With
+// ~128 tokens per expert the layer is weight-streaming bound (128 FLOP/B <
+// 251 FLOP/B ridge), so the ring is sized for bytes of weight in flight.
+// Roles: warp 0 TMA producer, warp 1 MMA issuer (one elected thread,
+// accumulators in TMEM, 2 accumulator stages), warps 2-5 epilogue
+// (tcgen05.ld -> GeLU -> bf16 -> global; TMEM lane = feature, column = token,
+// so each warp store writes 32 consecutive features of one token row).
 #include <cuda.h>
 
 #include <algorithm>
@@ -28,19 +32,23 @@
 namespace infmoe {
 namespace gemm {
 
-constexpr int BM = 128;          // UMMA M (token rows per sub-tile)
-constexpr int BN = 128;          // UMMA N (output columns per tile)
-constexpr int ROW_BYTES = 128;   // one SW128 row = BK elements
-constexpr int MSUB = 2;          // token sub-tiles sharing one weight tile
-constexpr int STAGES = 4;
-constexpr int ACC = 2;           // TMEM accumulator stages
-constexpr int TMEM_COLS = ACC * MSUB * BN;  // 512
-constexpr uint32_t A_TILE = BM * ROW_BYTES;  // 16 KiB
-constexpr uint32_t B_TILE = BN * ROW_BYTES;  // 16 KiB
-constexpr uint32_t STAGE_BYTES = MSUB * A_TILE + B_TILE;
+constexpr int BM = 128;          // weight rows (output features) per tile = UMMA M
+constexpr int ROW_BYTES = 128;   // one SW128 row = one K-block (64 bf16 / 32 f32)
+constexpr int TOK_BOX = 32;      // token rows per TMA box
+constexpr uint32_t W_TILE = BM * ROW_BYTES;  // 16 KiB
 constexpr int NUM_THREADS = 192;
-constexpr uint32_t SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
-static_assert(TMEM_COLS <= 512, "TMEM budget");
+
+template <int TOK, int STAGES>
+struct Cfg {
+  static constexpr uint32_t X_TILE = TOK * ROW_BYTES;
+  static constexpr uint32_t STAGE_BYTES = W_TILE + X_TILE;
+  static constexpr int ACC = 2;
+  static constexpr int ACC_COLS = TOK <= 128 ? 128 : 256;  // TMEM columns per accumulator
+  static constexpr int TMEM_COLS = ACC * ACC_COLS;
+  static constexpr uint32_t SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+  static_assert(TMEM_COLS <= 512, "TMEM budget");
+  static_assert(TOK % TOK_BOX == 0 && TOK <= 256, "token tile");
+};
 
 struct Params {
   int32_t N, K;
@@ -149,71 +157,72 @@ __device__ __forceinline__ float gelu_erf(float v) {
   return 0.5f * v * (1.0f + erff(v * 0.70710678118654752f));
 }
 
-// UMMA instruction descriptor: D f32, A/B bf16 (or tf32), both K-major.
+// UMMA instruction descriptor: D f32, A/B bf16 (or tf32), both K-major,
+// M = 128, runtime N (multiple of 16 in [16, 256]).
 template <bool kTF32>
-__host__ __device__ constexpr uint32_t make_idesc() {
-  return (1u << 4) | ((kTF32 ? 2u : 1u) << 7) | ((kTF32 ? 2u : 1u) << 10) |
-         (uint32_t(BN >> 3) << 17) | (uint32_t(BM >> 4) << 24);
+__device__ __forceinline__ uint32_t make_idesc(uint32_t n) {
+  return (1u << 4) | ((kTF32 ? 2u : 1u) << 7) | ((kTF32 ? 2u : 1u) << 10) | ((n >> 3) << 17) |
+         (uint32_t(BM >> 4) << 24);
 }
 
 // -------------------------------------------------------------- tile table
 struct TileTable {
   int32_t n_groups;
-  int32_t n_tiles_per_row;  // N / BN
+  int32_t fblocks;  // N / BM (feature blocks of the output)
   int32_t tile_start[kMaxGroups + 1];
-  int32_t mgroups[kMaxGroups];
+  int32_t chunks[kMaxGroups];
   int32_t row0[kMaxGroups];
   int32_t rows[kMaxGroups];
   int32_t slot[kMaxGroups];
 };
 
 struct Tile {
-  int32_t row0;       // first A row of this tile
-  int32_t rows;       // valid rows (<= MSUB*BM)
-  int32_t nsub;       // active 128-row sub-tiles
-  int32_t b_row0;     // first B row
-  int32_t n0;         // first output column
+  int32_t row0;    // first token row
+  int32_t ntok;    // valid token rows (<= TOK)
+  int32_t w_row0;  // first weight row
+  int32_t f0;      // first output column (feature)
 };
 
+template <int TOK>
 __device__ __forceinline__ Tile decode(const TileTable& tt, int32_t t, int32_t& g_cursor,
                                        int32_t N) {
   while (t >= tt.tile_start[g_cursor + 1]) ++g_cursor;
   const int32_t g = g_cursor;
   const int32_t local = t - tt.tile_start[g];
-  const int32_t mg = local % tt.mgroups[g];   // sub-tile groups fastest: neighbours
-  const int32_t nt = local / tt.mgroups[g];   // share the same weight tile in L2
+  const int32_t tc = local % tt.chunks[g];  // token chunks fastest: neighbours
+  const int32_t fb = local / tt.chunks[g];  // share the same weight tile in L2
   Tile r;
-  r.row0 = tt.row0[g] + mg * (MSUB * BM);
-  r.rows = min(MSUB * BM, tt.rows[g] - mg * (MSUB * BM));
-  r.nsub = (r.rows + BM - 1) / BM;
-  r.b_row0 = tt.slot[g] * N + nt * BN;
-  r.n0 = nt * BN;
+  r.row0 = tt.row0[g] + tc * TOK;
+  r.ntok = min(TOK, tt.rows[g] - tc * TOK);
+  r.w_row0 = tt.slot[g] * N + fb * BM;
+  r.f0 = fb * BM;
   return r;
 }
 
 // ------------------------------------------------------------------ kernel
-template <bool kTF32, bool kGelu>
+template <bool kTF32, bool kGelu, int TOK, int STAGES>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
-    grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
-                        const __grid_constant__ CUtensorMap tmap_b, const Params p) {
+    grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x,
+                        const __grid_constant__ CUtensorMap tmap_w, const Params p) {
+  using C = Cfg<TOK, STAGES>;
   extern __shared__ uint8_t smem_raw[];
   __shared__ TileTable tt;
   __shared__ uint32_t tmem_base_slot;
 
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;  // SW128 atoms need 1 KiB alignment
-  const uint32_t bar_base = base + STAGES * STAGE_BYTES;
+  const uint32_t bar_base = base + STAGES * C::STAGE_BYTES;
   auto full_bar = [&](int s) { return bar_base + 8u * s; };
   auto empty_bar = [&](int s) { return bar_base + 8u * (STAGES + s); };
   auto accf_bar = [&](int a) { return bar_base + 8u * (2 * STAGES + a); };
-  auto acce_bar = [&](int a) { return bar_base + 8u * (2 * STAGES + ACC + a); };
+  auto acce_bar = [&](int a) { return bar_base + 8u * (2 * STAGES + C::ACC + a); };
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
 
   if (threadIdx.x == 0) {
     tt.n_groups = p.n_groups;
-    tt.n_tiles_per_row = p.N / BN;
+    tt.fblocks = p.N / BM;
     int32_t acc = 0;
     for (int g = 0; g < p.n_groups; ++g) {
       const int e = p.experts[g];
@@ -222,16 +231,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       tt.row0[g] = r0;
       tt.rows[g] = rn;
       tt.slot[g] = p.slots[g];
-      tt.mgroups[g] = (rn + MSUB * BM - 1) / (MSUB * BM);
+      tt.chunks[g] = (rn + TOK - 1) / TOK;
       tt.tile_start[g] = acc;
-      acc += tt.mgroups[g] * tt.n_tiles_per_row;
+      acc += tt.chunks[g] * tt.fblocks;
     }
     tt.tile_start[p.n_groups] = acc;
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(full_bar(s), 1);
       mbar_init(empty_bar(s), 1);
     }
-    for (int a = 0; a < ACC; ++a) {
+    for (int a = 0; a < C::ACC; ++a) {
       mbar_init(accf_bar(a), 1);
       mbar_init(acce_bar(a), 4);
     }
@@ -241,7 +250,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(&tmem_base_slot)),
-                 "n"(TMEM_COLS)
+                 "n"(C::TMEM_COLS)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -250,60 +259,58 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem_base = tmem_base_slot;
   const int32_t n_tiles = tt.tile_start[tt.n_groups];
-  const int32_t kblocks = p.K / (ROW_BYTES / (kTF32 ? 4 : 2));
   const int32_t bk_elems = ROW_BYTES / (kTF32 ? 4 : 2);
+  const int32_t kblocks = p.K / bk_elems;
 
   if (warp == 0) {
     // ================= TMA producer =================
     if (lane == 0) {
       const uint64_t pol_w = policy_evict_first();  // weights: streamed once
-      const uint64_t pol_a = policy_evict_last();   // token rows: re-read per n-tile
+      const uint64_t pol_x = policy_evict_last();   // token rows: re-read per feature block
       int stage = 0;
       uint32_t phase = 0;
       int32_t gc = 0;
       for (int32_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-        const Tile tile = decode(tt, t, gc, p.N);
-        const uint32_t bytes = tile.nsub * A_TILE + B_TILE;
+        const Tile tile = decode<TOK>(tt, t, gc, p.N);
+        const int boxes = (tile.ntok + TOK_BOX - 1) / TOK_BOX;
+        const uint32_t bytes = W_TILE + boxes * (TOK_BOX * ROW_BYTES);
         for (int32_t kb = 0; kb < kblocks; ++kb) {
           mbar_wait(empty_bar(stage), phase ^ 1);
-          const uint32_t sA = base + stage * STAGE_BYTES;
-          const uint32_t sB = sA + MSUB * A_TILE;
+          const uint32_t sW = base + stage * C::STAGE_BYTES;
+          const uint32_t sX = sW + W_TILE;
           mbar_expect_tx(full_bar(stage), bytes);
-          for (int s = 0; s < tile.nsub; ++s)
-            tma_load_2d(sA + s * A_TILE, &tmap_a, full_bar(stage), kb * bk_elems,
-                        tile.row0 + s * BM, pol_a);
-          tma_load_2d(sB, &tmap_b, full_bar(stage), kb * bk_elems, tile.b_row0, pol_w);
+          tma_load_2d(sW, &tmap_w, full_bar(stage), kb * bk_elems, tile.w_row0, pol_w);
+          for (int b = 0; b < boxes; ++b)
+            tma_load_2d(sX + b * (TOK_BOX * ROW_BYTES), &tmap_x, full_bar(stage), kb * bk_elems,
+                        tile.row0 + b * TOK_BOX, pol_x);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
     // ================= MMA issuer =================
-    constexpr uint32_t idesc = make_idesc<kTF32>();
     int stage = 0;
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
     int32_t gc = 0;
     for (int32_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-      const Tile tile = decode(tt, t, gc, p.N);
+      const Tile tile = decode<TOK>(tt, t, gc, p.N);
+      const uint32_t n_mma = uint32_t((tile.ntok + 15) & ~15);  // UMMA N: multiple of 16
+      const uint32_t idesc = make_idesc<kTF32>(n_mma);
       mbar_wait(acce_bar(acc), acc_phase ^ 1);
       tc_fence_after();
-      const uint32_t d_base = tmem_base + acc * (MSUB * BN);
+      const uint32_t d_tmem = tmem_base + acc * C::ACC_COLS;
       for (int32_t kb = 0; kb < kblocks; ++kb) {
         mbar_wait(full_bar(stage), phase);
         tc_fence_after();
         if (lane == 0) {
-          const uint32_t sA = base + stage * STAGE_BYTES;
-          const uint32_t sB = sA + MSUB * A_TILE;
-          const uint64_t db = sdesc(sB);
-          for (int s = 0; s < tile.nsub; ++s) {
-            const uint64_t da = sdesc(sA + s * A_TILE);
+          const uint32_t sW = base + stage * C::STAGE_BYTES;
+          const uint64_t dw = sdesc(sW);
+          const uint64_t dx = sdesc(sW + W_TILE);
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk)  // 4 x 32 B of K per 128 B row
-              mma<kTF32>(d_base + s * BN, da + 2 * kk, db + 2 * kk, idesc,
-                         (kb | kk) != 0 ? 1u : 0u);
-          }
+          for (int kk = 0; kk < 4; ++kk)  // 4 x 32 B of K per 128 B row
+            mma<kTF32>(d_tmem, dw + 2 * kk, dx + 2 * kk, idesc, (kb | kk) != 0 ? 1u : 0u);
           tc_commit(empty_bar(stage));  // smem slot free once these MMAs retire
         }
         __syncwarp();
@@ -311,7 +318,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
       if (lane == 0) tc_commit(accf_bar(acc));  // accumulator ready for the epilogue
       __syncwarp();
-      if (++acc == ACC) { acc = 0; acc_phase ^= 1; }
+      if (++acc == C::ACC) { acc = 0; acc_phase ^= 1; }
     }
   } else {
     // ================= epilogue (warps 2..5) =================
@@ -320,59 +327,39 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     uint32_t acc_phase = 0;
     int32_t gc = 0;
     for (int32_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-      const Tile tile = decode(tt, t, gc, p.N);
+      const Tile tile = decode<TOK>(tt, t, gc, p.N);
       mbar_wait(accf_bar(acc), acc_phase);
       tc_fence_after();
-      for (int s = 0; s < tile.nsub; ++s) {
-        const int r_local = s * BM + quarter * 32 + lane;
-        const bool valid = r_local < tile.rows;
-        const int64_t row = int64_t(tile.row0) + r_local;
-        const uint32_t taddr =
-            tmem_base + (uint32_t(quarter * 32) << 16) + acc * (MSUB * BN) + s * BN;
-#pragma unroll 1
-        for (int cc = 0; cc < BN / 32; ++cc) {
-          uint32_t r[32];
-          tmem_ld32(taddr + cc * 32, r);
-          if (valid) {
-            if constexpr (kTF32) {
-              float* dst = reinterpret_cast<float*>(p.out) + row * p.ld_out + tile.n0 + cc * 32;
+      const int feat = tile.f0 + quarter * 32 + lane;
+      const uint32_t taddr = tmem_base + (uint32_t(quarter * 32) << 16) + acc * C::ACC_COLS;
+      const int chunks = (tile.ntok + 31) / 32;
+      for (int cc = 0; cc < chunks; ++cc) {
+        uint32_t r[32];
+        tmem_ld32(taddr + cc * 32, r);
+        const int nvalid = min(32, tile.ntok - cc * 32);
+        const int64_t row = int64_t(tile.row0) + cc * 32;
+        if constexpr (kTF32) {
+          float* dst = reinterpret_cast<float*>(p.out) + row * p.ld_out + feat;
 #pragma unroll
-              for (int q = 0; q < 8; ++q) {
-                float4 v;
-                v.x = __uint_as_float(r[4 * q + 0]);
-                v.y = __uint_as_float(r[4 * q + 1]);
-                v.z = __uint_as_float(r[4 * q + 2]);
-                v.w = __uint_as_float(r[4 * q + 3]);
-                if constexpr (kGelu) {
-                  v.x = gelu_erf(v.x); v.y = gelu_erf(v.y);
-                  v.z = gelu_erf(v.z); v.w = gelu_erf(v.w);
-                }
-                reinterpret_cast<float4*>(dst)[q] = v;
-              }
-            } else {
-              __nv_bfloat16* dst =
-                  reinterpret_cast<__nv_bfloat16*>(p.out) + row * p.ld_out + tile.n0 + cc * 32;
+          for (int i = 0; i < 32; ++i) {
+            float v = __uint_as_float(r[i]);
+            if constexpr (kGelu) v = gelu_erf(v);
+            if (i < nvalid) dst[int64_t(i) * p.ld_out] = v;
+          }
+        } else {
+          __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(p.out) + row * p.ld_out + feat;
 #pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                uint32_t w[4];
-#pragma unroll
-                for (int h = 0; h < 4; ++h) {
-                  float lo = __uint_as_float(r[8 * q + 2 * h]);
-                  float hi = __uint_as_float(r[8 * q + 2 * h + 1]);
-                  if constexpr (kGelu) { lo = gelu_erf(lo); hi = gelu_erf(hi); }
-                  __nv_bfloat162 b2 = __floats2bfloat162_rn(lo, hi);
-                  w[h] = *reinterpret_cast<uint32_t*>(&b2);
-                }
-                reinterpret_cast<uint4*>(dst)[q] = make_uint4(w[0], w[1], w[2], w[3]);
-              }
-            }
+          for (int i = 0; i < 32; ++i) {
+            float v = __uint_as_float(r[i]);
+            if constexpr (kGelu) v = gelu_erf(v);
+            if (i < nvalid) dst[int64_t(i) * p.ld_out] = __float2bfloat16_rn(v);
           }
         }
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(acce_bar(acc));
-      if (++acc == ACC) { acc = 0; acc_phase ^= 1; }
+      if (++acc == C::ACC) { acc = 0; acc_phase ^= 1; }
     }
   }
 
@@ -381,7 +368,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                 "n"(TMEM_COLS)
+                 "n"(C::TMEM_COLS)
                  : "memory");
   }
 }
@@ -425,19 +412,20 @@ CUtensorMap make_tmap(const void* base, uint64_t rows, uint64_t cols, bool f32,
   return m;
 }
 
-template <bool kTF32, bool kGelu>
+template <bool kTF32, bool kGelu, int TOK, int STAGES>
 void launch_impl(const GroupedGemmArgs& a, cudaStream_t stream) {
-  auto kern = grouped_gemm_kernel<kTF32, kGelu>;
+  using C = Cfg<TOK, STAGES>;
+  auto kern = grouped_gemm_kernel<kTF32, kGelu, TOK, STAGES>;
   static bool configured = false;
   if (!configured) {
     INFMOE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     int(SMEM_BYTES)));
+                                     int(C::SMEM_BYTES)));
     configured = true;
   }
-  const CUtensorMap ta = make_tmap(a.a, uint64_t(std::max<int64_t>(a.a_rows, 1)), uint64_t(a.K),
+  const CUtensorMap tx = make_tmap(a.a, uint64_t(std::max<int64_t>(a.a_rows, 1)), uint64_t(a.K),
+                                   kTF32, TOK_BOX);
+  const CUtensorMap tw = make_tmap(a.b, uint64_t(a.n_slots) * uint64_t(a.N), uint64_t(a.K),
                                    kTF32, BM);
-  const CUtensorMap tb = make_tmap(a.b, uint64_t(a.n_slots) * uint64_t(a.N), uint64_t(a.K),
-                                   kTF32, BN);
   Params p;
   std::memset(&p, 0, sizeof(p));
   p.N = a.N;
@@ -453,25 +441,42 @@ void launch_impl(const GroupedGemmArgs& a, cudaStream_t stream) {
   }
   int grid = device_sm_count();
   if (a.max_ctas > 0) grid = std::min(grid, a.max_ctas);
-  kern<<<grid, NUM_THREADS, SMEM_BYTES, stream>>>(ta, tb, p);
+  kern<<<grid, NUM_THREADS, C::SMEM_BYTES, stream>>>(tx, tw, p);
   INFMOE_LAUNCH_CHECK();
+}
+
+// Token-tile width: as wide as the largest expert when the host knows it (one
+// weight read per expert), else 192 (the ~128 +- 20 tokens/expert of a
+// balanced top-1 layer fit in one column).  Narrower tiles buy ring depth.
+template <bool kTF32, bool kGelu>
+void dispatch_tok(const GroupedGemmArgs& a, cudaStream_t s) {
+  const int hint = a.max_rows_hint;
+  if constexpr (kTF32) {
+    launch_impl<kTF32, kGelu, 128, 4>(a, s);  // f32 tiles are twice as wide in bytes per K
+  } else if (hint > 0 && hint <= 128) {
+    launch_impl<kTF32, kGelu, 128, 6>(a, s);
+  } else if (hint > 192) {
+    launch_impl<kTF32, kGelu, 256, 4>(a, s);
+  } else {
+    launch_impl<kTF32, kGelu, 192, 5>(a, s);
+  }
 }
 
 }  // namespace gemm
 
 void launch_grouped_gemm(const GroupedGemmArgs& a, cudaStream_t stream) {
   require(a.n_groups >= 1 && a.n_groups <= kMaxGroups, "grouped gemm: n_groups out of range");
-  require(a.N % gemm::BN == 0, "grouped gemm: N must be a multiple of 128");
+  require(a.N % gemm::BM == 0, "grouped gemm: N must be a multiple of 128");
   const int bk = a.dtype == kDtypeF32 ? 32 : 64;
   require(a.K % bk == 0 && a.K > 0, "grouped gemm: K must be a multiple of 64 (bf16) / 32 (f32)");
   require(a.a && a.b && a.out && a.offsets, "grouped gemm: NULL pointer");
   const bool tf32 = a.dtype == kDtypeF32;
   if (tf32) {
-    if (a.gelu) gemm::launch_impl<true, true>(a, stream);
-    else gemm::launch_impl<true, false>(a, stream);
+    if (a.gelu) gemm::dispatch_tok<true, true>(a, stream);
+    else gemm::dispatch_tok<true, false>(a, stream);
   } else {
-    if (a.gelu) gemm::launch_impl<false, true>(a, stream);
-    else gemm::launch_impl<false, false>(a, stream);
+    if (a.gelu) gemm::dispatch_tok<false, true>(a, stream);
+    else gemm::dispatch_tok<false, false>(a, stream);
   }
 }
 

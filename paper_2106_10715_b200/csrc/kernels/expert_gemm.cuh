@@ -27,6 +27,7 @@ struct GroupedGemmArgs {
   void* out;  // bf16 or f32 (same as dtype)
   int32_t gelu;
   int32_t max_ctas;  // 0 = one CTA per SM
+  int32_t max_rows_hint;  // largest group row count if known on the host, else 0
 };
 
 void launch_grouped_gemm(const GroupedGemmArgs& args, cudaStream_t stream);

@@ -9,6 +9,7 @@
 //                 gating.hpp:70-80; the reference build does not contract)
 // x and the gate weights are staged through shared memory in d-chunks so the
 // weight matrix is read once per CTA of tokens, not once per token.
+#include <algorithm>
 #include <cmath>
 
 #include "common.cuh"
@@ -16,8 +17,6 @@
 
 namespace infmoe {
 namespace {
-
-constexpr int kChunk = 32;  // d-chunk staged per iteration
 
 struct Cand {
   float v;
@@ -34,83 +33,179 @@ __device__ __forceinline__ bool better(const Cand& a, const Cand& b) {
   return a.i < b.i;
 }
 
+// Multi-stage cp.async ring shared by both gates: column chunks of the token
+// rows (raw dtype) and of the gate matrix are staged kGateStages-1 chunks ahead
+// of the math, so global latency (~1 us) is covered by ~2 us of in-flight work.
+constexpr int kGateStages = 4;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+  const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  const int n = valid ? 16 : 0;  // zero-fill when out of range
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(n)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// ---------------------------------------------------------------- N1a ----
+// Register-tiled logits: a warp's 32 lanes are 8 expert-groups x 4
+// token-groups; lane (eg, tg) owns experts {eg + 8q : q < EQ} for tokens
+// {tg*TPW + t : t < TPW}, i.e. EQ*TPW independent fmaf chains, each walking d
+// in ascending order (so every logit is bit-identical to oracle.c
+// or_gate_softmax).  Per 4 columns a lane issues TPW + EQ shared loads (x rows
+// broadcast within a token-group, gate-weight rows broadcast within an
+// expert-group) for 4*EQ*TPW FMAs.  Selection (top-k, softmax) then runs one
+// warp per token from the logits tile in shared memory.
+constexpr int kSoftWarps = 4;
+
 template <typename T, int EQ, int TPW>
-__global__ void __launch_bounds__(256) gate_softmax_kernel(
+struct SoftCfg {
+  static constexpr int CH = EQ >= 16 ? 32 : 64;        // columns per stage
+  static constexpr int EP = 8 * EQ;                    // experts covered (padded)
+  static constexpr int TW = 4 * TPW;                   // tokens per warp
+  static constexpr int TB = kSoftWarps * TW;           // tokens per block
+  static constexpr int V = 16 / sizeof(T);             // x elements per 16 B
+  static constexpr int XROW = CH + V;                  // +16 B per row
+  static constexpr int WROW = CH + 4;
+  static constexpr size_t X_BYTES = size_t(TB) * XROW * sizeof(T);
+  static constexpr size_t W_BYTES = size_t(EP) * WROW * sizeof(float);
+  static constexpr size_t STAGE = X_BYTES + W_BYTES;
+  static constexpr size_t LG_BYTES = size_t(TB) * (EP + 1) * sizeof(float);
+  static constexpr size_t SMEM = kGateStages * STAGE + LG_BYTES;
+};
+
+template <typename T, int EQ, int TPW>
+__global__ void __launch_bounds__(kSoftWarps * 32) gate_softmax_kernel(
     const T* __restrict__ x, int64_t N, int d, const float* __restrict__ wg,
     const float* __restrict__ bias, int E, int k, int32_t* __restrict__ topk_idx,
     float* __restrict__ topk_w, int32_t* __restrict__ counts) {
-  constexpr int EP = 32 * EQ;
-  constexpr int TB = 8 * TPW;
-  __shared__ float xs[TB][kChunk];
-  __shared__ float ws[kChunk][EP + 1];
-  __shared__ int hist[EP];
+  using C = SoftCfg<T, EQ, TPW>;
+  constexpr int NT = kSoftWarps * 32;
+  extern __shared__ __align__(16) uint8_t soft_smem[];
+  __shared__ int hist[C::EP];
+  float* lg_s = reinterpret_cast<float*>(soft_smem + kGateStages * C::STAGE);  // [TB][EP+1]
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int64_t tok0 = int64_t(blockIdx.x) * TB;
-  for (int i = threadIdx.x; i < EP; i += blockDim.x) hist[i] = 0;
+  const int eg = lane % 8, tg = lane / 8;
+  const int64_t tok0 = int64_t(blockIdx.x) * C::TB;
+  for (int i = threadIdx.x; i < C::EP; i += NT) hist[i] = 0;
 
-  float acc[TPW][EQ];
-#pragma unroll
-  for (int t = 0; t < TPW; ++t)
-#pragma unroll
-    for (int q = 0; q < EQ; ++q) acc[t][q] = 0.0f;
-
-  for (int c0 = 0; c0 < d; c0 += kChunk) {
-    const int cn = min(kChunk, d - c0);
-    __syncthreads();
-    for (int i = threadIdx.x; i < TB * kChunk; i += blockDim.x) {
-      const int t = i / kChunk, c = i % kChunk;
-      const int64_t tok = tok0 + t;
-      xs[t][c] = (tok < N && c < cn) ? load_as_f32(x, size_t(tok) * d + c0 + c) : 0.0f;
-    }
-    for (int i = threadIdx.x; i < EP * kChunk; i += blockDim.x) {
-      const int e = i / kChunk, c = i % kChunk;
-      ws[c][e] = (e < E && c < cn) ? wg[size_t(e) * d + c0 + c] : 0.0f;
-    }
-    __syncthreads();
-    for (int c = 0; c < cn; ++c) {
-      float wv[EQ];
-#pragma unroll
-      for (int q = 0; q < EQ; ++q) wv[q] = ws[c][lane + 32 * q];
-#pragma unroll
-      for (int t = 0; t < TPW; ++t) {
-        const float xv = xs[warp * TPW + t][c];
-#pragma unroll
-        for (int q = 0; q < EQ; ++q) acc[t][q] = fmaf(xv, wv[q], acc[t][q]);
+  auto xs = [&](int st) { return reinterpret_cast<T*>(soft_smem + st * C::STAGE); };
+  auto ws = [&](int st) { return reinterpret_cast<float*>(soft_smem + st * C::STAGE + C::X_BYTES); };
+  const int nch = (d + C::CH - 1) / C::CH;
+  auto issue = [&](int ch) {
+    if (ch < nch) {
+      const int c0 = ch * C::CH;
+      T* xd = xs(ch % kGateStages);
+      float* wd = ws(ch % kGateStages);
+      for (int i = threadIdx.x; i < C::TB * (C::CH / C::V); i += NT) {
+        const int t = i / (C::CH / C::V), c = (i % (C::CH / C::V)) * C::V;
+        const bool ok = tok0 + t < N && c0 + c < d;
+        cp_async16(xd + t * C::XROW + c, ok ? x + size_t(tok0 + t) * d + c0 + c : x, ok);
+      }
+      for (int i = threadIdx.x; i < C::EP * (C::CH / 4); i += NT) {
+        const int e = i / (C::CH / 4), c = (i % (C::CH / 4)) * 4;
+        const bool ok = e < E && c0 + c < d;
+        cp_async16(wd + e * C::WROW + c, ok ? wg + size_t(e) * d + c0 + c : wg, ok);
       }
     }
-  }
+    cp_async_commit();  // empty groups keep the wait count uniform
+  };
 
+  float acc[EQ][TPW];
 #pragma unroll
-  for (int t = 0; t < TPW; ++t) {
-    const int64_t tok = tok0 + warp * TPW + t;
-    float lg[EQ];
-    bool live[EQ];
+  for (int q = 0; q < EQ; ++q)
 #pragma unroll
-    for (int q = 0; q < EQ; ++q) {
+    for (int t = 0; t < TPW; ++t) acc[q][t] = 0.0f;
+  const int xrow0 = warp * C::TW + tg * TPW;
+
+  for (int ch = 0; ch < kGateStages - 1; ++ch) issue(ch);
+  for (int ch = 0; ch < nch; ++ch) {
+    cp_async_wait<kGateStages - 2>();  // chunk ch has landed (for this thread)
+    __syncthreads();                   // ... for every thread; slot ch-1 is free
+    issue(ch + kGateStages - 1);
+    const int cn = min(C::CH, d - ch * C::CH);
+    const T* xb = xs(ch % kGateStages);
+    const float* wb = ws(ch % kGateStages);
+    for (int c = 0; c < cn; c += 4) {  // d is a multiple of 4 (launcher check)
+      float xv[TPW][4];
+      float4 wv[EQ];
+#pragma unroll
+      for (int t = 0; t < TPW; ++t) {
+        const T* xp = xb + (xrow0 + t) * C::XROW + c;
+        if constexpr (sizeof(T) == 2) {  // 4 bf16 = one 8-byte load
+          const uint2 raw = *reinterpret_cast<const uint2*>(xp);
+          xv[t][0] = __uint_as_float(raw.x << 16);
+          xv[t][1] = __uint_as_float(raw.x & 0xffff0000u);
+          xv[t][2] = __uint_as_float(raw.y << 16);
+          xv[t][3] = __uint_as_float(raw.y & 0xffff0000u);
+        } else {
+          const float4 raw = *reinterpret_cast<const float4*>(xp);
+          xv[t][0] = raw.x; xv[t][1] = raw.y; xv[t][2] = raw.z; xv[t][3] = raw.w;
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < EQ; ++q)
+        wv[q] = *reinterpret_cast<const float4*>(wb + (eg + 8 * q) * C::WROW + c);
+#pragma unroll
+      for (int q = 0; q < EQ; ++q)
+#pragma unroll
+        for (int t = 0; t < TPW; ++t) {
+          acc[q][t] = fmaf(xv[t][0], wv[q].x, acc[q][t]);
+          acc[q][t] = fmaf(xv[t][1], wv[q].y, acc[q][t]);
+          acc[q][t] = fmaf(xv[t][2], wv[q].z, acc[q][t]);
+          acc[q][t] = fmaf(xv[t][3], wv[q].w, acc[q][t]);
+        }
+    }
+  }
+  cp_async_wait<0>();
+  // logits (+ bias, one fp32 add) into shared memory
+#pragma unroll
+  for (int q = 0; q < EQ; ++q) {
+    const int e = eg + 8 * q;
+#pragma unroll
+    for (int t = 0; t < TPW; ++t)
+      lg_s[(xrow0 + t) * (C::EP + 1) + e] =
+          (e < E && bias) ? __fadd_rn(acc[q][t], bias[e]) : acc[q][t];
+  }
+  __syncthreads();
+
+  constexpr int SQ = (C::EP + 31) / 32;  // logits per lane during selection
+  for (int tl = 0; tl < C::TW; ++tl) {
+    const int row = warp * C::TW + tl;
+    const int64_t tok = tok0 + row;
+    float lg[SQ];
+    bool live[SQ];
+#pragma unroll
+    for (int q = 0; q < SQ; ++q) {
       const int e = lane + 32 * q;
       live[q] = e < E;
-      lg[q] = live[q] ? (bias ? __fadd_rn(acc[t][q], bias[e]) : acc[t][q]) : 0.0f;
+      lg[q] = live[q] ? lg_s[row * (C::EP + 1) + e] : 0.0f;
     }
     // softmax denominator over all experts (fp32; weights are tolerance-checked)
     float mx = -INFINITY;
 #pragma unroll
-    for (int q = 0; q < EQ; ++q)
+    for (int q = 0; q < SQ; ++q)
       if (live[q] && !isnan(lg[q])) mx = fmaxf(mx, lg[q]);
     for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     float se = 0.0f;
 #pragma unroll
-    for (int q = 0; q < EQ; ++q)
+    for (int q = 0; q < SQ; ++q)
       if (live[q]) se += expf(lg[q] - mx);
     for (int o = 16; o; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
 
-    float pk[8];
-    int ik[8];
     float psum = 0.0f;
+    float pk_mine = 0.0f;
+    int ik_mine = 0;
     for (int j = 0; j < k; ++j) {
       Cand best{0.0f, -1};
 #pragma unroll
-      for (int q = 0; q < EQ; ++q) {
+      for (int q = 0; q < SQ; ++q) {
         Cand c{lg[q], live[q] ? lane + 32 * q : -1};
         if (better(c, best)) best = c;
       }
@@ -119,88 +214,147 @@ __global__ void __launch_bounds__(256) gate_softmax_kernel(
                    __shfl_xor_sync(0xffffffffu, best.i, o)};
         if (better(other, best)) best = other;
       }
-      ik[j] = best.i;
-      pk[j] = expf(best.v - mx) / se;
-      psum += pk[j];
+      const float pj = expf(best.v - mx) / se;
+      psum += pj;
+      if (lane == j) { pk_mine = pj; ik_mine = best.i; }  // lane j keeps pick j
 #pragma unroll
-      for (int q = 0; q < EQ; ++q)
+      for (int q = 0; q < SQ; ++q)
         if (lane + 32 * q == best.i) live[q] = false;  // exclude from the next pick
     }
-    if (lane == 0 && tok < N) {
-      for (int j = 0; j < k; ++j) {
-        topk_idx[tok * k + j] = ik[j];
-        topk_w[tok * k + j] = k > 1 ? pk[j] / psum : pk[j];
-        atomicAdd(&hist[ik[j]], 1);
-      }
+    if (lane < k && tok < N) {
+      topk_idx[tok * k + lane] = ik_mine;
+      topk_w[tok * k + lane] = k > 1 ? pk_mine / psum : pk_mine;
+      atomicAdd(&hist[ik_mine], 1);
     }
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < E; e += blockDim.x)
+  for (int e = threadIdx.x; e < E; e += NT)
     if (hist[e]) atomicAdd(&counts[e], hist[e]);
 }
 
-// LSH: lane = (token sub-slot, hash bit); tokens per warp = 32 / bits.
+// ---------------------------------------------------------------- N1b ----
+// LSH: lane = (token sub-slot, hash bit); tokens per warp G = 32 / bits.  Each
+// lane owns one sequential fp64 chain over d (gating.hpp:70-80: separate
+// multiply and add roundings), so the kernel is bound by the 8-cycle dadd
+// dependency chain.  x rows (raw dtype) and the hyperplane rows are staged
+// through the cp.async ring; each hyperplane row is read as 16-byte pairs
+// (rows padded onto distinct bank groups, broadcast across a token's lanes).
+constexpr int kLshWarps = 4;
+constexpr int kLshChunk = 128;
+
 template <typename T>
-__global__ void __launch_bounds__(128) gate_lsh_kernel(
+__global__ void __launch_bounds__(kLshWarps * 32) gate_lsh_kernel(
     const T* __restrict__ x, int64_t N, int d, const double* __restrict__ proj, int bits, int E,
     uint32_t* __restrict__ codes, int32_t* __restrict__ topk_idx, float* __restrict__ topk_w,
     int32_t* __restrict__ counts) {
-  constexpr int kWarps = 4;
-  constexpr int kLshChunk = 32;
-  __shared__ float xs[kWarps * 32][kLshChunk + 1];
-  __shared__ double ps[kLshChunk][32];
-  __shared__ int hist[1024];
-
-  const int G = 32 / bits;  // tokens per warp
-  const int TB = kWarps * G;
+  constexpr int NT = kLshWarps * 32;
+  constexpr int V = 16 / sizeof(T);
+  constexpr int XROW = kLshChunk + V;  // elements (+16 B)
+  constexpr int PROW = kLshChunk + 2;  // doubles (+16 B)
+  extern __shared__ __align__(16) uint8_t lsh_smem[];
+  const int G = 32 / bits;
+  const int TB = kLshWarps * G;
+  const size_t xbytes = size_t(TB) * XROW * sizeof(T);
+  const size_t stage = xbytes + size_t(bits) * PROW * sizeof(double);
+  auto xs = [&](int st) { return reinterpret_cast<T*>(lsh_smem + st * stage); };
+  auto ps = [&](int st) { return reinterpret_cast<double*>(lsh_smem + st * stage + xbytes); };
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int sub = lane / bits, j = lane % bits;
-  const bool active = sub < G;
+  const int local = warp * G + (sub < G ? sub : 0);
   const int64_t tok0 = int64_t(blockIdx.x) * TB;
-  const int local_tok = warp * G + (active ? sub : 0);
-  for (int i = threadIdx.x; i < E && i < 1024; i += blockDim.x) hist[i] = 0;
+  const int64_t tok = tok0 + local;
+  const bool active = sub < G && tok < N;
+  const int nch = (d + kLshChunk - 1) / kLshChunk;
+
+  auto issue = [&](int ch) {
+    if (ch < nch) {
+      const int c0 = ch * kLshChunk;
+      T* xd = xs(ch % kGateStages);
+      double* pd = ps(ch % kGateStages);
+      for (int i = threadIdx.x; i < TB * (kLshChunk / V); i += NT) {
+        const int t = i / (kLshChunk / V), c = (i % (kLshChunk / V)) * V;
+        const bool ok = tok0 + t < N && c0 + c < d;
+        cp_async16(xd + t * XROW + c, ok ? x + size_t(tok0 + t) * d + c0 + c : x, ok);
+      }
+      for (int i = threadIdx.x; i < bits * (kLshChunk / 2); i += NT) {
+        const int b = i / (kLshChunk / 2), c = (i % (kLshChunk / 2)) * 2;
+        const bool ok = c0 + c < d;
+        cp_async16(pd + b * PROW + c, ok ? proj + size_t(b) * d + c0 + c : proj, ok);
+      }
+    }
+    cp_async_commit();
+  };
 
   double dot = 0.0;
-  for (int c0 = 0; c0 < d; c0 += kLshChunk) {
-    const int cn = min(kLshChunk, d - c0);
+  for (int ch = 0; ch < kGateStages - 1; ++ch) issue(ch);
+  for (int ch = 0; ch < nch; ++ch) {
+    cp_async_wait<kGateStages - 2>();
     __syncthreads();
-    for (int i = threadIdx.x; i < TB * kLshChunk; i += blockDim.x) {
-      const int t = i / kLshChunk, c = i % kLshChunk;
-      const int64_t tok = tok0 + t;
-      xs[t][c] = (tok < N && c < cn) ? load_as_f32(x, size_t(tok) * d + c0 + c) : 0.0f;
-    }
-    for (int i = threadIdx.x; i < bits * kLshChunk; i += blockDim.x) {
-      const int b = i / kLshChunk, c = i % kLshChunk;
-      ps[c][b] = c < cn ? proj[size_t(b) * d + c0 + c] : 0.0;
-    }
-    __syncthreads();
+    issue(ch + kGateStages - 1);
+    const int cn = min(kLshChunk, d - ch * kLshChunk);  // a multiple of 8
     if (active) {
-      for (int c = 0; c < cn; ++c)
-        dot = __dadd_rn(dot, __dmul_rn(double(xs[local_tok][c]), ps[c][j]));
+      const T* xrow = xs(ch % kGateStages) + local * XROW;
+      const double2* prow = reinterpret_cast<const double2*>(ps(ch % kGateStages) + j * PROW);
+      for (int c = 0; c < cn; c += 8) {
+        const uint4 raw = *reinterpret_cast<const uint4*>(xrow + c);
+        double xv[8];
+        if constexpr (sizeof(T) == 2) {
+          const T* e = reinterpret_cast<const T*>(&raw);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) xv[i] = double(load_as_f32(e, i));
+        } else {
+          const uint4 raw2 = *reinterpret_cast<const uint4*>(xrow + c + 4);
+          const float* e = reinterpret_cast<const float*>(&raw);
+          const float* e2 = reinterpret_cast<const float*>(&raw2);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) { xv[i] = double(e[i]); xv[4 + i] = double(e2[i]); }
+        }
+        double prod[8];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const double2 pp = prow[c / 2 + i];
+          prod[2 * i] = __dmul_rn(xv[2 * i], pp.x);
+          prod[2 * i + 1] = __dmul_rn(xv[2 * i + 1], pp.y);
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) dot = __dadd_rn(dot, prod[i]);
+      }
     }
   }
+  cp_async_wait<0>();
   const unsigned mask = __ballot_sync(0xffffffffu, active && dot >= 0.0);
-  const int64_t tok = tok0 + local_tok;
-  if (active && j == 0 && tok < N) {
-    const uint32_t code = (mask >> (sub * bits)) & ((bits >= 32) ? 0xffffffffu : ((1u << bits) - 1u));
+  if (active && j == 0) {
+    const uint32_t code = (mask >> (sub * bits)) & ((1u << bits) - 1u);
     const int e = int(code % uint32_t(E));
     if (codes) codes[tok] = code;
     topk_idx[tok] = e;
     topk_w[tok] = 1.0f;
-    if (E <= 1024) atomicAdd(&hist[e], 1);
-    else atomicAdd(&counts[e], 1);
+    atomicAdd(&counts[e], 1);
   }
-  __syncthreads();
-  for (int e = threadIdx.x; e < E && e < 1024; e += blockDim.x)
-    if (hist[e]) atomicAdd(&counts[e], hist[e]);
 }
 
 template <typename T, int EQ, int TPW>
+void softmax_go(const void* x, int64_t N, int d, const float* wg, const float* bias, int E, int k,
+                int32_t* idx, float* w, int32_t* counts, cudaStream_t s) {
+  using C = SoftCfg<T, EQ, TPW>;
+  auto kern = gate_softmax_kernel<T, EQ, TPW>;
+  static bool configured = false;
+  if (!configured) {
+    INFMOE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM)));
+    configured = true;
+  }
+  kern<<<unsigned((N + C::TB - 1) / C::TB), kSoftWarps * 32, C::SMEM, s>>>(
+      reinterpret_cast<const T*>(x), N, d, wg, bias, E, k, idx, w, counts);
+}
+
+template <typename T, int EQ>
 void softmax_launch(const void* x, int64_t N, int d, const float* wg, const float* bias, int E,
                     int k, int32_t* idx, float* w, int32_t* counts, cudaStream_t s) {
-  const int64_t blocks = (N + 8 * TPW - 1) / (8 * TPW);
-  gate_softmax_kernel<T, EQ, TPW><<<unsigned(blocks), 256, 0, s>>>(
-      reinterpret_cast<const T*>(x), N, d, wg, bias, E, k, idx, w, counts);
+  // two tokens per lane when that still gives >= 2 CTAs per SM, else one
+  if ((N + SoftCfg<T, EQ, 2>::TB - 1) / SoftCfg<T, EQ, 2>::TB >= 2 * device_sm_count())
+    softmax_go<T, EQ, 2>(x, N, d, wg, bias, E, k, idx, w, counts, s);
+  else
+    softmax_go<T, EQ, 1>(x, N, d, wg, bias, E, k, idx, w, counts, s);
 }
 
 }  // namespace
@@ -211,19 +365,23 @@ void launch_gate_softmax(const void* x, int dtype, int64_t N, int d, const float
   require(E >= 1 && E <= 128, "softmax gate: n_experts must be in [1, 128]");
   require(k >= 1 && k <= 8 && k <= E, "softmax gate: top_k must be in [1, min(8, E)]");
   require(d >= 1, "softmax gate: d_model must be >= 1");
+  const size_t V = 16 / dtype_bytes(dtype);
+  require(d % int(V) == 0 && d % 4 == 0, "softmax gate: d_model must be a multiple of 8 (bf16) / 4 (f32)");
+  require(reinterpret_cast<uintptr_t>(x) % 16 == 0 && reinterpret_cast<uintptr_t>(wg) % 16 == 0,
+          "softmax gate: x and gate weights must be 16-byte aligned");
   INFMOE_CUDA(cudaMemsetAsync(counts, 0, sizeof(int32_t) * size_t(E), stream));
   if (N == 0) return;
   const bool bf = dtype == kDtypeBf16;
-  if (E <= 32) {
-    if (bf) softmax_launch<__nv_bfloat16, 1, 4>(x, N, d, wg, bias, E, k, topk_idx, topk_w, counts, stream);
-    else softmax_launch<float, 1, 4>(x, N, d, wg, bias, E, k, topk_idx, topk_w, counts, stream);
-  } else if (E <= 64) {
-    if (bf) softmax_launch<__nv_bfloat16, 2, 2>(x, N, d, wg, bias, E, k, topk_idx, topk_w, counts, stream);
-    else softmax_launch<float, 2, 2>(x, N, d, wg, bias, E, k, topk_idx, topk_w, counts, stream);
-  } else {
-    if (bf) softmax_launch<__nv_bfloat16, 4, 1>(x, N, d, wg, bias, E, k, topk_idx, topk_w, counts, stream);
-    else softmax_launch<float, 4, 1>(x, N, d, wg, bias, E, k, topk_idx, topk_w, counts, stream);
-  }
+#define INFMOE_SOFTMAX_CASE(EQ)                                                              \
+  if (bf) softmax_launch<__nv_bfloat16, EQ>(x, N, d, wg, bias, E, k, topk_idx, topk_w, counts, \
+                                            stream);                                          \
+  else softmax_launch<float, EQ>(x, N, d, wg, bias, E, k, topk_idx, topk_w, counts, stream);
+  if (E <= 8) { INFMOE_SOFTMAX_CASE(1) }
+  else if (E <= 16) { INFMOE_SOFTMAX_CASE(2) }
+  else if (E <= 32) { INFMOE_SOFTMAX_CASE(4) }
+  else if (E <= 64) { INFMOE_SOFTMAX_CASE(8) }
+  else { INFMOE_SOFTMAX_CASE(16) }
+#undef INFMOE_SOFTMAX_CASE
   INFMOE_LAUNCH_CHECK();
 }
 
@@ -233,18 +391,38 @@ void launch_gate_lsh(const void* x, int dtype, int64_t N, int d, const double* p
   require(bits >= 1 && bits <= 31, "gating: n_hash_bits must be in [1, 31]");
   require(E >= 1, "route_tokens: n_experts must be >= 1");
   require((1u << bits) >= uint32_t(E), "gating: 2^n_hash_bits must be >= n_experts");
+  const size_t esz = dtype_bytes(dtype);
+  require(d % 8 == 0, "lsh gate: d_model must be a multiple of 8");
+  require(reinterpret_cast<uintptr_t>(proj) % 16 == 0 && reinterpret_cast<uintptr_t>(x) % 16 == 0,
+          "lsh gate: x and proj must be 16-byte aligned");
   INFMOE_CUDA(cudaMemsetAsync(counts, 0, sizeof(int32_t) * size_t(E), stream));
   if (N == 0) return;
   const int G = 32 / bits;
-  const int64_t blocks = (N + 4 * G - 1) / (4 * G);
-  if (dtype == kDtypeBf16)
-    gate_lsh_kernel<<<unsigned(blocks), 128, 0, stream>>>(
+  const int TB = kLshWarps * G;
+  const int64_t blocks = (N + TB - 1) / TB;
+  const size_t smem = kGateStages * (size_t(TB) * (kLshChunk + 16 / esz) * esz +
+                                     size_t(bits) * (kLshChunk + 2) * sizeof(double));
+  if (dtype == kDtypeBf16) {
+    auto kern = gate_lsh_kernel<__nv_bfloat16>;
+    static size_t configured = 0;  // opt in to >48 KiB dynamic smem once per size
+    if (smem > configured) {
+      INFMOE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+      configured = smem;
+    }
+    kern<<<unsigned(blocks), kLshWarps * 32, smem, stream>>>(
         reinterpret_cast<const __nv_bfloat16*>(x), N, d, proj, bits, E, codes, topk_idx, topk_w,
         counts);
-  else
-    gate_lsh_kernel<<<unsigned(blocks), 128, 0, stream>>>(reinterpret_cast<const float*>(x), N, d,
-                                                           proj, bits, E, codes, topk_idx, topk_w,
-                                                           counts);
+  } else {
+    auto kern = gate_lsh_kernel<float>;
+    static size_t configured = 0;
+    if (smem > configured) {
+      INFMOE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+      configured = smem;
+    }
+    kern<<<unsigned(blocks), kLshWarps * 32, smem, stream>>>(reinterpret_cast<const float*>(x), N, d,
+                                                             proj, bits, E, codes, topk_idx,
+                                                             topk_w, counts);
+  }
   INFMOE_LAUNCH_CHECK();
 }
 

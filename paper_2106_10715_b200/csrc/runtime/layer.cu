@@ -154,7 +154,8 @@ void Layer::route(const void* x, int64_t N, cudaStream_t s) {
 }
 
 void Layer::ffn(const int32_t* experts, const int32_t* slots, int n, const void* w_in,
-                const void* w_out, int n_w_slots, int64_t rows, int max_ctas, cudaStream_t s) {
+                const void* w_out, int n_w_slots, int64_t rows, int max_ctas, int rows_hint,
+                cudaStream_t s) {
   GroupedGemmArgs g;
   std::memset(&g, 0, sizeof(g));
   g.a = xp;
@@ -173,6 +174,7 @@ void Layer::ffn(const int32_t* experts, const int32_t* slots, int n, const void*
   g.out = hbuf;
   g.gelu = 1;
   g.max_ctas = max_ctas;
+  g.max_rows_hint = rows_hint;
   launch_grouped_gemm(g, s);
   g.a = hbuf;
   g.b = w_out;
@@ -198,7 +200,7 @@ void Layer::forward(const void* x, int64_t N, void* y, infmoe_forward_out* out, 
   if (desc.residency == INFMOE_RESIDENT) {
     // one grouped launch per projection over all experts; no host round trip
     if (timed) INFMOE_CUDA(cudaEventRecord(t_comp0[0], s));
-    if (rows > 0) ffn(all.data(), all.data(), E, desc.w_in, desc.w_out, E, rows, 0, s);
+    if (rows > 0) ffn(all.data(), all.data(), E, desc.w_in, desc.w_out, E, rows, 0, 0, s);
     if (timed) INFMOE_CUDA(cudaEventRecord(t_comp1[0], s));
     launch_combine(yp, desc.dtype, inv, wts, N, k, desc.d_model, y, s);
     if (out && out->counts) {
@@ -255,8 +257,8 @@ void Layer::forward(const void* x, int64_t N, void* y, infmoe_forward_out* out, 
     const int32_t ex = e, sl = slot;
     const int64_t n_e = int64_t(cnt[size_t(e)]);
     if (n_e > 0) {
-      const int tiles = int((n_e + 255) / 256) * (desc.d_ff / 128);
-      ffn(&ex, &sl, 1, slot_in, slot_out, n_slots, rows, tiles, s);
+      const int tiles = int((n_e + 127) / 128) * (desc.d_ff / 128);
+      ffn(&ex, &sl, 1, slot_in, slot_out, n_slots, rows, tiles, int(n_e), s);
     }
     if (timed) INFMOE_CUDA(cudaEventRecord(t_comp1[size_t(j)], s));
     INFMOE_CUDA(cudaEventRecord(compute_done[size_t(j)], s));

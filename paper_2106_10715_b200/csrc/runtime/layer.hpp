@@ -22,7 +22,8 @@ struct Layer {
  private:
   void route(const void* x, int64_t N, cudaStream_t s);
   void ffn(const int32_t* experts, const int32_t* slots, int n, const void* w_in,
-           const void* w_out, int n_w_slots, int64_t rows, int max_ctas, cudaStream_t s);
+           const void* w_out, int n_w_slots, int64_t rows, int max_ctas, int rows_hint,
+           cudaStream_t s);
 
   infmoe_layer_desc desc;
   size_t esz = 2;
