@@ -200,6 +200,9 @@ int infmoe_expert_ffn(const void* x_perm, int64_t n_rows, int32_t d_model, int32
                       const void* w_in, const void* w_out, int32_t n_slots,
                       const int32_t* experts, const int32_t* slots, int32_t n_groups,
                       void* h, void* y_perm, void* stream);
+/* row scatter (inverse of the gather): dst[index[p]] = src[p] for p < rows */
+int infmoe_scatter_rows(const void* src, int32_t dtype, int64_t rows, int32_t d,
+                        const int32_t* index, void* dst, void* stream);
 /* N5 combine: y[t] = fmaf-chain over j<k of topk_w[t,j] * y_perm[inv[t,j]] */
 int infmoe_combine(const void* y_perm, int32_t dtype, const int32_t* inv,
                    const float* topk_w, int64_t N, int32_t k, int32_t d, void* y,
@@ -227,6 +230,11 @@ typedef struct {
   const void* w_in;
   const void* w_out;
   infmoe_hardware hw; /* cost model inputs for the scheduler (alpha, beta) */
+  /* expert parallelism: ep_size ranks, experts split into
+   * contiguous blocks of n_experts/ep_size; w_in/w_out then hold only this
+   * rank's block.  ep_comm from infmoe_ep_comm_init (NULL when ep_size == 1). */
+  int32_t ep_size, ep_rank;
+  void* ep_comm;
 } infmoe_layer_desc;
 
 /* per-forward outputs (all optional; host pointers unless noted) */
@@ -237,6 +245,21 @@ typedef struct {
   infmoe_event* events;  /* [2E] measured timeline (seconds from layer start) */
   double* exposed_copy_s;/* makespan - compute_busy on the measured timeline */
 } infmoe_forward_out;
+
+/* ---- expert parallelism (N7) ------------------------------------------ */
+/* Exchange plan for one rank: send_counts[E] (rows this rank routes to every
+ * global expert), recv_counts[P * E/P] (rows each source routes to this rank's
+ * experts, source-major).  Outputs: send_off/send_rows[P], recv_off/recv_rows[P],
+ * local_offsets[E/P + 1], local_index[n_recv] (local row <- receive row),
+ * *n_recv.  local_index may be NULL to query n_recv first. */
+int infmoe_ep_plan(int32_t P, int32_t rank, int32_t E, const int32_t* send_counts,
+                   const int32_t* recv_counts, int64_t* send_off, int64_t* send_rows,
+                   int64_t* recv_off, int64_t* recv_rows, int32_t* local_offsets,
+                   int32_t* local_index, int64_t* n_recv);
+/* NCCL communicator for the EP exchange (NCCL is loaded at run time) */
+int infmoe_ep_get_unique_id(uint8_t id[128]);
+int infmoe_ep_comm_init(const uint8_t id[128], int32_t nranks, int32_t rank, void** comm);
+int infmoe_ep_comm_destroy(void* comm);
 
 int infmoe_layer_create(const infmoe_layer_desc* desc, infmoe_layer** out);
 /* x, y: device [N, d_model] in dtype; stream: cudaStream_t or NULL. */

@@ -121,7 +121,8 @@ class LayerDesc(C.Structure):
                 ("max_tokens", C.c_int32), ("device", C.c_int32),
                 ("gate_weight", C.c_void_p), ("gate_bias", C.c_void_p),
                 ("lsh_seed", C.c_uint64), ("lsh_bits", C.c_int32),
-                ("w_in", C.c_void_p), ("w_out", C.c_void_p), ("hw", Hardware)]
+                ("w_in", C.c_void_p), ("w_out", C.c_void_p), ("hw", Hardware),
+                ("ep_size", C.c_int32), ("ep_rank", C.c_int32), ("ep_comm", C.c_void_p)]
 
 
 class ForwardOut(C.Structure):
@@ -173,6 +174,11 @@ _lib.infmoe_gather_rows.argtypes = [_vp, _i32, C.c_int64, _i32, _i32, _vp, _vp, 
 _lib.infmoe_expert_ffn.argtypes = [_vp, C.c_int64, _i32, _i32, _i32, _vp, _i32, _vp, _vp, _i32,
                                    _vp, _vp, _i32, _vp, _vp, _vp]
 _lib.infmoe_combine.argtypes = [_vp, _i32, _vp, _vp, C.c_int64, _i32, _i32, _vp, _vp]
+_lib.infmoe_scatter_rows.argtypes = [_vp, _i32, C.c_int64, _i32, _vp, _vp, _vp]
+_lib.infmoe_ep_plan.argtypes = [_i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]
+_lib.infmoe_ep_get_unique_id.argtypes = [_vp]
+_lib.infmoe_ep_comm_init.argtypes = [_vp, _i32, _i32, _P(_vp)]
+_lib.infmoe_ep_comm_destroy.argtypes = [_vp]
 _lib.infmoe_layer_create.argtypes = [_P(LayerDesc), _P(_vp)]
 _lib.infmoe_layer_forward.argtypes = [_vp, _vp, C.c_int64, _vp, _P(ForwardOut), _vp]
 _lib.infmoe_layer_set_host_weights.argtypes = [_vp, _vp, _vp]
@@ -442,6 +448,54 @@ def simulate_model(layer_costs: Sequence[CostVector], K: int, mode: str = "overl
 def lower_bound(c: CostVector) -> float:
     a = _f64arr(c.alphas)
     return float(_lib.infmoe_lower_bound(_ptr(a), len(a), c.beta))
+
+
+# ------------------------------------------------------ expert parallelism --
+
+
+@dataclass
+class EpPlan:
+    """Exchange plan of one EP rank (csrc/host/ep_plan.cpp)."""
+    send_off: np.ndarray
+    send_rows: np.ndarray
+    recv_off: np.ndarray
+    recv_rows: np.ndarray
+    local_offsets: np.ndarray
+    local_index: np.ndarray
+    n_recv: int
+
+
+def ep_plan(P: int, rank: int, E: int, send_counts, recv_counts) -> EpPlan:
+    sc = _i32arr(send_counts)
+    rc = _i32arr(recv_counts).reshape(-1)
+    if len(sc) != E or len(rc) != E:
+        raise ValueError("ep_plan: send_counts needs E entries, recv_counts P * E/P")
+    so, sr, ro, rr = (np.zeros(P, np.int64) for _ in range(4))
+    lo = np.zeros(E // max(P, 1) + 1, np.int32)
+    n = C.c_int64(0)
+    _check(_lib.infmoe_ep_plan(P, rank, E, _ptr(sc), _ptr(rc), _ptr(so), _ptr(sr), _ptr(ro),
+                               _ptr(rr), _ptr(lo), None, C.byref(n)))
+    li = np.zeros(max(n.value, 1), np.int32)
+    _check(_lib.infmoe_ep_plan(P, rank, E, _ptr(sc), _ptr(rc), None, None, None, None, None,
+                               _ptr(li), None))
+    return EpPlan(so, sr, ro, rr, lo, li[:n.value], n.value)
+
+
+def ep_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    _check(_lib.infmoe_ep_get_unique_id(buf))
+    return bytes(buf)
+
+
+def ep_comm_init(uid: bytes, nranks: int, rank: int) -> int:
+    buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+    comm = C.c_void_p()
+    _check(_lib.infmoe_ep_comm_init(buf, nranks, rank, C.byref(comm)))
+    return comm.value
+
+
+def ep_comm_destroy(comm: int) -> None:
+    _check(_lib.infmoe_ep_comm_destroy(C.c_void_p(comm)))
 
 
 from . import device  # noqa: E402,F401  (device-path wrappers over torch tensors)

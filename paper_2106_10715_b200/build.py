@@ -2,7 +2,8 @@
 
 nvcc cross-compiles the CUDA translation units (no GPU needed), g++ the host
 planner; everything links into one C-ABI shared library whose exports are
-declared in include/infmoe.h.  Usage: python -m paper_2106_10715_b200.build
+declared in include/infmoe.h.  Usage: python paper_2106_10715_b200/build.py
+(not `-m`: importing the package requires the library this script builds).
 """
 from __future__ import annotations
 
@@ -36,6 +37,8 @@ CU_SOURCES = [
 CXX_SOURCES = [
     "host/planner.cpp",
     "host/capi_host.cpp",
+    "host/ep_plan.cpp",
+    "runtime/nccl_shim.cpp",
 ]
 
 
@@ -81,7 +84,7 @@ def build(verbose: bool = False) -> Path:
     if LIB.exists() and LIB.stat().st_mtime >= newest:
         return LIB
     cmd = [NVCC, *ARCH, "-shared", "-ccbin", HOST_CXX, "-o", str(LIB), *map(str, objs),
-           "-lcudart", "-Xlinker", "-rpath,/usr/local/cuda/lib64"]
+           "-lcudart", "-ldl", "-Xlinker", "-rpath,/usr/local/cuda/lib64"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed\n{' '.join(cmd)}\n{r.stdout}\n{r.stderr}")

@@ -112,6 +112,18 @@ __global__ void gather_rows_kernel(const uint4* __restrict__ x, int64_t rows_out
   }
 }
 
+__global__ void scatter_rows_kernel(const uint4* __restrict__ src, int64_t rows, int vec_per_row,
+                                    const int32_t* __restrict__ index, uint4* __restrict__ dst) {
+  const int warps = blockDim.x / 32;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  for (int64_t p = int64_t(blockIdx.x) * warps + warp; p < rows;
+       p += int64_t(gridDim.x) * warps) {
+    const uint4* s = src + p * vec_per_row;
+    uint4* d = dst + int64_t(index[p]) * vec_per_row;
+    for (int v = lane; v < vec_per_row; v += 32) d[v] = __ldg(s + v);
+  }
+}
+
 template <typename T>
 __global__ void combine_kernel(const T* __restrict__ yp, const int32_t* __restrict__ inv,
                                const float* __restrict__ w, int64_t N, int k, int d,
@@ -187,6 +199,17 @@ void launch_gather_rows(const void* x, int dtype, int64_t N, int d, int k, const
   gather_rows_kernel<<<grid_for_rows(rows, 8), 256, 0, s>>>(
       reinterpret_cast<const uint4*>(x), rows, int(row_bytes / 16), k, perm,
       reinterpret_cast<uint4*>(x_perm));
+  INFMOE_LAUNCH_CHECK();
+}
+
+void launch_scatter_rows(const void* src, int dtype, int64_t rows, int d, const int32_t* index,
+                         void* dst, cudaStream_t s) {
+  const size_t row_bytes = size_t(d) * dtype_bytes(dtype);
+  require(row_bytes % 16 == 0, "scatter: row bytes must be a multiple of 16");
+  if (rows == 0) return;
+  scatter_rows_kernel<<<grid_for_rows(rows, 8), 256, 0, s>>>(
+      reinterpret_cast<const uint4*>(src), rows, int(row_bytes / 16), index,
+      reinterpret_cast<uint4*>(dst));
   INFMOE_LAUNCH_CHECK();
 }
 

@@ -27,6 +27,8 @@ void launch_dispatch(const int32_t* topk_idx, int64_t n_assign, int E, int32_t* 
                      int32_t* perm, int32_t* inv, void* workspace, cudaStream_t stream);
 void launch_gather_rows(const void* x, int dtype, int64_t N, int d, int k, const int32_t* perm,
                         void* x_perm, cudaStream_t stream);
+void launch_scatter_rows(const void* src, int dtype, int64_t rows, int d, const int32_t* index,
+                         void* dst, cudaStream_t stream);
 // N5
 void launch_combine(const void* y_perm, int dtype, const int32_t* inv, const float* topk_w,
                     int64_t N, int k, int d, void* y, cudaStream_t stream);

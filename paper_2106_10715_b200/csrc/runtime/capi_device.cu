@@ -7,7 +7,9 @@
 #include "../kernels/expert_gemm.cuh"
 #include "../kernels/kernels.cuh"
 #include "infmoe.h"
+#include "../host/ep_plan.hpp"
 #include "layer.hpp"
+#include "nccl_shim.hpp"
 
 using namespace infmoe;
 
@@ -107,6 +109,62 @@ int infmoe_expert_ffn(const void* x_perm, int64_t n_rows, int32_t d_model, int32
     g.out = y_perm;
     g.gelu = 0;
     launch_grouped_gemm(g, as_stream(stream));
+  });
+}
+
+int infmoe_scatter_rows(const void* src, int32_t dtype, int64_t rows, int32_t d,
+                        const int32_t* index, void* dst, void* stream) {
+  return guarded([&] {
+    require(src && index && dst, "scatter: NULL pointer");
+    launch_scatter_rows(src, dtype, rows, d, index, dst, as_stream(stream));
+  });
+}
+
+int infmoe_ep_plan(int32_t P, int32_t rank, int32_t E, const int32_t* send_counts,
+                   const int32_t* recv_counts, int64_t* send_off, int64_t* send_rows,
+                   int64_t* recv_off, int64_t* recv_rows, int32_t* local_offsets,
+                   int32_t* local_index, int64_t* n_recv) {
+  return guarded([&] {
+    EpPlan p = make_ep_plan(P, rank, E, send_counts, recv_counts);
+    auto put = [](int64_t* dst, const std::vector<int64_t>& v) {
+      if (dst) std::memcpy(dst, v.data(), v.size() * sizeof(int64_t));
+    };
+    put(send_off, p.send_off);
+    put(send_rows, p.send_rows);
+    put(recv_off, p.recv_off);
+    put(recv_rows, p.recv_rows);
+    if (local_offsets)
+      std::memcpy(local_offsets, p.local_offsets.data(), p.local_offsets.size() * sizeof(int32_t));
+    if (local_index)
+      std::memcpy(local_index, p.local_index.data(), p.local_index.size() * sizeof(int32_t));
+    if (n_recv) *n_recv = p.n_recv;
+  });
+}
+
+int infmoe_ep_get_unique_id(uint8_t id[128]) {
+  return guarded([&] {
+    require(id != nullptr, "ep: NULL id");
+    nccl::UniqueId u;
+    nccl::check(nccl::api().GetUniqueId(&u), "ncclGetUniqueId");
+    std::memcpy(id, u.internal, 128);
+  });
+}
+
+int infmoe_ep_comm_init(const uint8_t id[128], int32_t nranks, int32_t rank, void** comm) {
+  return guarded([&] {
+    require(id && comm && nranks >= 1 && rank >= 0 && rank < nranks, "ep: bad arguments");
+    nccl::UniqueId u;
+    std::memcpy(u.internal, id, 128);
+    nccl::Comm c = nullptr;
+    nccl::check(nccl::api().CommInitRank(&c, nranks, u, rank), "ncclCommInitRank");
+    *comm = c;
+  });
+}
+
+int infmoe_ep_comm_destroy(void* comm) {
+  return guarded([&] {
+    if (comm) nccl::check(nccl::api().CommDestroy(reinterpret_cast<nccl::Comm>(comm)),
+                          "ncclCommDestroy");
   });
 }
 

@@ -1,5 +1,6 @@
-// layer.cu — the MoE layer handle: N1 gate -> N2 dispatch -> N3/N4 expert FFN
-// -> N5 combine, resident or offloaded (N6 executor).
+// layer.cu — the MoE layer handle: N1 gate -> N2 dispatch -> [N7 EP exchange]
+// -> N3/N4 expert FFN (resident grouped GEMM, or the N6 offload executor) ->
+// [N7 EP return] -> N5 combine.
 //
 // Offloaded execution realises the two-lane recurrence of simulator.hpp:87-194
 // (and PAPER.md:366, "by using different CUDA streams, parameter-loading and
@@ -14,6 +15,12 @@
 //     semantics needs;
 //   * the compute stream runs expert j's grouped-GEMM pair once load j landed.
 // The per-layer counts read-back is the one device->host sync of the path.
+//
+// Expert parallelism: experts are split into ep_size contiguous
+// blocks; after routing, a count exchange and a token all-to-allv (grouped
+// NCCL send/recv over NVLink) move every routed row to its expert's owner, the
+// owner runs its local experts (resident or offloaded), and the reverse
+// all-to-allv brings the results home for the combine.
 #include <algorithm>
 #include <cstring>
 #include <memory>
@@ -25,6 +32,7 @@
 #include "../kernels/kernels.cuh"
 #include "infmoe.h"
 #include "layer.hpp"
+#include "nccl_shim.hpp"
 
 namespace infmoe {
 
@@ -39,14 +47,33 @@ T* dalloc(size_t n, std::vector<void*>& owned) {
 }
 }  // namespace
 
+template <class T>
+T* Layer::grow(T*& p, size_t& cap, size_t n) {
+  if (n > cap) {
+    if (p) INFMOE_CUDA(cudaFree(p));
+    p = nullptr;
+    cap = std::max<size_t>(n, cap + cap / 2);
+    INFMOE_CUDA(cudaMalloc(reinterpret_cast<void**>(&p), cap * sizeof(T)));
+  }
+  return p;
+}
+
 Layer::Layer(const infmoe_layer_desc& d) : desc(d) {
   require(d.d_model > 0 && d.d_ff > 0 && d.n_experts > 0, "layer: dimensions must be > 0");
-  require(d.n_experts <= kMaxGroups, "layer: at most 128 experts per layer");
   require(d.top_k >= 1 && d.top_k <= 8 && d.top_k <= d.n_experts, "layer: bad top_k");
   require(d.dtype == INFMOE_DTYPE_BF16 || d.dtype == INFMOE_DTYPE_F32, "layer: bad dtype");
   require(d.max_tokens >= 1, "layer: max_tokens must be >= 1");
   require(d.w_in && d.w_out, "layer: expert weights are NULL");
   if (d.gate_kind == INFMOE_GATE_LSH) require(d.top_k == 1, "layer: the LSH gate is top-1");
+  const int P = std::max(1, d.ep_size);
+  require(d.n_experts % P == 0, "layer: n_experts must be a multiple of ep_size");
+  require(d.ep_rank >= 0 && d.ep_rank < P, "layer: ep_rank out of range");
+  require(P == 1 || d.ep_comm != nullptr, "layer: ep_size > 1 needs ep_comm");
+  // (desc.ep_comm with ep_size == 1 runs the exchange path against itself)
+  n_local = d.n_experts / P;
+  require(n_local <= kMaxGroups, "layer: at most 128 experts per rank");
+  desc.ep_size = P;
+  comm = d.ep_comm;
   INFMOE_CUDA(cudaSetDevice(d.device));
   esz = dtype_bytes(d.dtype);
   const int64_t A = int64_t(d.max_tokens) * d.top_k;
@@ -58,8 +85,12 @@ Layer::Layer(const infmoe_layer_desc& d) : desc(d) {
   inv = dalloc<int32_t>(size_t(A), owned);
   dws = dalloc<uint8_t>(dispatch_workspace_bytes(A, d.n_experts), owned);
   xp = dalloc<uint8_t>(size_t(A) * d.d_model * esz, owned);
-  hbuf = dalloc<uint8_t>(size_t(A) * d.d_ff * esz, owned);
   yp = dalloc<uint8_t>(size_t(A) * d.d_model * esz, owned);
+  // the exchange path runs whenever a communicator is given (ep_size == 1 then
+  // exchanges with itself, which exercises the NCCL transport on one GPU)
+  use_ep = P > 1 || comm != nullptr;
+  if (!use_ep) hbuf = dalloc<uint8_t>(size_t(A) * d.d_ff * esz, owned);
+  else recv_counts_dev = dalloc<int32_t>(size_t(P) * n_local, owned);
 
   if (d.gate_kind == INFMOE_GATE_LSH) {
     std::vector<double> p = lsh_hyperplanes(d.lsh_seed, d.lsh_bits, d.d_model);
@@ -76,29 +107,23 @@ Layer::Layer(const infmoe_layer_desc& d) : desc(d) {
                              cudaMemcpyHostToDevice));
     }
   }
-  INFMOE_CUDA(cudaMallocHost(&counts_host, sizeof(int32_t) * d.n_experts));
+  INFMOE_CUDA(cudaMallocHost(&counts_host, sizeof(int32_t) * (d.n_experts + P * n_local)));
 
   expert_in_bytes = size_t(d.d_ff) * d.d_model * esz;
   if (d.residency == INFMOE_OFFLOADED) {
     require(d.K >= 1, "layer: offloaded mode needs K >= 1");
-    n_slots = std::min(d.K + 1, d.n_experts + 1);
+    n_slots = std::min(d.K + 1, n_local + 1);
     slot_in = dalloc<uint8_t>(size_t(n_slots) * expert_in_bytes, owned);
     slot_out = dalloc<uint8_t>(size_t(n_slots) * expert_in_bytes, owned);
     INFMOE_CUDA(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
-    const int E = d.n_experts;
-    load_done.resize(size_t(E));
-    compute_done.resize(size_t(E));
-    t_load0.resize(size_t(E));
-    t_load1.resize(size_t(E));
-    t_comp0.resize(size_t(E));
-    t_comp1.resize(size_t(E));
-    for (int j = 0; j < E; ++j) {
-      INFMOE_CUDA(cudaEventCreateWithFlags(&load_done[size_t(j)], cudaEventDisableTiming));
-      INFMOE_CUDA(cudaEventCreateWithFlags(&compute_done[size_t(j)], cudaEventDisableTiming));
-      INFMOE_CUDA(cudaEventCreate(&t_load0[size_t(j)]));
-      INFMOE_CUDA(cudaEventCreate(&t_load1[size_t(j)]));
-      INFMOE_CUDA(cudaEventCreate(&t_comp0[size_t(j)]));
-      INFMOE_CUDA(cudaEventCreate(&t_comp1[size_t(j)]));
+    const size_t E = size_t(n_local);
+    for (auto* v : {&load_done, &compute_done}) {
+      v->resize(E);
+      for (auto& e : *v) INFMOE_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    for (auto* v : {&t_load0, &t_load1, &t_comp0, &t_comp1}) {
+      v->resize(E);
+      for (auto& e : *v) INFMOE_CUDA(cudaEventCreate(&e));
     }
     set_host_weights(d.w_in, d.w_out);
   } else {
@@ -113,7 +138,7 @@ Layer::Layer(const infmoe_layer_desc& d) : desc(d) {
 void Layer::set_host_weights(const void* w_in, const void* w_out) {
   require(desc.residency == INFMOE_OFFLOADED, "set_host_weights: layer is resident");
   require(w_in && w_out, "set_host_weights: NULL weights");
-  const size_t bytes = expert_in_bytes * size_t(desc.n_experts);
+  const size_t bytes = expert_in_bytes * size_t(n_local);
   for (const void* p : {w_in, w_out}) {
     cudaPointerAttributes at;
     INFMOE_CUDA(cudaPointerGetAttributes(&at, p));
@@ -138,6 +163,11 @@ Layer::~Layer() {
   if (copy_stream) cudaStreamDestroy(copy_stream);
   for (void* p : registered) cudaHostUnregister(p);
   if (counts_host) cudaFreeHost(counts_host);
+  if (plan_host) cudaFreeHost(plan_host);
+  for (void* p : {static_cast<void*>(plan_dev), static_cast<void*>(recv_x),
+                  static_cast<void*>(loc_x), static_cast<void*>(loc_h),
+                  static_cast<void*>(loc_y), static_cast<void*>(recv_y)})
+    if (p) cudaFree(p);
   for (void* p : owned) cudaFree(p);
 }
 
@@ -153,95 +183,73 @@ void Layer::route(const void* x, int64_t N, cudaStream_t s) {
   launch_gather_rows(x, desc.dtype, N, desc.d_model, k, perm, xp, s);
 }
 
-void Layer::ffn(const int32_t* experts, const int32_t* slots, int n, const void* w_in,
-                const void* w_out, int n_w_slots, int64_t rows, int max_ctas, int rows_hint,
+void Layer::ffn(const Rows& r, const int32_t* experts, const int32_t* slots, int n,
+                const void* w_in, const void* w_out, int n_w_slots, int max_ctas, int rows_hint,
                 cudaStream_t s) {
   GroupedGemmArgs g;
   std::memset(&g, 0, sizeof(g));
-  g.a = xp;
-  g.a_rows = rows;
+  g.a = r.a;
+  g.a_rows = r.rows;
   g.b = w_in;
   g.n_slots = n_w_slots;
   g.N = desc.d_ff;
   g.K = desc.d_model;
   g.dtype = desc.dtype;
-  g.offsets = offsets;
+  g.offsets = r.offsets;
   g.n_groups = n;
   for (int i = 0; i < n; ++i) {
     g.experts[i] = experts[i];
     g.slots[i] = slots[i];
   }
-  g.out = hbuf;
+  g.out = r.h;
   g.gelu = 1;
   g.max_ctas = max_ctas;
   g.max_rows_hint = rows_hint;
   launch_grouped_gemm(g, s);
-  g.a = hbuf;
+  g.a = r.h;
   g.b = w_out;
   g.N = desc.d_model;
   g.K = desc.d_ff;
-  g.out = yp;
+  g.out = r.y;
   g.gelu = 0;
   launch_grouped_gemm(g, s);
 }
 
-void Layer::forward(const void* x, int64_t N, void* y, infmoe_forward_out* out, cudaStream_t s) {
-  require(N >= 0 && N <= desc.max_tokens, "forward: N exceeds max_tokens");
-  INFMOE_CUDA(cudaSetDevice(desc.device));
-  const int E = desc.n_experts, k = desc.top_k;
-  const int64_t rows = N * k;
-  const bool timed = out && (out->events || out->exposed_copy_s);
-  INFMOE_CUDA(cudaEventRecord(t_start, s));
-  route(x, N, s);
+// one grouped launch per projection over all local experts; no host round trip
+void Layer::compute_resident(const Rows& r, bool timed, cudaStream_t s) {
+  std::vector<int32_t> all(static_cast<size_t>(n_local));
+  for (int e = 0; e < n_local; ++e) all[size_t(e)] = e;
+  int hint = 0;
+  if (r.counts) hint = *std::max_element(r.counts, r.counts + n_local);
+  if (timed) INFMOE_CUDA(cudaEventRecord(t_comp0[0], s));
+  if (r.rows > 0)
+    ffn(r, all.data(), all.data(), n_local, desc.w_in, desc.w_out, n_local, 0, hint, s);
+  if (timed) INFMOE_CUDA(cudaEventRecord(t_comp1[0], s));
+}
 
-  std::vector<int32_t> all(static_cast<size_t>(E));
-  for (int e = 0; e < E; ++e) all[size_t(e)] = e;
-
-  if (desc.residency == INFMOE_RESIDENT) {
-    // one grouped launch per projection over all experts; no host round trip
-    if (timed) INFMOE_CUDA(cudaEventRecord(t_comp0[0], s));
-    if (rows > 0) ffn(all.data(), all.data(), E, desc.w_in, desc.w_out, E, rows, 0, 0, s);
-    if (timed) INFMOE_CUDA(cudaEventRecord(t_comp1[0], s));
-    launch_combine(yp, desc.dtype, inv, wts, N, k, desc.d_model, y, s);
-    if (out && out->counts) {
-      INFMOE_CUDA(cudaMemcpyAsync(counts_host, counts, sizeof(int32_t) * E,
-                                  cudaMemcpyDeviceToHost, s));
-    }
-    if (out && (out->counts || timed)) INFMOE_CUDA(cudaStreamSynchronize(s));
-    if (out && out->counts) std::memcpy(out->counts, counts_host, sizeof(int32_t) * E);
-    if (timed) {
-      float a = 0, b = 0;
-      INFMOE_CUDA(cudaEventElapsedTime(&a, t_start, t_comp0[0]));
-      INFMOE_CUDA(cudaEventElapsedTime(&b, t_start, t_comp1[0]));
-      if (out->events) out->events[0] = {INFMOE_STREAM_COMPUTE, 0, -1, a * 1e-3, b * 1e-3};
-      if (out->exposed_copy_s) *out->exposed_copy_s = 0.0;
-    }
-    return;
-  }
-
-  // ---- offloaded: counts -> schedule (host) ----
-  INFMOE_CUDA(cudaMemcpyAsync(counts_host, counts, sizeof(int32_t) * E, cudaMemcpyDeviceToHost, s));
-  INFMOE_CUDA(cudaStreamSynchronize(s));
+void Layer::compute_offloaded(const Rows& r, bool timed, infmoe_forward_out* out,
+                              cudaStream_t s) {
+  const int E = n_local;
   std::vector<uint64_t> cnt(static_cast<size_t>(E));
-  for (int e = 0; e < E; ++e) cnt[size_t(e)] = uint64_t(counts_host[e]);
+  for (int e = 0; e < E; ++e) cnt[size_t(e)] = uint64_t(r.counts[e]);
   Geometry geo{1, 1, 1, desc.d_model, desc.d_ff, E, int(esz)};
   Hardware hw{desc.hw.peak_flops, desc.hw.h2d_bandwidth, desc.hw.device_memory,
               desc.hw.reserved_memory};
   Costs c = derive_costs(cnt.data(), E, geo, hw);
-  Plan plan;
+  Plan pl;
   switch (desc.policy) {
-    case INFMOE_POLICY_NAIVE: plan = plan_identity(c, desc.K); break;
-    case INFMOE_POLICY_GREEDY: plan = plan_greedy(c, desc.K); break;
-    case INFMOE_POLICY_EXACT: plan = plan_exact(c, desc.K, 12); break;
-    default: plan = plan_auto(c, desc.K, 12); break;
+    case INFMOE_POLICY_NAIVE: pl = plan_identity(c, desc.K); break;
+    case INFMOE_POLICY_GREEDY: pl = plan_greedy(c, desc.K); break;
+    case INFMOE_POLICY_EXACT: pl = plan_exact(c, desc.K, 12); break;
+    default: pl = plan_auto(c, desc.K, 12); break;
   }
-
   // ---- copy lane / compute lane ----
   INFMOE_CUDA(cudaStreamWaitEvent(copy_stream, t_start, 0));  // drain: after previous layer
   for (int j = 0; j < E; ++j) {
-    const int e = plan.order[size_t(j)];
+    const int e = pl.order[size_t(j)];
     const int slot = j % n_slots;
-    if (j >= n_slots) INFMOE_CUDA(cudaStreamWaitEvent(copy_stream, compute_done[size_t(j - n_slots)], 0));
+    if (j >= n_slots)
+      INFMOE_CUDA(cudaStreamWaitEvent(copy_stream, compute_done[size_t(j - n_slots)], 0));
     if (timed) INFMOE_CUDA(cudaEventRecord(t_load0[size_t(j)], copy_stream));
     INFMOE_CUDA(cudaMemcpyAsync(slot_in + size_t(slot) * expert_in_bytes,
                                 host_in + size_t(e) * expert_in_bytes, expert_in_bytes,
@@ -258,37 +266,151 @@ void Layer::forward(const void* x, int64_t N, void* y, infmoe_forward_out* out, 
     const int64_t n_e = int64_t(cnt[size_t(e)]);
     if (n_e > 0) {
       const int tiles = int((n_e + 127) / 128) * (desc.d_ff / 128);
-      ffn(&ex, &sl, 1, slot_in, slot_out, n_slots, rows, tiles, int(n_e), s);
+      ffn(r, &ex, &sl, 1, slot_in, slot_out, n_slots, tiles, int(n_e), s);
     }
     if (timed) INFMOE_CUDA(cudaEventRecord(t_comp1[size_t(j)], s));
     INFMOE_CUDA(cudaEventRecord(compute_done[size_t(j)], s));
   }
+  if (out) {
+    if (out->order) std::memcpy(out->order, pl.order.data(), sizeof(int32_t) * E);
+    if (out->feasible) *out->feasible = pl.feasible ? 1 : 0;
+  }
+}
+
+void Layer::ep_exchange_out(int64_t N, cudaStream_t s) {
+  (void)N;
+  const auto& nc = nccl::api();
+  auto* cm = reinterpret_cast<nccl::Comm>(comm);
+  const int P = desc.ep_size, E = desc.n_experts, El = n_local;
+  // 1. count exchange: rows routed to each of the peer's experts
+  nccl::check(nc.GroupStart(), "ncclGroupStart");
+  for (int r = 0; r < P; ++r) {
+    nccl::check(nc.Send(counts + size_t(r) * El, size_t(El), nccl::kInt32, r, cm, s), "ncclSend");
+    nccl::check(nc.Recv(recv_counts_dev + size_t(r) * El, size_t(El), nccl::kInt32, r, cm, s),
+                "ncclRecv");
+  }
+  nccl::check(nc.GroupEnd(), "ncclGroupEnd");
+  INFMOE_CUDA(cudaMemcpyAsync(counts_host, counts, sizeof(int32_t) * E, cudaMemcpyDeviceToHost, s));
+  INFMOE_CUDA(cudaMemcpyAsync(counts_host + E, recv_counts_dev, sizeof(int32_t) * P * El,
+                              cudaMemcpyDeviceToHost, s));
+  INFMOE_CUDA(cudaStreamSynchronize(s));
+  // 2. plan (host) + upload of the local layout
+  plan = make_ep_plan(P, desc.ep_rank, E, counts_host, counts_host + E);
+  const size_t pn = size_t(El) + 1 + size_t(plan.n_recv);
+  grow(plan_dev, plan_cap, pn);
+  if (pn > plan_host_cap) {
+    if (plan_host) INFMOE_CUDA(cudaFreeHost(plan_host));
+    plan_host_cap = std::max(pn, plan_host_cap * 2);
+    INFMOE_CUDA(cudaMallocHost(&plan_host, plan_host_cap * sizeof(int32_t)));
+  }
+  std::memcpy(plan_host, plan.local_offsets.data(), sizeof(int32_t) * (El + 1));
+  std::memcpy(plan_host + El + 1, plan.local_index.data(), sizeof(int32_t) * plan.n_recv);
+  INFMOE_CUDA(cudaMemcpyAsync(plan_dev, plan_host, sizeof(int32_t) * pn, cudaMemcpyHostToDevice, s));
+  const size_t rowb = size_t(desc.d_model) * esz;
+  const size_t nr = size_t(std::max<int64_t>(plan.n_recv, 1));
+  grow(recv_x, cap_x, nr * rowb);
+  grow(loc_x, cap_lx, nr * rowb);
+  grow(loc_h, cap_h, nr * size_t(desc.d_ff) * esz);
+  grow(loc_y, cap_ly, nr * rowb);
+  grow(recv_y, cap_ry, nr * rowb);
+  // 3. token all-to-allv (dispatch)
+  nccl::check(nc.GroupStart(), "ncclGroupStart");
+  for (int r = 0; r < P; ++r) {
+    nccl::check(nc.Send(xp + size_t(plan.send_off[size_t(r)]) * rowb,
+                        size_t(plan.send_rows[size_t(r)]) * rowb, nccl::kUint8, r, cm, s),
+                "ncclSend");
+    nccl::check(nc.Recv(recv_x + size_t(plan.recv_off[size_t(r)]) * rowb,
+                        size_t(plan.recv_rows[size_t(r)]) * rowb, nccl::kUint8, r, cm, s),
+                "ncclRecv");
+  }
+  nccl::check(nc.GroupEnd(), "ncclGroupEnd");
+  // 4. expert-contiguous local rows
+  launch_gather_rows(recv_x, desc.dtype, plan.n_recv, desc.d_model, 1, plan_dev + El + 1, loc_x,
+                     s);
+}
+
+void Layer::ep_exchange_back(cudaStream_t s) {
+  const auto& nc = nccl::api();
+  auto* cm = reinterpret_cast<nccl::Comm>(comm);
+  const int P = desc.ep_size, El = n_local;
+  const size_t rowb = size_t(desc.d_model) * esz;
+  launch_scatter_rows(loc_y, desc.dtype, plan.n_recv, desc.d_model, plan_dev + El + 1, recv_y, s);
+  nccl::check(nc.GroupStart(), "ncclGroupStart");
+  for (int r = 0; r < P; ++r) {
+    nccl::check(nc.Send(recv_y + size_t(plan.recv_off[size_t(r)]) * rowb,
+                        size_t(plan.recv_rows[size_t(r)]) * rowb, nccl::kUint8, r, cm, s),
+                "ncclSend");
+    nccl::check(nc.Recv(yp + size_t(plan.send_off[size_t(r)]) * rowb,
+                        size_t(plan.send_rows[size_t(r)]) * rowb, nccl::kUint8, r, cm, s),
+                "ncclRecv");
+  }
+  nccl::check(nc.GroupEnd(), "ncclGroupEnd");
+}
+
+void Layer::forward(const void* x, int64_t N, void* y, infmoe_forward_out* out, cudaStream_t s) {
+  require(N >= 0 && N <= desc.max_tokens, "forward: N exceeds max_tokens");
+  INFMOE_CUDA(cudaSetDevice(desc.device));
+  const int E = desc.n_experts, k = desc.top_k;
+  const bool offloaded = desc.residency == INFMOE_OFFLOADED;
+  const bool timed = out && (out->events || out->exposed_copy_s);
+  INFMOE_CUDA(cudaEventRecord(t_start, s));
+  route(x, N, s);
+
+  Rows r;
+  std::vector<int32_t> local_counts;
+  if (!use_ep) {
+    r = Rows{xp, offsets, N * k, hbuf, yp, nullptr};
+    if (offloaded || (out && out->counts)) {
+      INFMOE_CUDA(cudaMemcpyAsync(counts_host, counts, sizeof(int32_t) * E,
+                                  cudaMemcpyDeviceToHost, s));
+      if (offloaded) {
+        INFMOE_CUDA(cudaStreamSynchronize(s));
+        r.counts = counts_host;
+      }
+    }
+  } else {
+    ep_exchange_out(N, s);
+    local_counts.resize(size_t(n_local));
+    for (int e = 0; e < n_local; ++e)
+      local_counts[size_t(e)] = plan.local_offsets[size_t(e) + 1] - plan.local_offsets[size_t(e)];
+    r = Rows{loc_x, plan_dev, plan.n_recv, loc_h, loc_y, local_counts.data()};
+  }
+
+  if (offloaded) compute_offloaded(r, timed, out, s);
+  else compute_resident(r, timed, s);
+
+  if (use_ep) ep_exchange_back(s);
   launch_combine(yp, desc.dtype, inv, wts, N, k, desc.d_model, y, s);
 
-  if (out) {
-    if (out->counts) std::memcpy(out->counts, counts_host, sizeof(int32_t) * E);
-    if (out->order) std::memcpy(out->order, plan.order.data(), sizeof(int32_t) * E);
-    if (out->feasible) *out->feasible = plan.feasible ? 1 : 0;
-    if (timed) {
-      INFMOE_CUDA(cudaStreamSynchronize(s));
-      double busy = 0.0, makespan = 0.0;
-      for (int j = 0; j < E; ++j) {
-        float a = 0, b = 0, c0 = 0, c1 = 0;
-        INFMOE_CUDA(cudaEventElapsedTime(&a, t_start, t_load0[size_t(j)]));
-        INFMOE_CUDA(cudaEventElapsedTime(&b, t_start, t_load1[size_t(j)]));
-        INFMOE_CUDA(cudaEventElapsedTime(&c0, t_start, t_comp0[size_t(j)]));
-        INFMOE_CUDA(cudaEventElapsedTime(&c1, t_start, t_comp1[size_t(j)]));
-        const int e = plan.order[size_t(j)];
-        if (out->events) {
-          out->events[2 * j] = {INFMOE_STREAM_LOAD, 0, e, a * 1e-3, b * 1e-3};
-          out->events[2 * j + 1] = {INFMOE_STREAM_COMPUTE, 0, e, c0 * 1e-3, c1 * 1e-3};
-        }
-        busy += (c1 - c0) * 1e-3;
-        makespan = std::max(makespan, double(c1) * 1e-3);
-      }
-      if (out->exposed_copy_s) *out->exposed_copy_s = makespan - busy;
-    }
+  if (!out) return;
+  const bool need_sync = timed || (out->counts && !offloaded && !use_ep);
+  if (need_sync) INFMOE_CUDA(cudaStreamSynchronize(s));
+  if (out->counts) std::memcpy(out->counts, counts_host, sizeof(int32_t) * E);
+  if (!timed) return;
+  if (!offloaded) {
+    float a = 0, b = 0;
+    INFMOE_CUDA(cudaEventElapsedTime(&a, t_start, t_comp0[0]));
+    INFMOE_CUDA(cudaEventElapsedTime(&b, t_start, t_comp1[0]));
+    if (out->events) out->events[0] = {INFMOE_STREAM_COMPUTE, 0, -1, a * 1e-3, b * 1e-3};
+    if (out->exposed_copy_s) *out->exposed_copy_s = 0.0;
+    return;
   }
+  double busy = 0.0, makespan = 0.0;
+  for (int j = 0; j < n_local; ++j) {
+    float a = 0, b = 0, c0 = 0, c1 = 0;
+    INFMOE_CUDA(cudaEventElapsedTime(&a, t_start, t_load0[size_t(j)]));
+    INFMOE_CUDA(cudaEventElapsedTime(&b, t_start, t_load1[size_t(j)]));
+    INFMOE_CUDA(cudaEventElapsedTime(&c0, t_start, t_comp0[size_t(j)]));
+    INFMOE_CUDA(cudaEventElapsedTime(&c1, t_start, t_comp1[size_t(j)]));
+    const int e = out->order ? out->order[j] : j;
+    if (out->events) {
+      out->events[2 * j] = {INFMOE_STREAM_LOAD, 0, e, a * 1e-3, b * 1e-3};
+      out->events[2 * j + 1] = {INFMOE_STREAM_COMPUTE, 0, e, c0 * 1e-3, c1 * 1e-3};
+    }
+    busy += (c1 - c0) * 1e-3;
+    makespan = std::max(makespan, double(c1) * 1e-3);
+  }
+  if (out->exposed_copy_s) *out->exposed_copy_s = makespan - busy;
 }
 
 }  // namespace infmoe

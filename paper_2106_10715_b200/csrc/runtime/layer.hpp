@@ -1,11 +1,13 @@
 // layer.hpp — state owned by one infmoe_layer handle (device buffers sized for
-// max_tokens, K+1 weight slots, copy stream, per-position events).
+// max_tokens, K+1 weight slots, copy stream, per-position events, and the
+// expert-parallel exchange buffers).
 #pragma once
 
 #include <cuda_runtime.h>
 
 #include <vector>
 
+#include "../host/ep_plan.hpp"
 #include "infmoe.h"
 
 namespace infmoe {
@@ -20,13 +22,28 @@ struct Layer {
   void set_host_weights(const void* w_in, const void* w_out);
 
  private:
+  // the rows one expert-compute pass works on
+  struct Rows {
+    const void* a;            // [rows, d_model] expert-contiguous token rows
+    const int32_t* offsets;   // device [n_local + 1]
+    int64_t rows;
+    void* h;                  // [rows, d_ff]
+    void* y;                  // [rows, d_model]
+    const int32_t* counts;    // host [n_local] rows per local expert (may be NULL: resident)
+  };
   void route(const void* x, int64_t N, cudaStream_t s);
-  void ffn(const int32_t* experts, const int32_t* slots, int n, const void* w_in,
-           const void* w_out, int n_w_slots, int64_t rows, int max_ctas, int rows_hint,
-           cudaStream_t s);
+  void compute_resident(const Rows& r, bool timed, cudaStream_t s);  // grouped GEMM pair
+  void compute_offloaded(const Rows& r, bool timed, infmoe_forward_out* out, cudaStream_t s);
+  void ffn(const Rows& r, const int32_t* experts, const int32_t* slots, int n, const void* w_in,
+           const void* w_out, int n_w_slots, int max_ctas, int rows_hint, cudaStream_t s);
+  void ep_exchange_out(int64_t N, cudaStream_t s);   // dispatch all-to-allv
+  void ep_exchange_back(cudaStream_t s);             // combine all-to-allv
+  template <class T>
+  T* grow(T*& p, size_t& cap, size_t n);
 
   infmoe_layer_desc desc;
   size_t esz = 2;
+  int n_local = 0;  // experts held by this rank (E / ep_size)
   std::vector<void*> owned;
   std::vector<void*> registered;
   // routing / dispatch buffers
@@ -43,7 +60,7 @@ struct Layer {
   double* proj = nullptr;
   float* gate_w = nullptr;
   float* gate_b = nullptr;
-  int32_t* counts_host = nullptr;
+  int32_t* counts_host = nullptr;  // pinned [E + ep_size * n_local]
   // offload executor
   size_t expert_in_bytes = 0;  // = bytes of W_in = bytes of W_out of one expert
   int n_slots = 0;
@@ -55,6 +72,20 @@ struct Layer {
   std::vector<cudaEvent_t> load_done, compute_done;
   std::vector<cudaEvent_t> t_load0, t_load1, t_comp0, t_comp1;
   cudaEvent_t t_start = nullptr;
+  // expert parallelism
+  void* comm = nullptr;
+  bool use_ep = false;
+  EpPlan plan;
+  int32_t* recv_counts_dev = nullptr;  // [ep_size * n_local]
+  int32_t* plan_dev = nullptr;         // [n_local + 1 | n_recv] offsets + index
+  int32_t* plan_host = nullptr;        // pinned staging for plan_dev
+  size_t plan_cap = 0, plan_host_cap = 0;
+  uint8_t* recv_x = nullptr;   // receive buffer, source-major
+  uint8_t* loc_x = nullptr;    // expert-contiguous rows
+  uint8_t* loc_h = nullptr;
+  uint8_t* loc_y = nullptr;
+  uint8_t* recv_y = nullptr;   // results in receive layout (sent back)
+  size_t cap_x = 0, cap_lx = 0, cap_h = 0, cap_ly = 0, cap_ry = 0;
 };
 
 }  // namespace infmoe

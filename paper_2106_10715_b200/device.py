@@ -132,6 +132,17 @@ def expert_ffn(x_perm, offsets, w_in, w_out, experts: Optional[Sequence[int]] = 
     return h, y_perm
 
 
+def scatter_rows(src, index, n_out: int, out=None):
+    """out[index[p]] = src[p]."""
+    torch = _torch()
+    R, d = src.shape
+    if out is None:
+        out = torch.empty((n_out, d), dtype=src.dtype, device=src.device)
+    _check(_lib.infmoe_scatter_rows(_p(src), _dtype_code(src), R, d, _p(index), _p(out),
+                                    _stream_ptr()))
+    return out
+
+
 def combine(y_perm, inv, topk_w, N: int, k: int):
     torch = _torch()
     d = y_perm.shape[1]
@@ -148,7 +159,8 @@ class MoELayer:
                  dtype: str = "bf16", gate: str = "lsh", gate_weight=None, gate_bias=None,
                  lsh_seed: int = 0, lsh_bits: int = 5, offloaded: bool = False, K: int = 4,
                  policy: int = POLICY_AUTO, max_tokens: int = 4096, device: int = 0,
-                 hw: Optional[Hardware] = None):
+                 hw: Optional[Hardware] = None, ep_size: int = 1, ep_rank: int = 0,
+                 ep_comm: Optional[int] = None):
         d = LayerDesc()
         d.d_model, d.d_ff, d.n_experts, d.top_k = d_model, d_ff, n_experts, top_k
         d.dtype = DTYPE_BF16 if dtype == "bf16" else DTYPE_F32
@@ -168,8 +180,10 @@ class MoELayer:
         d.w_in, d.w_out = w_in.data_ptr(), w_out.data_ptr()
         self._keep += [w_in, w_out]
         d.hw = hw if hw is not None else Hardware(1643.6e12, 55.5e9, 180 << 30, 8 << 30)
+        d.ep_size, d.ep_rank, d.ep_comm = ep_size, ep_rank, ep_comm
         self.desc = d
         self.n_experts = n_experts
+        self.n_local = n_experts // max(ep_size, 1)
         self._h = C.c_void_p()
         _check(_lib.infmoe_layer_create(C.byref(d), C.byref(self._h)))
 
@@ -183,12 +197,12 @@ class MoELayer:
         N = x.shape[0]
         if y is None:
             y = torch.empty_like(x)
-        E = self.n_experts
+        E, El = self.n_experts, self.n_local
         counts = np.zeros(E, dtype=np.int32)
-        order = np.zeros(E, dtype=np.int32)
+        order = np.zeros(El, dtype=np.int32)
         feas = C.c_int32(0)
         exposed = C.c_double(0.0)
-        events = (Event * (2 * E))()
+        events = (Event * (2 * El))()
         out = ForwardOut(counts.ctypes.data, order.ctypes.data, C.addressof(feas),
                          C.addressof(events) if want_timeline else None,
                          C.addressof(exposed) if want_timeline else None)
