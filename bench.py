@@ -182,9 +182,10 @@ def run_reference_arm(args, cfg, rank: int) -> None:
         lib.or_fill_uniform_bf16(seed, n, scale, out.ctypes.data_as(C.c_void_p))
         return out
     x_bits = fill(im.derive_seed(SEED, 0), n_tok * d, SQRT3)
-    w_in = fill(im.derive_seed(SEED, 1000), E * f * d, SQRT3 / np.sqrt(d)).reshape(E, f * d)
-    w_out = fill(im.derive_seed(SEED, 1001), E * d * f,
-                 GELU_GAIN * SQRT3 / np.sqrt(f)).reshape(E, d * f)
+    w_in = np.stack([fill(im.derive_seed(SEED, 10_000 + 2 * e), f * d, SQRT3 / np.sqrt(d))
+                     for e in range(E)])
+    w_out = np.stack([fill(im.derive_seed(SEED, 10_001 + 2 * e), d * f,
+                           GELU_GAIN * SQRT3 / np.sqrt(f)) for e in range(E)])
     proj = np.ascontiguousarray(im.gating_projection(im.derive_seed(SEED, 100), cfg["bits"], d))
     times = []
     for i in range(args.warmup + args.steps):
@@ -196,7 +197,7 @@ def run_reference_arm(args, cfg, rank: int) -> None:
     line = {"metric": "moe_stack_tokens_per_s", "value": value, "unit": "tokens/s",
             "impl": "reference", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_layer * cfg["L"] * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": {"workload": cfg["workload"], "tokens": cfg["N"], "layers": cfg["L"],
                        "d_model": d, "d_ff": f, "experts": E, "top_k": cfg["k"]},
@@ -246,9 +247,18 @@ def main() -> None:
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     peaks = measured_peaks()
-    d, f, E, k, N, L = cfg["d"], cfg["f"], cfg["E"], cfg["k"], cfg["N"], cfg["L"]
+    d, f, E, k, N_glob, L = cfg["d"], cfg["f"], cfg["E"], cfg["k"], cfg["N"], cfg["L"]
+    P = world                      # expert parallelism over all ranks (strong scaling)
+    if E % P or N_glob % P:
+        raise SystemExit(f"experts ({E}) and tokens ({N_glob}) must divide by {P} ranks")
+    El, N = E // P, N_glob // P    # experts and tokens owned by this rank
     bf = torch.bfloat16
     stream = torch.cuda.current_stream()
+    comm = None
+    if P > 1:  # the layers' own NCCL communicator (id shared through torch.distributed)
+        uid = [im.ep_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = im.ep_comm_init(uid[0], P, rank)
 
     # --- pinned H2D peak on this box (roofline denominator for the host link)
     probe_h = torch.empty(1 << 30, dtype=torch.uint8, pin_memory=True)
@@ -263,18 +273,25 @@ def main() -> None:
         h2d_peak = max(h2d_peak, (1 << 30) / (e0.elapsed_time(e1) * 1e-3) / 1e9)
     del probe_h, probe_d
 
-    # --- weights: n_sets distinct sets, device copies + one pinned host pool
+    # --- weights: n_sets distinct sets of this rank's experts, device copies +
+    # one pinned host pool (expert e of set s is drawn from seed (s, e): the
+    # same values whatever the rank count)
     n_sets = max(1, min(args.host_sets, L))
-    per = E * f * d
-    host_pool = torch.empty(n_sets * 2 * per, dtype=bf, pin_memory=True)
+    per_e = f * d
+    host_pool = torch.empty(n_sets * 2 * El * per_e, dtype=bf, pin_memory=True)
     w_dev, w_host = [], []
     for s in range(n_sets):
-        wi = torch.empty((E, f, d), dtype=bf, device=dev)
-        wo = torch.empty((E, d, f), dtype=bf, device=dev)
-        dv.fill_uniform(wi, im.derive_seed(SEED, 1000 + 2 * s), SQRT3 / d ** 0.5)
-        dv.fill_uniform(wo, im.derive_seed(SEED, 1001 + 2 * s), GELU_GAIN * SQRT3 / f ** 0.5)
-        hi = host_pool[(2 * s) * per:(2 * s + 1) * per].view(E, f, d)
-        ho = host_pool[(2 * s + 1) * per:(2 * s + 2) * per].view(E, d, f)
+        wi = torch.empty((El, f, d), dtype=bf, device=dev)
+        wo = torch.empty((El, d, f), dtype=bf, device=dev)
+        for e in range(El):
+            ge = rank * El + e
+            dv.fill_uniform(wi[e], im.derive_seed(SEED, 10_000 * (s + 1) + 2 * ge),
+                            SQRT3 / d ** 0.5)
+            dv.fill_uniform(wo[e], im.derive_seed(SEED, 10_000 * (s + 1) + 2 * ge + 1),
+                            GELU_GAIN * SQRT3 / f ** 0.5)
+        base = 2 * s * El * per_e
+        hi = host_pool[base:base + El * per_e].view(El, f, d)
+        ho = host_pool[base + El * per_e:base + 2 * El * per_e].view(El, d, f)
         hi.copy_(wi)
         ho.copy_(wo)
         w_dev.append((wi, wo))
@@ -282,9 +299,11 @@ def main() -> None:
     torch.cuda.synchronize()
 
     hw = im.Hardware(float(peaks["bf16_tflops"]) * 1e12, h2d_peak * 1e9, 180 << 30, 8 << 30)
+    x_all = torch.empty((N_glob, d), dtype=bf, device=dev)
+    dv.fill_uniform(x_all, im.derive_seed(SEED, 0), SQRT3)
+    x_dev = x_all[rank * N:(rank + 1) * N].clone()
+    del x_all
     x_host = torch.empty((N, d), dtype=bf, pin_memory=True)
-    x_dev = torch.empty((N, d), dtype=bf, device=dev)
-    dv.fill_uniform(x_dev, im.derive_seed(SEED + rank, 0), SQRT3)
     x_host.copy_(x_dev)
     y_host = torch.empty((N, d), dtype=bf, pin_memory=True)
 
@@ -293,9 +312,10 @@ def main() -> None:
         for l in range(L):
             s = l % n_sets
             wi, wo = (w_host if offloaded else w_dev)[s]
-            out.append(dv.MoELayer(d, f, E, k, wi, wo, gate="lsh", lsh_seed=im.derive_seed(SEED, 100 + l),
-                                   lsh_bits=cfg["bits"], offloaded=offloaded, K=cfg["K"],
-                                   max_tokens=N, device=local, hw=hw))
+            out.append(dv.MoELayer(d, f, E, k, wi, wo, gate="lsh",
+                                   lsh_seed=im.derive_seed(SEED, 100 + l), lsh_bits=cfg["bits"],
+                                   offloaded=offloaded, K=cfg["K"], max_tokens=N, device=local,
+                                   hw=hw, ep_size=P, ep_rank=rank, ep_comm=comm))
         return out
 
     off_layers = make_layers(True)
@@ -352,15 +372,16 @@ def main() -> None:
     wbytes = 2 * d * f * 2
     for infos in all_infos:
         for info in infos:
-            cnt = info["counts"]
+            rows = info["local_rows"]  # rows this rank computed per local expert
             exposed.append(info["exposed_copy_s"])
-            launches += 6 + 2 * int((cnt > 0).sum())
+            # gate + 3 dispatch + gather (+ EP gather/scatter) + GEMM pair per expert + combine
+            launches += 6 + (2 if P > 1 else 0) + 2 * int((rows > 0).sum())
             for (st, _l, e, s0, s1) in info["events"]:
-                if st == 1 and cnt[e] > 0:
+                if st == 1 and rows[e] > 0:
                     ffn_secs += s1 - s0
-                    ffn_bytes += wbytes + int(cnt[e]) * (2 * d + 2 * f) * 2
+                    ffn_bytes += wbytes + int(rows[e]) * (2 * d + 2 * f) * 2
     launches //= max(1, args.steps)
-    h2d_bytes_step = L * E * wbytes
+    h2d_bytes_step = L * El * wbytes          # this rank's host link
     h2d_gbs = h2d_bytes_step / (t_in * 1e-3) / 1e9
 
     # ---------------- resident stack (all experts in HBM) --------------------
@@ -379,8 +400,8 @@ def main() -> None:
     rg_secs = sum(i["events"][0][4] - i["events"][0][3] for i in rinfos)
     rg_bytes = 0
     for i in rinfos:
-        cnt = i["counts"]
-        rg_bytes += int((cnt > 0).sum()) * wbytes + int(cnt.sum()) * (2 * d + 2 * f) * 2
+        rows = i["local_rows"]
+        rg_bytes += int((rows > 0).sum()) * wbytes + int(rows.sum()) * (2 * d + 2 * f) * 2
     parity_equal = bool(torch.equal(y_res.view(torch.int16), y_off.view(torch.int16)))
 
     # ---------------- CPU baseline (rank 0, N=1 only) ------------------------
@@ -402,27 +423,29 @@ def main() -> None:
     hbm_peak = float(peaks["hbm_gbs"])
     ffn_gbs = ffn_bytes / ffn_secs / 1e9 if ffn_secs else 0.0
     rg_gbs = rg_bytes / rg_secs / 1e9 if rg_secs else 0.0
-    value = N * world / (t_in * 1e-3)
+    value = N_glob / (t_in * 1e-3)
     line = {
         "metric": "moe_stack_tokens_per_s", "value": value, "unit": "tokens/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_in,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (counter-hash uniform, unit variance; random-init expert weights)",
-        "config": {"workload": cfg["workload"], "tokens": N, "layers": L, "d_model": d,
+        "config": {"workload": cfg["workload"], "tokens": N_glob, "layers": L, "d_model": d,
                    "d_ff": f, "experts": E, "top_k": k, "gate": cfg["gate"], "K": cfg["K"],
                    "device_slots": cfg["K"] + 1, "policy": "infmoe_greedy(auto_order)",
                    "host_weight_sets": n_sets,
+                   "parallelism": f"ep{P}" if P > 1 else "single",
                    "l2": "inputs larger than L2 (5.37 GB of expert weights per layer)"},
-        "e2e": {"value": N * world / (t_out * 1e-3), "unit": "tokens/s",
+        "e2e": {"value": N_glob / (t_out * 1e-3), "unit": "tokens/s",
                 "h2d_bytes_per_step": N * d * 2, "d2h_bytes_per_step": N * d * 2},
         "h2d": {"achieved_gbs": h2d_gbs, "peak_gbs": h2d_peak, "frac": h2d_gbs / h2d_peak,
                 "bytes_per_step": h2d_bytes_step, "peak_src": "measured pinned 1 GiB copy",
+                "per": "rank (each rank streams its own experts over its own host link)",
                 "exposed_copy_ms_per_layer": 1e3 * float(np.mean(exposed))},
         "roofline": {"kernel": "expert FFN (tcgen05 GEMM1+GeLU, GEMM2) per offloaded expert",
                      "bound": "hbm", "achieved": ffn_gbs, "peak": hbm_peak, "unit": "GB/s",
                      "frac": ffn_gbs / hbm_peak, "traffic": None,
                      "peak_src": peaks["_src"]},
-        "resident": {"tokens_per_s": N * world / (t_res * 1e-3), "ms_per_step": t_res,
+        "resident": {"tokens_per_s": N_glob / (t_res * 1e-3), "ms_per_step": t_res,
                      "ms_per_layer": t_res / L,
                      "grouped_ffn_gbs": rg_gbs, "grouped_ffn_frac": rg_gbs / hbm_peak,
                      "grouped_ffn_share": rg_secs * 1e3 / t_res if t_res else None,
@@ -436,6 +459,8 @@ def main() -> None:
         print(json.dumps(line), flush=True)
     for lay in off_layers + res_layers:
         lay.close()
+    if comm is not None:
+        im.ep_comm_destroy(comm)
     if world > 1:
         dist.destroy_process_group()
 

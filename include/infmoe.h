@@ -157,6 +157,17 @@ int infmoe_simulate_model(int32_t n_layers, const int32_t* T, const double* alph
                           infmoe_layer_report* per_layer);
 /* lower_bound simulator.hpp:53-56 */
 double infmoe_lower_bound(const double* alphas, int32_t T, double beta);
+/* Timeline audit (the rules of verification.hpp:108-198, re-implemented for
+ * MEASURED timelines): per-stream exclusivity, load-before-compute per
+ * (layer, expert), at most max_resident experts resident per layer (load end
+ * to compute end, departures before arrivals at ties), malformed events, and
+ * (check_durations != 0) event lengths equal to beta / alpha.  Returns the
+ * violation count in *n_violations and per-kind counts in kinds[6] (overlap,
+ * causality, residency, duration, makespan, malformed). */
+int infmoe_replay_check(const infmoe_event* events, int32_t n_events, int32_t n_layers,
+                        const int32_t* T, const double* alphas, const double* betas,
+                        int32_t max_resident, int32_t check_durations, double tol_s,
+                        int32_t* n_violations, int32_t* kinds);
 
 /* ======================================================================
  * Device path: the MoE layer forward the paper's TensorRT plugin ran
@@ -235,6 +246,9 @@ typedef struct {
    * rank's block.  ep_comm from infmoe_ep_comm_init (NULL when ep_size == 1). */
   int32_t ep_size, ep_rank;
   void* ep_comm;
+  /* skip_empty_experts (scenario.hpp:99; default off as in the
+   * reference): experts that received no rows are neither scheduled nor loaded */
+  int32_t skip_empty_experts;
 } infmoe_layer_desc;
 
 /* per-forward outputs (all optional; host pointers unless noted) */
@@ -244,6 +258,7 @@ typedef struct {
   int32_t* feasible;     /* scheduler verdict */
   infmoe_event* events;  /* [2E] measured timeline (seconds from layer start) */
   double* exposed_copy_s;/* makespan - compute_busy on the measured timeline */
+  int32_t* local_rows;   /* [E/ep_size] rows this rank computed per local expert */
 } infmoe_forward_out;
 
 /* ---- expert parallelism (N7) ------------------------------------------ */

@@ -745,31 +745,7 @@ void or_dispatch(const int32_t* topk_idx, uint64_t N, int k, int E, int32_t* off
   free(cur);
 }
 
-void or_expert_ffn(const float* x, uint64_t n, int d, int f, const float* w_in,
-                   const float* w_out, int round_h, float* y) {
-#pragma omp parallel
-  {
-    double* h = (double*)malloc(sizeof(double) * (size_t)f);
-#pragma omp for schedule(static)
-    for (long long r = 0; r < (long long)n; ++r) {
-      const float* xr = x + (uint64_t)r * (uint64_t)d;
-      for (int j = 0; j < f; ++j) {
-        const float* wr = w_in + (uint64_t)j * (uint64_t)d;
-        double acc = 0.0;
-        for (int c = 0; c < d; ++c) acc += (double)xr[c] * (double)wr[c];
-        double g = or_gelu(acc);
-        h[j] = round_h ? (double)or_bf16_to_f32(or_f32_to_bf16((float)g)) : g;
-      }
-      for (int c = 0; c < d; ++c) {
-        const float* wr = w_out + (uint64_t)c * (uint64_t)f;
-        double acc = 0.0;
-        for (int j = 0; j < f; ++j) acc += h[j] * (double)wr[j];
-        y[(uint64_t)r * (uint64_t)d + c] = (float)acc;
-      }
-    }
-    free(h);
-  }
-}
+/* or_expert_ffn lives in oracle_ffn.c (vectorised, OpenMP over rows x columns) */
 
 void or_combine(const float* y_perm, const int32_t* inv, const float* topk_w,
                 uint64_t N, int k, int d, float* y) {

@@ -122,12 +122,14 @@ class LayerDesc(C.Structure):
                 ("gate_weight", C.c_void_p), ("gate_bias", C.c_void_p),
                 ("lsh_seed", C.c_uint64), ("lsh_bits", C.c_int32),
                 ("w_in", C.c_void_p), ("w_out", C.c_void_p), ("hw", Hardware),
-                ("ep_size", C.c_int32), ("ep_rank", C.c_int32), ("ep_comm", C.c_void_p)]
+                ("ep_size", C.c_int32), ("ep_rank", C.c_int32), ("ep_comm", C.c_void_p),
+                ("skip_empty_experts", C.c_int32)]
 
 
 class ForwardOut(C.Structure):
     _fields_ = [("counts", C.c_void_p), ("order", C.c_void_p), ("feasible", C.c_void_p),
-                ("events", C.c_void_p), ("exposed_copy_s", C.c_void_p)]
+                ("events", C.c_void_p), ("exposed_copy_s", C.c_void_p),
+                ("local_rows", C.c_void_p)]
 
 
 DTYPE_BF16, DTYPE_F32 = 0, 1
@@ -174,6 +176,8 @@ _lib.infmoe_gather_rows.argtypes = [_vp, _i32, C.c_int64, _i32, _i32, _vp, _vp, 
 _lib.infmoe_expert_ffn.argtypes = [_vp, C.c_int64, _i32, _i32, _i32, _vp, _i32, _vp, _vp, _i32,
                                    _vp, _vp, _i32, _vp, _vp, _vp]
 _lib.infmoe_combine.argtypes = [_vp, _i32, _vp, _vp, C.c_int64, _i32, _i32, _vp, _vp]
+_lib.infmoe_replay_check.argtypes = [_vp, _i32, _i32, _vp, _vp, _vp, _i32, _i32, _f64, _vp,
+                                     _vp]
 _lib.infmoe_scatter_rows.argtypes = [_vp, _i32, C.c_int64, _i32, _vp, _vp, _vp]
 _lib.infmoe_ep_plan.argtypes = [_i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]
 _lib.infmoe_ep_get_unique_id.argtypes = [_vp]
@@ -443,6 +447,29 @@ def simulate_model(layer_costs: Sequence[CostVector], K: int, mode: str = "overl
     return (_events_list(ev, 2 * total),
             SimReport(rep.makespan, rep.compute_busy, rep.load_busy, rep.compute_stall,
                       rep.peak_resident_experts, rep.overlap_efficiency, layers), out_orders)
+
+
+VIOLATION_KINDS = ("stream_overlap", "causality", "residency_exceeded", "duration_mismatch",
+                   "makespan_mismatch", "malformed_event")
+
+
+def replay_check(events, layer_costs: Sequence[CostVector], max_resident: int,
+                 check_durations: bool = True, tol_s: float = 0.0) -> dict:
+    """Audit a (simulated or measured) timeline with the rules of replay_check
+    (verification.hpp:108-198).  events: (stream, layer, expert, start, end).
+    Returns {kind: count} for the kinds that occurred."""
+    ev = (Event * max(len(events), 1))()
+    for i, (st, l, e, a, b) in enumerate(events):
+        ev[i] = Event(st, l, e, a, b)
+    Ts = _i32arr([cv.size() for cv in layer_costs])
+    al = _f64arr(np.concatenate([_f64arr(cv.alphas) for cv in layer_costs]))
+    be = _f64arr([cv.beta for cv in layer_costs])
+    n = C.c_int32(0)
+    kinds = np.zeros(6, np.int32)
+    _check(_lib.infmoe_replay_check(ev, len(events), len(Ts), _ptr(Ts), _ptr(al), _ptr(be),
+                                    max_resident, int(check_durations), tol_s, C.byref(n),
+                                    _ptr(kinds)))
+    return {k: int(v) for k, v in zip(VIOLATION_KINDS, kinds) if v}
 
 
 def lower_bound(c: CostVector) -> float:

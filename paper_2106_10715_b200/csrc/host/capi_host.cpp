@@ -233,6 +233,30 @@ int infmoe_simulate_model(int32_t n_layers, const int32_t* T, const double* alph
   });
 }
 
+int infmoe_replay_check(const infmoe_event* events, int32_t n_events, int32_t n_layers,
+                        const int32_t* T, const double* alphas, const double* betas,
+                        int32_t max_resident, int32_t check_durations, double tol_s,
+                        int32_t* n_violations, int32_t* kinds) {
+  return guarded([&] {
+    require(events || n_events == 0, "replay_check: events is NULL");
+    require(T && alphas && betas && n_layers >= 1, "replay_check: NULL costs");
+    std::vector<Costs> cs;
+    std::size_t off = 0;
+    for (int32_t l = 0; l < n_layers; ++l) {
+      cs.push_back(to_costs(alphas + off, T[l], betas[l]));
+      off += std::size_t(T[l]);
+    }
+    std::vector<Event> ev(static_cast<std::size_t>(n_events));
+    for (int32_t i = 0; i < n_events; ++i)
+      ev[std::size_t(i)] = {events[i].stream, events[i].layer_id, events[i].expert_id,
+                            events[i].start, events[i].end};
+    int k6[6];
+    const int n = audit_timeline(ev, cs, max_resident, check_durations != 0, tol_s, k6);
+    if (n_violations) *n_violations = n;
+    if (kinds) for (int i = 0; i < 6; ++i) kinds[i] = k6[i];
+  });
+}
+
 double infmoe_lower_bound(const double* alphas, int32_t T, double beta) {
   if (!alphas || T < 1) return 0.0;
   return makespan_floor(to_costs(alphas, T, beta));

@@ -349,7 +349,7 @@ double makespan_floor(const Costs& c) {  // simulator.hpp:53-56
 namespace {
 // Max simultaneous residents: +1 at load completion, -1 at compute completion,
 // departures ordered before arrivals at equal instants.
-int max_resident(std::vector<std::pair<double, int>>& marks) {
+int max_resident_count(std::vector<std::pair<double, int>>& marks) {
   std::sort(marks.begin(), marks.end());
   int now = 0, peak = 0;
   for (const auto& mk : marks) peak = std::max(peak, now += mk.second);
@@ -423,7 +423,7 @@ TimelineStats run_timeline(std::span<const std::vector<int>> orders,
     }
     ls.start = first_start;
     ls.end = layer_end;
-    ls.peak_resident = max_resident(marks);
+    ls.peak_resident = max_resident_count(marks);
     st.load_busy += ls.load_busy;
     st.compute_busy += ls.compute_busy;
     st.peak_resident = std::max(st.peak_resident, ls.peak_resident);
@@ -432,6 +432,60 @@ TimelineStats run_timeline(std::span<const std::vector<int>> orders,
   }
   st.overlap_efficiency = st.makespan > 0.0 ? st.compute_busy / st.makespan : 0.0;
   return st;
+}
+
+// ============================================================ timeline audit
+// The rules of replay_check (verification.hpp:108-198) for measured timelines:
+// measured durations are never exactly alpha/beta, so the duration rule is
+// optional and comparisons take an absolute tolerance on top of the usual one.
+int audit_timeline(const std::vector<Event>& ev, std::span<const Costs> costs, int max_resident,
+                   bool check_durations, double tol_s, int kinds[6]) {
+  for (int i = 0; i < 6; ++i) kinds[i] = 0;
+  const int L = int(costs.size());
+  auto leq = [&](double a, double b) { return a <= b + tol_s || at_most(a, b); };
+  for (const Event& e : ev) {  // malformed events skip only the duration rule
+    if (e.end < e.start || e.layer < 0 || e.layer >= L || e.expert < 0 ||
+        e.expert >= costs[size_t(e.layer)].size()) {
+      ++kinds[5];
+      continue;
+    }
+    if (check_durations) {
+      const Costs& c = costs[size_t(e.layer)];
+      const double want = e.stream == 0 ? c.beta : c.alpha[size_t(e.expert)];
+      if (std::fabs((e.end - e.start) - want) > std::max(tol_s, tol(e.end - e.start, want)))
+        ++kinds[3];
+    }
+  }
+  for (int lane = 0; lane < 2; ++lane) {  // one lane per stream, across layers
+    std::vector<const Event*> v;
+    for (const Event& e : ev)
+      if (e.stream == lane) v.push_back(&e);
+    std::stable_sort(v.begin(), v.end(),
+                     [](const Event* a, const Event* b) { return a->start < b->start; });
+    for (size_t i = 1; i < v.size(); ++i)
+      if (!leq(v[i - 1]->end, v[i]->start)) ++kinds[0];
+  }
+  // causality per (layer, expert), residency per layer
+  std::map<std::pair<int, int>, std::pair<const Event*, const Event*>> pairs;
+  for (const Event& e : ev) {
+    if (e.layer < 0 || e.layer >= L) continue;
+    auto& slot = pairs[{e.layer, e.expert}];
+    (e.stream == 0 ? slot.first : slot.second) = &e;
+  }
+  std::map<int, std::vector<std::pair<double, int>>> marks;
+  for (const auto& [key, pr] : pairs) {
+    const Event* a = pr.first;
+    const Event* b = pr.second;
+    if (!a || !b) { ++kinds[1]; continue; }
+    if (!leq(a->end, b->start)) ++kinds[1];
+    marks[key.first].emplace_back(a->end, +1);
+    marks[key.first].emplace_back(b->end, -1);
+  }
+  for (auto& [layer, m] : marks)
+    if (max_resident > 0 && max_resident_count(m) > max_resident) ++kinds[2];
+  int n = 0;
+  for (int i = 0; i < 6; ++i) n += kinds[i];
+  return n;
 }
 
 }  // namespace infmoe

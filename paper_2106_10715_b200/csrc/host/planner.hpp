@@ -99,4 +99,9 @@ TimelineStats run_timeline(std::span<const std::vector<int>> orders,
                            std::span<const Costs> costs, int K, bool serial,
                            bool continuous_loads, std::vector<Event>* events);
 
+// Timeline audit for measured (or simulated) event lists; kinds[6] counts
+// overlap, causality, residency, duration, makespan, malformed violations.
+int audit_timeline(const std::vector<Event>& ev, std::span<const Costs> costs, int max_resident,
+                   bool check_durations, double tol_s, int kinds[6]);
+
 }  // namespace infmoe

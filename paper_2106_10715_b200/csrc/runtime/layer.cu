@@ -229,9 +229,16 @@ void Layer::compute_resident(const Rows& r, bool timed, cudaStream_t s) {
 
 void Layer::compute_offloaded(const Rows& r, bool timed, infmoe_forward_out* out,
                               cudaStream_t s) {
-  const int E = n_local;
+  // experts taking part: all of them (reference default), or only those that
+  // received rows when skip_empty_experts is set
+  std::vector<int> members;
+  for (int e = 0; e < n_local; ++e)
+    if (!desc.skip_empty_experts || r.counts[e] > 0) members.push_back(e);
+  const int E = int(members.size());
+  n_scheduled = E;
+  if (E == 0) return;
   std::vector<uint64_t> cnt(static_cast<size_t>(E));
-  for (int e = 0; e < E; ++e) cnt[size_t(e)] = uint64_t(r.counts[e]);
+  for (int i = 0; i < E; ++i) cnt[size_t(i)] = uint64_t(r.counts[members[size_t(i)]]);
   Geometry geo{1, 1, 1, desc.d_model, desc.d_ff, E, int(esz)};
   Hardware hw{desc.hw.peak_flops, desc.hw.h2d_bandwidth, desc.hw.device_memory,
               desc.hw.reserved_memory};
@@ -246,7 +253,7 @@ void Layer::compute_offloaded(const Rows& r, bool timed, infmoe_forward_out* out
   // ---- copy lane / compute lane ----
   INFMOE_CUDA(cudaStreamWaitEvent(copy_stream, t_start, 0));  // drain: after previous layer
   for (int j = 0; j < E; ++j) {
-    const int e = pl.order[size_t(j)];
+    const int e = members[size_t(pl.order[size_t(j)])];
     const int slot = j % n_slots;
     if (j >= n_slots)
       INFMOE_CUDA(cudaStreamWaitEvent(copy_stream, compute_done[size_t(j - n_slots)], 0));
@@ -263,7 +270,7 @@ void Layer::compute_offloaded(const Rows& r, bool timed, infmoe_forward_out* out
     INFMOE_CUDA(cudaStreamWaitEvent(s, load_done[size_t(j)], 0));
     if (timed) INFMOE_CUDA(cudaEventRecord(t_comp0[size_t(j)], s));
     const int32_t ex = e, sl = slot;
-    const int64_t n_e = int64_t(cnt[size_t(e)]);
+    const int64_t n_e = int64_t(r.counts[e]);
     if (n_e > 0) {
       const int tiles = int((n_e + 127) / 128) * (desc.d_ff / 128);
       ffn(r, &ex, &sl, 1, slot_in, slot_out, n_slots, tiles, int(n_e), s);
@@ -272,7 +279,10 @@ void Layer::compute_offloaded(const Rows& r, bool timed, infmoe_forward_out* out
     INFMOE_CUDA(cudaEventRecord(compute_done[size_t(j)], s));
   }
   if (out) {
-    if (out->order) std::memcpy(out->order, pl.order.data(), sizeof(int32_t) * E);
+    if (out->order) {
+      for (int j = 0; j < n_local; ++j) out->order[j] = -1;  // -1: not loaded (skipped)
+      for (int j = 0; j < E; ++j) out->order[j] = members[size_t(pl.order[size_t(j)])];
+    }
     if (out->feasible) *out->feasible = pl.feasible ? 1 : 0;
   }
 }
@@ -360,7 +370,7 @@ void Layer::forward(const void* x, int64_t N, void* y, infmoe_forward_out* out, 
   std::vector<int32_t> local_counts;
   if (!use_ep) {
     r = Rows{xp, offsets, N * k, hbuf, yp, nullptr};
-    if (offloaded || (out && out->counts)) {
+    if (offloaded || (out && (out->counts || out->local_rows))) {
       INFMOE_CUDA(cudaMemcpyAsync(counts_host, counts, sizeof(int32_t) * E,
                                   cudaMemcpyDeviceToHost, s));
       if (offloaded) {
@@ -383,9 +393,13 @@ void Layer::forward(const void* x, int64_t N, void* y, infmoe_forward_out* out, 
   launch_combine(yp, desc.dtype, inv, wts, N, k, desc.d_model, y, s);
 
   if (!out) return;
-  const bool need_sync = timed || (out->counts && !offloaded && !use_ep);
+  const bool need_sync = timed || ((out->counts || out->local_rows) && !offloaded && !use_ep);
   if (need_sync) INFMOE_CUDA(cudaStreamSynchronize(s));
   if (out->counts) std::memcpy(out->counts, counts_host, sizeof(int32_t) * E);
+  if (out->local_rows) {
+    if (use_ep) std::memcpy(out->local_rows, local_counts.data(), sizeof(int32_t) * n_local);
+    else std::memcpy(out->local_rows, counts_host, sizeof(int32_t) * n_local);
+  }
   if (!timed) return;
   if (!offloaded) {
     float a = 0, b = 0;
@@ -396,7 +410,9 @@ void Layer::forward(const void* x, int64_t N, void* y, infmoe_forward_out* out, 
     return;
   }
   double busy = 0.0, makespan = 0.0;
-  for (int j = 0; j < n_local; ++j) {
+  if (out->events)
+    for (int j = 0; j < 2 * n_local; ++j) out->events[j] = {-1, 0, -1, 0.0, 0.0};
+  for (int j = 0; j < n_scheduled; ++j) {
     float a = 0, b = 0, c0 = 0, c1 = 0;
     INFMOE_CUDA(cudaEventElapsedTime(&a, t_start, t_load0[size_t(j)]));
     INFMOE_CUDA(cudaEventElapsedTime(&b, t_start, t_load1[size_t(j)]));

@@ -44,6 +44,7 @@ struct Layer {
   infmoe_layer_desc desc;
   size_t esz = 2;
   int n_local = 0;  // experts held by this rank (E / ep_size)
+  int n_scheduled = 0;  // experts loaded by the last offloaded forward
   std::vector<void*> owned;
   std::vector<void*> registered;
   // routing / dispatch buffers

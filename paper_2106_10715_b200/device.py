@@ -160,7 +160,7 @@ class MoELayer:
                  lsh_seed: int = 0, lsh_bits: int = 5, offloaded: bool = False, K: int = 4,
                  policy: int = POLICY_AUTO, max_tokens: int = 4096, device: int = 0,
                  hw: Optional[Hardware] = None, ep_size: int = 1, ep_rank: int = 0,
-                 ep_comm: Optional[int] = None):
+                 ep_comm: Optional[int] = None, skip_empty_experts: bool = False):
         d = LayerDesc()
         d.d_model, d.d_ff, d.n_experts, d.top_k = d_model, d_ff, n_experts, top_k
         d.dtype = DTYPE_BF16 if dtype == "bf16" else DTYPE_F32
@@ -181,6 +181,7 @@ class MoELayer:
         self._keep += [w_in, w_out]
         d.hw = hw if hw is not None else Hardware(1643.6e12, 55.5e9, 180 << 30, 8 << 30)
         d.ep_size, d.ep_rank, d.ep_comm = ep_size, ep_rank, ep_comm
+        d.skip_empty_experts = int(skip_empty_experts)
         self.desc = d
         self.n_experts = n_experts
         self.n_local = n_experts // max(ep_size, 1)
@@ -203,13 +204,17 @@ class MoELayer:
         feas = C.c_int32(0)
         exposed = C.c_double(0.0)
         events = (Event * (2 * El))()
+        local_rows = np.zeros(El, dtype=np.int32)
         out = ForwardOut(counts.ctypes.data, order.ctypes.data, C.addressof(feas),
                          C.addressof(events) if want_timeline else None,
-                         C.addressof(exposed) if want_timeline else None)
+                         C.addressof(exposed) if want_timeline else None,
+                         local_rows.ctypes.data)
         _check(_lib.infmoe_layer_forward(self._h, _p(x), N, _p(y), C.byref(out), _stream_ptr()))
-        info = {"counts": counts, "order": order, "feasible": bool(feas.value)}
+        info = {"counts": counts, "order": order, "feasible": bool(feas.value),
+                "local_rows": local_rows}
         if want_timeline:
-            info["events"] = [(e.stream, e.layer_id, e.expert_id, e.start, e.end) for e in events]
+            info["events"] = [(e.stream, e.layer_id, e.expert_id, e.start, e.end)
+                              for e in events if e.stream >= 0]
             info["exposed_copy_s"] = exposed.value
         return y, info
 

@@ -144,3 +144,39 @@ def test_layer_rejects_bad_config(cuda):
     with pytest.raises(ValueError):
         dv.MoELayer(128, 100, 2, 1, wi, wi, gate="lsh", lsh_bits=1).forward(
             torch.zeros(4, 128, dtype=torch.bfloat16, device=cuda))  # d_ff % 128
+
+
+def test_offloaded_skip_empty_experts_and_measured_timeline(cuda):
+    """skip_empty_experts: with few tokens most experts get no
+    rows; they are neither scheduled nor loaded, the output is unchanged, and
+    the MEASURED timeline passes the replay_check rules (one lane per stream,
+    causality, <= K+1 residents)."""
+    from paper_2106_10715_b200 import trace
+    N, d, f, E, K = 24, 256, 384, 16, 2
+    (_, _, _), (x, wi, wo) = _setup(cuda, N, d, f, E, seed=21)
+    res = dv.MoELayer(d, f, E, 1, wi.to(cuda), wo.to(cuda), gate="lsh", lsh_seed=2, lsh_bits=4,
+                      max_tokens=N)
+    y_res, info_r = res.forward(x)
+    full = dv.MoELayer(d, f, E, 1, wi.pin_memory(), wo.pin_memory(), gate="lsh", lsh_seed=2,
+                       lsh_bits=4, offloaded=True, K=K, max_tokens=N)
+    skip = dv.MoELayer(d, f, E, 1, wi.pin_memory(), wo.pin_memory(), gate="lsh", lsh_seed=2,
+                       lsh_bits=4, offloaded=True, K=K, max_tokens=N, skip_empty_experts=True)
+    y_full, info_f = full.forward(x, want_timeline=True)
+    y_skip, info_s = skip.forward(x, want_timeline=True)
+    torch.cuda.synchronize()
+    assert torch.equal(y_res.view(torch.int16), y_full.view(torch.int16))
+    assert torch.equal(y_res.view(torch.int16), y_skip.view(torch.int16))
+    nonempty = int((info_r["counts"] > 0).sum())
+    assert nonempty < E
+    loaded = [e for e in info_s["order"].tolist() if e >= 0]
+    assert sorted(loaded) == sorted(np.nonzero(info_r["counts"])[0].tolist())
+    assert len(info_s["events"]) == 2 * nonempty and len(info_f["events"]) == 2 * E
+    g = im.make_geometry(d, f, E, 2)
+    cv = im.compute_costs(info_r["counts"].astype(np.uint64), g,
+                          im.Hardware(1643.6e12, 55.5e9, 180 << 30, 8 << 30))
+    for info in (info_f, info_s):
+        assert im.replay_check(info["events"], [cv], K + 1, check_durations=False,
+                               tol_s=2e-6) == {}
+    trace.write(info_f["events"], "/tmp/infmoe_layer_timeline")
+    for lay in (res, full, skip):
+        lay.close()
