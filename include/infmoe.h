@@ -211,6 +211,17 @@ int infmoe_expert_ffn(const void* x_perm, int64_t n_rows, int32_t d_model, int32
                       const void* w_in, const void* w_out, int32_t n_slots,
                       const int32_t* experts, const int32_t* slots, int32_t n_groups,
                       void* h, void* y_perm, void* stream);
+/* N3+N4 in ONE persistent launch (phase-2 tiles of an expert start once its
+ * H rows are complete; see csrc/kernels/expert_gemm.cuh).  bf16 only.
+ * done: >= n_groups int32 of device scratch.  perm/topk_w (top-1 only, or
+ * NULL): fuse the combine, y[perm[r]] = bf16(fmaf(topk_w[perm[r]], bf16(acc_r), 0)),
+ * in which case y is [N, d_model]; otherwise y is y_perm [n_rows, d_model]. */
+int infmoe_expert_ffn_fused(const void* x_perm, int64_t n_rows, int32_t d_model, int32_t d_ff,
+                            const int32_t* offsets, int32_t E, const void* w_in,
+                            const void* w_out, int32_t n_slots, const int32_t* experts,
+                            const int32_t* slots, int32_t n_groups, void* h, void* y,
+                            const int32_t* perm, const float* topk_w, int32_t* done,
+                            void* stream);
 /* row scatter (inverse of the gather): dst[index[p]] = src[p] for p < rows */
 int infmoe_scatter_rows(const void* src, int32_t dtype, int64_t rows, int32_t d,
                         const int32_t* index, void* dst, void* stream);

@@ -178,6 +178,8 @@ _lib.infmoe_expert_ffn.argtypes = [_vp, C.c_int64, _i32, _i32, _i32, _vp, _i32, 
 _lib.infmoe_combine.argtypes = [_vp, _i32, _vp, _vp, C.c_int64, _i32, _i32, _vp, _vp]
 _lib.infmoe_replay_check.argtypes = [_vp, _i32, _i32, _vp, _vp, _vp, _i32, _i32, _f64, _vp,
                                      _vp]
+_lib.infmoe_expert_ffn_fused.argtypes = [_vp, C.c_int64, _i32, _i32, _vp, _i32, _vp, _vp, _i32,
+                                         _vp, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _vp]
 _lib.infmoe_scatter_rows.argtypes = [_vp, _i32, C.c_int64, _i32, _vp, _vp, _vp]
 _lib.infmoe_ep_plan.argtypes = [_i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]
 _lib.infmoe_ep_get_unique_id.argtypes = [_vp]

@@ -462,6 +462,332 @@ void dispatch_tok(const GroupedGemmArgs& a, cudaStream_t s) {
   }
 }
 
+
+// =================================================================== fused
+// Two-phase persistent kernel (see FusedFfnArgs).  Tiles are numbered phase-1
+// first (expert-major), then phase 2; every CTA walks its tiles in increasing
+// order, so all phase-1 tiles are issued before any phase-2 tile and the
+// per-group waits always make progress (grid <= #SMs, 1 CTA per SM).
+struct FusedParams {
+  int32_t d, f;
+  int32_t n_groups;
+  const int32_t* offsets;
+  void* h;
+  void* y;
+  int32_t* done;
+  const int32_t* perm;
+  const float* topk_w;
+  int32_t experts[kMaxGroups];
+  int32_t slots[kMaxGroups];
+};
+
+struct FusedTable {
+  int32_t n_groups, fb1, fb2, total1;
+  int32_t start1[kMaxGroups + 1];
+  int32_t start2[kMaxGroups + 1];
+  int32_t chunks[kMaxGroups];
+  int32_t row0[kMaxGroups];
+  int32_t rows[kMaxGroups];
+  int32_t slot[kMaxGroups];
+};
+
+struct FTile {
+  int32_t phase;  // 0: x . w_in -> GeLU -> h ; 1: h . w_out -> y
+  int32_t g;
+  int32_t row0, ntok, w_row0, f0;
+};
+
+template <int TOK>
+__device__ __forceinline__ FTile fdecode(const FusedTable& tt, int32_t t, int32_t& c1,
+                                         int32_t& c2, int32_t d, int32_t f) {
+  FTile r;
+  if (t < tt.total1) {
+    while (t >= tt.start1[c1 + 1]) ++c1;
+    const int32_t local = t - tt.start1[c1];
+    const int32_t tc = local % tt.chunks[c1], fb = local / tt.chunks[c1];
+    r.phase = 0;
+    r.g = c1;
+    r.row0 = tt.row0[c1] + tc * TOK;
+    r.ntok = min(TOK, tt.rows[c1] - tc * TOK);
+    r.w_row0 = tt.slot[c1] * f + fb * BM;
+    r.f0 = fb * BM;
+  } else {
+    t -= tt.total1;
+    while (t >= tt.start2[c2 + 1]) ++c2;
+    const int32_t local = t - tt.start2[c2];
+    const int32_t tc = local % tt.chunks[c2], fb = local / tt.chunks[c2];
+    r.phase = 1;
+    r.g = c2;
+    r.row0 = tt.row0[c2] + tc * TOK;
+    r.ntok = min(TOK, tt.rows[c2] - tc * TOK);
+    r.w_row0 = tt.slot[c2] * d + fb * BM;
+    r.f0 = fb * BM;
+  }
+  return r;
+}
+
+__device__ __forceinline__ int32_t ld_acquire(const int32_t* p) {
+  int32_t v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_add(int32_t* p, int32_t v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+template <int TOK, int STAGES>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    fused_ffn_kernel(const __grid_constant__ CUtensorMap tmap_x,
+                     const __grid_constant__ CUtensorMap tmap_w1,
+                     const __grid_constant__ CUtensorMap tmap_h,
+                     const __grid_constant__ CUtensorMap tmap_w2, const FusedParams p) {
+  using C = Cfg<TOK, STAGES>;
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ FusedTable tt;
+  __shared__ uint32_t tmem_base_slot;
+
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  const uint32_t bar_base = base + STAGES * C::STAGE_BYTES;
+  auto full_bar = [&](int s) { return bar_base + 8u * s; };
+  auto empty_bar = [&](int s) { return bar_base + 8u * (STAGES + s); };
+  auto accf_bar = [&](int a) { return bar_base + 8u * (2 * STAGES + a); };
+  auto acce_bar = [&](int a) { return bar_base + 8u * (2 * STAGES + C::ACC + a); };
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+
+  if (threadIdx.x == 0) {
+    tt.n_groups = p.n_groups;
+    tt.fb1 = p.f / BM;
+    tt.fb2 = p.d / BM;
+    int32_t a1 = 0, a2 = 0;
+    for (int g = 0; g < p.n_groups; ++g) {
+      const int e = p.experts[g];
+      const int32_t r0 = p.offsets[e];
+      const int32_t rn = p.offsets[e + 1] - r0;
+      tt.row0[g] = r0;
+      tt.rows[g] = rn;
+      tt.slot[g] = p.slots[g];
+      tt.chunks[g] = (rn + TOK - 1) / TOK;
+      tt.start1[g] = a1;
+      tt.start2[g] = a2;
+      a1 += tt.chunks[g] * tt.fb1;
+      a2 += tt.chunks[g] * tt.fb2;
+    }
+    tt.start1[p.n_groups] = a1;
+    tt.start2[p.n_groups] = a2;
+    tt.total1 = a1;
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full_bar(s), 1);
+      mbar_init(empty_bar(s), 1);
+    }
+    for (int a = 0; a < C::ACC; ++a) {
+      mbar_init(accf_bar(a), 1);
+      mbar_init(acce_bar(a), 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&tmem_base_slot)),
+                 "n"(C::TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = tmem_base_slot;
+  const int32_t n_tiles = tt.total1 + tt.start2[tt.n_groups];
+  constexpr int32_t bk = ROW_BYTES / 2;  // bf16 elements per K-block
+
+  if (warp == 0) {
+    // ================= TMA producer =================
+    if (lane == 0) {
+      const uint64_t pol_w = policy_evict_first();
+      const uint64_t pol_x = policy_evict_last();
+      int stage = 0;
+      uint32_t phase = 0;
+      int32_t c1 = 0, c2 = 0, ready_g = -1;
+      for (int32_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+        const FTile tile = fdecode<TOK>(tt, t, c1, c2, p.d, p.f);
+        if (tile.phase == 1 && tile.g != ready_g) {
+          // every phase-1 tile of this group has published its H rows
+          const int32_t target = tt.chunks[tile.g] * tt.fb1;
+          uint32_t spins = 0;
+          while (ld_acquire(p.done + tile.g) < target) {
+            __nanosleep(64);
+            if (++spins == (1u << 28)) __trap();  // a broken invariant must not hang the GPU
+          }
+          fence_proxy_async_global();  // generic-proxy H stores -> async-proxy TMA reads
+          ready_g = tile.g;
+        }
+        const CUtensorMap* ta = tile.phase ? &tmap_h : &tmap_x;
+        const CUtensorMap* tb = tile.phase ? &tmap_w2 : &tmap_w1;
+        const int32_t kblocks = (tile.phase ? p.f : p.d) / bk;
+        const int boxes = (tile.ntok + TOK_BOX - 1) / TOK_BOX;
+        const uint32_t bytes = W_TILE + boxes * (TOK_BOX * ROW_BYTES);
+        for (int32_t kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(empty_bar(stage), phase ^ 1);
+          const uint32_t sW = base + stage * C::STAGE_BYTES;
+          const uint32_t sX = sW + W_TILE;
+          mbar_expect_tx(full_bar(stage), bytes);
+          tma_load_2d(sW, tb, full_bar(stage), kb * bk, tile.w_row0, pol_w);
+          for (int b = 0; b < boxes; ++b)
+            tma_load_2d(sX + b * (TOK_BOX * ROW_BYTES), ta, full_bar(stage), kb * bk,
+                        tile.row0 + b * TOK_BOX, pol_x);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ================= MMA issuer =================
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    int32_t c1 = 0, c2 = 0;
+    for (int32_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      const FTile tile = fdecode<TOK>(tt, t, c1, c2, p.d, p.f);
+      const uint32_t n_mma = uint32_t((tile.ntok + 15) & ~15);
+      const uint32_t idesc = make_idesc<false>(n_mma);
+      const int32_t kblocks = (tile.phase ? p.f : p.d) / bk;
+      mbar_wait(acce_bar(acc), acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + acc * C::ACC_COLS;
+      for (int32_t kb = 0; kb < kblocks; ++kb) {
+        mbar_wait(full_bar(stage), phase);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t sW = base + stage * C::STAGE_BYTES;
+          const uint64_t dw = sdesc(sW);
+          const uint64_t dx = sdesc(sW + W_TILE);
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            mma<false>(d_tmem, dw + 2 * kk, dx + 2 * kk, idesc, (kb | kk) != 0 ? 1u : 0u);
+          tc_commit(empty_bar(stage));
+        }
+        __syncwarp();
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+      if (lane == 0) tc_commit(accf_bar(acc));
+      __syncwarp();
+      if (++acc == C::ACC) { acc = 0; acc_phase ^= 1; }
+    }
+  } else {
+    // ================= epilogue (warps 2..5) =================
+    const int quarter = warp & 3;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    int32_t c1 = 0, c2 = 0;
+    for (int32_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      const FTile tile = fdecode<TOK>(tt, t, c1, c2, p.d, p.f);
+      mbar_wait(accf_bar(acc), acc_phase);
+      tc_fence_after();
+      const int feat = tile.f0 + quarter * 32 + lane;
+      const uint32_t taddr = tmem_base + (uint32_t(quarter * 32) << 16) + acc * C::ACC_COLS;
+      const int chunks = (tile.ntok + 31) / 32;
+      for (int cc = 0; cc < chunks; ++cc) {
+        uint32_t r[32];
+        tmem_ld32(taddr + cc * 32, r);
+        const int nvalid = min(32, tile.ntok - cc * 32);
+        const int64_t row = int64_t(tile.row0) + cc * 32;
+        if (tile.phase == 0) {
+          __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(p.h) + row * p.f + feat;
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (i < nvalid)
+              dst[int64_t(i) * p.f] = __float2bfloat16_rn(gelu_erf(__uint_as_float(r[i])));
+        } else if (p.perm == nullptr) {
+          __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(p.y) + row * p.d + feat;
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (i < nvalid) dst[int64_t(i) * p.d] = __float2bfloat16_rn(__uint_as_float(r[i]));
+        } else {
+          // fused top-1 combine: token of each row and its gate weight, broadcast
+          const int tok_l = lane < nvalid ? p.perm[row + lane] : 0;
+          const float w_l = lane < nvalid ? p.topk_w[tok_l] : 0.0f;
+          __nv_bfloat16* yb = reinterpret_cast<__nv_bfloat16*>(p.y);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const int tok = __shfl_sync(0xffffffffu, tok_l, i);
+            const float w = __shfl_sync(0xffffffffu, w_l, i);
+            if (i < nvalid) {
+              const float yb16 = __bfloat162float(__float2bfloat16_rn(__uint_as_float(r[i])));
+              yb[int64_t(tok) * p.d + feat] = __float2bfloat16_rn(fmaf(w, yb16, 0.0f));
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      if (tile.phase == 0) {
+        // all four epilogue warps stored this tile's H rows -> publish
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (warp == 2 && lane == 0) {
+          __threadfence();
+          fence_proxy_async_global();
+          red_release_add(p.done + tile.g, 1);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(acce_bar(acc));
+      if (++acc == C::ACC) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "n"(C::TMEM_COLS)
+                 : "memory");
+  }
+}
+
+template <int TOK, int STAGES>
+void fused_launch(const FusedFfnArgs& a, cudaStream_t stream) {
+  using C = Cfg<TOK, STAGES>;
+  auto kern = fused_ffn_kernel<TOK, STAGES>;
+  static bool configured = false;
+  if (!configured) {
+    INFMOE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(C::SMEM_BYTES)));
+    configured = true;
+  }
+  const uint64_t rows = uint64_t(std::max<int64_t>(a.rows, 1));
+  const CUtensorMap tx = make_tmap(a.x, rows, uint64_t(a.d_model), false, TOK_BOX);
+  const CUtensorMap tw1 = make_tmap(a.w_in, uint64_t(a.n_slots) * a.d_ff, uint64_t(a.d_model),
+                                    false, BM);
+  const CUtensorMap th = make_tmap(a.h, rows, uint64_t(a.d_ff), false, TOK_BOX);
+  const CUtensorMap tw2 = make_tmap(a.w_out, uint64_t(a.n_slots) * a.d_model, uint64_t(a.d_ff),
+                                    false, BM);
+  FusedParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.d = a.d_model;
+  p.f = a.d_ff;
+  p.n_groups = a.n_groups;
+  p.offsets = a.offsets;
+  p.h = a.h;
+  p.y = a.y;
+  p.done = a.done;
+  p.perm = a.perm;
+  p.topk_w = a.topk_w;
+  for (int g = 0; g < a.n_groups; ++g) {
+    p.experts[g] = a.experts[g];
+    p.slots[g] = a.slots[g];
+  }
+  INFMOE_CUDA(cudaMemsetAsync(a.done, 0, sizeof(int32_t) * size_t(a.n_groups), stream));
+  int grid = device_sm_count();
+  if (a.max_ctas > 0) grid = std::min(grid, a.max_ctas);
+  kern<<<grid, NUM_THREADS, C::SMEM_BYTES, stream>>>(tx, tw1, th, tw2, p);
+  INFMOE_LAUNCH_CHECK();
+}
+
 }  // namespace gemm
 
 void launch_grouped_gemm(const GroupedGemmArgs& a, cudaStream_t stream) {
@@ -478,6 +804,20 @@ void launch_grouped_gemm(const GroupedGemmArgs& a, cudaStream_t stream) {
     if (a.gelu) gemm::dispatch_tok<false, true>(a, stream);
     else gemm::dispatch_tok<false, false>(a, stream);
   }
+}
+
+void launch_expert_ffn_fused(const FusedFfnArgs& a, cudaStream_t stream) {
+  require(a.dtype == kDtypeBf16, "fused expert FFN: bf16 only (f32 uses the two-launch path)");
+  require(a.n_groups >= 1 && a.n_groups <= kMaxGroups, "fused expert FFN: n_groups out of range");
+  require(a.d_model % gemm::BM == 0 && a.d_ff % gemm::BM == 0,
+          "fused expert FFN: d_model and d_ff must be multiples of 128");
+  require(a.x && a.w_in && a.w_out && a.h && a.y && a.offsets && a.done,
+          "fused expert FFN: NULL pointer");
+  require((a.perm == nullptr) == (a.topk_w == nullptr), "fused expert FFN: perm needs topk_w");
+  const int hint = a.max_rows_hint;
+  if (hint > 0 && hint <= 128) gemm::fused_launch<128, 6>(a, stream);
+  else if (hint > 192) gemm::fused_launch<256, 4>(a, stream);
+  else gemm::fused_launch<192, 5>(a, stream);
 }
 
 }  // namespace infmoe

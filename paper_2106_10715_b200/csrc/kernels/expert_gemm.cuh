@@ -32,4 +32,34 @@ struct GroupedGemmArgs {
 
 void launch_grouped_gemm(const GroupedGemmArgs& args, cudaStream_t stream);
 
+// Both projections of the expert FFN in ONE persistent launch:
+//   phase 1  h[rows(g)] = GeLU(x[rows(g)] . w_in[slot(g)]^T)     (N = d_ff,   K = d_model)
+//   phase 2  y[rows(g)] = h[rows(g)] . w_out[slot(g)]^T           (N = d_model, K = d_ff)
+// A phase-2 tile of group g starts as soon as every phase-1 tile of g has
+// stored its H rows (per-group completion counters, release/acquire), so the
+// wave tail of phase 1 and the launch gap disappear.  With `perm` and `topk_w`
+// (top-1 only) the phase-2 epilogue also performs the combine:
+//   y_out[perm[r]] = bf16(fmaf(topk_w[perm[r]], bf16(acc_r), 0))   (== N5 combine)
+struct FusedFfnArgs {
+  const void* x;        // [rows, d_model]
+  int64_t rows;
+  const void* w_in;     // [n_slots, d_ff, d_model]
+  const void* w_out;    // [n_slots, d_model, d_ff]
+  int32_t n_slots;
+  int32_t d_model, d_ff;
+  int32_t dtype;        // bf16 only (kind::f16)
+  const int32_t* offsets;
+  int32_t n_groups;
+  int32_t experts[kMaxGroups];
+  int32_t slots[kMaxGroups];
+  void* h;              // [rows, d_ff] scratch
+  void* y;              // [rows, d_model] (or [N, d_model] when the combine is fused)
+  const int32_t* perm;  // fused top-1 combine: row -> token, or NULL
+  const float* topk_w;  // weight per token (with perm)
+  int32_t* done;        // >= n_groups counters in device memory (zeroed by the launcher)
+  int32_t max_ctas;
+  int32_t max_rows_hint;
+};
+void launch_expert_ffn_fused(const FusedFfnArgs& args, cudaStream_t stream);
+
 }  // namespace infmoe

@@ -268,18 +268,15 @@ __global__ void __launch_bounds__(kLshWarps * 32) gate_lsh_kernel(
     int32_t* __restrict__ counts) {
   constexpr int NT = kLshWarps * 32;
   constexpr int V = 16 / sizeof(T);
-  constexpr int XROW = kLshChunk + V;  // raw elements per staged row (+16 B)
-  constexpr int DROW = kLshChunk + 2;  // doubles per converted / hyperplane row (+16 B)
+  constexpr int XROW = kLshChunk + V;  // elements (+16 B)
+  constexpr int PROW = kLshChunk + 2;  // doubles (+16 B)
   extern __shared__ __align__(16) uint8_t lsh_smem[];
   const int G = 32 / bits;
   const int TB = kLshWarps * G;
   const size_t xbytes = size_t(TB) * XROW * sizeof(T);
-  const size_t stage = xbytes + size_t(bits) * DROW * sizeof(double);
+  const size_t stage = xbytes + size_t(bits) * PROW * sizeof(double);
   auto xs = [&](int st) { return reinterpret_cast<T*>(lsh_smem + st * stage); };
   auto ps = [&](int st) { return reinterpret_cast<double*>(lsh_smem + st * stage + xbytes); };
-  // fp64 copy of the current chunk's token rows: converted once per block, not
-  // once per hash-bit lane (F2F.F64 is a quarter-rate instruction)
-  double* xd = reinterpret_cast<double*>(lsh_smem + kGateStages * stage);  // [TB][DROW]
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int sub = lane / bits, j = lane % bits;
   const int local = warp * G + (sub < G ? sub : 0);
@@ -291,17 +288,17 @@ __global__ void __launch_bounds__(kLshWarps * 32) gate_lsh_kernel(
   auto issue = [&](int ch) {
     if (ch < nch) {
       const int c0 = ch * kLshChunk;
-      T* xdst = xs(ch % kGateStages);
+      T* xd = xs(ch % kGateStages);
       double* pd = ps(ch % kGateStages);
       for (int i = threadIdx.x; i < TB * (kLshChunk / V); i += NT) {
         const int t = i / (kLshChunk / V), c = (i % (kLshChunk / V)) * V;
         const bool ok = tok0 + t < N && c0 + c < d;
-        cp_async16(xdst + t * XROW + c, ok ? x + size_t(tok0 + t) * d + c0 + c : x, ok);
+        cp_async16(xd + t * XROW + c, ok ? x + size_t(tok0 + t) * d + c0 + c : x, ok);
       }
       for (int i = threadIdx.x; i < bits * (kLshChunk / 2); i += NT) {
         const int b = i / (kLshChunk / 2), c = (i % (kLshChunk / 2)) * 2;
         const bool ok = c0 + c < d;
-        cp_async16(pd + b * DROW + c, ok ? proj + size_t(b) * d + c0 + c : proj, ok);
+        cp_async16(pd + b * PROW + c, ok ? proj + size_t(b) * d + c0 + c : proj, ok);
       }
     }
     cp_async_commit();
@@ -311,42 +308,35 @@ __global__ void __launch_bounds__(kLshWarps * 32) gate_lsh_kernel(
   for (int ch = 0; ch < kGateStages - 1; ++ch) issue(ch);
   for (int ch = 0; ch < nch; ++ch) {
     cp_async_wait<kGateStages - 2>();
-    __syncthreads();  // chunk ch landed everywhere; xd and slot ch-1 are free
+    __syncthreads();
     issue(ch + kGateStages - 1);
     const int cn = min(kLshChunk, d - ch * kLshChunk);  // a multiple of 8
-    {  // widen the chunk's token rows to fp64 once
-      const T* xr = xs(ch % kGateStages);
-      for (int i = threadIdx.x; i < TB * (cn / 2); i += NT) {
-        const int t = i / (cn / 2), c = (i % (cn / 2)) * 2;
-        *reinterpret_cast<double2*>(xd + t * DROW + c) =
-            make_double2(double(load_as_f32(xr + t * XROW, c)),
-                         double(load_as_f32(xr + t * XROW, c + 1)));
-      }
-    }
-    __syncthreads();
     if (active) {
-      const double2* xrow = reinterpret_cast<const double2*>(xd + local * DROW);
-      const double2* prow = reinterpret_cast<const double2*>(ps(ch % kGateStages) + j * DROW);
-      // software pipeline over 8-column groups: the next group's operands are
-      // in flight while this group's dependent dadd chain retires
-      double2 xa[4], pa[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) { xa[i] = xrow[i]; pa[i] = prow[i]; }
+      const T* xrow = xs(ch % kGateStages) + local * XROW;
+      const double2* prow = reinterpret_cast<const double2*>(ps(ch % kGateStages) + j * PROW);
       for (int c = 0; c < cn; c += 8) {
-        const int nx = (c + 8 < cn ? c + 8 : c) / 2;
-        double2 xb[4], pb[4];
+        const uint4 raw = *reinterpret_cast<const uint4*>(xrow + c);
+        double xv[8];
+        if constexpr (sizeof(T) == 2) {
+          const T* e = reinterpret_cast<const T*>(&raw);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) { xb[i] = xrow[nx + i]; pb[i] = prow[nx + i]; }
+          for (int i = 0; i < 8; ++i) xv[i] = double(load_as_f32(e, i));
+        } else {
+          const uint4 raw2 = *reinterpret_cast<const uint4*>(xrow + c + 4);
+          const float* e = reinterpret_cast<const float*>(&raw);
+          const float* e2 = reinterpret_cast<const float*>(&raw2);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) { xv[i] = double(e[i]); xv[4 + i] = double(e2[i]); }
+        }
         double prod[8];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          prod[2 * i] = __dmul_rn(xa[i].x, pa[i].x);
-          prod[2 * i + 1] = __dmul_rn(xa[i].y, pa[i].y);
+          const double2 pp = prow[c / 2 + i];
+          prod[2 * i] = __dmul_rn(xv[2 * i], pp.x);
+          prod[2 * i + 1] = __dmul_rn(xv[2 * i + 1], pp.y);
         }
 #pragma unroll
         for (int i = 0; i < 8; ++i) dot = __dadd_rn(dot, prod[i]);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) { xa[i] = xb[i]; pa[i] = pb[i]; }
       }
     }
   }
@@ -375,6 +365,7 @@ void softmax_go(const void* x, int64_t N, int d, const float* wg, const float* b
   kern<<<unsigned((N + C::TB - 1) / C::TB), kSoftWarps * 32, C::SMEM, s>>>(
       reinterpret_cast<const T*>(x), N, d, wg, bias, E, k, idx, w, counts);
 }
+
 
 template <typename T, int EQ>
 void softmax_launch(const void* x, int64_t N, int d, const float* wg, const float* bias, int E,
@@ -430,8 +421,7 @@ void launch_gate_lsh(const void* x, int dtype, int64_t N, int d, const double* p
   const int TB = kLshWarps * G;
   const int64_t blocks = (N + TB - 1) / TB;
   const size_t smem = kGateStages * (size_t(TB) * (kLshChunk + 16 / esz) * esz +
-                                     size_t(bits) * (kLshChunk + 2) * sizeof(double)) +
-                      size_t(TB) * (kLshChunk + 2) * sizeof(double);
+                                     size_t(bits) * (kLshChunk + 2) * sizeof(double));
   if (dtype == kDtypeBf16) {
     auto kern = gate_lsh_kernel<__nv_bfloat16>;
     static size_t configured = 0;  // opt in to >48 KiB dynamic smem once per size

@@ -112,6 +112,46 @@ int infmoe_expert_ffn(const void* x_perm, int64_t n_rows, int32_t d_model, int32
   });
 }
 
+int infmoe_expert_ffn_fused(const void* x_perm, int64_t n_rows, int32_t d_model, int32_t d_ff,
+                            const int32_t* offsets, int32_t E, const void* w_in,
+                            const void* w_out, int32_t n_slots, const int32_t* experts,
+                            const int32_t* slots, int32_t n_groups, void* h, void* y,
+                            const int32_t* perm, const float* topk_w, int32_t* done,
+                            void* stream) {
+  return guarded([&] {
+    FusedFfnArgs a;
+    std::memset(&a, 0, sizeof(a));
+    if (!experts) {
+      n_groups = E;
+      require(n_slots >= E, "expert_ffn_fused: n_slots < E with experts == NULL");
+    }
+    require(n_groups >= 1 && n_groups <= kMaxGroups, "expert_ffn_fused: n_groups out of range");
+    for (int i = 0; i < n_groups; ++i) {
+      a.experts[i] = experts ? experts[i] : i;
+      a.slots[i] = experts ? slots[i] : i;
+      require(a.experts[i] >= 0 && a.experts[i] < E, "expert_ffn_fused: expert id out of range");
+      require(a.slots[i] >= 0 && a.slots[i] < n_slots, "expert_ffn_fused: slot out of range");
+    }
+    a.x = x_perm;
+    a.rows = n_rows;
+    a.w_in = w_in;
+    a.w_out = w_out;
+    a.n_slots = n_slots;
+    a.d_model = d_model;
+    a.d_ff = d_ff;
+    a.dtype = INFMOE_DTYPE_BF16;
+    a.offsets = offsets;
+    a.n_groups = n_groups;
+    a.h = h;
+    a.y = y;
+    a.perm = perm;
+    a.topk_w = topk_w;
+    a.done = done;
+    if (n_rows == 0) return;
+    launch_expert_ffn_fused(a, as_stream(stream));
+  });
+}
+
 int infmoe_scatter_rows(const void* src, int32_t dtype, int64_t rows, int32_t d,
                         const int32_t* index, void* dst, void* stream) {
   return guarded([&] {

@@ -84,6 +84,7 @@ Layer::Layer(const infmoe_layer_desc& d) : desc(d) {
   perm = dalloc<int32_t>(size_t(A), owned);
   inv = dalloc<int32_t>(size_t(A), owned);
   dws = dalloc<uint8_t>(dispatch_workspace_bytes(A, d.n_experts), owned);
+  done_ctr = dalloc<int32_t>(size_t(d.n_experts), owned);
   xp = dalloc<uint8_t>(size_t(A) * d.d_model * esz, owned);
   yp = dalloc<uint8_t>(size_t(A) * d.d_model * esz, owned);
   // the exchange path runs whenever a communicator is given (ep_size == 1 then
@@ -186,6 +187,36 @@ void Layer::route(const void* x, int64_t N, cudaStream_t s) {
 void Layer::ffn(const Rows& r, const int32_t* experts, const int32_t* slots, int n,
                 const void* w_in, const void* w_out, int n_w_slots, int max_ctas, int rows_hint,
                 cudaStream_t s) {
+  if (desc.dtype == INFMOE_DTYPE_BF16) {  // both projections in one persistent launch
+    FusedFfnArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.x = r.a;
+    a.rows = r.rows;
+    a.w_in = w_in;
+    a.w_out = w_out;
+    a.n_slots = n_w_slots;
+    a.d_model = desc.d_model;
+    a.d_ff = desc.d_ff;
+    a.dtype = desc.dtype;
+    a.offsets = r.offsets;
+    a.n_groups = n;
+    for (int i = 0; i < n; ++i) {
+      a.experts[i] = experts[i];
+      a.slots[i] = slots[i];
+    }
+    a.h = r.h;
+    a.y = r.y;
+    if (fused_out) {  // top-1, no exchange: the GEMM2 epilogue writes y directly
+      a.y = fused_out;
+      a.perm = perm;
+      a.topk_w = wts;
+    }
+    a.done = done_ctr;
+    a.max_ctas = max_ctas;
+    a.max_rows_hint = rows_hint;
+    launch_expert_ffn_fused(a, s);
+    return;
+  }
   GroupedGemmArgs g;
   std::memset(&g, 0, sizeof(g));
   g.a = r.a;
@@ -272,7 +303,7 @@ void Layer::compute_offloaded(const Rows& r, bool timed, infmoe_forward_out* out
     const int32_t ex = e, sl = slot;
     const int64_t n_e = int64_t(r.counts[e]);
     if (n_e > 0) {
-      const int tiles = int((n_e + 127) / 128) * (desc.d_ff / 128);
+      const int tiles = int((n_e + 127) / 128) * (std::max(desc.d_ff, desc.d_model) / 128);
       ffn(r, &ex, &sl, 1, slot_in, slot_out, n_slots, tiles, int(n_e), s);
     }
     if (timed) INFMOE_CUDA(cudaEventRecord(t_comp1[size_t(j)], s));
@@ -386,11 +417,13 @@ void Layer::forward(const void* x, int64_t N, void* y, infmoe_forward_out* out, 
     r = Rows{loc_x, plan_dev, plan.n_recv, loc_h, loc_y, local_counts.data()};
   }
 
+  // top-1 without an exchange: the combine is fused into the GEMM2 epilogue
+  fused_out = (k == 1 && !use_ep && desc.dtype == INFMOE_DTYPE_BF16) ? y : nullptr;
   if (offloaded) compute_offloaded(r, timed, out, s);
   else compute_resident(r, timed, s);
 
   if (use_ep) ep_exchange_back(s);
-  launch_combine(yp, desc.dtype, inv, wts, N, k, desc.d_model, y, s);
+  if (!fused_out) launch_combine(yp, desc.dtype, inv, wts, N, k, desc.d_model, y, s);
 
   if (!out) return;
   const bool need_sync = timed || ((out->counts || out->local_rows) && !offloaded && !use_ep);

@@ -62,6 +62,8 @@ struct Layer {
   float* gate_w = nullptr;
   float* gate_b = nullptr;
   int32_t* counts_host = nullptr;  // pinned [E + ep_size * n_local]
+  int32_t* done_ctr = nullptr;     // fused FFN per-group completion counters
+  void* fused_out = nullptr;       // y when the combine is fused into the GEMM2 epilogue
   // offload executor
   size_t expert_in_bytes = 0;  // = bytes of W_in = bytes of W_out of one expert
   int n_slots = 0;

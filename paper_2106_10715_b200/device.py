@@ -132,6 +132,35 @@ def expert_ffn(x_perm, offsets, w_in, w_out, experts: Optional[Sequence[int]] = 
     return h, y_perm
 
 
+def expert_ffn_fused(x_perm, offsets, w_in, w_out, experts=None, slots=None, perm=None,
+                     topk_w=None, n_tokens: Optional[int] = None):
+    """Both projections in one persistent launch.  With perm/topk_w (top-1) the
+    combine is fused and the result is y [n_tokens, d]; else y_perm [rows, d]."""
+    torch = _torch()
+    _need_cuda(x_perm, offsets, w_in, w_out)
+    R, d = x_perm.shape
+    n_slots, f, _ = w_in.shape
+    E = offsets.numel() - 1
+    h = torch.empty((R, f), dtype=x_perm.dtype, device=x_perm.device)
+    rows_out = n_tokens if perm is not None else R
+    y = torch.empty((rows_out, d), dtype=x_perm.dtype, device=x_perm.device)
+    done = torch.empty(max(E, 1), dtype=torch.int32, device=x_perm.device)
+    if experts is None:
+        ex = sl = None
+        n = E
+    else:
+        ex = np.ascontiguousarray(np.asarray(experts, dtype=np.int32))
+        sl = np.ascontiguousarray(np.asarray(slots if slots is not None else experts,
+                                             dtype=np.int32))
+        n = len(ex)
+    _check(_lib.infmoe_expert_ffn_fused(
+        _p(x_perm), R, d, f, _p(offsets), E, _p(w_in), _p(w_out), n_slots,
+        None if ex is None else ex.ctypes.data_as(C.c_void_p),
+        None if sl is None else sl.ctypes.data_as(C.c_void_p), n, _p(h), _p(y), _p(perm),
+        _p(topk_w), _p(done), _stream_ptr()))
+    return h, y
+
+
 def scatter_rows(src, index, n_out: int, out=None):
     """out[index[p]] = src[p]."""
     torch = _torch()
@@ -193,11 +222,17 @@ class MoELayer:
         _check(_lib.infmoe_layer_set_host_weights(self._h, C.c_void_p(w_in.data_ptr()),
                                                   C.c_void_p(w_out.data_ptr())))
 
-    def forward(self, x, y=None, *, want_timeline: bool = False):
+    def forward(self, x, y=None, *, want_timeline: bool = False, want_info: bool = True):
+        """Run the layer on x [N, d_model] (device).  want_info=False passes no
+        output struct: a resident layer then never synchronises with the host
+        (and can be captured in a CUDA graph)."""
         torch = _torch()
         N = x.shape[0]
         if y is None:
             y = torch.empty_like(x)
+        if not want_info and not want_timeline:
+            _check(_lib.infmoe_layer_forward(self._h, _p(x), N, _p(y), None, _stream_ptr()))
+            return y, None
         E, El = self.n_experts, self.n_local
         counts = np.zeros(E, dtype=np.int32)
         order = np.zeros(El, dtype=np.int32)

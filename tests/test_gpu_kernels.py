@@ -230,3 +230,31 @@ def test_combine_bitexact(cuda, k, dtype):
                               f32_to_bf16_bits(ref))
     else:
         assert np.array_equal(y.cpu().numpy().view(np.uint32), ref.view(np.uint32))
+
+
+@pytest.mark.parametrize("counts", [[128, 0, 1, 300, 127, 129, 256, 513], [150] * 32])
+def test_fused_ffn_equals_two_launch_path(cuda, counts):
+    """The one-launch FFN (phase-2 tiles gated on per-expert completion
+    counters) is bit-identical to the two-launch path, and its fused top-1
+    combine is bit-identical to the separate combine kernel."""
+    E, d, f = len(counts), 256, 512
+    R = int(sum(counts))
+    offs = torch.tensor(np.concatenate([[0], np.cumsum(counts)]), dtype=torch.int32, device=cuda)
+    g = torch.Generator(device="cpu").manual_seed(3)
+    x = torch.randn(R, d, generator=g).to(torch.bfloat16).to(cuda)
+    wi = (torch.randn(E, f, d, generator=g) / d ** 0.5).to(torch.bfloat16).to(cuda)
+    wo = (torch.randn(E, d, f, generator=g) / f ** 0.5).to(torch.bfloat16).to(cuda)
+    h2, y2 = dv.expert_ffn(x, offs, wi, wo)
+    h1, y1 = dv.expert_ffn_fused(x, offs, wi, wo)
+    torch.cuda.synchronize()
+    assert torch.equal(h1.view(torch.int16), h2.view(torch.int16))
+    assert torch.equal(y1.view(torch.int16), y2.view(torch.int16))
+    # fused combine: rows are a permutation of R tokens (top-1)
+    perm = torch.randperm(R, generator=g).to(torch.int32).to(cuda)
+    inv = torch.empty_like(perm)
+    inv[perm.long()] = torch.arange(R, dtype=torch.int32, device=cuda)
+    w = torch.rand(R, generator=g).to(cuda)
+    _, yc = dv.expert_ffn_fused(x, offs, wi, wo, perm=perm, topk_w=w, n_tokens=R)
+    ref = dv.combine(y2, inv, w, R, 1)
+    torch.cuda.synchronize()
+    assert torch.equal(yc.view(torch.int16), ref.view(torch.int16))

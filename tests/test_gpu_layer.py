@@ -180,3 +180,34 @@ def test_offloaded_skip_empty_experts_and_measured_timeline(cuda):
     trace.write(info_f["events"], "/tmp/infmoe_layer_timeline")
     for lay in (res, full, skip):
         lay.close()
+
+
+def test_resident_stack_cuda_graph_replay_matches_eager(cuda):
+    """A resident layer never synchronises with the host, so a multi-layer
+    stack is capturable as one CUDA graph; replay must equal eager bit for bit."""
+    N, d, f, E, L = 512, 256, 384, 8, 3
+    (_, _, _), (x, wi, wo) = _setup(cuda, N, d, f, E, seed=31)
+    wi, wo = wi.to(cuda), wo.to(cuda)
+    layers = [dv.MoELayer(d, f, E, 1, wi, wo, gate="lsh", lsh_seed=40 + l, lsh_bits=3,
+                          max_tokens=N) for l in range(L)]
+    bufs = [torch.empty_like(x) for _ in range(2)]
+
+    def run():
+        cur = x
+        for i, lay in enumerate(layers):
+            lay.forward(cur, bufs[i % 2], want_info=False)
+            cur = bufs[i % 2]
+        return cur
+
+    eager = run().clone()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        out = run()
+    bufs[0].zero_()
+    bufs[1].zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out.view(torch.int16), eager.view(torch.int16))
+    for lay in layers:
+        lay.close()

@@ -35,6 +35,32 @@ def ev():
     return torch.cuda.Event(enable_timing=True)
 
 
+def step_fused():
+    """gate -> dispatch -> gather -> one-launch FFN with the top-1 combine fused"""
+    e = [ev() for _ in range(5)]
+    torch.cuda._sleep(20_000_000)
+    e[0].record()
+    if a.gate == "lsh":
+        _, idx, w, cnt = dv.gate_lsh(x, proj, E)
+    else:
+        idx, w, cnt = dv.gate_softmax_topk(x, gw, k)
+    off, perm, inv = dv.dispatch(idx, E)
+    e[1].record()
+    xp = dv.gather_rows(x, perm, k)
+    e[2].record()
+    if k == 1:
+        dv.expert_ffn_fused(xp, off, wi, wo, perm=perm, topk_w=w.reshape(-1), n_tokens=N)
+        e[3].record()
+        e[4].record()
+    else:
+        _, yp = dv.expert_ffn_fused(xp, off, wi, wo)
+        e[3].record()
+        dv.combine(yp, inv, w, N, k)
+        e[4].record()
+    torch.cuda.synchronize()
+    return [e[i].elapsed_time(e[i + 1]) for i in range(4)]
+
+
 def step():
     e = [ev() for _ in range(7)]
     torch.cuda._sleep(20_000_000)  # ~10 ms: the host queues every launch before e[0] fires
@@ -70,4 +96,15 @@ out = {n: round(v * 1e3, 1) for n, v in zip(names, acc)}
 out["total_us"] = round(sum(acc) * 1e3, 1)
 out["ffn_GBps"] = round((wbytes + act) / (acc[3] * 1e-3) / 1e9, 1)
 out["counts_minmax"] = [int(cnt.min()), int(cnt.max())]
+fz = [0.0] * 4
+for i in range(a.iters + 3):
+    flush.zero_()
+    t = step_fused()
+    if i >= 3:
+        fz = [p + q for p, q in zip(fz, t)]
+fz = [v / a.iters for v in fz]
+out["fused"] = {"route_us": round(fz[0] * 1e3, 1), "gather_us": round(fz[1] * 1e3, 1),
+                "ffn_fused_us": round(fz[2] * 1e3, 1), "combine_us": round(fz[3] * 1e3, 1),
+                "total_us": round(sum(fz) * 1e3, 1),
+                "ffn_GBps": round((wbytes + act) / (fz[2] * 1e-3) / 1e9, 1)}
 print(json.dumps(out))
