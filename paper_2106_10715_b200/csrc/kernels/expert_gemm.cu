@@ -781,11 +781,13 @@ void fused_launch(const FusedFfnArgs& a, cudaStream_t stream) {
     p.experts[g] = a.experts[g];
     p.slots[g] = a.slots[g];
   }
-  INFMOE_CUDA(cudaMemsetAsync(a.done, 0, sizeof(int32_t) * size_t(a.n_groups), stream));
   int grid = device_sm_count();
   if (a.max_ctas > 0) grid = std::min(grid, a.max_ctas);
+  if (a.ev_begin) INFMOE_CUDA(cudaEventRecord(a.ev_begin, stream));
+  INFMOE_CUDA(cudaMemsetAsync(a.done, 0, sizeof(int32_t) * size_t(a.n_groups), stream));
   kern<<<grid, NUM_THREADS, C::SMEM_BYTES, stream>>>(tx, tw1, th, tw2, p);
   INFMOE_LAUNCH_CHECK();
+  if (a.ev_end) INFMOE_CUDA(cudaEventRecord(a.ev_end, stream));
 }
 
 }  // namespace gemm

@@ -59,6 +59,9 @@ struct FusedFfnArgs {
   int32_t* done;        // >= n_groups counters in device memory (zeroed by the launcher)
   int32_t max_ctas;
   int32_t max_rows_hint;
+  // optional events recorded right around the kernel, after all host-side
+  // preparation (tensor-map encoding), so a timed interval holds GPU work only
+  cudaEvent_t ev_begin, ev_end;
 };
 void launch_expert_ffn_fused(const FusedFfnArgs& args, cudaStream_t stream);
 

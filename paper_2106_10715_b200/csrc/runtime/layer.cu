@@ -186,7 +186,7 @@ void Layer::route(const void* x, int64_t N, cudaStream_t s) {
 
 void Layer::ffn(const Rows& r, const int32_t* experts, const int32_t* slots, int n,
                 const void* w_in, const void* w_out, int n_w_slots, int max_ctas, int rows_hint,
-                cudaStream_t s) {
+                cudaStream_t s, cudaEvent_t ev_begin, cudaEvent_t ev_end) {
   if (desc.dtype == INFMOE_DTYPE_BF16) {  // both projections in one persistent launch
     FusedFfnArgs a;
     std::memset(&a, 0, sizeof(a));
@@ -214,9 +214,12 @@ void Layer::ffn(const Rows& r, const int32_t* experts, const int32_t* slots, int
     a.done = done_ctr;
     a.max_ctas = max_ctas;
     a.max_rows_hint = rows_hint;
+    a.ev_begin = ev_begin;
+    a.ev_end = ev_end;
     launch_expert_ffn_fused(a, s);
     return;
   }
+  if (ev_begin) INFMOE_CUDA(cudaEventRecord(ev_begin, s));
   GroupedGemmArgs g;
   std::memset(&g, 0, sizeof(g));
   g.a = r.a;
@@ -244,6 +247,7 @@ void Layer::ffn(const Rows& r, const int32_t* experts, const int32_t* slots, int
   g.out = r.y;
   g.gelu = 0;
   launch_grouped_gemm(g, s);
+  if (ev_end) INFMOE_CUDA(cudaEventRecord(ev_end, s));
 }
 
 // one grouped launch per projection over all local experts; no host round trip
@@ -252,10 +256,13 @@ void Layer::compute_resident(const Rows& r, bool timed, cudaStream_t s) {
   for (int e = 0; e < n_local; ++e) all[size_t(e)] = e;
   int hint = 0;
   if (r.counts) hint = *std::max_element(r.counts, r.counts + n_local);
-  if (timed) INFMOE_CUDA(cudaEventRecord(t_comp0[0], s));
-  if (r.rows > 0)
-    ffn(r, all.data(), all.data(), n_local, desc.w_in, desc.w_out, n_local, 0, hint, s);
-  if (timed) INFMOE_CUDA(cudaEventRecord(t_comp1[0], s));
+  cudaEvent_t e0 = timed ? t_comp0[0] : nullptr, e1 = timed ? t_comp1[0] : nullptr;
+  if (r.rows > 0) {
+    ffn(r, all.data(), all.data(), n_local, desc.w_in, desc.w_out, n_local, 0, hint, s, e0, e1);
+  } else if (timed) {
+    INFMOE_CUDA(cudaEventRecord(e0, s));
+    INFMOE_CUDA(cudaEventRecord(e1, s));
+  }
 }
 
 void Layer::compute_offloaded(const Rows& r, bool timed, infmoe_forward_out* out,
@@ -299,14 +306,17 @@ void Layer::compute_offloaded(const Rows& r, bool timed, infmoe_forward_out* out
     INFMOE_CUDA(cudaEventRecord(load_done[size_t(j)], copy_stream));
 
     INFMOE_CUDA(cudaStreamWaitEvent(s, load_done[size_t(j)], 0));
-    if (timed) INFMOE_CUDA(cudaEventRecord(t_comp0[size_t(j)], s));
     const int32_t ex = e, sl = slot;
     const int64_t n_e = int64_t(r.counts[e]);
+    cudaEvent_t e0 = timed ? t_comp0[size_t(j)] : nullptr;
+    cudaEvent_t e1 = timed ? t_comp1[size_t(j)] : nullptr;
     if (n_e > 0) {
       const int tiles = int((n_e + 127) / 128) * (std::max(desc.d_ff, desc.d_model) / 128);
-      ffn(r, &ex, &sl, 1, slot_in, slot_out, n_slots, tiles, int(n_e), s);
+      ffn(r, &ex, &sl, 1, slot_in, slot_out, n_slots, tiles, int(n_e), s, e0, e1);
+    } else if (timed) {
+      INFMOE_CUDA(cudaEventRecord(e0, s));
+      INFMOE_CUDA(cudaEventRecord(e1, s));
     }
-    if (timed) INFMOE_CUDA(cudaEventRecord(t_comp1[size_t(j)], s));
     INFMOE_CUDA(cudaEventRecord(compute_done[size_t(j)], s));
   }
   if (out) {

@@ -35,7 +35,8 @@ struct Layer {
   void compute_resident(const Rows& r, bool timed, cudaStream_t s);  // grouped GEMM pair
   void compute_offloaded(const Rows& r, bool timed, infmoe_forward_out* out, cudaStream_t s);
   void ffn(const Rows& r, const int32_t* experts, const int32_t* slots, int n, const void* w_in,
-           const void* w_out, int n_w_slots, int max_ctas, int rows_hint, cudaStream_t s);
+           const void* w_out, int n_w_slots, int max_ctas, int rows_hint, cudaStream_t s,
+           cudaEvent_t ev_begin = nullptr, cudaEvent_t ev_end = nullptr);
   void ep_exchange_out(int64_t N, cudaStream_t s);   // dispatch all-to-allv
   void ep_exchange_back(cudaStream_t s);             // combine all-to-allv
   template <class T>
