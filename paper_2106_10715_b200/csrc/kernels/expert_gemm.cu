@@ -23,6 +23,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -790,6 +791,356 @@ void fused_launch(const FusedFfnArgs& a, cudaStream_t stream) {
   if (a.ev_end) INFMOE_CUDA(cudaEventRecord(a.ev_end, stream));
 }
 
+
+// ============================================================ 2-SM variant
+// Same two-phase schedule, but a tile is owned by a CTA PAIR (cluster of 2 on
+// one TPC) issuing cta_group::2 MMAs with M = 256: each CTA streams its 128
+// weight rows and HALF of the token rows, the leader (rank 0) issues the MMAs
+// for both, and each CTA's TMEM receives its 128 x N accumulator.  Halving the
+// token bytes per SM leaves room for a deeper weight ring (7 stages at
+// TOK=192), which is what the weight-streaming bound needs.
+constexpr uint32_t kPeerMask = 0xFEFFFFFFu;  // shared::cluster address of the leader CTA
+
+// mbarrier wait that traps instead of hanging if a pair-protocol invariant is
+// ever broken (a legitimate wait here lasts microseconds)
+__device__ __forceinline__ void mbar_wait_guarded(uint32_t bar, uint32_t parity) {
+  uint32_t done = 0, spins = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n}"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    if (!done && ++spins == (1u << 24)) __trap();
+  } while (!done);
+}
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const void* tmap, uint32_t bar,
+                                                 int32_t c_inner, int32_t c_outer,
+                                                 uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".L2::cache_hint [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(bar & kPeerMask), "r"(c_inner), "r"(c_outer),
+      "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void mma_pair(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+// MMA completion -> arrive on the barrier at this offset in BOTH CTAs
+__device__ __forceinline__ void commit_pair(uint32_t bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
+      "[%0], %1;" ::"r"(bar),
+      "h"(uint16_t(3))
+      : "memory");
+}
+__device__ __forceinline__ void arrive_leader(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(bar & kPeerMask) : "memory");
+}
+
+template <int TOK, int STAGES>
+struct PairCfg {
+  static constexpr int XH = TOK / 2;                      // token rows per CTA
+  static constexpr uint32_t X_TILE = XH * ROW_BYTES;
+  static constexpr uint32_t STAGE_BYTES = W_TILE + X_TILE;
+  static constexpr int ACC = 2;
+  static constexpr int ACC_COLS = TOK <= 128 ? 128 : 256;
+  static constexpr int TMEM_COLS = ACC * ACC_COLS;
+  static constexpr uint32_t SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+  static_assert(XH % TOK_BOX == 0, "token half-tile must be whole TMA boxes");
+  static_assert(TMEM_COLS <= 512, "TMEM budget");
+};
+
+template <int TOK>
+__device__ __forceinline__ FTile pdecode(const FusedTable& tt, int32_t t, int32_t& c1, int32_t& c2,
+                                         int32_t d, int32_t f, uint32_t rank) {
+  // identical to fdecode with 256-row weight tiles; this CTA owns half 'rank'
+  FTile r = fdecode<TOK>(tt, t, c1, c2, d, f);
+  const int32_t fb = r.f0 / BM;  // fdecode's fb counts 256-row pair tiles here (fb1/fb2 halved)
+  const int32_t n = r.phase ? d : f;
+  r.f0 = fb * 2 * BM + int32_t(rank) * BM;
+  r.w_row0 = tt.slot[r.g] * n + r.f0;
+  return r;
+}
+
+template <int TOK, int STAGES>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+    fused_ffn_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
+                          const __grid_constant__ CUtensorMap tmap_w1,
+                          const __grid_constant__ CUtensorMap tmap_h,
+                          const __grid_constant__ CUtensorMap tmap_w2, const FusedParams p) {
+  using C = PairCfg<TOK, STAGES>;
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ FusedTable tt;
+  __shared__ uint32_t tmem_base_slot;
+
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  const uint32_t bar_base = base + STAGES * C::STAGE_BYTES;
+  auto full_bar = [&](int s) { return bar_base + 8u * s; };
+  auto empty_bar = [&](int s) { return bar_base + 8u * (STAGES + s); };
+  auto accf_bar = [&](int a) { return bar_base + 8u * (2 * STAGES + a); };
+  auto acce_bar = [&](int a) { return bar_base + 8u * (2 * STAGES + C::ACC + a); };
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int32_t pair = int32_t(blockIdx.x / 2), n_pairs = int32_t(gridDim.x / 2);
+
+  if (threadIdx.x == 0) {
+    tt.n_groups = p.n_groups;
+    tt.fb1 = p.f / (2 * BM);
+    tt.fb2 = p.d / (2 * BM);
+    int32_t a1 = 0, a2 = 0;
+    for (int g = 0; g < p.n_groups; ++g) {
+      const int e = p.experts[g];
+      const int32_t r0 = p.offsets[e];
+      const int32_t rn = p.offsets[e + 1] - r0;
+      tt.row0[g] = r0;
+      tt.rows[g] = rn;
+      tt.slot[g] = p.slots[g];
+      tt.chunks[g] = (rn + TOK - 1) / TOK;
+      tt.start1[g] = a1;
+      tt.start2[g] = a2;
+      a1 += tt.chunks[g] * tt.fb1;
+      a2 += tt.chunks[g] * tt.fb2;
+    }
+    tt.start1[p.n_groups] = a1;
+    tt.start2[p.n_groups] = a2;
+    tt.total1 = a1;
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full_bar(s), 1);   // leader producer's expect_tx; both CTAs' bytes land here
+      mbar_init(empty_bar(s), 1);  // one multicast MMA commit per stage
+    }
+    for (int a = 0; a < C::ACC; ++a) {
+      mbar_init(accf_bar(a), 1);   // one multicast commit per tile
+      mbar_init(acce_bar(a), 8);   // 4 epilogue warps x 2 CTAs (the leader's copy is used)
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 1) {  // same warp id in both CTAs, same destination slot
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&tmem_base_slot)),
+                 "n"(C::TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();  // peer barriers initialised before any remote arrive / TMA
+  tc_fence_after();
+  const uint32_t tmem_base = tmem_base_slot;
+  const int32_t n_tiles = tt.total1 + tt.start2[tt.n_groups];
+  constexpr int32_t bk = ROW_BYTES / 2;
+
+  if (warp == 0) {
+    // ================= TMA producer (both CTAs) =================
+    if (lane == 0) {
+      const uint64_t pol_w = policy_evict_first();
+      const uint64_t pol_x = policy_evict_last();
+      int stage = 0;
+      uint32_t phase = 0;
+      int32_t c1 = 0, c2 = 0, ready_g = -1;
+      for (int32_t t = pair; t < n_tiles; t += n_pairs) {
+        const FTile tile = pdecode<TOK>(tt, t, c1, c2, p.d, p.f, rank);
+        if (tile.phase == 1 && tile.g != ready_g) {
+          const int32_t target = tt.chunks[tile.g] * tt.fb1 * 2;  // both halves of every tile
+          uint32_t spins = 0;
+          while (ld_acquire(p.done + tile.g) < target) {
+            __nanosleep(64);
+            if (++spins == (1u << 28)) __trap();
+          }
+          fence_proxy_async_global();
+          ready_g = tile.g;
+        }
+        const int32_t n_mma = (tile.ntok + 15) & ~15;
+        const int32_t half = n_mma / 2;
+        const int32_t xrow0 = tile.row0 + int32_t(rank) * half;
+        const int boxes = (half + TOK_BOX - 1) / TOK_BOX;
+        const uint32_t bytes_pair = 2u * (W_TILE + boxes * (TOK_BOX * ROW_BYTES));
+        const CUtensorMap* ta = tile.phase ? &tmap_h : &tmap_x;
+        const CUtensorMap* tb = tile.phase ? &tmap_w2 : &tmap_w1;
+        const int32_t kblocks = (tile.phase ? p.f : p.d) / bk;
+        for (int32_t kb = 0; kb < kblocks; ++kb) {
+          mbar_wait_guarded(empty_bar(stage), phase ^ 1);
+          const uint32_t sW = base + stage * C::STAGE_BYTES;
+          const uint32_t sX = sW + W_TILE;
+          if (leader) mbar_expect_tx(full_bar(stage), bytes_pair);
+          tma_load_2d_pair(sW, tb, full_bar(stage), kb * bk, tile.w_row0, pol_w);
+          for (int b = 0; b < boxes; ++b)
+            tma_load_2d_pair(sX + b * (TOK_BOX * ROW_BYTES), ta, full_bar(stage), kb * bk,
+                             xrow0 + b * TOK_BOX, pol_x);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ================= MMA issuer (leader CTA only) =================
+    if (leader) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      int32_t c1 = 0, c2 = 0;
+      for (int32_t t = pair; t < n_tiles; t += n_pairs) {
+        const FTile tile = pdecode<TOK>(tt, t, c1, c2, p.d, p.f, rank);
+        const uint32_t n_mma = uint32_t((tile.ntok + 15) & ~15);
+        const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((n_mma >> 3) << 17) |
+                               (uint32_t((2 * BM) >> 4) << 24);  // M = 256
+        const int32_t kblocks = (tile.phase ? p.f : p.d) / bk;
+        mbar_wait_guarded(acce_bar(acc), acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * C::ACC_COLS;
+        for (int32_t kb = 0; kb < kblocks; ++kb) {
+          mbar_wait_guarded(full_bar(stage), phase);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t sW = base + stage * C::STAGE_BYTES;
+            const uint64_t dw = sdesc(sW);
+            const uint64_t dx = sdesc(sW + W_TILE);
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+              mma_pair(d_tmem, dw + 2 * kk, dx + 2 * kk, idesc, (kb | kk) != 0 ? 1u : 0u);
+            commit_pair(empty_bar(stage));
+          }
+          __syncwarp();
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        if (lane == 0) commit_pair(accf_bar(acc));
+        __syncwarp();
+        if (++acc == C::ACC) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else {
+    // ================= epilogue (warps 2..5, both CTAs) =================
+    const int quarter = warp & 3;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    int32_t c1 = 0, c2 = 0;
+    for (int32_t t = pair; t < n_tiles; t += n_pairs) {
+      const FTile tile = pdecode<TOK>(tt, t, c1, c2, p.d, p.f, rank);
+      mbar_wait_guarded(accf_bar(acc), acc_phase);
+      tc_fence_after();
+      const int feat = tile.f0 + quarter * 32 + lane;
+      const uint32_t taddr = tmem_base + (uint32_t(quarter * 32) << 16) + acc * C::ACC_COLS;
+      const int chunks = (tile.ntok + 31) / 32;
+      for (int cc = 0; cc < chunks; ++cc) {
+        uint32_t r[32];
+        tmem_ld32(taddr + cc * 32, r);
+        const int nvalid = min(32, tile.ntok - cc * 32);
+        const int64_t row = int64_t(tile.row0) + cc * 32;
+        if (tile.phase == 0) {
+          __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(p.h) + row * p.f + feat;
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (i < nvalid)
+              dst[int64_t(i) * p.f] = __float2bfloat16_rn(gelu_erf(__uint_as_float(r[i])));
+        } else if (p.perm == nullptr) {
+          __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(p.y) + row * p.d + feat;
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (i < nvalid) dst[int64_t(i) * p.d] = __float2bfloat16_rn(__uint_as_float(r[i]));
+        } else {
+          const int tok_l = lane < nvalid ? p.perm[row + lane] : 0;
+          const float w_l = lane < nvalid ? p.topk_w[tok_l] : 0.0f;
+          __nv_bfloat16* yb = reinterpret_cast<__nv_bfloat16*>(p.y);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const int tok = __shfl_sync(0xffffffffu, tok_l, i);
+            const float w = __shfl_sync(0xffffffffu, w_l, i);
+            if (i < nvalid) {
+              const float yb16 = __bfloat162float(__float2bfloat16_rn(__uint_as_float(r[i])));
+              yb[int64_t(tok) * p.d + feat] = __float2bfloat16_rn(fmaf(w, yb16, 0.0f));
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      if (tile.phase == 0) {
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (warp == 2 && lane == 0) {
+          __threadfence();
+          fence_proxy_async_global();
+          red_release_add(p.done + tile.g, 1);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) arrive_leader(acce_bar(acc));
+      if (++acc == C::ACC) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();  // no MMA, TMA or remote arrive of either CTA is still in flight
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "n"(C::TMEM_COLS)
+                 : "memory");
+  }
+}
+
+template <int TOK, int STAGES>
+void fused_pair_launch(const FusedFfnArgs& a, cudaStream_t stream) {
+  using C = PairCfg<TOK, STAGES>;
+  auto kern = fused_ffn_pair_kernel<TOK, STAGES>;
+  static bool configured = false;
+  if (!configured) {
+    INFMOE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(C::SMEM_BYTES)));
+    configured = true;
+  }
+  const uint64_t rows = uint64_t(std::max<int64_t>(a.rows, 1));
+  const CUtensorMap tx = make_tmap(a.x, rows, uint64_t(a.d_model), false, TOK_BOX);
+  const CUtensorMap tw1 = make_tmap(a.w_in, uint64_t(a.n_slots) * a.d_ff, uint64_t(a.d_model),
+                                    false, BM);
+  const CUtensorMap th = make_tmap(a.h, rows, uint64_t(a.d_ff), false, TOK_BOX);
+  const CUtensorMap tw2 = make_tmap(a.w_out, uint64_t(a.n_slots) * a.d_model, uint64_t(a.d_ff),
+                                    false, BM);
+  FusedParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.d = a.d_model;
+  p.f = a.d_ff;
+  p.n_groups = a.n_groups;
+  p.offsets = a.offsets;
+  p.h = a.h;
+  p.y = a.y;
+  p.done = a.done;
+  p.perm = a.perm;
+  p.topk_w = a.topk_w;
+  for (int g = 0; g < a.n_groups; ++g) {
+    p.experts[g] = a.experts[g];
+    p.slots[g] = a.slots[g];
+  }
+  int grid = device_sm_count() & ~1;
+  if (a.max_ctas > 0) grid = std::min(grid, (a.max_ctas + 1) & ~1);
+  grid = std::max(grid, 2);
+  if (a.ev_begin) INFMOE_CUDA(cudaEventRecord(a.ev_begin, stream));
+  INFMOE_CUDA(cudaMemsetAsync(a.done, 0, sizeof(int32_t) * size_t(a.n_groups), stream));
+  kern<<<grid, NUM_THREADS, C::SMEM_BYTES, stream>>>(tx, tw1, th, tw2, p);
+  INFMOE_LAUNCH_CHECK();
+  if (a.ev_end) INFMOE_CUDA(cudaEventRecord(a.ev_end, stream));
+}
+
 }  // namespace gemm
 
 void launch_grouped_gemm(const GroupedGemmArgs& a, cudaStream_t stream) {
@@ -817,9 +1168,25 @@ void launch_expert_ffn_fused(const FusedFfnArgs& a, cudaStream_t stream) {
           "fused expert FFN: NULL pointer");
   require((a.perm == nullptr) == (a.topk_w == nullptr), "fused expert FFN: perm needs topk_w");
   const int hint = a.max_rows_hint;
+  if (ffn_pair_mode() && a.d_model % (2 * gemm::BM) == 0 && a.d_ff % (2 * gemm::BM) == 0) {
+    if (hint > 0 && hint <= 128) gemm::fused_pair_launch<128, 8>(a, stream);
+    else if (hint > 192) gemm::fused_pair_launch<256, 6>(a, stream);
+    else gemm::fused_pair_launch<192, 7>(a, stream);
+    return;
+  }
   if (hint > 0 && hint <= 128) gemm::fused_launch<128, 6>(a, stream);
   else if (hint > 192) gemm::fused_launch<256, 4>(a, stream);
   else gemm::fused_launch<192, 5>(a, stream);
 }
+
+// INFMOE_FFN_PAIR=1 selects the cta_group::2 kernel (0 / unset: one SM per tile)
+bool ffn_pair_mode() {
+  static int mode = [] {
+    const char* v = std::getenv("INFMOE_FFN_PAIR");
+    return v ? std::atoi(v) : 0;
+  }();
+  return mode != 0;
+}
+void set_ffn_pair_mode(bool on) { setenv("INFMOE_FFN_PAIR", on ? "1" : "0", 1); }
 
 }  // namespace infmoe

@@ -64,5 +64,6 @@ struct FusedFfnArgs {
   cudaEvent_t ev_begin, ev_end;
 };
 void launch_expert_ffn_fused(const FusedFfnArgs& args, cudaStream_t stream);
+bool ffn_pair_mode();
 
 }  // namespace infmoe
