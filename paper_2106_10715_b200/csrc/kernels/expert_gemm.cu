@@ -1179,11 +1179,11 @@ void launch_expert_ffn_fused(const FusedFfnArgs& a, cudaStream_t stream) {
   else gemm::fused_launch<192, 5>(a, stream);
 }
 
-// INFMOE_FFN_PAIR=1 selects the cta_group::2 kernel (0 / unset: one SM per tile)
+// The cta_group::2 kernel is the default; INFMOE_FFN_PAIR=0 selects one SM per tile
 bool ffn_pair_mode() {
   static int mode = [] {
     const char* v = std::getenv("INFMOE_FFN_PAIR");
-    return v ? std::atoi(v) : 0;
+    return v ? std::atoi(v) : 1;
   }();
   return mode != 0;
 }

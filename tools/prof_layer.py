@@ -30,6 +30,6 @@ layer = dv.MoELayer(d, f, E, a.k, wi, wo, gate=a.gate, gate_weight=gw, lsh_seed=
                     max_tokens=N)
 y = torch.empty_like(x)
 for _ in range(a.iters):
-    layer.forward(x, y)
+    layer.forward(x, y, want_info=False)
 torch.cuda.synchronize()
 print("ok")
