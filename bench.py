@@ -211,6 +211,17 @@ def run_reference_arm(args, cfg, rank: int) -> None:
 
 # ------------------------------------------------------------------ GPU arm --
 
+def _smi_state(tag):
+    q = ("clocks.sm,clocks.mem,power.draw,power.limit,enforced.power.limit,temperature.gpu,"
+         "temperature.memory,clocks_event_reasons.active")
+    try:
+        out = subprocess.run(["nvidia-smi", "--id=0", f"--query-gpu={q}", "--format=csv,noheader"],
+                             capture_output=True, text=True, timeout=10).stdout.strip()
+    except Exception as exc:  # noqa: BLE001
+        out = repr(exc)
+    print(f"[{tag}] {out}", file=sys.stderr)
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -333,6 +344,14 @@ def main() -> None:
             cur = y
         return cur, infos
 
+    if os.environ.get("BENCH_VERBOSE"):
+        for rep in range(2):
+            _, pre = stack(res_layers, x_dev, timeline=True)
+        _smi_state("pre")
+        for l, i in enumerate(pre[:6]):
+            print(f"pre resident layer {l}: ffn {(i['events'][0][4] - i['events'][0][3]) * 1e6:.1f} us",
+                  file=sys.stderr)
+
     # ---------------- offloaded stack: warm-up, then timed steps -------------
     for _ in range(args.warmup):
         stack(off_layers, x_dev)
@@ -341,7 +360,7 @@ def main() -> None:
         dist.barrier()
     ev = lambda: torch.cuda.Event(enable_timing=True)
     inner_ms, outer_ms, all_infos = [], [], []
-    with ClockSampler(local) as clocks:
+    with (ClockSampler(local) if not os.environ.get("BENCH_NOSMI") else ClockSampler(-1)) as clocks:
         for _ in range(args.steps):
             torch.cuda.synchronize()
             a, b, c, dd = ev(), ev(), ev(), ev()
@@ -381,6 +400,13 @@ def main() -> None:
                     ffn_secs += s1 - s0
                     ffn_bytes += wbytes + int(rows[e]) * (2 * d + 2 * f) * 2
     launches //= max(1, args.steps)
+    if os.environ.get("BENCH_VERBOSE"):
+        for l, info in enumerate(all_infos[-1]):
+            ld = [(s1 - s0) for (st, _l, _e, s0, s1) in info["events"] if st == 0]
+            ce = max(s1 for (st, _l, _e, s0, s1) in info["events"] if st == 1)
+            print(f"offloaded layer {l} (set {l % n_sets}): load rate "
+                  f"{2 * d * f * 2 * len(ld) / sum(ld) / 1e9:.2f} GB/s, layer {ce * 1e3:.2f} ms",
+                  file=sys.stderr)
     h2d_bytes_step = L * El * wbytes          # this rank's host link
     h2d_gbs = h2d_bytes_step / (t_in * 1e-3) / 1e9
 
@@ -392,6 +418,12 @@ def main() -> None:
     for _ in range(3):
         stack(res_layers, x_dev, info=False)
     torch.cuda.synchronize()
+    if os.environ.get("BENCH_VERBOSE"):
+        _, mid = stack(res_layers, x_dev, timeline=True)
+        _smi_state("mid")
+        for l, i in enumerate(mid[:4]):
+            print(f"mid resident layer {l}: ffn {(i['events'][0][4] - i['events'][0][3]) * 1e6:.1f} us",
+                  file=sys.stderr)
     if P == 1:
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph):
@@ -399,15 +431,19 @@ def main() -> None:
         graph.replay()
         torch.cuda.synchronize()
     a, b = ev(), ev()
-    a.record(stream)
-    for _ in range(args.resident_steps):
-        if graph is not None:
-            graph.replay()
-            y_res = y_graph
-        else:
-            y_res, _ = stack(res_layers, x_dev, info=False)
-    b.record(stream)
-    b.synchronize()
+    with ClockSampler(local) as res_clocks:
+        a.record(stream)
+        for _ in range(args.resident_steps):
+            if graph is not None:
+                graph.replay()
+                y_res = y_graph
+            else:
+                y_res, _ = stack(res_layers, x_dev, info=False)
+        b.record(stream)
+        b.synchronize()
+    if os.environ.get("BENCH_VERBOSE"):
+        print("resident clocks", res_clocks.summary(), [r[1:4] for r in res_clocks.rows],
+              file=sys.stderr)
     t_res = a.elapsed_time(b) / args.resident_steps
     if world > 1:
         tt = torch.tensor([t_res], device=dev)
@@ -416,6 +452,10 @@ def main() -> None:
     # one timeline pass for the grouped-GEMM share
     _, rinfos = stack(res_layers, x_dev, timeline=True)
     rg_secs = sum(i["events"][0][4] - i["events"][0][3] for i in rinfos)
+    if os.environ.get("BENCH_VERBOSE"):
+        for l, i in enumerate(rinfos):
+            print(f"resident layer {l}: ffn {(i['events'][0][4] - i['events'][0][3]) * 1e6:.1f} us "
+                  f"max_rows {int(i['local_rows'].max())}", file=sys.stderr)
     rg_bytes = 0
     for i in rinfos:
         rows = i["local_rows"]
@@ -475,7 +515,8 @@ def main() -> None:
                      "cuda_graph": graph is not None,
                      "ms_per_layer": t_res / L,
                      "grouped_ffn_share": rg_secs * 1e3 / t_res if t_res else None,
-                     "bit_identical_to_offloaded": parity_equal},
+                     "bit_identical_to_offloaded": parity_equal,
+                     "clocks": res_clocks.summary()},
         "gpu_launches": launches,
         "clocks": clocks.summary(),
     }

@@ -670,44 +670,50 @@ double or_gelu(double v) { return 0.5 * v * (1.0 + erf(v * 0.7071067811865475244
 void or_gate_softmax(const float* x, uint64_t N, int d, const float* wg,
                      const float* bias, int E, int k, int32_t* topk_idx,
                      float* topk_w, int32_t* counts) {
-  float* lg = (float*)malloc(sizeof(float) * (size_t)E);
-  memset(counts, 0, sizeof(int32_t) * (size_t)E);
-  for (uint64_t t = 0; t < N; ++t) {
-    const float* xr = x + t * (uint64_t)d;
-    for (int e = 0; e < E; ++e) {
-      const float* wr = wg + (uint64_t)e * (uint64_t)d;
-      float acc = 0.0f;
-      for (int c = 0; c < d; ++c) acc = fmaf(xr[c], wr[c], acc);
-      if (bias) acc = acc + bias[e];
-      lg[e] = acc;
-    }
-    int picked[8];
-    for (int j = 0; j < k; ++j) {
-      int best = -1;
+  /* tokens are independent: OpenMP over tokens, counts tallied afterwards */
+#pragma omp parallel
+  {
+    float* lg = (float*)malloc(sizeof(float) * (size_t)E);
+#pragma omp for schedule(static)
+    for (int64_t ti = 0; ti < (int64_t)N; ++ti) {
+      const uint64_t t = (uint64_t)ti;
+      const float* xr = x + t * (uint64_t)d;
       for (int e = 0; e < E; ++e) {
-        int used = 0;
-        for (int q = 0; q < j; ++q) used |= (picked[q] == e);
-        if (used) continue;
-        if (best < 0) { best = e; continue; }
-        if (lg[e] > lg[best] || (lg[best] != lg[best] && lg[e] == lg[e])) best = e;
+        const float* wr = wg + (uint64_t)e * (uint64_t)d;
+        float acc = 0.0f;
+        for (int c = 0; c < d; ++c) acc = fmaf(xr[c], wr[c], acc);
+        if (bias) acc = acc + bias[e];
+        lg[e] = acc;
       }
-      picked[j] = best;
-      topk_idx[t * k + j] = best;
-      counts[best]++;
+      int picked[8];
+      for (int j = 0; j < k; ++j) {
+        int best = -1;
+        for (int e = 0; e < E; ++e) {
+          int used = 0;
+          for (int q = 0; q < j; ++q) used |= (picked[q] == e);
+          if (used) continue;
+          if (best < 0) { best = e; continue; }
+          if (lg[e] > lg[best] || (lg[best] != lg[best] && lg[e] == lg[e])) best = e;
+        }
+        picked[j] = best;
+        topk_idx[t * k + j] = best;
+      }
+      /* softmax over all E in fp64 */
+      double mx = -INFINITY;
+      for (int e = 0; e < E; ++e) if (lg[e] > mx) mx = lg[e];
+      double s = 0.0;
+      for (int e = 0; e < E; ++e) s += exp((double)lg[e] - mx);
+      double p[8], ps = 0.0;
+      for (int j = 0; j < k; ++j) {
+        p[j] = exp((double)lg[picked[j]] - mx) / s;
+        ps += p[j];
+      }
+      for (int j = 0; j < k; ++j) topk_w[t * k + j] = (float)(k > 1 ? p[j] / ps : p[j]);
     }
-    /* softmax over all E in fp64 */
-    double mx = -INFINITY;
-    for (int e = 0; e < E; ++e) if (lg[e] > mx) mx = lg[e];
-    double s = 0.0;
-    for (int e = 0; e < E; ++e) s += exp((double)lg[e] - mx);
-    double p[8], ps = 0.0;
-    for (int j = 0; j < k; ++j) {
-      p[j] = exp((double)lg[picked[j]] - mx) / s;
-      ps += p[j];
-    }
-    for (int j = 0; j < k; ++j) topk_w[t * k + j] = (float)(k > 1 ? p[j] / ps : p[j]);
+    free(lg);
   }
-  free(lg);
+  memset(counts, 0, sizeof(int32_t) * (size_t)E);
+  for (uint64_t a = 0; a < N * (uint64_t)k; ++a) counts[topk_idx[a]]++;
 }
 
 void or_gate_lsh(const float* x, uint64_t N, int d, const double* proj, int bits,

@@ -1,0 +1,149 @@
+"""Full-size parity on the GPU (BASELINE.json's C2/C3 layer and C5), through
+size-independent properties plus a sampled oracle check:
+
+* routing: counts bit-exact against the reference (`route_tokens`,
+  gating.hpp:87-104, compiled in oracle/_ref) for the C3 LSH layer, and against
+  the oracle softmax/top-k gate for C5 (E=64, top-2, Zipf-skewed by a logit
+  bias);
+* offloaded (K=4, InfMoE order) output bit-identical to the resident output;
+* executed order == the reference `auto_order` (scheduler.hpp:243) for the
+  realised counts;
+* a sample of tokens (those routed to a few experts) against the fp64 oracle
+  FFN + combine, at the bf16 tolerance of DESIGN.md §6.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2106_10715_b200 as im
+from paper_2106_10715_b200 import device as dv
+from oracle_lib import O, REF, bf16_bits_to_f32, f32_to_bf16_bits, ptr, schedule
+
+pytestmark = pytest.mark.gpu
+
+ATOL, RTOL = 3e-2, 2e-2
+SQRT3 = 1.7320508075688772
+GELU_GAIN = 1.5340
+
+
+def _weights(cuda, E, d, f, seed):
+    wi = torch.empty((E, f, d), dtype=torch.bfloat16, device=cuda)
+    wo = torch.empty((E, d, f), dtype=torch.bfloat16, device=cuda)
+    for e in range(E):
+        dv.fill_uniform(wi[e], im.derive_seed(seed, 2 * e), SQRT3 / math.sqrt(d))
+        dv.fill_uniform(wo[e], im.derive_seed(seed, 2 * e + 1), GELU_GAIN * SQRT3 / math.sqrt(f))
+    hi = torch.empty(wi.shape, dtype=torch.bfloat16, pin_memory=True)
+    ho = torch.empty(wo.shape, dtype=torch.bfloat16, pin_memory=True)
+    hi.copy_(wi)
+    ho.copy_(wo)
+    return wi, wo, hi, ho
+
+
+def _bits(t):
+    return t.view(torch.int16).numpy().view(np.uint16)
+
+
+def _sampled_oracle_check(x_host, hi, ho, y, idx, w, experts, d, f, k, n_max=24):
+    """Tokens whose k experts all lie in `experts`: fp64 oracle FFN + combine."""
+    sel = [t for t in range(idx.shape[0]) if all(int(e) in experts for e in idx[t])][:n_max]
+    assert sel, "no token routed only to the sampled experts"
+    xf = bf16_bits_to_f32(_bits(x_host[sel]).reshape(-1)).reshape(len(sel), d)
+    yp = {}
+    for e in experts:
+        rows = [(i, j) for i, t in enumerate(sel) for j in range(k) if idx[t, j] == e]
+        if not rows:
+            continue
+        xe = np.ascontiguousarray(xf[[i for i, _ in rows]])
+        wif = np.ascontiguousarray(bf16_bits_to_f32(_bits(hi[e]).reshape(-1)))
+        wof = np.ascontiguousarray(bf16_bits_to_f32(_bits(ho[e]).reshape(-1)))
+        out = np.zeros((len(rows), d), np.float32)
+        O.or_expert_ffn(ptr(xe), len(rows), d, f, ptr(wif), ptr(wof), 1, ptr(out))
+        out = bf16_bits_to_f32(f32_to_bf16_bits(out)).reshape(len(rows), d)  # y_perm is bf16
+        for r, (i, j) in enumerate(rows):
+            yp[(i, j)] = out[r]
+    got = y[sel].float().cpu().numpy()
+    for i, t in enumerate(sel):
+        ref = np.zeros(d, np.float32)
+        for j in range(k):  # the combine's fmaf chain in slot order (oracle.c or_combine)
+            ref = np.float32(w[t, j]) * yp[(i, j)] + ref
+        err = np.abs(got[i] - ref)
+        assert np.all(err <= ATOL + RTOL * np.abs(ref)), (t, float(err.max()))
+    return len(sel)
+
+
+def _check_order(counts, d, f, hw, K, order):
+    g = im.make_geometry(d, f, len(counts), 2)
+    cv = im.compute_costs(np.asarray(counts, np.uint64), g, hw)
+    want = schedule("ref" if REF is not None else "or", cv.alphas, cv.beta, K, "auto")[1]
+    assert list(order) == want
+
+
+def test_c3_layer_fullsize(cuda):
+    """One C3 layer: N=4096, d=4096, f=10240, E=32, LSH 5 bits, offloaded K=4."""
+    N, d, f, E, K = 4096, 4096, 10240, 32, 4
+    wi, wo, hi, ho = _weights(cuda, E, d, f, seed=901)
+    x = torch.empty((N, d), dtype=torch.bfloat16, device=cuda)
+    dv.fill_uniform(x, 902, SQRT3)
+    seed = im.derive_seed(903, 0)
+    hw = im.Hardware(1643.6e12, 55.5e9, 180 << 30, 8 << 30)
+    res = dv.MoELayer(d, f, E, 1, wi, wo, gate="lsh", lsh_seed=seed, lsh_bits=5, max_tokens=N)
+    off = dv.MoELayer(d, f, E, 1, hi, ho, gate="lsh", lsh_seed=seed, lsh_bits=5, offloaded=True,
+                      K=K, max_tokens=N, hw=hw)
+    y_res, info_r = res.forward(x)
+    y_off, info = off.forward(x)
+    torch.cuda.synchronize()
+    assert torch.equal(y_res.view(torch.int16), y_off.view(torch.int16))
+    # routing counts == the reference's route_tokens on the fp64 promotion of x
+    x_host = x.cpu()
+    xd = bf16_bits_to_f32(_bits(x_host).reshape(-1)).astype(np.float64)
+    cnt = np.zeros(E, np.uint64)
+    route = REF.ref_route_tokens if REF is not None else O.or_route_tokens
+    assert route(seed, 5, d, ptr(xd), N, E, ptr(cnt)) == 0
+    assert np.array_equal(info["counts"].astype(np.uint64), cnt)
+    _check_order(info["counts"], d, f, hw, K, info["order"])
+    # sampled tokens through the oracle FFN (top-1, weight 1.0)
+    _, idx_all, w_all, _ = dv.gate_lsh(x, torch.from_numpy(im.gating_projection(seed, 5, d)).to(cuda), E)
+    idx_h = idx_all.cpu().numpy().reshape(N, 1)
+    w_h = w_all.cpu().numpy().reshape(N, 1)
+    n = _sampled_oracle_check(x_host, hi, ho, y_off, idx_h, w_h, {0, 1}, d, f, 1)
+    assert n >= 8
+    res.close()
+    off.close()
+
+
+def test_c5_layer_fullsize(cuda):
+    """C5: N=16384, E=64, top-2 softmax gate skewed by b_e = -ln(e+1), offloaded K=4."""
+    N, d, f, E, k, K = 16384, 4096, 10240, 64, 2, 4
+    wi, wo, hi, ho = _weights(cuda, E, d, f, seed=911)
+    x = torch.empty((N, d), dtype=torch.bfloat16, device=cuda)
+    dv.fill_uniform(x, 912, SQRT3)
+    gw = (np.random.default_rng(913).standard_normal((E, d)) / math.sqrt(d)).astype(np.float32)
+    bias = (-1.0 * np.log(np.arange(1, E + 1))).astype(np.float32)
+    hw = im.Hardware(1643.6e12, 55.5e9, 180 << 30, 8 << 30)
+    kw = dict(gate="softmax", gate_weight=gw, gate_bias=bias, max_tokens=N)
+    res = dv.MoELayer(d, f, E, k, wi, wo, **kw)
+    off = dv.MoELayer(d, f, E, k, hi, ho, offloaded=True, K=K, hw=hw, **kw)
+    y_res, info_r = res.forward(x)
+    y_off, info = off.forward(x)
+    torch.cuda.synchronize()
+    assert torch.equal(y_res.view(torch.int16), y_off.view(torch.int16))
+    # gate: indices, weights and counts against the oracle gate (fp32 fmaf chains)
+    x_host = x.cpu()
+    xf = np.ascontiguousarray(bf16_bits_to_f32(_bits(x_host).reshape(-1)).reshape(N, d))
+    idx = np.zeros((N, k), np.int32)
+    w = np.zeros((N, k), np.float32)
+    cnt = np.zeros(E, np.int32)
+    O.or_gate_softmax(ptr(xf), N, d, ptr(gw), ptr(bias), E, k, ptr(idx), ptr(w), ptr(cnt))
+    assert np.array_equal(info["counts"], cnt)
+    assert cnt[0] > 4 * cnt[E - 1]  # the bias skews the load (realised counts reported)
+    _check_order(info["counts"], d, f, hw, K, info["order"])
+    idx_g, w_g, _ = dv.gate_softmax_topk(x, torch.from_numpy(gw).to(cuda), k,
+                                         bias=torch.from_numpy(bias).to(cuda))
+    assert np.array_equal(idx_g.cpu().numpy().reshape(N, k), idx)
+    np.testing.assert_allclose(w_g.cpu().numpy().reshape(N, k), w, rtol=1e-5, atol=1e-7)
+    n = _sampled_oracle_check(x_host, hi, ho, y_off, idx, w, {0, 1, 2}, d, f, k)
+    assert n >= 8
+    res.close()
+    off.close()

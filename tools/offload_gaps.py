@@ -1,0 +1,72 @@
+"""Dev tool: where does the host link idle in the offloaded executor?
+
+Runs a short offloaded LSH stack (bench.py's C3 shapes) with timelines and
+reports, per layer: time to the first load, the sum of load durations, the
+gaps between consecutive loads, and the tail after the last load.
+"""
+import argparse
+import math
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import bench  # noqa: E402
+import paper_2106_10715_b200 as im  # noqa: E402
+from paper_2106_10715_b200 import device as dv  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--layers", type=int, default=4)
+    a = ap.parse_args()
+    d, f, E, N = 4096, 10240, 32, 4096
+    bf = torch.bfloat16
+    dev = torch.device("cuda:0")
+    wi = torch.empty((E, f, d), dtype=bf, device=dev)
+    wo = torch.empty((E, d, f), dtype=bf, device=dev)
+    dv.fill_uniform(wi, 11, bench.SQRT3 / d ** 0.5)
+    dv.fill_uniform(wo, 12, bench.GELU_GAIN * bench.SQRT3 / f ** 0.5)
+    hi = torch.empty(wi.shape, dtype=bf, pin_memory=True)
+    ho = torch.empty(wo.shape, dtype=bf, pin_memory=True)
+    hi.copy_(wi)
+    ho.copy_(wo)
+    del wi, wo
+    x = torch.empty((N, d), dtype=bf, device=dev)
+    dv.fill_uniform(x, 3, math.sqrt(3.0))
+    layers = [dv.MoELayer(d, f, E, 1, hi, ho, gate="lsh", lsh_seed=100 + l, lsh_bits=5,
+                          offloaded=True, K=4, max_tokens=N) for l in range(a.layers)]
+    bufs = [torch.empty_like(x) for _ in range(2)]
+    for rep in range(2):
+        cur = x
+        t0 = torch.cuda.Event(enable_timing=True)
+        t0.record()
+        infos = []
+        for l, layer in enumerate(layers):
+            _, info = layer.forward(cur, bufs[l % 2], want_timeline=True)
+            infos.append(info)
+            cur = bufs[l % 2]
+        t1 = torch.cuda.Event(enable_timing=True)
+        t1.record()
+        torch.cuda.synchronize()
+    total = t0.elapsed_time(t1)
+    nbytes = 2 * d * f * 2
+    for l, info in enumerate(infos):
+        loads = sorted([(s0, s1) for st, _, _, s0, s1 in info["events"] if st == 0])
+        comps = [(s0, s1) for st, _, _, s0, s1 in info["events"] if st == 1]
+        dur = [b - a for a, b in loads]
+        gaps = [loads[i + 1][0] - loads[i][1] for i in range(len(loads) - 1)]
+        end = max(c[1] for c in comps)
+        print(f"layer {l}: first load at {loads[0][0] * 1e3:.3f} ms, loads {sum(dur) * 1e3:.2f} ms "
+              f"(mean {np.mean(dur) * 1e3:.3f} ms = {nbytes / np.mean(dur) / 1e9:.2f} GB/s), "
+              f"gaps sum {sum(gaps) * 1e3:.3f} ms max {max(gaps) * 1e6:.1f} us, "
+              f"tail after last load {(end - loads[-1][1]) * 1e3:.3f} ms, layer {end * 1e3:.2f} ms")
+    print(f"stack {total:.2f} ms, ideal at per-load rate {a.layers * E * np.mean(dur) * 1e3:.2f} ms")
+    for layer in layers:
+        layer.close()
+
+
+if __name__ == "__main__":
+    main()
