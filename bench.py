@@ -479,6 +479,10 @@ def main() -> None:
                          f"combine), {secs:.2f} s, scaled to the {L}-layer stack"}
 
     hbm_peak = float(peaks["hbm_gbs"])
+    traffic = None  # DRAM bytes per launch of the same kernel from the committed ncu capture
+    tp = ROOT / "profiles" / "r01_ffn_traffic.json"
+    if tp.exists():
+        traffic = json.loads(tp.read_text()).get("traffic_bytes_per_launch")
     ffn_gbs = ffn_bytes / ffn_secs / 1e9 if ffn_secs else 0.0
     rg_gbs = rg_bytes / rg_secs / 1e9 if rg_secs else 0.0
     value = N_glob / (t_in * 1e-3)
@@ -505,7 +509,8 @@ def main() -> None:
         "roofline": {"kernel": "fused expert FFN (tcgen05 GEMM1+GeLU -> GEMM2 [+top-1 combine]), "
                                "all local experts in one launch",
                      "bound": "hbm", "achieved": rg_gbs, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": rg_gbs / hbm_peak, "traffic": None,
+                     "frac": rg_gbs / hbm_peak, "traffic": traffic,
+                     "traffic_src": "profiles/r01_ffn_traffic.json (ncu dram__bytes_read+write)",
                      "bytes_per_launch": rg_bytes / max(1, len(rinfos)),
                      "launches_timed": len(rinfos), "peak_src": peaks["_src"]},
         "offloaded_ffn": {"kernel": "same kernel, one expert per launch behind each H2D copy "
