@@ -164,6 +164,63 @@ def cpu_layer_sample(cfg, x_bits: np.ndarray, w_in_bits, w_out_bits, proj, n_tok
     return secs, int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
 
 
+def reference_pieces(cfg) -> dict | None:
+    """Time the reference's own CPU pieces of this path as shipped (the moesim
+    headers compiled in place into oracle/_ref, single thread): gaussian_tokens,
+    route_tokens, compute_costs + auto_order per layer, simulate_model over the
+    stack (SURVEY.md 8(d) "CPU path timed beside the GPU", item i)."""
+    so = ROOT / "oracle" / "_ref" / "libmoesim_ref.so"
+    if not so.exists() or cfg["gate"] != "lsh":
+        return None
+    lib = C.CDLL(str(so))
+    vp, u64 = C.c_void_p, C.c_uint64
+    lib.ref_gaussian_tokens.argtypes = [u64, u64, C.c_int, vp]
+    lib.ref_route_tokens.argtypes = [u64, C.c_int, C.c_int, vp, u64, C.c_int, vp]
+    lib.ref_derive_seed.restype = u64
+    lib.ref_derive_seed.argtypes = [u64, u64]
+    lib.ref_compute_costs.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, vp,
+                                      C.c_int, vp, vp]
+    lib.ref_schedule.argtypes = [vp, C.c_int, C.c_double, C.c_int, C.c_int, C.c_int, vp, vp, vp,
+                                 vp]
+    lib.ref_simulate_model.argtypes = [C.c_int, vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int,
+                                       C.c_int, vp, vp, vp]
+    P = lambda a: a.ctypes.data_as(vp)
+    d, E, N, L, bits, K = cfg["d"], cfg["E"], cfg["N"], cfg["L"], cfg["bits"], cfg["K"]
+    out = {"impl": "oracle/_ref (reference headers, g++ -O2, 1 thread)",
+           "shape": f"{N} tokens x d {d}, {bits} bits, E {E}, {L} layers, K {K}"}
+    x = np.empty(N * d, np.float64)
+    t0 = time.perf_counter()
+    lib.ref_gaussian_tokens(lib.ref_derive_seed(SEED, 0), N, d, P(x))
+    out["gaussian_tokens_ms"] = (time.perf_counter() - t0) * 1e3
+    cnt = np.zeros(E, np.uint64)
+    t0 = time.perf_counter()
+    lib.ref_route_tokens(lib.ref_derive_seed(SEED, 100), bits, d, P(x), N, E, P(cnt))
+    out["route_tokens_ms"] = (time.perf_counter() - t0) * 1e3
+    alphas = np.zeros(E, np.float64)
+    beta = C.c_double(0.0)
+    order = np.zeros(E, np.int32)
+    fz = [np.zeros(1, np.int32) for _ in range(3)]
+    reps = 200
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        lib.ref_compute_costs(d, cfg["f"], 2, 1643.6e12, 55.5e9, P(cnt), E, P(alphas),
+                              C.byref(beta))
+        lib.ref_schedule(P(alphas), E, beta.value, K, 0, 12, P(order), P(fz[0]), P(fz[1]),
+                         P(fz[2]))
+    out["costs_plus_auto_order_us"] = (time.perf_counter() - t0) / reps * 1e6
+    Ts = np.full(L, E, np.int32)
+    al = np.tile(alphas, L)
+    be = np.full(L, beta.value)
+    orders = np.zeros(L * E, np.int32)
+    ev = np.zeros(2 * L * E * 5, np.float64)  # 2 events per expert, 40 B each (>= ref_event)
+    rep = np.zeros(8, np.float64)
+    t0 = time.perf_counter()
+    lib.ref_simulate_model(L, P(Ts), P(al), P(be), K, 0, 0, 0, 12, P(orders), P(ev), P(rep))
+    out["simulate_model_ms"] = (time.perf_counter() - t0) * 1e3
+    out["simulated_makespan_s"] = float(rep[0])
+    return out
+
+
 def run_reference_arm(args, cfg, rank: int) -> None:
     """--impl reference: the CPU path (oracle port of the layer; the
     reference's own moesim code covers only routing and scheduling) on the
@@ -206,6 +263,9 @@ def run_reference_arm(args, cfg, rank: int) -> None:
                                        f"the same), scaled to the {cfg['L']}-layer stack"},
             "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
+    pieces = reference_pieces(cfg)
+    if pieces is not None:
+        line["reference_pieces"] = pieces
     print(json.dumps(line), flush=True)
 
 
@@ -400,6 +460,13 @@ def main() -> None:
                     ffn_secs += s1 - s0
                     ffn_bytes += wbytes + int(rows[e]) * (2 * d + 2 * f) * 2
     launches //= max(1, args.steps)
+    # the reference simulator's prediction for the realised counts, with the
+    # link bandwidth measured on this box (simulate_model, simulator.hpp:241)
+    g_loc = im.make_geometry(d, f, El, 2)
+    hw_meas = im.Hardware(float(peaks["bf16_tflops"]) * 1e12, h2d_peak * 1e9, 180 << 30, 8 << 30)
+    costs = [im.compute_costs(info["local_rows"].astype(np.uint64), g_loc, hw_meas)
+             for info in all_infos[-1]]
+    _, sim_rep, _ = im.simulate_model(costs, cfg["K"])
     if os.environ.get("BENCH_VERBOSE"):
         for l, info in enumerate(all_infos[-1]):
             ld = [(s1 - s0) for (st, _l, _e, s0, s1) in info["events"] if st == 0]
@@ -502,7 +569,9 @@ def main() -> None:
         "h2d": {"achieved_gbs": h2d_gbs, "peak_gbs": h2d_peak, "frac": h2d_gbs / h2d_peak,
                 "bytes_per_step": h2d_bytes_step, "peak_src": "measured pinned 1 GiB copy",
                 "per": "rank (each rank streams its own experts over its own host link)",
-                "exposed_copy_ms_per_layer": 1e3 * float(np.mean(exposed))},
+                "exposed_copy_ms_per_layer": 1e3 * float(np.mean(exposed)),
+                "simulated_ms_per_step": sim_rep.makespan * 1e3,
+                "measured_over_simulated": t_in / (sim_rep.makespan * 1e3)},
         # dominant kernel of the path: the expert FFN (both tcgen05 projections in
         # one persistent launch), timed with CUDA events on its stream over the
         # resident 24-layer pass; bytes = weights of routed experts + activations
