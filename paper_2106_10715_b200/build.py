@@ -80,14 +80,19 @@ def build(verbose: bool = False) -> Path:
     srcs = CU_SOURCES + CXX_SOURCES
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
         objs = list(ex.map(lambda s: _compile(s, digest, verbose), srcs))
-    newest = max(o.stat().st_mtime for o in objs)
-    if LIB.exists() and LIB.stat().st_mtime >= newest:
+    # relink whenever the set of object contents changed (content keys, not
+    # mtimes: a copied-in or restored library must not be mistaken for fresh)
+    link_key = hashlib.sha256("".join(o.with_suffix(".stamp").read_text() for o in objs)
+                              .encode()).hexdigest()
+    link_stamp = OBJ_DIR / "libinfmoe.stamp"
+    if LIB.exists() and link_stamp.exists() and link_stamp.read_text() == link_key:
         return LIB
     cmd = [NVCC, *ARCH, "-shared", "-ccbin", HOST_CXX, "-o", str(LIB), *map(str, objs),
            "-lcudart", "-ldl", "-Xlinker", "-rpath,/usr/local/cuda/lib64"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed\n{' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
+    link_stamp.write_text(link_key)
     return LIB
 
 
