@@ -11,6 +11,7 @@
 // weight matrix is read once per CTA of tokens, not once per token.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -352,6 +353,236 @@ __global__ void __launch_bounds__(kLshWarps * 32) gate_lsh_kernel(
   }
 }
 
+// ------------------------------------------------------- N1b fast path ----
+// The reference only consumes the SIGN of each sequential dot (bit j =
+// dot >= 0, gating.hpp:76-79), so most bits can be decided without running
+// the 4096-step dependent chain.  Certified fast path:
+//   S  = sum_i x_i*w_i accumulated with DFMA in any order (lanes split d,
+//        then a butterfly reduction);
+//   |S_seq - S| <= (gamma_n + (1+u)gamma_{n-1} + u) * sum|x_i w_i|
+//              <= 2.0003 n u ||x||_2 ||w||_2                  (Cauchy-Schwarz),
+// where S_seq is the reference's left-to-right sum of the rounded products
+// and u = 2^-53.  If |S| > thr = 8 n u ||x|| ||w|| (computed norms, a 4x
+// margin), S_seq has S's sign and is nonzero, so the bit is S > 0.  An
+// all-zero row gives S_seq = +0 (bit 1).  Anything else — |S| <= thr, NaN,
+// Inf — re-runs the exact sequential chain for that (token, bit) pair, so the
+// codes are identical to the reference's by construction.  Each warp owns
+// kLshFastTW tokens; lanes take 8-element slices of d (16 B loads of x,
+// streamed past L1; hyperplane rows are L1-resident).
+constexpr int kLshFastTW = 2;      // tokens per warp
+constexpr int kLshFastWarps = 8;   // warps per CTA (16 tokens)
+constexpr int kLshFastChunk = 256; // columns per ring stage (8 per lane)
+
+template <typename T, int BMAX>
+struct LshFastCfg {
+  static constexpr int TB = kLshFastWarps * kLshFastTW;
+  static constexpr int XROW = kLshFastChunk + 16 / int(sizeof(T));  // +16 B
+  static constexpr size_t XBYTES = size_t(TB) * XROW * sizeof(T);
+  static constexpr size_t WBYTES = size_t(BMAX) * kLshFastChunk * sizeof(double);
+  static constexpr size_t STAGE = XBYTES + WBYTES;
+  static constexpr size_t SMEM = kGateStages * STAGE + size_t(kLshFastWarps) * BMAX * sizeof(double);
+  // stage stride for `bits` hyperplane rows (the ring only holds what is used)
+  static constexpr size_t stage_bytes(int bits) {
+    return XBYTES + size_t(bits) * kLshFastChunk * sizeof(double);
+  }
+  static constexpr size_t smem_bytes(int bits) {
+    return kGateStages * stage_bytes(bits) + size_t(kLshFastWarps) * BMAX * sizeof(double);
+  }
+};
+
+template <typename T, int BMAX>
+__global__ void __launch_bounds__(kLshFastWarps * 32) gate_lsh_fast_kernel(
+    const T* __restrict__ x, int64_t N, int d, const double* __restrict__ proj, int bits, int E,
+    int force_exact, uint32_t* __restrict__ codes, int32_t* __restrict__ topk_idx,
+    float* __restrict__ topk_w, int32_t* __restrict__ counts) {
+  using C = LshFastCfg<T, BMAX>;
+  constexpr int TW = kLshFastTW, NT = kLshFastWarps * 32, CH = kLshFastChunk;
+  constexpr int V = 16 / int(sizeof(T));
+  extern __shared__ __align__(16) uint8_t lshf_smem[];
+  const size_t stage = C::stage_bytes(bits);
+  auto xs = [&](int st) { return reinterpret_cast<T*>(lshf_smem + st * stage); };
+  auto ws = [&](int st) { return reinterpret_cast<double*>(lshf_smem + st * stage + C::XBYTES); };
+  double* wnorm = reinterpret_cast<double*>(lshf_smem + kGateStages * stage);  // [warps][BMAX]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t tok0 = int64_t(blockIdx.x) * C::TB;
+  const int nch = (d + CH - 1) / CH;
+
+  // per-thread copy assignments are the same for every chunk (only c0 moves):
+  // x: TB*CH/V 16-B pieces, XPT per thread; w: one pair per thread per bit
+  constexpr int XPT = C::TB * (CH / V) / NT;
+  static_assert(C::TB * (CH / V) % NT == 0 && NT % (CH / 2) == 0, "LSH fast ring shape");
+  // thread -> (row t = i / (CH/V), column c = (i % (CH/V)) * V), i = tid + NT*r:
+  // the column is the same for every r (NT is a multiple of CH/V)
+  static_assert(NT % (CH / V) == 0, "LSH fast ring shape");
+  const int x_c = (threadIdx.x % (CH / V)) * V;
+  const int x_t0 = threadIdx.x / (CH / V);
+  // hyperplane pairs lane-interleaved: pair p (columns 2p, 2p+1 of the chunk)
+  // of lane p/4 lands at slot (p%4)*32 + p/4, so the 16-B reads of one pair
+  // index by the 32 lanes are contiguous (conflict-free)
+  const int pr = threadIdx.x % (CH / 2), b_first = threadIdx.x / (CH / 2);
+  const int w_dst = ((pr & 3) * 32 + (pr >> 2)) * 2;
+  auto issue = [&](int ch) {
+    if (ch < nch) {
+      const int c0 = ch * CH;
+      T* xd = xs(ch % kGateStages);
+      double* wd = ws(ch % kGateStages);
+      const bool cok = c0 + x_c < d;
+#pragma unroll
+      for (int r = 0; r < XPT; ++r) {
+        const int t = x_t0 + r * (NT / (CH / V));
+        const bool ok = cok && tok0 + t < N;
+        cp_async16(xd + t * C::XROW + x_c, ok ? x + (tok0 + t) * int64_t(d) + c0 + x_c : x, ok);
+      }
+      const bool wok = c0 + 2 * pr < d;
+      for (int b = b_first; b < bits; b += NT / (CH / 2))
+        cp_async16(wd + b * CH + w_dst, wok ? proj + size_t(b) * d + c0 + 2 * pr : proj, wok);
+    }
+    cp_async_commit();
+  };
+
+  double acc[TW][BMAX], xx[TW], ww[BMAX];
+#pragma unroll
+  for (int t = 0; t < TW; ++t) {
+    xx[t] = 0.0;
+#pragma unroll
+    for (int b = 0; b < BMAX; ++b) acc[t][b] = 0.0;
+  }
+#pragma unroll
+  for (int b = 0; b < BMAX; ++b) ww[b] = 0.0;
+
+  for (int ch = 0; ch < kGateStages - 1; ++ch) issue(ch);
+  for (int ch = 0; ch < nch; ++ch) {
+    cp_async_wait<kGateStages - 2>();
+    __syncthreads();
+    issue(ch + kGateStages - 1);
+    const T* xb = xs(ch % kGateStages) + (warp * TW) * C::XROW + lane * 8;
+    const double* wb = ws(ch % kGateStages) + lane * 2;
+    double xv[TW][8];
+#pragma unroll
+    for (int t = 0; t < TW; ++t) {
+      if constexpr (sizeof(T) == 2) {
+        const uint4 raw = *reinterpret_cast<const uint4*>(xb + t * C::XROW);
+        const T* e = reinterpret_cast<const T*>(&raw);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) xv[t][i] = double(load_as_f32(e, i));
+      } else {
+        const float4 r0 = *reinterpret_cast<const float4*>(xb + t * C::XROW);
+        const float4 r1 = *reinterpret_cast<const float4*>(xb + t * C::XROW + 4);
+        xv[t][0] = r0.x; xv[t][1] = r0.y; xv[t][2] = r0.z; xv[t][3] = r0.w;
+        xv[t][4] = r1.x; xv[t][5] = r1.y; xv[t][6] = r1.z; xv[t][7] = r1.w;
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) xx[t] = fma(xv[t][i], xv[t][i], xx[t]);
+    }
+#pragma unroll
+    for (int b = 0; b < BMAX; ++b) {
+      if (b < bits) {
+        double wv[8];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const double2 q = *reinterpret_cast<const double2*>(wb + b * CH + k * 64);
+          wv[2 * k] = q.x;
+          wv[2 * k + 1] = q.y;
+        }
+        if ((b & (kLshFastWarps - 1)) == warp) {  // each warp sums the norms of its bits
+#pragma unroll
+          for (int i = 0; i < 8; ++i) ww[b] = fma(wv[i], wv[i], ww[b]);
+        }
+#pragma unroll
+        for (int t = 0; t < TW; ++t)
+#pragma unroll
+          for (int i = 0; i < 8; ++i) acc[t][b] = fma(xv[t][i], wv[i], acc[t][b]);
+      }
+    }
+  }
+  cp_async_wait<0>();
+  // butterfly: every lane ends with the full sums
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+    for (int t = 0; t < TW; ++t) {
+      xx[t] += __shfl_xor_sync(0xffffffffu, xx[t], off);
+#pragma unroll
+      for (int b = 0; b < BMAX; ++b) acc[t][b] += __shfl_xor_sync(0xffffffffu, acc[t][b], off);
+    }
+#pragma unroll
+    for (int b = 0; b < BMAX; ++b) ww[b] += __shfl_xor_sync(0xffffffffu, ww[b], off);
+  }
+  if (lane == 0)
+#pragma unroll
+    for (int b = 0; b < BMAX; ++b) wnorm[warp * BMAX + b] = ww[b];
+  __syncthreads();
+  // lane j < TW*bits decides pair (t, b) = (j / bits, j % bits) of this warp
+  const int64_t wtok0 = tok0 + warp * TW;
+  uint32_t mybit = 0;
+  const int j = lane;
+  const int t = j / bits, b = j % bits;
+  if (j < TW * bits && wtok0 + t < N) {
+    double S = 0.0, xn = 0.0;
+#pragma unroll
+    for (int tt = 0; tt < TW; ++tt)
+#pragma unroll
+      for (int bb = 0; bb < BMAX; ++bb)
+        if (tt == t && bb == b) { S = acc[tt][bb]; xn = xx[tt]; }
+    const double wn = wnorm[(b & (kLshFastWarps - 1)) * BMAX + b];
+    const double thr = 8.0 * double(d) * 0x1p-53 * sqrt(xn) * sqrt(wn) + 0x1p-1000;
+    bool bit;
+    if (xn == 0.0) {
+      bit = true;  // all products are +-0: the chain stays +0, and +0 >= 0
+    } else if (!force_exact && fabs(S) > thr) {
+      bit = S > 0.0;
+    } else {  // ambiguous, NaN or Inf: the reference's sequential chain
+      const T* xr = x + (wtok0 + t) * int64_t(d);
+      const double* wr = proj + size_t(b) * d;
+      double dot = 0.0;
+      for (int i = 0; i < d; ++i)
+        dot = __dadd_rn(dot, __dmul_rn(double(load_as_f32(xr, i)), wr[i]));
+      bit = dot >= 0.0;
+    }
+    mybit = bit ? (1u << b) : 0u;
+  }
+  // OR the bits of each token: lanes t*bits .. t*bits+bits-1
+  uint32_t code = 0;
+#pragma unroll
+  for (int tt = 0; tt < TW; ++tt) {
+    uint32_t part = (j < TW * bits && t == tt) ? mybit : 0u;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) part |= __shfl_xor_sync(0xffffffffu, part, off);
+    if (lane == tt) code = part;
+  }
+  if (lane < TW && wtok0 + lane < N) {
+    const int64_t tk = wtok0 + lane;
+    const int e = int(code % uint32_t(E));
+    if (codes) codes[tk] = code;
+    topk_idx[tk] = e;
+    topk_w[tk] = 1.0f;
+    atomicAdd(&counts[e], 1);
+  }
+}
+
+// INFMOE_LSH_FORCE_EXACT=1: every bit through the exact chain of the fast
+// kernel (tests); INFMOE_LSH_FAST=0: the all-sequential ring kernel.
+int lsh_env(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v ? std::atoi(v) : dflt;
+}
+
+template <typename T, int BMAX>
+void lsh_fast_go(const void* x, int64_t N, int d, const double* proj, int bits, int E,
+                 uint32_t* codes, int32_t* idx, float* w, int32_t* counts, cudaStream_t s) {
+  static const int force = lsh_env("INFMOE_LSH_FORCE_EXACT", 0);
+  using C = LshFastCfg<T, BMAX>;
+  auto kern = gate_lsh_fast_kernel<T, BMAX>;
+  static bool configured = false;
+  if (!configured) {
+    INFMOE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM)));
+    configured = true;
+  }
+  const unsigned blocks = unsigned((N + C::TB - 1) / C::TB);
+  kern<<<blocks, kLshFastWarps * 32, C::smem_bytes(bits), s>>>(
+      reinterpret_cast<const T*>(x), N, d, proj, bits, E, force, codes, idx, w, counts);
+}
+
 template <typename T, int EQ, int TPW>
 void softmax_go(const void* x, int64_t N, int d, const float* wg, const float* bias, int E, int k,
                 int32_t* idx, float* w, int32_t* counts, cudaStream_t s) {
@@ -417,6 +648,19 @@ void launch_gate_lsh(const void* x, int dtype, int64_t N, int d, const double* p
           "lsh gate: x and proj must be 16-byte aligned");
   INFMOE_CUDA(cudaMemsetAsync(counts, 0, sizeof(int32_t) * size_t(E), stream));
   if (N == 0) return;
+  static const int fast = lsh_env("INFMOE_LSH_FAST", 1);
+  if (fast && bits <= 8) {
+    const bool bf = dtype == kDtypeBf16;
+    if (bits <= 4) {
+      if (bf) lsh_fast_go<__nv_bfloat16, 4>(x, N, d, proj, bits, E, codes, topk_idx, topk_w, counts, stream);
+      else lsh_fast_go<float, 4>(x, N, d, proj, bits, E, codes, topk_idx, topk_w, counts, stream);
+    } else {
+      if (bf) lsh_fast_go<__nv_bfloat16, 8>(x, N, d, proj, bits, E, codes, topk_idx, topk_w, counts, stream);
+      else lsh_fast_go<float, 8>(x, N, d, proj, bits, E, codes, topk_idx, topk_w, counts, stream);
+    }
+    INFMOE_LAUNCH_CHECK();
+    return;
+  }
   const int G = 32 / bits;
   const int TB = kLshWarps * G;
   const int64_t blocks = (N + TB - 1) / TB;
