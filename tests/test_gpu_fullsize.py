@@ -1,4 +1,4 @@
-"""Full-size parity on the GPU (BASELINE.json's C2/C3 layer and C5), through
+"""Full-size parity on the GPU (BASELINE.json's C1, C2/C3 layer and C5), through
 size-independent properties plus a sampled oracle check:
 
 * routing: counts bit-exact against the reference (`route_tokens`,
@@ -145,5 +145,56 @@ def test_c5_layer_fullsize(cuda):
     np.testing.assert_allclose(w_g.cpu().numpy().reshape(N, k), w, rtol=1e-5, atol=1e-7)
     n = _sampled_oracle_check(x_host, hi, ho, y_off, idx, w, {0, 1, 2}, d, f, k)
     assert n >= 8
+    res.close()
+    off.close()
+
+
+def test_c1_layer_fullsize(cuda):
+    """C1: N=512, d=768, f=3072, E=8, top-1 softmax gate, fp32 (tf32 tensor cores);
+    every token against the fp64 oracle chain, resident and offloaded (K=2)."""
+    N, d, f, E, k, K = 512, 768, 3072, 8, 1, 2
+    g = torch.Generator(device="cpu").manual_seed(921)
+    x = torch.randn(N, d, generator=g)
+    wi = torch.randn(E, f, d, generator=g) / math.sqrt(d)
+    wo = torch.randn(E, d, f, generator=g) * (GELU_GAIN / math.sqrt(f))
+    gw = (torch.randn(E, d, generator=g) / math.sqrt(d)).numpy()
+    hw = im.Hardware(1643.6e12, 55.5e9, 180 << 30, 8 << 30)
+    kw = dict(dtype="f32", gate="softmax", gate_weight=gw, max_tokens=N)
+    res = dv.MoELayer(d, f, E, k, wi.to(cuda), wo.to(cuda), **kw)
+    off = dv.MoELayer(d, f, E, k, wi.pin_memory(), wo.pin_memory(), offloaded=True, K=K, hw=hw,
+                      **kw)
+    xc = x.to(cuda)
+    y_res, info_r = res.forward(xc)
+    y_off, info = off.forward(xc)
+    torch.cuda.synchronize()
+    assert torch.equal(y_res, y_off)
+    xf = np.ascontiguousarray(x.numpy())
+    idx = np.zeros((N, k), np.int32)
+    w = np.zeros((N, k), np.float32)
+    cnt = np.zeros(E, np.int32)
+    O.or_gate_softmax(ptr(xf), N, d, ptr(np.ascontiguousarray(gw)), None, E, k, ptr(idx), ptr(w),
+                      ptr(cnt))
+    assert np.array_equal(info["counts"], cnt)
+    g4 = im.make_geometry(d, f, E, 4)  # fp32 experts: 4 bytes per parameter
+    cv = im.compute_costs(np.asarray(info["counts"], np.uint64), g4, hw)
+    want = schedule("ref" if REF is not None else "or", cv.alphas, cv.beta, K, "auto")[1]
+    assert list(info["order"]) == want
+    off_ = np.zeros(E + 1, np.int32)
+    perm = np.zeros(N * k, np.int32)
+    inv = np.zeros(N * k, np.int32)
+    O.or_dispatch(ptr(idx), N, k, E, ptr(off_), ptr(perm), ptr(inv))
+    xp = np.ascontiguousarray(xf[perm // k])
+    yp = np.zeros((N * k, d), np.float32)
+    wif, wof = wi.numpy(), wo.numpy()
+    for e in range(E):
+        a, b = off_[e], off_[e + 1]
+        if b > a:
+            O.or_expert_ffn(ptr(np.ascontiguousarray(xp[a:b])), b - a, d, f,
+                            ptr(np.ascontiguousarray(wif[e])), ptr(np.ascontiguousarray(wof[e])),
+                            0, ptr(yp[a:b]))  # fp32 path keeps H in fp32
+    ref = np.zeros((N, d), np.float32)
+    O.or_combine(ptr(yp), ptr(inv), ptr(w), N, k, d, ptr(ref))
+    err = np.abs(y_off.cpu().numpy() - ref)
+    assert np.all(err <= 2e-2 + 2e-2 * np.abs(ref)), float(err.max())
     res.close()
     off.close()
