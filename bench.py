@@ -375,6 +375,10 @@ def main() -> None:
     x_host.copy_(x_dev)
     y_host = torch.empty((N, d), dtype=bf, pin_memory=True)
 
+    # one pool of K+1 expert slots shared by all offloaded layers: K experts on
+    # the GPU for the whole stack, as the reference's resident_capacity models it
+    pool = dv.SlotPool(cfg["K"], d, f, device=local)
+
     def make_layers(offloaded: bool):
         out = []
         for l in range(L):
@@ -383,7 +387,8 @@ def main() -> None:
             out.append(dv.MoELayer(d, f, E, k, wi, wo, gate="lsh",
                                    lsh_seed=im.derive_seed(SEED, 100 + l), lsh_bits=cfg["bits"],
                                    offloaded=offloaded, K=cfg["K"], max_tokens=N, device=local,
-                                   hw=hw, ep_size=P, ep_rank=rank, ep_comm=comm))
+                                   hw=hw, ep_size=P, ep_rank=rank, ep_comm=comm,
+                                   slot_pool=pool if offloaded else None))
         return out
 
     off_layers = make_layers(True)
@@ -558,7 +563,9 @@ def main() -> None:
         "data": "synthetic (counter-hash uniform, unit variance; random-init expert weights)",
         "config": {"workload": cfg["workload"], "tokens": N_glob, "layers": L, "d_model": d,
                    "d_ff": f, "experts": E, "top_k": k, "gate": cfg["gate"], "K": cfg["K"],
-                   "device_slots": cfg["K"] + 1, "policy": "infmoe_greedy(auto_order)",
+                   "device_slots": cfg["K"] + 1,
+                   "slot_pool": "one pool of K+1 slots shared by all layers",
+                   "policy": "infmoe_greedy(auto_order)",
                    "host_weight_sets": n_sets,
                    "parallelism": f"ep{P}" if P > 1 else "single",
                    "l2": "inputs larger than L2 (5.37 GB of expert weights per layer)"},
@@ -598,6 +605,7 @@ def main() -> None:
         print(json.dumps(line), flush=True)
     for lay in off_layers + res_layers:
         lay.close()
+    pool.close()
     if comm is not None:
         im.ep_comm_destroy(comm)
     if world > 1:

@@ -232,6 +232,13 @@ int infmoe_combine(const void* y_perm, int32_t dtype, const int32_t* inv,
 
 /* ---- the layer handle (N6 offload executor + N8) ---------------------- */
 typedef struct infmoe_layer infmoe_layer;
+/* A device pool of K+1 expert slots (W_in + W_out each) that offloaded layers
+ * of one shape share: the InfMoE memory model, K experts resident on the GPU
+ * for the whole stack plus the one load in flight (resident_capacity,
+ * cost_model.hpp:65).  Layers sharing a pool must be forwarded one
+ * after another on one stream (a layer's loads start after the previous
+ * layer's computes: the reference's drain mode, simulator.hpp:131-133). */
+typedef struct infmoe_slot_pool infmoe_slot_pool;
 typedef struct {
   int32_t d_model, d_ff, n_experts, top_k;
   int32_t dtype;      /* INFMOE_DTYPE_* */
@@ -260,6 +267,8 @@ typedef struct {
   /* skip_empty_experts (scenario.hpp:99; default off as in the
    * reference): experts that received no rows are neither scheduled nor loaded */
   int32_t skip_empty_experts;
+  /* offloaded: shared slot pool (NULL: the handle owns its own K+1 slots) */
+  infmoe_slot_pool* slot_pool;
 } infmoe_layer_desc;
 
 /* per-forward outputs (all optional; host pointers unless noted) */
@@ -286,6 +295,11 @@ int infmoe_ep_plan(int32_t P, int32_t rank, int32_t E, const int32_t* send_count
 int infmoe_ep_get_unique_id(uint8_t id[128]);
 int infmoe_ep_comm_init(const uint8_t id[128], int32_t nranks, int32_t rank, void** comm);
 int infmoe_ep_comm_destroy(void* comm);
+
+/* K+1 slots of expert_matrix_bytes (= d_ff * d_model * bytes/param) per matrix */
+int infmoe_slot_pool_create(int32_t device, int32_t K, uint64_t expert_matrix_bytes,
+                            infmoe_slot_pool** out);
+int infmoe_slot_pool_destroy(infmoe_slot_pool* pool);
 
 int infmoe_layer_create(const infmoe_layer_desc* desc, infmoe_layer** out);
 /* x, y: device [N, d_model] in dtype; stream: cudaStream_t or NULL. */

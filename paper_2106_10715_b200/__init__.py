@@ -123,7 +123,7 @@ class LayerDesc(C.Structure):
                 ("lsh_seed", C.c_uint64), ("lsh_bits", C.c_int32),
                 ("w_in", C.c_void_p), ("w_out", C.c_void_p), ("hw", Hardware),
                 ("ep_size", C.c_int32), ("ep_rank", C.c_int32), ("ep_comm", C.c_void_p),
-                ("skip_empty_experts", C.c_int32)]
+                ("skip_empty_experts", C.c_int32), ("slot_pool", C.c_void_p)]
 
 
 class ForwardOut(C.Structure):
@@ -189,6 +189,8 @@ _lib.infmoe_layer_create.argtypes = [_P(LayerDesc), _P(_vp)]
 _lib.infmoe_layer_forward.argtypes = [_vp, _vp, C.c_int64, _vp, _P(ForwardOut), _vp]
 _lib.infmoe_layer_set_host_weights.argtypes = [_vp, _vp, _vp]
 _lib.infmoe_layer_destroy.argtypes = [_vp]
+_lib.infmoe_slot_pool_create.argtypes = [_i32, _i32, _u64, _P(_vp)]
+_lib.infmoe_slot_pool_destroy.argtypes = [_vp]
 
 
 def _f64arr(a) -> np.ndarray:

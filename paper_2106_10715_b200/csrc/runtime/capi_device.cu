@@ -216,6 +216,39 @@ int infmoe_combine(const void* y_perm, int32_t dtype, const int32_t* inv, const 
   });
 }
 
+int infmoe_slot_pool_create(int32_t device, int32_t K, uint64_t expert_matrix_bytes,
+                            infmoe_slot_pool** out) {
+  return guarded([&] {
+    require(out != nullptr, "slot_pool_create: NULL argument");
+    *out = nullptr;
+    require(K >= 1, "slot_pool_create: K must be >= 1");
+    require(expert_matrix_bytes > 0, "slot_pool_create: expert_matrix_bytes must be > 0");
+    INFMOE_CUDA(cudaSetDevice(device));
+    auto* p = new SlotPool{device, K, K + 1, size_t(expert_matrix_bytes), nullptr, nullptr};
+    const size_t n = size_t(p->n_slots) * p->matrix_bytes;
+    cudaError_t e1 = cudaMalloc(&p->slot_in, n);
+    cudaError_t e2 = e1 == cudaSuccess ? cudaMalloc(&p->slot_out, n) : e1;
+    if (e2 != cudaSuccess) {
+      if (p->slot_in) cudaFree(p->slot_in);
+      delete p;
+      INFMOE_CUDA(e2);
+    }
+    *out = reinterpret_cast<infmoe_slot_pool*>(p);
+  });
+}
+
+int infmoe_slot_pool_destroy(infmoe_slot_pool* pool) {
+  return guarded([&] {
+    if (!pool) return;
+    auto* p = reinterpret_cast<SlotPool*>(pool);
+    cudaSetDevice(p->device);
+    cudaDeviceSynchronize();  // no layer may still be copying into the slots
+    cudaFree(p->slot_in);
+    cudaFree(p->slot_out);
+    delete p;
+  });
+}
+
 int infmoe_layer_create(const infmoe_layer_desc* desc, infmoe_layer** out) {
   return guarded([&] {
     require(desc && out, "layer_create: NULL argument");

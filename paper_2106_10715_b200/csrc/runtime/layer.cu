@@ -113,9 +113,20 @@ Layer::Layer(const infmoe_layer_desc& d) : desc(d) {
   expert_in_bytes = size_t(d.d_ff) * d.d_model * esz;
   if (d.residency == INFMOE_OFFLOADED) {
     require(d.K >= 1, "layer: offloaded mode needs K >= 1");
-    n_slots = std::min(d.K + 1, n_local + 1);
-    slot_in = dalloc<uint8_t>(size_t(n_slots) * expert_in_bytes, owned);
-    slot_out = dalloc<uint8_t>(size_t(n_slots) * expert_in_bytes, owned);
+    if (d.slot_pool) {  // K+1 slots shared with the other layers of the stack
+      const auto* pool = reinterpret_cast<const SlotPool*>(d.slot_pool);
+      require(pool->device == d.device, "layer: slot pool lives on another device");
+      require(pool->K == d.K, "layer: slot pool K differs from the layer's K");
+      require(pool->matrix_bytes == expert_in_bytes,
+              "layer: slot pool expert size differs from the layer's");
+      n_slots = pool->n_slots;
+      slot_in = pool->slot_in;
+      slot_out = pool->slot_out;
+    } else {
+      n_slots = std::min(d.K + 1, n_local + 1);
+      slot_in = dalloc<uint8_t>(size_t(n_slots) * expert_in_bytes, owned);
+      slot_out = dalloc<uint8_t>(size_t(n_slots) * expert_in_bytes, owned);
+    }
     INFMOE_CUDA(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
     const size_t E = size_t(n_local);
     for (auto* v : {&load_done, &compute_done}) {

@@ -12,6 +12,14 @@
 
 namespace infmoe {
 
+// K+1 shared expert slots (infmoe_slot_pool)
+struct SlotPool {
+  int device = 0, K = 0, n_slots = 0;
+  size_t matrix_bytes = 0;
+  uint8_t* slot_in = nullptr;
+  uint8_t* slot_out = nullptr;
+};
+
 struct Layer {
   explicit Layer(const infmoe_layer_desc& d);
   ~Layer();

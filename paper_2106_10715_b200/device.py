@@ -181,6 +181,32 @@ def combine(y_perm, inv, topk_w, N: int, k: int):
     return y
 
 
+class SlotPool:
+    """K+1 device expert slots shared by the offloaded layers of a stack
+    (infmoe_slot_pool: K experts resident on the GPU in total + one in flight)."""
+
+    def __init__(self, K: int, d_model: int, d_ff: int, dtype: str = "bf16", device: int = 0):
+        esz = 2 if dtype == "bf16" else 4
+        self.K = K
+        self._h = C.c_void_p()
+        _check(_lib.infmoe_slot_pool_create(device, K, d_model * d_ff * esz, C.byref(self._h)))
+
+    @property
+    def handle(self):
+        return self._h.value
+
+    def close(self) -> None:
+        if self._h:
+            _lib.infmoe_slot_pool_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+
 class MoELayer:
     """Owning wrapper of an infmoe_layer handle (the paper's MoE plugin)."""
 
@@ -189,7 +215,8 @@ class MoELayer:
                  lsh_seed: int = 0, lsh_bits: int = 5, offloaded: bool = False, K: int = 4,
                  policy: int = POLICY_AUTO, max_tokens: int = 4096, device: int = 0,
                  hw: Optional[Hardware] = None, ep_size: int = 1, ep_rank: int = 0,
-                 ep_comm: Optional[int] = None, skip_empty_experts: bool = False):
+                 ep_comm: Optional[int] = None, skip_empty_experts: bool = False,
+                 slot_pool: Optional["SlotPool"] = None):
         d = LayerDesc()
         d.d_model, d.d_ff, d.n_experts, d.top_k = d_model, d_ff, n_experts, top_k
         d.dtype = DTYPE_BF16 if dtype == "bf16" else DTYPE_F32
@@ -211,6 +238,9 @@ class MoELayer:
         d.hw = hw if hw is not None else Hardware(1643.6e12, 55.5e9, 180 << 30, 8 << 30)
         d.ep_size, d.ep_rank, d.ep_comm = ep_size, ep_rank, ep_comm
         d.skip_empty_experts = int(skip_empty_experts)
+        if slot_pool is not None:
+            d.slot_pool = slot_pool.handle
+            self._keep.append(slot_pool)  # the pool outlives the layer
         self.desc = d
         self.n_experts = n_experts
         self.n_local = n_experts // max(ep_size, 1)

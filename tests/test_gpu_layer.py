@@ -211,3 +211,49 @@ def test_resident_stack_cuda_graph_replay_matches_eager(cuda):
     assert torch.equal(out.view(torch.int16), eager.view(torch.int16))
     for lay in layers:
         lay.close()
+
+
+def test_offloaded_stack_shares_one_slot_pool(cuda):
+    """Offloaded layers of a stack sharing ONE pool of K+1 slots (the InfMoE
+    memory model: K experts on the GPU in total) give the same bits as layers
+    with private slots and as the resident stack; every layer's measured
+    timeline passes replay_check with <= K+1 residents; a pool of another K or
+    expert size is rejected."""
+    N, d, f, E, K, L = 700, 256, 384, 8, 2, 3
+    sets = [_setup(cuda, N, d, f, E, seed=50 + l)[1] for l in range(L)]
+    x = sets[0][0]
+    pool = dv.SlotPool(K, d, f)
+    kw = dict(gate="lsh", lsh_bits=3, max_tokens=N)
+    shared = [dv.MoELayer(d, f, E, 1, s[1].pin_memory(), s[2].pin_memory(), lsh_seed=60 + l,
+                          offloaded=True, K=K, slot_pool=pool, **kw) for l, s in enumerate(sets)]
+    private = [dv.MoELayer(d, f, E, 1, s[1].pin_memory(), s[2].pin_memory(), lsh_seed=60 + l,
+                           offloaded=True, K=K, **kw) for l, s in enumerate(sets)]
+    resident = [dv.MoELayer(d, f, E, 1, s[1].to(cuda), s[2].to(cuda), lsh_seed=60 + l, **kw)
+                for l, s in enumerate(sets)]
+    outs, infos = [], []
+    for stack in (shared, private, resident):
+        cur = x
+        for lay in stack:
+            cur, info = lay.forward(cur, want_timeline=stack is shared)
+            if stack is shared:
+                infos.append(info)
+        outs.append(cur)
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0].view(torch.int16), outs[1].view(torch.int16))
+    assert torch.equal(outs[0].view(torch.int16), outs[2].view(torch.int16))
+    g = im.make_geometry(d, f, E, 2)
+    hw = im.Hardware(1643.6e12, 55.5e9, 180 << 30, 8 << 30)
+    for info in infos:
+        cv = im.compute_costs(info["counts"].astype(np.uint64), g, hw)
+        assert im.replay_check(info["events"], [cv], K + 1, check_durations=False,
+                               tol_s=2e-6) == {}
+    with pytest.raises(ValueError):
+        dv.MoELayer(d, f, E, 1, sets[0][1].pin_memory(), sets[0][2].pin_memory(), lsh_seed=1,
+                    offloaded=True, K=K + 1, slot_pool=pool, **kw)
+    with pytest.raises(ValueError):
+        dv.MoELayer(d, 2 * f, E, 1, torch.zeros(E, 2 * f, d, dtype=torch.bfloat16).pin_memory(),
+                    torch.zeros(E, d, 2 * f, dtype=torch.bfloat16).pin_memory(), lsh_seed=1,
+                    offloaded=True, K=K, slot_pool=pool, **kw)
+    for lay in shared + private + resident:
+        lay.close()
+    pool.close()
