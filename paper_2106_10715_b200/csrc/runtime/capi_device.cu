@@ -261,7 +261,7 @@ int infmoe_layer_create(const infmoe_layer_desc* desc, infmoe_layer** out) {
 int infmoe_layer_forward(infmoe_layer* layer, const void* x, int64_t N, void* y,
                          infmoe_forward_out* out, void* stream) {
   return guarded([&] {
-    require(layer && layer->impl && x && y, "layer_forward: NULL argument");
+    require(layer && layer->impl && (N == 0 || (x && y)), "layer_forward: NULL argument");
     layer->impl->forward(x, N, y, out, as_stream(stream));
   });
 }

@@ -257,3 +257,35 @@ def test_offloaded_stack_shares_one_slot_pool(cuda):
     for lay in shared + private + resident:
         lay.close()
     pool.close()
+
+
+@pytest.mark.parametrize("gate,k", [("lsh", 1), ("softmax", 2)])
+@pytest.mark.parametrize("offloaded", [False, True])
+def test_layer_edge_token_counts(cuda, gate, k, offloaded):
+    """N = 0 (nothing routed: every expert empty) and N = 1 through the layer
+    handle, resident and offloaded; N = 1 matches the oracle chain."""
+    N, d, f, E = 64, 256, 384, 6
+    (xb, wib, wob), (x, wi, wo) = _setup(cuda, N, d, f, E, seed=71)
+    gw = (np.random.default_rng(1).standard_normal((E, d)) / np.sqrt(d)).astype(np.float32)
+    wts = (wi.pin_memory(), wo.pin_memory()) if offloaded else (wi.to(cuda), wo.to(cuda))
+    layer = dv.MoELayer(d, f, E, k, *wts, gate=gate, gate_weight=gw, lsh_seed=9, lsh_bits=3,
+                        offloaded=offloaded, K=2, max_tokens=N)
+    y0, info0 = layer.forward(x[:0])
+    torch.cuda.synchronize()
+    assert y0.shape == (0, d) and int(info0["counts"].sum()) == 0
+    y1, info1 = layer.forward(x[:1])
+    torch.cuda.synchronize()
+    xf = bf16_bits_to_f32(xb).reshape(N, d)[:1].copy()
+    idx = np.zeros((1, k), np.int32)
+    w = np.zeros((1, k), np.float32)
+    cnt = np.zeros(E, np.int32)
+    if gate == "lsh":
+        proj = np.ascontiguousarray(im.gating_projection(9, 3, d))
+        O.or_gate_lsh(ptr(xf), 1, d, ptr(proj), 3, E, ptr(idx), ptr(w), ptr(cnt))
+    else:
+        O.or_gate_softmax(ptr(xf), 1, d, ptr(gw), None, E, k, ptr(idx), ptr(w), ptr(cnt))
+    assert np.array_equal(info1["counts"], cnt)
+    ref = _oracle_layer(xb[:d], wib, wob, 1, d, f, E, k, idx, w)
+    err = np.abs(y1.float().cpu().numpy() - ref)
+    assert np.all(err <= ATOL + RTOL * np.abs(ref)), err.max()
+    layer.close()
