@@ -680,8 +680,30 @@ void or_gate_softmax(const float* x, uint64_t N, int d, const float* wg,
       const float* xr = x + t * (uint64_t)d;
       for (int e = 0; e < E; ++e) {
         const float* wr = wg + (uint64_t)e * (uint64_t)d;
-        float acc = 0.0f;
-        for (int c = 0; c < d; ++c) acc = fmaf(xr[c], wr[c], acc);
+        /* the gate's reduction order (gate.cu N1a): d is walked in chunks of
+         * 256 columns; lane l (of 32) owns columns 8l..8l+7 of every chunk
+         * and keeps one fmaf chain over them in ascending order (columns past
+         * d, up to the chunk end, contribute fmaf(0, 0, acc)); the 32 partial
+         * sums are then combined by a butterfly (offsets 16, 8, 4, 2, 1:
+         * p[l] = p[l] + p[l ^ off]) and the bias is added last */
+        float part[32];
+        const int dpad = (d + 255) / 256 * 256;
+        for (int l = 0; l < 32; ++l) {
+          float acc = 0.0f;
+          for (int c0 = 0; c0 < dpad; c0 += 256)
+            for (int i = 0; i < 8; ++i) {
+              const int c = c0 + 8 * l + i;
+              const float xv = c < d ? xr[c] : 0.0f, wv = c < d ? wr[c] : 0.0f;
+              acc = fmaf(xv, wv, acc);
+            }
+          part[l] = acc;
+        }
+        for (int off = 16; off > 0; off >>= 1) {
+          float nxt[32];
+          for (int l = 0; l < 32; ++l) nxt[l] = part[l] + part[l ^ off];
+          for (int l = 0; l < 32; ++l) part[l] = nxt[l];
+        }
+        float acc = part[0];
         if (bias) acc = acc + bias[e];
         lg[e] = acc;
       }

@@ -104,8 +104,11 @@ int or_replay_check(const or_event* ev, int n_ev, int n_layers, const int* T,
                     int check_durations, int* kinds6);
 
 /* ---- MoE layer forward (parity UNPINNED by the reference) --------------- */
-/* softmax/top-k gate.  logits[t][e] = fmaf-chain over c = 0..d-1 ascending of
- * x[t][c] * wg[e][c] starting at +0.0f, then + bias[e] (one fp32 add).  top-k
+/* softmax/top-k gate.  logits[t][e] = x[t] . wg[e] in fp32 in the gate
+ * kernel's warp order: 32 lane-partial fmaf chains (lane l owns columns
+ * 8l..8l+7 of every 256-column chunk, ascending, zero-padded to the chunk),
+ * combined by the butterfly p[l] += p[l^off], off = 16..1; then + bias[e] (one
+ * fp32 add).  top-k
  * by repeated strict-greater argmax (ties -> lower expert index, NaN never
  * wins; all-NaN -> expert 0 then 1).  Weights: softmax probabilities in fp64,
  * renormalised over the k picks when k > 1. */

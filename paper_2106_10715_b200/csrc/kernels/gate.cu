@@ -54,158 +54,145 @@ __device__ __forceinline__ void cp_async_wait() {
 }
 
 // ---------------------------------------------------------------- N1a ----
-// Register-tiled logits: a warp's 32 lanes are 8 expert-groups x 4
-// token-groups; lane (eg, tg) owns experts {eg + 8q : q < EQ} for tokens
-// {tg*TPW + t : t < TPW}, i.e. EQ*TPW independent fmaf chains, each walking d
-// in ascending order (so every logit is bit-identical to oracle.c
-// or_gate_softmax).  Per 4 columns a lane issues TPW + EQ shared loads (x rows
-// broadcast within a token-group, gate-weight rows broadcast within an
-// expert-group) for 4*EQ*TPW FMAs.  Selection (top-k, softmax) then runs one
-// warp per token from the logits tile in shared memory.
-constexpr int kSoftWarps = 4;
+// Softmax / top-k gate.  The logit reduction order is defined by the warp
+// (the reference leaves this gate unspecified; oracle.c
+// or_gate_softmax restates the same order): d is walked in 256-column chunks,
+// lane l owns columns 8l..8l+7 of every chunk and keeps one fmaf chain per
+// (token, expert) over them; the 32 lane partials are combined by a butterfly
+// (p += shfl_xor(p, off), off = 16..1), then the bias is added.  So a warp
+// streams 16-byte slices of x and W_g with no dependent chain longer than d/32
+// steps.  A CTA owns TT tokens and all experts: warp w holds experts
+// [w*EB, w*EB+EB) for the TT tokens (TT*EB = 64 accumulators per lane), the
+// x tile of a chunk is staged once per CTA through the cp.async ring, and the
+// gate weights (E x d fp32, L1/L2-resident) are read straight from global.
+// Selection (top-k, softmax) then runs one warp per token from the logits
+// tile in shared memory.
+constexpr int kSoftChunk = 256;
 
-template <typename T, int EQ, int TPW>
+template <typename T, int EB>
 struct SoftCfg {
-  static constexpr int CH = EQ >= 16 ? 32 : 64;        // columns per stage
-  static constexpr int EP = 8 * EQ;                    // experts covered (padded)
-  static constexpr int TW = 4 * TPW;                   // tokens per warp
-  static constexpr int TB = kSoftWarps * TW;           // tokens per block
-  static constexpr int V = 16 / sizeof(T);             // x elements per 16 B
-  static constexpr int XROW = CH + V;                  // +16 B per row
-  static constexpr int WROW = CH + 4;
-  static constexpr size_t X_BYTES = size_t(TB) * XROW * sizeof(T);
-  static constexpr size_t W_BYTES = size_t(EP) * WROW * sizeof(float);
-  static constexpr size_t STAGE = X_BYTES + W_BYTES;
-  static constexpr size_t LG_BYTES = size_t(TB) * (EP + 1) * sizeof(float);
-  static constexpr size_t SMEM = kGateStages * STAGE + LG_BYTES;
+  static constexpr int TT = 64 / EB;                    // tokens per CTA
+  static constexpr int V = 16 / int(sizeof(T));         // x elements per 16 B
+  static constexpr int XROW = kSoftChunk + V;           // +16 B per row
+  static constexpr size_t STAGE = size_t(TT) * XROW * sizeof(T);
+  // warps per CTA (E <= MAXW*EB): 16 while the 64 accumulators + 4 weight
+  // slices fit 128 registers (EB <= 4), else 8
+  static constexpr int MAXW = EB <= 4 ? 16 : 8;
+  static size_t smem(int E) {
+    return kGateStages * STAGE + size_t(TT) * (E + 1) * sizeof(float);
+  }
 };
 
-template <typename T, int EQ, int TPW>
-__global__ void __launch_bounds__(kSoftWarps * 32) gate_softmax_kernel(
+template <typename T, int EB>
+__global__ void __launch_bounds__(SoftCfg<T, EB>::MAXW * 32) gate_softmax_kernel(
     const T* __restrict__ x, int64_t N, int d, const float* __restrict__ wg,
     const float* __restrict__ bias, int E, int k, int32_t* __restrict__ topk_idx,
     float* __restrict__ topk_w, int32_t* __restrict__ counts) {
-  using C = SoftCfg<T, EQ, TPW>;
-  constexpr int NT = kSoftWarps * 32;
+  using C = SoftCfg<T, EB>;
+  constexpr int TT = C::TT, V = C::V, CH = kSoftChunk;
   extern __shared__ __align__(16) uint8_t soft_smem[];
-  __shared__ int hist[C::EP];
-  float* lg_s = reinterpret_cast<float*>(soft_smem + kGateStages * C::STAGE);  // [TB][EP+1]
-
+  __shared__ int hist[128];
+  const int NT = blockDim.x, nwarps = NT / 32;
+  float* lg_s = reinterpret_cast<float*>(soft_smem + kGateStages * C::STAGE);  // [TT][E+1]
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int eg = lane % 8, tg = lane / 8;
-  const int64_t tok0 = int64_t(blockIdx.x) * C::TB;
-  for (int i = threadIdx.x; i < C::EP; i += NT) hist[i] = 0;
+  const int64_t tok0 = int64_t(blockIdx.x) * TT;
+  for (int i = threadIdx.x; i < E; i += NT) hist[i] = 0;
 
   auto xs = [&](int st) { return reinterpret_cast<T*>(soft_smem + st * C::STAGE); };
-  auto ws = [&](int st) { return reinterpret_cast<float*>(soft_smem + st * C::STAGE + C::X_BYTES); };
-  const int nch = (d + C::CH - 1) / C::CH;
+  const int nch = (d + CH - 1) / CH;
   auto issue = [&](int ch) {
     if (ch < nch) {
-      const int c0 = ch * C::CH;
+      const int c0 = ch * CH;
       T* xd = xs(ch % kGateStages);
-      float* wd = ws(ch % kGateStages);
-      for (int i = threadIdx.x; i < C::TB * (C::CH / C::V); i += NT) {
-        const int t = i / (C::CH / C::V), c = (i % (C::CH / C::V)) * C::V;
+      for (int i = threadIdx.x; i < TT * (CH / V); i += NT) {
+        const int t = i / (CH / V), c = (i % (CH / V)) * V;
         const bool ok = tok0 + t < N && c0 + c < d;
         cp_async16(xd + t * C::XROW + c, ok ? x + size_t(tok0 + t) * d + c0 + c : x, ok);
-      }
-      for (int i = threadIdx.x; i < C::EP * (C::CH / 4); i += NT) {
-        const int e = i / (C::CH / 4), c = (i % (C::CH / 4)) * 4;
-        const bool ok = e < E && c0 + c < d;
-        cp_async16(wd + e * C::WROW + c, ok ? wg + size_t(e) * d + c0 + c : wg, ok);
       }
     }
     cp_async_commit();  // empty groups keep the wait count uniform
   };
 
-  float acc[EQ][TPW];
+  float acc[TT][EB];
 #pragma unroll
-  for (int q = 0; q < EQ; ++q)
+  for (int t = 0; t < TT; ++t)
 #pragma unroll
-    for (int t = 0; t < TPW; ++t) acc[q][t] = 0.0f;
-  const int xrow0 = warp * C::TW + tg * TPW;
+    for (int e = 0; e < EB; ++e) acc[t][e] = 0.0f;
+  const int e0 = warp * EB;
 
   for (int ch = 0; ch < kGateStages - 1; ++ch) issue(ch);
   for (int ch = 0; ch < nch; ++ch) {
     cp_async_wait<kGateStages - 2>();  // chunk ch has landed (for this thread)
     __syncthreads();                   // ... for every thread; slot ch-1 is free
     issue(ch + kGateStages - 1);
-    const int cn = min(C::CH, d - ch * C::CH);
-    const T* xb = xs(ch % kGateStages);
-    const float* wb = ws(ch % kGateStages);
-    // software pipeline over 4-column groups: operands of group c+4 load while
-    // the FMAs of group c issue
-    auto load_x = [&](int c, float (&xv)[TPW][4]) {
+    const int c = ch * CH + lane * 8;  // this lane's 8 columns (zero past d)
+    const T* xb = xs(ch % kGateStages) + lane * 8;
+    constexpr int EG = EB < 4 ? EB : 4;  // experts whose weight slices sit in registers
 #pragma unroll
-      for (int t = 0; t < TPW; ++t) {
-        const T* xp = xb + (xrow0 + t) * C::XROW + c;
-        if constexpr (sizeof(T) == 2) {  // 4 bf16 = one 8-byte load
-          const uint2 raw = *reinterpret_cast<const uint2*>(xp);
-          xv[t][0] = __uint_as_float(raw.x << 16);
-          xv[t][1] = __uint_as_float(raw.x & 0xffff0000u);
-          xv[t][2] = __uint_as_float(raw.y << 16);
-          xv[t][3] = __uint_as_float(raw.y & 0xffff0000u);
-        } else {
-          const float4 raw = *reinterpret_cast<const float4*>(xp);
-          xv[t][0] = raw.x; xv[t][1] = raw.y; xv[t][2] = raw.z; xv[t][3] = raw.w;
-        }
+    for (int g = 0; g < EB; g += EG) {
+    float wv[EG][8];
+#pragma unroll
+    for (int e = 0; e < EG; ++e) {
+      float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
+      if (e0 + g + e < E && c < d) {
+        const float4* wp = reinterpret_cast<const float4*>(wg + size_t(e0 + g + e) * d + c);
+        a = __ldg(wp);
+        b = __ldg(wp + 1);
       }
-    };
-    auto load_w = [&](int c, float4 (&wv)[EQ]) {
+      wv[e][0] = a.x; wv[e][1] = a.y; wv[e][2] = a.z; wv[e][3] = a.w;
+      wv[e][4] = b.x; wv[e][5] = b.y; wv[e][6] = b.z; wv[e][7] = b.w;
+    }
 #pragma unroll
-      for (int q = 0; q < EQ; ++q)
-        wv[q] = *reinterpret_cast<const float4*>(wb + (eg + 8 * q) * C::WROW + c);
-    };
-    float xa[TPW][4];
-    float4 wa[EQ];
-    load_x(0, xa);
-    load_w(0, wa);
-    for (int c = 0; c < cn; c += 4) {  // d is a multiple of 4 (launcher check)
-      const int cnext = c + 4 < cn ? c + 4 : c;
-      float xn[TPW][4];
-      float4 wn[EQ];
-      load_x(cnext, xn);
-      load_w(cnext, wn);
+    for (int t = 0; t < TT; ++t) {
+      float xv[8];
+      if constexpr (sizeof(T) == 2) {
+        const uint4 raw = *reinterpret_cast<const uint4*>(xb + t * C::XROW);
+        xv[0] = __uint_as_float(raw.x << 16); xv[1] = __uint_as_float(raw.x & 0xffff0000u);
+        xv[2] = __uint_as_float(raw.y << 16); xv[3] = __uint_as_float(raw.y & 0xffff0000u);
+        xv[4] = __uint_as_float(raw.z << 16); xv[5] = __uint_as_float(raw.z & 0xffff0000u);
+        xv[6] = __uint_as_float(raw.w << 16); xv[7] = __uint_as_float(raw.w & 0xffff0000u);
+      } else {
+        const float4 r0 = *reinterpret_cast<const float4*>(xb + t * C::XROW);
+        const float4 r1 = *reinterpret_cast<const float4*>(xb + t * C::XROW + 4);
+        xv[0] = r0.x; xv[1] = r0.y; xv[2] = r0.z; xv[3] = r0.w;
+        xv[4] = r1.x; xv[5] = r1.y; xv[6] = r1.z; xv[7] = r1.w;
+      }
 #pragma unroll
-      for (int q = 0; q < EQ; ++q)
+      for (int e = 0; e < EG; ++e)
 #pragma unroll
-        for (int t = 0; t < TPW; ++t) {
-          acc[q][t] = fmaf(xa[t][0], wa[q].x, acc[q][t]);
-          acc[q][t] = fmaf(xa[t][1], wa[q].y, acc[q][t]);
-          acc[q][t] = fmaf(xa[t][2], wa[q].z, acc[q][t]);
-          acc[q][t] = fmaf(xa[t][3], wa[q].w, acc[q][t]);
-        }
-#pragma unroll
-      for (int t = 0; t < TPW; ++t)
-#pragma unroll
-        for (int i = 0; i < 4; ++i) xa[t][i] = xn[t][i];
-#pragma unroll
-      for (int q = 0; q < EQ; ++q) wa[q] = wn[q];
+        for (int i = 0; i < 8; ++i) acc[t][g + e] = fmaf(xv[i], wv[e][i], acc[t][g + e]);
+    }
     }
   }
   cp_async_wait<0>();
-  // logits (+ bias, one fp32 add) into shared memory
+  // butterfly over the 32 lane partials (every lane ends with the sum)
 #pragma unroll
-  for (int q = 0; q < EQ; ++q) {
-    const int e = eg + 8 * q;
+  for (int off = 16; off > 0; off >>= 1)
 #pragma unroll
-    for (int t = 0; t < TPW; ++t)
-      lg_s[(xrow0 + t) * (C::EP + 1) + e] =
-          (e < E && bias) ? __fadd_rn(acc[q][t], bias[e]) : acc[q][t];
-  }
+    for (int t = 0; t < TT; ++t)
+#pragma unroll
+      for (int e = 0; e < EB; ++e) acc[t][e] += __shfl_xor_sync(0xffffffffu, acc[t][e], off);
+  // logits (+ bias, one fp32 add) into shared memory: lane t writes token t
+#pragma unroll
+  for (int t = 0; t < TT; ++t)
+    if (lane == (t & 31))
+#pragma unroll
+      for (int e = 0; e < EB; ++e)
+        if (e0 + e < E)
+          lg_s[t * (E + 1) + e0 + e] = bias ? __fadd_rn(acc[t][e], bias[e0 + e]) : acc[t][e];
   __syncthreads();
 
-  constexpr int SQ = (C::EP + 31) / 32;  // logits per lane during selection
-  for (int tl = 0; tl < C::TW; ++tl) {
-    const int row = warp * C::TW + tl;
+  constexpr int SQ = 4;  // logits per lane during selection (E <= 128)
+  for (int row = warp; row < TT; row += nwarps) {
     const int64_t tok = tok0 + row;
+    if (tok >= N) break;
     float lg[SQ];
     bool live[SQ];
 #pragma unroll
     for (int q = 0; q < SQ; ++q) {
       const int e = lane + 32 * q;
       live[q] = e < E;
-      lg[q] = live[q] ? lg_s[row * (C::EP + 1) + e] : 0.0f;
+      lg[q] = live[q] ? lg_s[row * (E + 1) + e] : 0.0f;
     }
     // softmax denominator over all experts (fp32; weights are tolerance-checked)
     float mx = -INFINITY;
@@ -241,7 +228,7 @@ __global__ void __launch_bounds__(kSoftWarps * 32) gate_softmax_kernel(
       for (int q = 0; q < SQ; ++q)
         if (lane + 32 * q == best.i) live[q] = false;  // exclude from the next pick
     }
-    if (lane < k && tok < N) {
+    if (lane < k) {
       topk_idx[tok * k + lane] = ik_mine;
       topk_w[tok * k + lane] = k > 1 ? pk_mine / psum : pk_mine;
       atomicAdd(&hist[ik_mine], 1);
@@ -583,29 +570,31 @@ void lsh_fast_go(const void* x, int64_t N, int d, const double* proj, int bits, 
       reinterpret_cast<const T*>(x), N, d, proj, bits, E, force, codes, idx, w, counts);
 }
 
-template <typename T, int EQ, int TPW>
+template <typename T, int EB>
 void softmax_go(const void* x, int64_t N, int d, const float* wg, const float* bias, int E, int k,
                 int32_t* idx, float* w, int32_t* counts, cudaStream_t s) {
-  using C = SoftCfg<T, EQ, TPW>;
-  auto kern = gate_softmax_kernel<T, EQ, TPW>;
-  static bool configured = false;
-  if (!configured) {
-    INFMOE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM)));
-    configured = true;
+  using C = SoftCfg<T, EB>;
+  auto kern = gate_softmax_kernel<T, EB>;
+  const size_t smem = C::smem(E);
+  static size_t configured = 0;  // opt in to > 48 KiB dynamic smem once per size
+  if (smem > configured) {
+    INFMOE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    configured = smem;
   }
-  kern<<<unsigned((N + C::TB - 1) / C::TB), kSoftWarps * 32, C::SMEM, s>>>(
+  const int warps = (E + EB - 1) / EB;
+  kern<<<unsigned((N + C::TT - 1) / C::TT), warps * 32, smem, s>>>(
       reinterpret_cast<const T*>(x), N, d, wg, bias, E, k, idx, w, counts);
 }
 
-
-template <typename T, int EQ>
+template <typename T>
 void softmax_launch(const void* x, int64_t N, int d, const float* wg, const float* bias, int E,
                     int k, int32_t* idx, float* w, int32_t* counts, cudaStream_t s) {
-  // two tokens per lane when that still gives >= 2 CTAs per SM, else one
-  if ((N + SoftCfg<T, EQ, 2>::TB - 1) / SoftCfg<T, EQ, 2>::TB >= 2 * device_sm_count())
-    softmax_go<T, EQ, 2>(x, N, d, wg, bias, E, k, idx, w, counts, s);
-  else
-    softmax_go<T, EQ, 1>(x, N, d, wg, bias, E, k, idx, w, counts, s);
+  // experts per warp EB (TT*EB = 64 accumulators per lane): 4 experts x 16
+  // tokens up to 64 experts (measured best at E = 32 and 64: each CTA streams
+  // all of W_g once, the weight slices stay in registers across 16 tokens),
+  // 16 x 4 beyond
+  if (E <= 64) softmax_go<T, 4>(x, N, d, wg, bias, E, k, idx, w, counts, s);
+  else softmax_go<T, 16>(x, N, d, wg, bias, E, k, idx, w, counts, s);
 }
 
 }  // namespace
@@ -616,23 +605,15 @@ void launch_gate_softmax(const void* x, int dtype, int64_t N, int d, const float
   require(E >= 1 && E <= 128, "softmax gate: n_experts must be in [1, 128]");
   require(k >= 1 && k <= 8 && k <= E, "softmax gate: top_k must be in [1, min(8, E)]");
   require(d >= 1, "softmax gate: d_model must be >= 1");
-  const size_t V = 16 / dtype_bytes(dtype);
-  require(d % int(V) == 0 && d % 4 == 0, "softmax gate: d_model must be a multiple of 8 (bf16) / 4 (f32)");
+  require(d % 8 == 0, "softmax gate: d_model must be a multiple of 8");
   require(reinterpret_cast<uintptr_t>(x) % 16 == 0 && reinterpret_cast<uintptr_t>(wg) % 16 == 0,
           "softmax gate: x and gate weights must be 16-byte aligned");
   INFMOE_CUDA(cudaMemsetAsync(counts, 0, sizeof(int32_t) * size_t(E), stream));
   if (N == 0) return;
-  const bool bf = dtype == kDtypeBf16;
-#define INFMOE_SOFTMAX_CASE(EQ)                                                              \
-  if (bf) softmax_launch<__nv_bfloat16, EQ>(x, N, d, wg, bias, E, k, topk_idx, topk_w, counts, \
-                                            stream);                                          \
-  else softmax_launch<float, EQ>(x, N, d, wg, bias, E, k, topk_idx, topk_w, counts, stream);
-  if (E <= 8) { INFMOE_SOFTMAX_CASE(1) }
-  else if (E <= 16) { INFMOE_SOFTMAX_CASE(2) }
-  else if (E <= 32) { INFMOE_SOFTMAX_CASE(4) }
-  else if (E <= 64) { INFMOE_SOFTMAX_CASE(8) }
-  else { INFMOE_SOFTMAX_CASE(16) }
-#undef INFMOE_SOFTMAX_CASE
+  if (dtype == kDtypeBf16)
+    softmax_launch<__nv_bfloat16>(x, N, d, wg, bias, E, k, topk_idx, topk_w, counts, stream);
+  else
+    softmax_launch<float>(x, N, d, wg, bias, E, k, topk_idx, topk_w, counts, stream);
   INFMOE_LAUNCH_CHECK();
 }
 
