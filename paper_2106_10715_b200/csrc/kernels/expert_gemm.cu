@@ -1187,6 +1187,5 @@ bool ffn_pair_mode() {
   }();
   return mode != 0;
 }
-void set_ffn_pair_mode(bool on) { setenv("INFMOE_FFN_PAIR", on ? "1" : "0", 1); }
 
 }  // namespace infmoe
