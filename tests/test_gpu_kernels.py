@@ -60,6 +60,8 @@ def _oracle_softmax(xf, wg, bias, E, k):
     (777, 1024, 64, 2, "bf16", True),    # C5-style top-2 with Zipf bias
     (37, 200, 5, 2, "bf16", True),       # d not a multiple of the chunk, E < 32
     (64, 256, 128, 3, "f32", False),
+    (300, 512, 100, 8, "bf16", True),    # > 64 experts (16 per warp), k = 8
+    (5, 8, 3, 3, "bf16", False),         # d = 8: one partial chunk, k = E
 ])
 def test_gate_softmax_topk_bitexact(cuda, N, d, E, k, dtype, use_bias):
     seed = 99 + N
