@@ -3,6 +3,8 @@
 
 #include <dlfcn.h>
 
+#include <cstdlib>
+
 #include <mutex>
 #include <string>
 
@@ -25,7 +27,15 @@ void bind(void* h, F& fn, const char* name) {
 const Api& api() {
   static std::once_flag once;
   std::call_once(once, [] {
-    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);  // torch's copy, if loaded
+    // INFMOE_NCCL_LIB names another implementation of these entry points
+    // (tests/loopback_nccl: P ranks as threads on one GPU)
+    const char* over = std::getenv("INFMOE_NCCL_LIB");
+    void* h = over ? dlopen(over, RTLD_NOW | RTLD_LOCAL) : nullptr;
+    if (over && !h) {
+      g_error = std::string("cannot dlopen INFMOE_NCCL_LIB: ") + dlerror();
+      return;
+    }
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);  // torch's copy, if loaded
     if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
     if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
     if (!h) {
