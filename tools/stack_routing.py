@@ -109,13 +109,17 @@ def main():
                 print(f"layer {l:2d}: max_rows {int(rows.max()):5d} nonempty {int((rows > 0).sum()):2d} "
                       f"ffn {us:8.1f} us  {by / us / 1e3:7.1f} GB/s  std(x) {cur.float().std().item():.3f}")
     print(f"mean ffn {sum(tot) / len(tot):.1f} us")
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with bench.ClockSampler(0) as ck:
+        e0.record()
         for _ in range(20):
             cur = x
             for l, layer in enumerate(layers):
                 layer.forward(cur, bufs[l % 2], want_info=False)
                 cur = bufs[l % 2]
+        e1.record()
         torch.cuda.synchronize()
+    print(f"stack pass {e0.elapsed_time(e1) / 20:.3f} ms ({e0.elapsed_time(e1) / 20 / len(layers) * 1e3:.1f} us/layer)")
     print("clocks", ck.summary(), "power", [r[3] for r in ck.rows][:12])
     del extra
     for layer in layers:
