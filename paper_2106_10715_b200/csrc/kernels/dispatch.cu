@@ -1,9 +1,10 @@
 // dispatch.cu — N2 token dispatch (stable counting sort + row gather) and N5
 // combine (its gate-weighted inverse).
 //
-// Dispatch is a three-launch stable counting sort over the N*k (token, slot)
-// assignments, so the permutation is deterministic and equals oracle.c
-// or_dispatch bit for bit:
+// Dispatch is a stable counting sort over the N*k (token, slot) assignments,
+// so the permutation is deterministic and equals oracle.c or_dispatch bit for
+// bit.  Up to 32768 assignments and 128 experts it is one single-CTA launch
+// (dispatch_small_kernel); beyond, three launches:
 //   1. per-chunk histograms               (one CTA per 2048 assignments)
 //   2. exclusive scan -> offsets[E+1] and each chunk's base per expert
 //   3. per-chunk stable scatter: warps own contiguous sub-ranges, ranks inside a
@@ -79,6 +80,68 @@ __global__ void __launch_bounds__(kScatterWarps * 32)
       run += c;
     }
   }
+  __syncthreads();
+  const unsigned lt = (1u << lane) - 1u;
+  for (int64_t base = a0; base < a1; base += 32) {
+    const int64_t a = base + lane;
+    const bool live = a < a1;
+    const unsigned act = __ballot_sync(0xffffffffu, live);
+    if (live) {
+      const int e = idx[a];
+      const unsigned peers = __match_any_sync(act, e);
+      const int pos = wb[warp * E + e] + __popc(peers & lt);
+      perm[pos] = int32_t(a);
+      inv[a] = pos;
+      __syncwarp(act);
+      if ((peers & lt) == 0) wb[warp * E + e] += __popc(peers);  // group leader advances
+    }
+    __syncwarp();
+  }
+}
+
+// Small problems (<= kSmallAssign assignments, <= kSmallExperts experts):
+// the same stable counting sort in ONE CTA of 32 warps — per-warp histograms
+// of contiguous sub-ranges, one scan, then the match_any scatter — so the
+// dispatch is one launch instead of three.
+constexpr int kSmallWarps = 32;
+constexpr int64_t kSmallAssign = 32768;
+constexpr int kSmallExperts = 128;
+
+__global__ void __launch_bounds__(kSmallWarps * 32)
+    dispatch_small_kernel(const int32_t* __restrict__ idx, int64_t n, int E,
+                          int32_t* __restrict__ offsets, int32_t* __restrict__ perm,
+                          int32_t* __restrict__ inv) {
+  __shared__ int wb[kSmallWarps * kSmallExperts];  // per-warp counts, then bases
+  __shared__ int tot[kSmallExperts + 1];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int64_t per = (n + kSmallWarps - 1) / kSmallWarps;
+  const int64_t a0 = min(n, int64_t(warp) * per), a1 = min(n, a0 + per);
+  for (int i = threadIdx.x; i < kSmallWarps * E; i += blockDim.x) wb[i] = 0;
+  __syncthreads();
+  for (int64_t a = a0 + lane; a < a1; a += 32) atomicAdd(&wb[warp * E + idx[a]], 1);
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {  // running sum over warps
+    int run = 0;
+    for (int w = 0; w < kSmallWarps; ++w) {
+      const int c = wb[w * E + e];
+      wb[w * E + e] = run;
+      run += c;
+    }
+    tot[e] = run;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {  // exclusive scan over experts
+    int acc = 0;
+    for (int e = 0; e < E; ++e) {
+      const int c = tot[e];
+      tot[e] = acc;
+      offsets[e] = acc;
+      acc += c;
+    }
+    offsets[E] = acc;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kSmallWarps * E; i += blockDim.x) wb[i] += tot[i % E];
   __syncthreads();
   const unsigned lt = (1u << lane) - 1u;
   for (int64_t base = a0; base < a1; base += 32) {
@@ -177,6 +240,11 @@ void launch_dispatch(const int32_t* idx, int64_t n, int E, int32_t* offsets, int
                      int32_t* inv, void* workspace, cudaStream_t s) {
   require(E >= 1 && E <= kMaxExpertsDispatch, "dispatch: n_experts must be in [1, 1024]");
   require(workspace != nullptr, "dispatch: workspace is NULL");
+  if (n <= kSmallAssign && E <= kSmallExperts) {
+    dispatch_small_kernel<<<1, kSmallWarps * 32, 0, s>>>(idx, n, E, offsets, perm, inv);
+    INFMOE_LAUNCH_CHECK();
+    return;
+  }
   const int64_t chunks = std::max<int64_t>(1, (n + kChunkAssign - 1) / kChunkAssign);
   int32_t* ch = reinterpret_cast<int32_t*>(workspace);
   chunk_histogram_kernel<<<unsigned(chunks), 256, E * sizeof(int), s>>>(idx, n, E, ch);

@@ -121,7 +121,9 @@ def test_gate_lsh_matches_reference(cuda, N, d, E, bits):
 
 
 @pytest.mark.parametrize("N,k,E,skew", [(4096, 1, 32, 0.0), (16384, 2, 64, 1.0), (5, 2, 7, 0.0),
-                                        (3000, 1, 16, 3.0), (1, 1, 1, 0.0)])
+                                        (3000, 1, 16, 3.0), (1, 1, 1, 0.0),
+                                        (20000, 2, 64, 1.0),    # > 32768: multi-CTA path
+                                        (4096, 1, 300, 0.5)])  # > 128 experts: multi-CTA
 def test_dispatch_bitexact(cuda, N, k, E, skew):
     rng = np.random.default_rng(N + E)
     p = np.arange(1, E + 1, dtype=np.float64) ** (-skew)
