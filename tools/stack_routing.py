@@ -120,6 +120,21 @@ def main():
         e1.record()
         torch.cuda.synchronize()
     print(f"stack pass {e0.elapsed_time(e1) / 20:.3f} ms ({e0.elapsed_time(e1) / 20 / len(layers) * 1e3:.1f} us/layer)")
+    # the same stack as one CUDA graph (bench.py's resident path)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        cur = x
+        for l, layer in enumerate(layers):
+            layer.forward(cur, bufs[l % 2], want_info=False)
+            cur = bufs[l % 2]
+    g.replay()
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(20):
+        g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    print(f"graph pass {e0.elapsed_time(e1) / 20:.3f} ms ({e0.elapsed_time(e1) / 20 / len(layers) * 1e3:.1f} us/layer)")
     print("clocks", ck.summary(), "power", [r[3] for r in ck.rows][:12])
     del extra
     for layer in layers:
