@@ -450,14 +450,16 @@ def main() -> None:
     ffn_bytes = ffn_secs = 0.0
     exposed = []
     launches = 0
+    # dispatch is one single-CTA launch up to 32768 assignments / 128 experts
+    dispatch_launches = 1 if N * k <= 32768 and E <= 128 else 3
     wbytes = 2 * d * f * 2
     for infos in all_infos:
         for info in infos:
             rows = info["local_rows"]  # rows this rank computed per local expert
             exposed.append(info["exposed_copy_s"])
-            # gate + 3 dispatch + gather + one fused FFN per expert with rows (the top-1
+            # gate + dispatch + gather + one fused FFN per expert with rows (the top-1
             # combine is fused into it); EP adds the receive-side gather and the combine
-            launches += 5 + int((rows > 0).sum()) + (2 if P > 1 else 0)
+            launches += 3 + dispatch_launches + int((rows > 0).sum()) + (2 if P > 1 else 0)
             for (st, _l, e, s0, s1) in info["events"]:
                 if st == 1 and rows[e] > 0:
                     ffn_secs += s1 - s0
