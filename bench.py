@@ -293,6 +293,9 @@ def main() -> None:
     ap.add_argument("--resident-steps", type=int, default=20)
     ap.add_argument("--cpu-sample", type=int, default=4096)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ep-transport", default="nccl", choices=["nccl", "peer"],
+                    help="expert-parallel exchange for N > 1: grouped NCCL send/recv, or rows "
+                         "pushed over peer memory (CUDA IPC) with the return fused into the FFN")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     if args.K:
@@ -388,6 +391,7 @@ def main() -> None:
                                    lsh_seed=im.derive_seed(SEED, 100 + l), lsh_bits=cfg["bits"],
                                    offloaded=offloaded, K=cfg["K"], max_tokens=N, device=local,
                                    hw=hw, ep_size=P, ep_rank=rank, ep_comm=comm,
+                                   ep_transport=args.ep_transport,
                                    slot_pool=pool if offloaded else None))
         return out
 
@@ -611,6 +615,7 @@ def main() -> None:
                    "policy": "infmoe_greedy(auto_order)",
                    "host_weight_sets": n_sets,
                    "parallelism": f"ep{P}" if P > 1 else "single",
+                   "ep_transport": args.ep_transport if P > 1 else None,
                    "l2": "inputs larger than L2 (5.37 GB of expert weights per layer)"},
         "e2e": {"value": N_glob / (t_out * 1e-3), "unit": "tokens/s",
                 "h2d_bytes_per_step": N * d * 2, "d2h_bytes_per_step": N * d * 2},

@@ -269,7 +269,14 @@ typedef struct {
   int32_t skip_empty_experts;
   /* offloaded: shared slot pool (NULL: the handle owns its own K+1 slots) */
   infmoe_slot_pool* slot_pool;
+  /* expert-parallel transport: INFMOE_EP_NCCL (grouped ncclSend/ncclRecv
+   * all-to-allv, host-planned) or INFMOE_EP_PEER (rows pushed straight into the
+   * owner's expert-contiguous buffer over peer memory, results written back by
+   * the expert FFN's epilogue, plan computed on the device; peers are mapped
+   * with CUDA IPC at create; NCCL only for 1-int barriers) */
+  int32_t ep_transport;
 } infmoe_layer_desc;
+enum { INFMOE_EP_NCCL = 0, INFMOE_EP_PEER = 1 };
 
 /* per-forward outputs (all optional; host pointers unless noted) */
 typedef struct {

@@ -123,7 +123,8 @@ class LayerDesc(C.Structure):
                 ("lsh_seed", C.c_uint64), ("lsh_bits", C.c_int32),
                 ("w_in", C.c_void_p), ("w_out", C.c_void_p), ("hw", Hardware),
                 ("ep_size", C.c_int32), ("ep_rank", C.c_int32), ("ep_comm", C.c_void_p),
-                ("skip_empty_experts", C.c_int32), ("slot_pool", C.c_void_p)]
+                ("skip_empty_experts", C.c_int32), ("slot_pool", C.c_void_p),
+                ("ep_transport", C.c_int32)]
 
 
 class ForwardOut(C.Structure):
@@ -136,6 +137,7 @@ DTYPE_BF16, DTYPE_F32 = 0, 1
 GATE_SOFTMAX, GATE_LSH = 0, 1
 RESIDENT, OFFLOADED = 0, 1
 POLICY_AUTO, POLICY_GREEDY, POLICY_EXACT, POLICY_NAIVE = 0, 1, 2, 3
+EP_NCCL, EP_PEER = 0, 1
 DIAG = {-1: None, 0: "feasible", 1: "too_little_compute", 2: "imbalanced"}
 METHOD = {0: "greedy", 1: "exact_fallback", 2: "naive"}
 

@@ -31,6 +31,7 @@ CU_SOURCES = [
     "kernels/gate.cu",
     "kernels/dispatch.cu",
     "kernels/expert_gemm.cu",
+    "kernels/ep_peer.cu",
     "runtime/layer.cu",
     "runtime/capi_device.cu",
 ]

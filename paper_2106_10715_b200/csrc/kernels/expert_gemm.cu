@@ -478,6 +478,10 @@ struct FusedParams {
   int32_t* done;
   const int32_t* perm;
   const float* topk_w;
+  // expert-parallel return (PEER transport): output row r goes to rank
+  // ret[r].x's y_back at row ret[r].y (peer_y = every rank's y_back)
+  const int2* ret;
+  void* peer_y[kMaxPeers];
   int32_t experts[kMaxGroups];
   int32_t slots[kMaxGroups];
 };
@@ -703,6 +707,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           for (int i = 0; i < 32; ++i)
             if (i < nvalid)
               dst[int64_t(i) * p.f] = __float2bfloat16_rn(gelu_erf(__uint_as_float(r[i])));
+        } else if (p.ret != nullptr) {
+          // expert-parallel return: each row straight into its source rank's
+          // y_back over NVLink (the combine then runs at the source)
+          const int2 rt_l = lane < nvalid ? p.ret[row + lane] : make_int2(0, 0);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const int rk = __shfl_sync(0xffffffffu, rt_l.x, i);
+            const int pos = __shfl_sync(0xffffffffu, rt_l.y, i);
+            if (i < nvalid)
+              reinterpret_cast<__nv_bfloat16*>(p.peer_y[rk])[int64_t(pos) * p.d + feat] =
+                  __float2bfloat16_rn(__uint_as_float(r[i]));
+          }
         } else if (p.perm == nullptr) {
           __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(p.y) + row * p.d + feat;
 #pragma unroll
@@ -738,6 +754,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       if (lane == 0) mbar_arrive(acce_bar(acc));
       if (++acc == C::ACC) { acc = 0; acc_phase ^= 1; }
     }
+    if (p.ret) __threadfence_system();  // results stored to peers are visible system-wide
   }
 
   tc_fence_before();
@@ -778,6 +795,8 @@ void fused_launch(const FusedFfnArgs& a, cudaStream_t stream) {
   p.done = a.done;
   p.perm = a.perm;
   p.topk_w = a.topk_w;
+  p.ret = a.ret;
+  for (int r = 0; r < a.n_peers && r < kMaxPeers; ++r) p.peer_y[r] = a.peer_y[r];
   for (int g = 0; g < a.n_groups; ++g) {
     p.experts[g] = a.experts[g];
     p.slots[g] = a.slots[g];
@@ -1053,6 +1072,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           for (int i = 0; i < 32; ++i)
             if (i < nvalid)
               dst[int64_t(i) * p.f] = __float2bfloat16_rn(gelu_erf(__uint_as_float(r[i])));
+        } else if (p.ret != nullptr) {
+          // expert-parallel return: each row straight into its source rank's
+          // y_back over NVLink (the combine then runs at the source)
+          const int2 rt_l = lane < nvalid ? p.ret[row + lane] : make_int2(0, 0);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const int rk = __shfl_sync(0xffffffffu, rt_l.x, i);
+            const int pos = __shfl_sync(0xffffffffu, rt_l.y, i);
+            if (i < nvalid)
+              reinterpret_cast<__nv_bfloat16*>(p.peer_y[rk])[int64_t(pos) * p.d + feat] =
+                  __float2bfloat16_rn(__uint_as_float(r[i]));
+          }
         } else if (p.perm == nullptr) {
           __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(p.y) + row * p.d + feat;
 #pragma unroll
@@ -1086,6 +1117,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       if (lane == 0) arrive_leader(acce_bar(acc));
       if (++acc == C::ACC) { acc = 0; acc_phase ^= 1; }
     }
+    if (p.ret) __threadfence_system();  // results stored to peers are visible system-wide
   }
 
   tc_fence_before();
@@ -1127,6 +1159,8 @@ void fused_pair_launch(const FusedFfnArgs& a, cudaStream_t stream) {
   p.done = a.done;
   p.perm = a.perm;
   p.topk_w = a.topk_w;
+  p.ret = a.ret;
+  for (int r = 0; r < a.n_peers && r < kMaxPeers; ++r) p.peer_y[r] = a.peer_y[r];
   for (int g = 0; g < a.n_groups; ++g) {
     p.experts[g] = a.experts[g];
     p.slots[g] = a.slots[g];
@@ -1167,6 +1201,8 @@ void launch_expert_ffn_fused(const FusedFfnArgs& a, cudaStream_t stream) {
   require(a.x && a.w_in && a.w_out && a.h && a.y && a.offsets && a.done,
           "fused expert FFN: NULL pointer");
   require((a.perm == nullptr) == (a.topk_w == nullptr), "fused expert FFN: perm needs topk_w");
+  require(a.ret == nullptr || (a.perm == nullptr && a.n_peers >= 1 && a.n_peers <= kMaxPeers),
+          "fused expert FFN: return mode needs 1..16 peers and no fused combine");
   const int hint = a.max_rows_hint;
   if (ffn_pair_mode() && a.d_model % (2 * gemm::BM) == 0 && a.d_ff % (2 * gemm::BM) == 0) {
     if (hint > 0 && hint <= 128) gemm::fused_pair_launch<128, 8>(a, stream);

@@ -7,6 +7,7 @@
 namespace infmoe {
 
 constexpr int kMaxGroups = 128;
+constexpr int kMaxPeers = 16;  // expert-parallel ranks reachable over peer memory
 
 // One launch computes out[rows of group g, :] = epi(A[rows] . B[slot_g]^T) for
 // every listed group.  A is [a_rows, K] row-major (token rows, K contiguous);
@@ -56,6 +57,11 @@ struct FusedFfnArgs {
   void* y;              // [rows, d_model] (or [N, d_model] when the combine is fused)
   const int32_t* perm;  // fused top-1 combine: row -> token, or NULL
   const float* topk_w;  // weight per token (with perm)
+  // expert-parallel return (PEER transport): row r of the output is stored at
+  // row ret[r].y of peer_y[ret[r].x] (device pointers, one per rank)
+  const int2* ret;
+  void* peer_y[kMaxPeers];
+  int32_t n_peers;
   int32_t* done;        // >= n_groups counters in device memory (zeroed by the launcher)
   int32_t max_ctas;
   int32_t max_rows_hint;

@@ -26,6 +26,8 @@
 #include <memory>
 #include <vector>
 
+#include <unistd.h>
+
 #include "../host/planner.hpp"
 #include "../kernels/common.cuh"
 #include "../kernels/expert_gemm.cuh"
@@ -90,8 +92,26 @@ Layer::Layer(const infmoe_layer_desc& d) : desc(d) {
   // the exchange path runs whenever a communicator is given (ep_size == 1 then
   // exchanges with itself, which exercises the NCCL transport on one GPU)
   use_ep = P > 1 || comm != nullptr;
+  ep_peer = use_ep && d.ep_transport == INFMOE_EP_PEER;
+  require(d.ep_transport == INFMOE_EP_NCCL || d.ep_transport == INFMOE_EP_PEER,
+          "layer: unknown ep_transport");
+  require(!ep_peer || (P <= kMaxPeers && d.dtype == INFMOE_DTYPE_BF16),
+          "layer: the PEER transport takes bf16 and at most 16 ranks");
   if (!use_ep) hbuf = dalloc<uint8_t>(size_t(A) * d.d_ff * esz, owned);
   else recv_counts_dev = dalloc<int32_t>(size_t(P) * n_local, owned);
+  if (ep_peer) {
+    cap_recv = int64_t(P) * A;
+    sym_x = dalloc<uint8_t>(size_t(cap_recv) * d.d_model * esz, owned);
+    sym_ret = dalloc<int2>(size_t(cap_recv), owned);
+    sym_y = dalloc<uint8_t>(size_t(A) * d.d_model * esz, owned);
+    sym_counts = dalloc<int32_t>(size_t(P) * d.n_experts, owned);
+    dest_base = dalloc<int32_t>(size_t(d.n_experts), owned);
+    loc_offsets = dalloc<int32_t>(size_t(n_local) + 1, owned);
+    bar_buf = dalloc<int32_t>(1, owned);
+    cap_h = size_t(cap_recv) * d.d_ff * esz;  // freed with the other exchange buffers
+    INFMOE_CUDA(cudaMalloc(&loc_h, cap_h));
+    peer_setup();
+  }
 
   if (d.gate_kind == INFMOE_GATE_LSH) {
     std::vector<double> p = lsh_hyperplanes(d.lsh_seed, d.lsh_bits, d.d_model);
@@ -108,7 +128,9 @@ Layer::Layer(const infmoe_layer_desc& d) : desc(d) {
                              cudaMemcpyHostToDevice));
     }
   }
-  INFMOE_CUDA(cudaMallocHost(&counts_host, sizeof(int32_t) * (d.n_experts + P * n_local)));
+  // [E] counts | [P * n_local] received counts (NCCL) or [n_local + 1] offsets (PEER)
+  const int tail = std::max(P * n_local, n_local + 1);
+  INFMOE_CUDA(cudaMallocHost(&counts_host, sizeof(int32_t) * size_t(d.n_experts + tail)));
 
   expert_in_bytes = size_t(d.d_ff) * d.d_model * esz;
   if (d.residency == INFMOE_OFFLOADED) {
@@ -168,6 +190,7 @@ void Layer::set_host_weights(const void* w_in, const void* w_out) {
 
 Layer::~Layer() {
   cudaSetDevice(desc.device);
+  for (void* p : ipc_opened) cudaIpcCloseMemHandle(p);
   if (copy_stream) cudaStreamSynchronize(copy_stream);
   for (auto* v : {&load_done, &compute_done, &t_load0, &t_load1, &t_comp0, &t_comp1})
     for (cudaEvent_t e : *v) cudaEventDestroy(e);
@@ -217,6 +240,11 @@ void Layer::ffn(const Rows& r, const int32_t* experts, const int32_t* slots, int
     }
     a.h = r.h;
     a.y = r.y;
+    if (ep_peer) {  // results straight back to the token owners over peer memory
+      a.ret = sym_ret;
+      a.n_peers = desc.ep_size;
+      for (int q = 0; q < desc.ep_size; ++q) a.peer_y[q] = peer_y[size_t(q)];
+    }
     if (fused_out) {  // top-1, no exchange: the GEMM2 epilogue writes y directly
       a.y = fused_out;
       a.perm = perm;
@@ -339,6 +367,74 @@ void Layer::compute_offloaded(const Rows& r, bool timed, infmoe_forward_out* out
   }
 }
 
+// PEER transport: publish (pid, pointers, IPC handles) of the symmetric
+// buffers through an NCCL all-gather and map every peer's buffers: a raw
+// pointer when the peer lives in this process (ranks as threads), else a CUDA
+// IPC mapping (NVLink peer access is enabled lazily by the runtime).
+void Layer::peer_setup() {
+  struct Info {
+    int64_t pid;
+    uint64_t ptr[4];
+    cudaIpcMemHandle_t h[4];
+  };
+  const int P = desc.ep_size, me = desc.ep_rank;
+  Info mine{};
+  mine.pid = int64_t(getpid());
+  void* bufs[4] = {sym_x, sym_ret, sym_y, sym_counts};
+  for (int i = 0; i < 4; ++i) {
+    mine.ptr[i] = reinterpret_cast<uint64_t>(bufs[i]);
+    INFMOE_CUDA(cudaIpcGetMemHandle(&mine.h[i], bufs[i]));
+  }
+  uint8_t* dev = nullptr;
+  INFMOE_CUDA(cudaMalloc(&dev, sizeof(Info) * size_t(P + 1)));
+  INFMOE_CUDA(cudaMemcpy(dev + sizeof(Info) * size_t(P), &mine, sizeof(Info),
+                         cudaMemcpyHostToDevice));
+  cudaStream_t s;
+  INFMOE_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  const auto& nc = nccl::api();
+  nccl::check(nc.AllGather(dev + sizeof(Info) * size_t(P), dev, sizeof(Info), nccl::kUint8,
+                           reinterpret_cast<nccl::Comm>(comm), s),
+              "ncclAllGather");
+  INFMOE_CUDA(cudaStreamSynchronize(s));
+  INFMOE_CUDA(cudaStreamDestroy(s));
+  std::vector<Info> all(static_cast<size_t>(P));
+  INFMOE_CUDA(cudaMemcpy(all.data(), dev, sizeof(Info) * size_t(P), cudaMemcpyDeviceToHost));
+  INFMOE_CUDA(cudaFree(dev));
+  std::vector<void*> px(static_cast<size_t>(P)), pr(static_cast<size_t>(P)), pc(static_cast<size_t>(P));
+  peer_y.assign(size_t(P), nullptr);
+  for (int r = 0; r < P; ++r) {
+    void* q[4];
+    for (int i = 0; i < 4; ++i) {
+      if (r == me || all[size_t(r)].pid == mine.pid) {
+        q[i] = reinterpret_cast<void*>(all[size_t(r)].ptr[i]);
+      } else {
+        INFMOE_CUDA(cudaIpcOpenMemHandle(&q[i], all[size_t(r)].h[i],
+                                         cudaIpcMemLazyEnablePeerAccess));
+        ipc_opened.push_back(q[i]);
+      }
+    }
+    px[size_t(r)] = q[0];
+    pr[size_t(r)] = q[1];
+    peer_y[size_t(r)] = q[2];
+    pc[size_t(r)] = q[3];
+  }
+  d_peer_x = dalloc<void*>(size_t(P), owned);
+  d_peer_ret = dalloc<int2*>(size_t(P), owned);
+  d_peer_counts = dalloc<int32_t*>(size_t(P), owned);
+  INFMOE_CUDA(cudaMemcpy(d_peer_x, px.data(), sizeof(void*) * P, cudaMemcpyHostToDevice));
+  INFMOE_CUDA(cudaMemcpy(d_peer_ret, pr.data(), sizeof(void*) * P, cudaMemcpyHostToDevice));
+  INFMOE_CUDA(cudaMemcpy(d_peer_counts, pc.data(), sizeof(void*) * P, cudaMemcpyHostToDevice));
+}
+
+// every rank's work enqueued before this point has finished before any rank's
+// work after it starts: a 1-int all-reduce on the stream
+void Layer::peer_barrier(cudaStream_t s) {
+  const auto& nc = nccl::api();
+  nccl::check(nc.AllReduce(bar_buf, bar_buf, 1, nccl::kInt32, nccl::kSum,
+                           reinterpret_cast<nccl::Comm>(comm), s),
+              "ncclAllReduce");
+}
+
 void Layer::ep_exchange_out(int64_t N, cudaStream_t s) {
   (void)N;
   const auto& nc = nccl::api();
@@ -430,6 +526,30 @@ void Layer::forward(const void* x, int64_t N, void* y, infmoe_forward_out* out, 
         r.counts = counts_host;
       }
     }
+  } else if (ep_peer) {
+    // PEER transport: counts to every rank, plan on the device, rows pushed
+    // into the owners' expert-contiguous buffers; no host round trip unless
+    // the offload order (or the caller) needs the local counts
+    const int P = desc.ep_size, me = desc.ep_rank;
+    launch_ep_counts_push(counts, E, me, P, d_peer_counts, s);
+    peer_barrier(s);
+    launch_ep_plan(sym_counts, P, E, me, dest_base, loc_offsets, s);
+    launch_ep_dispatch_push(xp, desc.dtype, N * k, desc.d_model, offsets, E, P, dest_base, me,
+                            d_peer_x, d_peer_ret, s);
+    peer_barrier(s);
+    const bool need_counts = offloaded || (out && (out->local_rows || out->counts));
+    if (need_counts) {
+      INFMOE_CUDA(cudaMemcpyAsync(counts_host, counts, sizeof(int32_t) * E,
+                                  cudaMemcpyDeviceToHost, s));
+      INFMOE_CUDA(cudaMemcpyAsync(counts_host + E, loc_offsets, sizeof(int32_t) * (n_local + 1),
+                                  cudaMemcpyDeviceToHost, s));
+      INFMOE_CUDA(cudaStreamSynchronize(s));
+      local_counts.resize(size_t(n_local));
+      for (int e = 0; e < n_local; ++e)
+        local_counts[size_t(e)] = counts_host[E + e + 1] - counts_host[E + e];
+    }
+    r = Rows{sym_x, loc_offsets, cap_recv, loc_h, sym_y,
+             need_counts ? local_counts.data() : nullptr};
   } else {
     ep_exchange_out(N, s);
     local_counts.resize(size_t(n_local));
@@ -443,8 +563,13 @@ void Layer::forward(const void* x, int64_t N, void* y, infmoe_forward_out* out, 
   if (offloaded) compute_offloaded(r, timed, out, s);
   else compute_resident(r, timed, s);
 
-  if (use_ep) ep_exchange_back(s);
-  if (!fused_out) launch_combine(yp, desc.dtype, inv, wts, N, k, desc.d_model, y, s);
+  if (ep_peer) {
+    peer_barrier(s);  // every owner has written my rows' results into sym_y
+    launch_combine(sym_y, desc.dtype, inv, wts, N, k, desc.d_model, y, s);
+  } else {
+    if (use_ep) ep_exchange_back(s);
+    if (!fused_out) launch_combine(yp, desc.dtype, inv, wts, N, k, desc.d_model, y, s);
+  }
 
   if (!out) return;
   const bool need_sync = timed || ((out->counts || out->local_rows) && !offloaded && !use_ep);

@@ -47,6 +47,8 @@ struct Layer {
            cudaEvent_t ev_begin = nullptr, cudaEvent_t ev_end = nullptr);
   void ep_exchange_out(int64_t N, cudaStream_t s);   // dispatch all-to-allv
   void ep_exchange_back(cudaStream_t s);             // combine all-to-allv
+  void peer_setup();                                 // PEER transport: map the peers
+  void peer_barrier(cudaStream_t s);                 // stream-ordered, all ranks
   template <class T>
   T* grow(T*& p, size_t& cap, size_t n);
 
@@ -98,6 +100,21 @@ struct Layer {
   uint8_t* loc_y = nullptr;
   uint8_t* recv_y = nullptr;   // results in receive layout (sent back)
   size_t cap_x = 0, cap_lx = 0, cap_h = 0, cap_ly = 0, cap_ry = 0;
+  // PEER transport (ep_peer.cu): symmetric buffers peers write into
+  bool ep_peer = false;
+  int64_t cap_recv = 0;           // rows this rank can receive (P * max_tokens * k)
+  uint8_t* sym_x = nullptr;       // [cap_recv, d] received rows, expert-contiguous
+  int2* sym_ret = nullptr;        // [cap_recv] (source rank, source row)
+  uint8_t* sym_y = nullptr;       // [max_tokens*k, d] results for my rows
+  int32_t* sym_counts = nullptr;  // [P, E] every source's histogram
+  int32_t* dest_base = nullptr;   // [E]
+  int32_t* loc_offsets = nullptr; // [n_local + 1]
+  int32_t* bar_buf = nullptr;     // 1-int all-reduce of the barrier
+  void** d_peer_x = nullptr;      // device arrays of the peers' buffers
+  int2** d_peer_ret = nullptr;
+  int32_t** d_peer_counts = nullptr;
+  std::vector<void*> peer_y;      // host copy (FFN kernel parameter)
+  std::vector<void*> ipc_opened;  // peer mappings to close
 };
 
 }  // namespace infmoe

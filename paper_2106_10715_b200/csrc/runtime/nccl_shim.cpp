@@ -49,6 +49,8 @@ const Api& api() {
     bind(h, g_api.GroupEnd, "ncclGroupEnd");
     bind(h, g_api.Send, "ncclSend");
     bind(h, g_api.Recv, "ncclRecv");
+    bind(h, g_api.AllGather, "ncclAllGather");
+    bind(h, g_api.AllReduce, "ncclAllReduce");
     bind(h, g_api.GetErrorString, "ncclGetErrorString");
     bind(h, g_api.GetVersion, "ncclGetVersion");
   });

@@ -17,6 +17,7 @@ struct UniqueId {
   char internal[128];
 };
 enum DataType { kUint8 = 1, kInt32 = 2 };
+enum RedOp { kSum = 0 };
 
 struct Api {
   int (*GetUniqueId)(UniqueId*) = nullptr;
@@ -26,6 +27,8 @@ struct Api {
   int (*GroupEnd)() = nullptr;
   int (*Send)(const void*, size_t, int, int, Comm, cudaStream_t) = nullptr;
   int (*Recv)(void*, size_t, int, int, Comm, cudaStream_t) = nullptr;
+  int (*AllGather)(const void*, void*, size_t, int, Comm, cudaStream_t) = nullptr;
+  int (*AllReduce)(const void*, void*, size_t, int, int, Comm, cudaStream_t) = nullptr;
   const char* (*GetErrorString)(int) = nullptr;
   int (*GetVersion)(int*) = nullptr;
 };

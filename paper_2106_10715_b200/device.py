@@ -216,7 +216,7 @@ class MoELayer:
                  policy: int = POLICY_AUTO, max_tokens: int = 4096, device: int = 0,
                  hw: Optional[Hardware] = None, ep_size: int = 1, ep_rank: int = 0,
                  ep_comm: Optional[int] = None, skip_empty_experts: bool = False,
-                 slot_pool: Optional["SlotPool"] = None):
+                 slot_pool: Optional["SlotPool"] = None, ep_transport: str = "nccl"):
         d = LayerDesc()
         d.d_model, d.d_ff, d.n_experts, d.top_k = d_model, d_ff, n_experts, top_k
         d.dtype = DTYPE_BF16 if dtype == "bf16" else DTYPE_F32
@@ -238,6 +238,7 @@ class MoELayer:
         d.hw = hw if hw is not None else Hardware(1643.6e12, 55.5e9, 180 << 30, 8 << 30)
         d.ep_size, d.ep_rank, d.ep_comm = ep_size, ep_rank, ep_comm
         d.skip_empty_experts = int(skip_empty_experts)
+        d.ep_transport = {"nccl": 0, "peer": 1}[ep_transport]
         if slot_pool is not None:
             d.slot_pool = slot_pool.handle
             self._keep.append(slot_pool)  # the pool outlives the layer

@@ -147,6 +147,48 @@ int ncclRecv(void* buf, size_t count, int dt, int peer, Comm* comm, cudaStream_t
   if (t_depth > 0) { t_ops.push_back(o); return 0; }
   return run({o});
 }
+// collectives as P-1 sends + P-1 receives per rank through the same matcher,
+// plus a local copy / reduction; a sum all-reduce of int32 or float only
+int ncclAllGather(const void* send, void* recv, size_t count, int dt, Comm* comm,
+                  cudaStream_t s) {
+  const size_t bytes = count * elem_size(dt);
+  std::vector<Op> ops;
+  for (int r = 0; r < comm->nranks; ++r) {
+    if (r == comm->rank) continue;
+    ops.push_back(Op{true, const_cast<void*>(send), bytes, r, comm, s});
+    ops.push_back(Op{false, static_cast<uint8_t*>(recv) + size_t(r) * bytes, bytes, r, comm, s});
+  }
+  if (bytes) cudaMemcpyAsync(static_cast<uint8_t*>(recv) + size_t(comm->rank) * bytes, send, bytes,
+                             cudaMemcpyDeviceToDevice, s);
+  return run(ops);
+}
+int ncclAllReduce(const void* send, void* recv, size_t count, int dt, int op, Comm* comm,
+                  cudaStream_t s) {
+  if (op != 0 || !(dt == 2 || dt == 7)) return 5;  // ncclInvalidUsage: sum of int32/f32 only
+  const size_t bytes = count * 4;
+  std::vector<uint8_t> mine(bytes), other(bytes), acc(bytes);
+  void* stage = nullptr;
+  cudaMalloc(&stage, bytes * size_t(comm->nranks));
+  int rc = ncclAllGather(send, stage, count, dt, comm, s);
+  if (rc) return rc;
+  cudaStreamSynchronize(s);  // host reduction (test transport: correctness, not speed)
+  std::vector<uint8_t> all(bytes * size_t(comm->nranks));
+  cudaMemcpy(all.data(), stage, all.size(), cudaMemcpyDeviceToHost);
+  for (size_t i = 0; i < count; ++i) {
+    if (dt == 2) {
+      int32_t v = 0;
+      for (int r = 0; r < comm->nranks; ++r) v += reinterpret_cast<int32_t*>(all.data() + r * bytes)[i];
+      reinterpret_cast<int32_t*>(acc.data())[i] = v;
+    } else {
+      float v = 0.f;
+      for (int r = 0; r < comm->nranks; ++r) v += reinterpret_cast<float*>(all.data() + r * bytes)[i];
+      reinterpret_cast<float*>(acc.data())[i] = v;
+    }
+  }
+  cudaMemcpy(recv, acc.data(), bytes, cudaMemcpyHostToDevice);
+  cudaFree(stage);
+  return 0;
+}
 const char* ncclGetErrorString(int r) { return r ? "loopback transport error" : "no error"; }
 int ncclGetVersion(int* v) {
   *v = 22809;

@@ -3,9 +3,10 @@
    product's kernels (gate, dispatch, gather, EP plan, expert FFN on the rank's
    expert shard, scatter, combine) with device copies as the transport; the
    result must equal the one-GPU layer bit for bit;
-2) the layer's NCCL transport (grouped ncclSend/ncclRecv, loaded at run time)
-   runs on a 1-rank communicator (self exchange), resident and offloaded, and
-   must equal the plain layer bit for bit."""
+2) the layer's transports run on a real 1-rank NCCL communicator (self
+   exchange), resident and offloaded, and must equal the plain layer bit for
+   bit: NCCL (grouped ncclSend/ncclRecv) and PEER (all-gather of the buffer
+   addresses, device-side plan, pushes, 1-int all-reduce barriers)."""
 import numpy as np
 import pytest
 import torch
@@ -75,8 +76,9 @@ def test_virtual_ranks_equal_single_gpu(cuda, P, k):
     ref_layer.close()
 
 
+@pytest.mark.parametrize("transport", ["nccl", "peer"])
 @pytest.mark.parametrize("offloaded", [False, True])
-def test_layer_nccl_transport_self_exchange(cuda, offloaded):
+def test_layer_nccl_transport_self_exchange(cuda, offloaded, transport):
     N, d, f, E = 512, 256, 384, 8
     x, wi, wo = _weights(cuda, E, d, f, seed=9)
     x = x[:N].contiguous()
@@ -89,7 +91,7 @@ def test_layer_nccl_transport_self_exchange(cuda, offloaded):
         w_out = wo.pin_memory() if offloaded else wo.to(cuda)
         ep = dv.MoELayer(d, f, E, 1, w_in, w_out, gate="lsh", lsh_seed=3, lsh_bits=3,
                          offloaded=offloaded, K=2, max_tokens=N, ep_size=1, ep_rank=0,
-                         ep_comm=comm)
+                         ep_comm=comm, ep_transport=transport)
         y1, info1 = ep.forward(x)
         y2, _ = ep.forward(x)  # buffers reused
         torch.cuda.synchronize()
