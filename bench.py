@@ -487,9 +487,9 @@ def main() -> None:
     h2d_gbs = h2d_bytes_step / (t_in * 1e-3) / 1e9
 
     # ---------------- resident stack (all experts in HBM) --------------------
-    # no host round trip on this path (P == 1), so the 24-layer stack is
-    # captured once as a CUDA graph and replayed; EP needs its per-layer count
-    # exchange on the host and runs eagerly.
+    # no host round trip on this path (one GPU, or EP over the PEER transport),
+    # so the 24-layer stack is captured once as a CUDA graph and replayed; the
+    # NCCL transport plans the exchange on the host and runs eagerly.
     graph = None
     for _ in range(3):
         stack(res_layers, x_dev, info=False)
@@ -500,7 +500,7 @@ def main() -> None:
         for l, i in enumerate(mid[:4]):
             print(f"mid resident layer {l}: ffn {(i['events'][0][4] - i['events'][0][3]) * 1e6:.1f} us",
                   file=sys.stderr)
-    if P == 1:
+    if P == 1 or args.ep_transport == "peer":  # no host round trip: capturable
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph):
             y_graph, _ = stack(res_layers, x_dev, info=False)

@@ -101,3 +101,40 @@ def test_layer_nccl_transport_self_exchange(cuda, offloaded, transport):
     finally:
         im.ep_comm_destroy(comm)
     plain.close()
+
+
+def test_peer_transport_resident_stack_is_graph_capturable(cuda):
+    """The PEER transport plans on the device and barriers on the stream, so a
+    resident expert-parallel stack has no host round trip: it is captured as
+    one CUDA graph (real NCCL, 1-rank communicator) and replays bit-identical
+    to eager execution."""
+    N, d, f, E, L = 512, 256, 384, 8, 3
+    x, wi, wo = _weights(cuda, E, d, f, seed=13)
+    x = x[:N].contiguous()
+    comm = im.ep_comm_init(im.ep_unique_id(), 1, 0)
+    try:
+        layers = [dv.MoELayer(d, f, E, 1, wi.to(cuda), wo.to(cuda), gate="lsh", lsh_seed=20 + l,
+                              lsh_bits=3, max_tokens=N, ep_size=1, ep_rank=0, ep_comm=comm,
+                              ep_transport="peer") for l in range(L)]
+        bufs = [torch.empty_like(x) for _ in range(2)]
+
+        def run():
+            cur = x
+            for i, lay in enumerate(layers):
+                lay.forward(cur, bufs[i % 2], want_info=False)
+                cur = bufs[i % 2]
+            return cur
+
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            y_eager = run().clone()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=s):
+                y_graph = run()
+            g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(y_graph.view(torch.int16), y_eager.view(torch.int16))
+        for lay in layers:
+            lay.close()
+    finally:
+        im.ep_comm_destroy(comm)
