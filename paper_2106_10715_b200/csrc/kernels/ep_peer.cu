@@ -58,9 +58,11 @@ __global__ void ep_plan_kernel(const int32_t* __restrict__ C, int P, int E, int 
   }
 }
 
-// one warp per x_perm row: find its expert, push the row (16-byte stores over
-// NVLink) and its return address into the owner's buffers
-__global__ void ep_dispatch_push_kernel(const uint4* __restrict__ xp, int64_t rows, int vec_per_row,
+// one warp per x_perm row p: find its expert, push token row x[perm[p] / k]
+// (16-byte stores over NVLink; no x_perm is materialised) and its return
+// address into the owner's buffers
+__global__ void ep_dispatch_push_kernel(const uint4* __restrict__ x, const int32_t* __restrict__ perm,
+                                        int k, int64_t rows, int vec_per_row,
                                         const int32_t* __restrict__ offsets, int E, int El,
                                         const int32_t* __restrict__ dest_base, int me,
                                         uint4* const* __restrict__ peer_x,
@@ -76,7 +78,7 @@ __global__ void ep_dispatch_push_kernel(const uint4* __restrict__ xp, int64_t ro
     }
     const int e = lo, r = e / El;
     const int64_t dst = int64_t(dest_base[e]) + (p - offsets[e]);
-    const uint4* s = xp + p * vec_per_row;
+    const uint4* s = x + int64_t(perm[p] / k) * vec_per_row;
     uint4* dptr = peer_x[r] + dst * vec_per_row;
     for (int v = lane; v < vec_per_row; v += 32) dptr[v] = __ldg(s + v);
     if (lane == 0) peer_ret[r][dst] = make_int2(me, int32_t(p));
@@ -100,8 +102,8 @@ void launch_ep_plan(const int32_t* all_counts, int P, int E, int me, int32_t* de
   INFMOE_LAUNCH_CHECK();
 }
 
-void launch_ep_dispatch_push(const void* x_perm, int dtype, int64_t rows, int d,
-                             const int32_t* offsets, int E, int P, const int32_t* dest_base,
+void launch_ep_dispatch_push(const void* x, const int32_t* perm, int k, int dtype, int64_t rows,
+                             int d, const int32_t* offsets, int E, int P, const int32_t* dest_base,
                              int me, void* const* peer_x, int2* const* peer_ret, cudaStream_t s) {
   const size_t row_bytes = size_t(d) * dtype_bytes(dtype);
   require(row_bytes % 16 == 0, "ep dispatch: row bytes must be a multiple of 16");
@@ -109,7 +111,7 @@ void launch_ep_dispatch_push(const void* x_perm, int dtype, int64_t rows, int d,
   const int64_t want = (rows + 7) / 8;
   const int grid = int(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(device_sm_count()) * 8)));
   ep_dispatch_push_kernel<<<grid, 256, 0, s>>>(
-      reinterpret_cast<const uint4*>(x_perm), rows, int(row_bytes / 16), offsets, E, E / P,
+      reinterpret_cast<const uint4*>(x), perm, k, rows, int(row_bytes / 16), offsets, E, E / P,
       dest_base, me, reinterpret_cast<uint4* const*>(peer_x), peer_ret);
   INFMOE_LAUNCH_CHECK();
 }

@@ -34,8 +34,8 @@ void launch_ep_counts_push(const int32_t* counts, int E, int me, int P, int32_t*
                            cudaStream_t s);
 void launch_ep_plan(const int32_t* all_counts, int P, int E, int me, int32_t* dest_base,
                     int32_t* local_offsets, cudaStream_t s);
-void launch_ep_dispatch_push(const void* x_perm, int dtype, int64_t rows, int d,
-                             const int32_t* offsets, int E, int P, const int32_t* dest_base,
+void launch_ep_dispatch_push(const void* x, const int32_t* perm, int k, int dtype, int64_t rows,
+                             int d, const int32_t* offsets, int E, int P, const int32_t* dest_base,
                              int me, void* const* peer_x, int2* const* peer_ret, cudaStream_t s);
 // N5
 void launch_combine(const void* y_perm, int dtype, const int32_t* inv, const float* topk_w,

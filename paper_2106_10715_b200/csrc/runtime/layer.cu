@@ -215,7 +215,8 @@ void Layer::route(const void* x, int64_t N, cudaStream_t s) {
     launch_gate_softmax(x, desc.dtype, N, desc.d_model, gate_w, gate_b, E, k, idx, wts, counts,
                         s);
   launch_dispatch(idx, N * k, E, offsets, perm, inv, dws, s);
-  launch_gather_rows(x, desc.dtype, N, desc.d_model, k, perm, xp, s);
+  // the PEER transport pushes token rows straight from x (no x_perm)
+  if (!ep_peer) launch_gather_rows(x, desc.dtype, N, desc.d_model, k, perm, xp, s);
 }
 
 void Layer::ffn(const Rows& r, const int32_t* experts, const int32_t* slots, int n,
@@ -534,8 +535,8 @@ void Layer::forward(const void* x, int64_t N, void* y, infmoe_forward_out* out, 
     launch_ep_counts_push(counts, E, me, P, d_peer_counts, s);
     peer_barrier(s);
     launch_ep_plan(sym_counts, P, E, me, dest_base, loc_offsets, s);
-    launch_ep_dispatch_push(xp, desc.dtype, N * k, desc.d_model, offsets, E, P, dest_base, me,
-                            d_peer_x, d_peer_ret, s);
+    launch_ep_dispatch_push(x, perm, k, desc.dtype, N * k, desc.d_model, offsets, E, P,
+                            dest_base, me, d_peer_x, d_peer_ret, s);
     peer_barrier(s);
     const bool need_counts = offloaded || (out && (out->local_rows || out->counts));
     if (need_counts) {
