@@ -161,6 +161,16 @@ def cpu_layer_sample(cfg, x_bits: np.ndarray, w_in_bits, w_out_bits, proj, n_tok
     return secs, int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
 
 
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip() + f" ({os.cpu_count()} logical cpus)"
+    except OSError:
+        pass
+    return f"unknown ({os.cpu_count()} logical cpus)"
+
+
 def reference_pieces(cfg) -> dict | None:
     """Time the reference's own CPU pieces of this path as shipped (the moesim
     headers compiled in place into oracle/_ref, single thread): gaussian_tokens,
@@ -183,28 +193,46 @@ def reference_pieces(cfg) -> dict | None:
                                        C.c_int, vp, vp, vp]
     P = lambda a: a.ctypes.data_as(vp)
     d, E, N, L, bits, K = cfg["d"], cfg["E"], cfg["N"], cfg["L"], cfg["bits"], cfg["K"]
-    out = {"impl": "oracle/_ref (reference headers, g++ -O2, 1 thread)",
+    out = {"impl": "oracle/_ref (reference headers, g++ -O2, 1 thread)", "cpu": cpu_model(),
            "shape": f"{N} tokens x d {d}, {bits} bits, E {E}, {L} layers, K {K}"}
     x = np.empty(N * d, np.float64)
     t0 = time.perf_counter()
     lib.ref_gaussian_tokens(lib.ref_derive_seed(SEED, 0), N, d, P(x))
     out["gaussian_tokens_ms"] = (time.perf_counter() - t0) * 1e3
+    # route_tokens (the LSH gate) at the C1 / C2 / C5 shapes
+    route = {}
+    for name, (n, dd, b, e) in {"c1_512x768_3b": (512, 768, 3, 8), "c2_4096x4096_5b": (N, d, bits, E),
+                                "c5_16384x4096_6b": (16384, 4096, 6, 64)}.items():
+        xs = x if (n, dd) == (N, d) else np.empty(n * dd, np.float64)
+        if xs is not x:
+            lib.ref_gaussian_tokens(lib.ref_derive_seed(SEED, 7), n, dd, P(xs))
+        cnt = np.zeros(e, np.uint64)
+        t0 = time.perf_counter()
+        lib.ref_route_tokens(lib.ref_derive_seed(SEED, 100), b, dd, P(xs), n, e, P(cnt))
+        route[name] = (time.perf_counter() - t0) * 1e3
+    out["route_tokens_ms"] = route
     cnt = np.zeros(E, np.uint64)
-    t0 = time.perf_counter()
     lib.ref_route_tokens(lib.ref_derive_seed(SEED, 100), bits, d, P(x), N, E, P(cnt))
-    out["route_tokens_ms"] = (time.perf_counter() - t0) * 1e3
+    # compute_costs + auto_order per layer at T = 32 and 64
+    co = {}
+    for T in (32, 64):
+        cT = np.resize(cnt, T).astype(np.uint64)
+        alphas = np.zeros(T, np.float64)
+        beta = C.c_double(0.0)
+        order = np.zeros(T, np.int32)
+        fz = [np.zeros(1, np.int32) for _ in range(3)]
+        reps = 200
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            lib.ref_compute_costs(d, cfg["f"], 2, 1643.6e12, 55.5e9, P(cT), T, P(alphas),
+                                  C.byref(beta))
+            lib.ref_schedule(P(alphas), T, beta.value, K, 0, 12, P(order), P(fz[0]), P(fz[1]),
+                             P(fz[2]))
+        co[f"T{T}"] = (time.perf_counter() - t0) / reps * 1e6
+    out["costs_plus_auto_order_us"] = co
     alphas = np.zeros(E, np.float64)
     beta = C.c_double(0.0)
-    order = np.zeros(E, np.int32)
-    fz = [np.zeros(1, np.int32) for _ in range(3)]
-    reps = 200
-    t0 = time.perf_counter()
-    for _ in range(reps):
-        lib.ref_compute_costs(d, cfg["f"], 2, 1643.6e12, 55.5e9, P(cnt), E, P(alphas),
-                              C.byref(beta))
-        lib.ref_schedule(P(alphas), E, beta.value, K, 0, 12, P(order), P(fz[0]), P(fz[1]),
-                         P(fz[2]))
-    out["costs_plus_auto_order_us"] = (time.perf_counter() - t0) / reps * 1e6
+    lib.ref_compute_costs(d, cfg["f"], 2, 1643.6e12, 55.5e9, P(cnt), E, P(alphas), C.byref(beta))
     Ts = np.full(L, E, np.int32)
     al = np.tile(alphas, L)
     be = np.full(L, beta.value)
@@ -256,6 +284,7 @@ def run_reference_arm(args, cfg, rank: int) -> None:
             "config": {"workload": cfg["workload"], "tokens": cfg["N"], "layers": cfg["L"],
                        "d_model": d, "d_ff": f, "experts": E, "top_k": cfg["k"]},
             "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "port",
+                             "cpu": cpu_model(),
                              "sample": f"{n_tok} tokens x 1 layer per step (all layers cost "
                                        f"the same), scaled to the {cfg['L']}-layer stack"},
             "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
@@ -592,6 +621,7 @@ def main() -> None:
             cfg, xb, wi_h.view(torch.int16).numpy().view(np.uint16).reshape(E, -1),
             wo_h.view(torch.int16).numpy().view(np.uint16).reshape(E, -1), proj, n_tok)
         cpu = {"value": n_tok / (secs * L), "unit": "tokens/s", "cores": cores, "kind": "port",
+               "cpu": cpu_model(),
                "sample": f"{n_tok} tokens through layer 0 (LSH gate, dispatch, fp64 FFN, "
                          f"combine), {secs:.2f} s, scaled to the {L}-layer stack"}
 
