@@ -492,7 +492,7 @@ def main() -> None:
             exposed.append(info["exposed_copy_s"])
             # gate + dispatch + gather + one fused FFN per expert with rows (the top-1
             # combine is fused into it); EP adds the receive-side gather and the combine
-            launches += 3 + dispatch_launches + int((rows > 0).sum()) + (2 if P > 1 else 0)
+            launches += 2 + dispatch_launches + int((rows > 0).sum()) + (2 if P > 1 else 0)
             for (st, _l, e, s0, s1) in info["events"]:
                 if st == 1 and rows[e] > 0:
                     ffn_secs += s1 - s0
