@@ -570,6 +570,157 @@ void lsh_fast_go(const void* x, int64_t N, int d, const double* proj, int bits, 
       reinterpret_cast<const T*>(x), N, d, proj, bits, E, force, codes, idx, w, counts);
 }
 
+// ------------------------------------------- N1b fast path on fp64 MMA ----
+// The same certified decision as gate_lsh_fast_kernel, with the parallel dot
+// products on the fp64 tensor cores: S[16 tokens][8 bits] += X[16 x 4] .
+// W[4 x 8] per mma.sync.m16n8k4.f64 (DMMA; 37 TF/s on B200, the DFMA pipe's
+// rate, but 512 FMAs per instruction instead of 32, so the kernel is no longer
+// issue-bound).  The reduction order is free (the bound covers any order), so
+// the k index is permuted: thread (gid, tig) of a warp owns the 8 contiguous
+// columns c0 + 8*tig .. +7 of every 32-column chunk and feeds them to 8
+// consecutive mmas — its A fragment (x rows gid and gid+8) and B fragment
+// (hyperplane row gid) are exactly the 16-byte / 64-byte slices it loads, so
+// no shared memory or shuffles sit in the main loop.  A CTA owns 16 tokens;
+// its 4 warps take the 32-column chunks round-robin and meet in shared memory
+// for the final sums, norms and the certified decision.
+constexpr int kLshMmaWarps = 8;  // 16 tokens per CTA, 8 warps splitting d (2 CTAs per SM: one wave)
+
+__device__ __forceinline__ void dmma_16x8x4(double (&c)[4], double a0, double a1, double b0) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, "
+      "{%0,%1,%2,%3};"
+      : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+      : "d"(a0), "d"(a1), "d"(b0));
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kLshMmaWarps * 32) gate_lsh_mma_kernel(
+    const T* __restrict__ x, int64_t N, int d, const double* __restrict__ proj, int bits, int E,
+    int force_exact, uint32_t* __restrict__ codes, int32_t* __restrict__ topk_idx,
+    float* __restrict__ topk_w, int32_t* __restrict__ counts) {
+  constexpr int W = kLshMmaWarps;
+  __shared__ double s_part[W][16][9];  // per-warp partial S (padded)
+  __shared__ double s_xx[W][16];
+  __shared__ double s_ww[W][8];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int gid = lane / 4, tig = lane % 4;
+  const int64_t tok0 = int64_t(blockIdx.x) * 16;
+  const bool r0ok = tok0 + gid < N, r1ok = tok0 + gid + 8 < N;
+  const bool bok = gid < bits;
+  const T* x0 = x + (r0ok ? tok0 + gid : 0) * int64_t(d);
+  const T* x1 = x + (r1ok ? tok0 + gid + 8 : 0) * int64_t(d);
+  const double* w0 = proj + size_t(bok ? gid : 0) * d;
+
+  double acc[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};  // two independent mma chains
+  double xx0 = 0.0, xx1 = 0.0, ww = 0.0;
+  const int nch = (d + 31) / 32;
+  // raw operands of the next chunk in flight ahead of the math (loads of
+  // chunk ch + W issue before chunk ch's mmas); x stays raw until it is used
+  constexpr int XV = sizeof(T) == 2 ? 1 : 2;  // 16-byte vectors per 8 x values
+  struct Raw {
+    uint4 x0[XV], x1[XV];
+    double2 w[4];
+  };
+  auto load = [&](int ch, Raw& r) {
+    const int c = ch * 32 + tig * 8;
+    const bool cok = ch < nch && c < d;  // d % 8 == 0: a slice is all in or all out
+#pragma unroll
+    for (int v = 0; v < XV; ++v) {
+      r.x0[v] = r0ok && cok ? __ldcs(reinterpret_cast<const uint4*>(x0 + c) + v) : make_uint4(0, 0, 0, 0);
+      r.x1[v] = r1ok && cok ? __ldcs(reinterpret_cast<const uint4*>(x1 + c) + v) : make_uint4(0, 0, 0, 0);
+    }
+    const double2* wp = reinterpret_cast<const double2*>(w0 + c);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) r.w[i] = bok && cok ? __ldg(wp + i) : make_double2(0.0, 0.0);
+  };
+  auto widen = [&](const uint4 (&raw)[XV], double (&v)[8]) {
+    const T* e = reinterpret_cast<const T*>(&raw[0]);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = double(load_as_f32(e, i));
+  };
+  Raw cur, nxt;
+  load(warp, cur);
+  for (int ch = warp; ch < nch; ch += W) {
+    load(ch + W, nxt);
+    double a[8], b[8];
+    widen(cur.x0, a);
+    widen(cur.x1, b);
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+      const double wm = (m & 1) ? cur.w[m / 2].y : cur.w[m / 2].x;
+      dmma_16x8x4(acc[m & 1], a[m], b[m], wm);
+      xx0 = fma(a[m], a[m], xx0);
+      xx1 = fma(b[m], b[m], xx1);
+      ww = fma(wm, wm, ww);
+    }
+    cur = nxt;
+  }
+  // D fragment: acc[.][0..1] = S[gid][2tig, 2tig+1], acc[.][2..3] = S[gid+8][...]
+  s_part[warp][gid][2 * tig] = acc[0][0] + acc[1][0];
+  s_part[warp][gid][2 * tig + 1] = acc[0][1] + acc[1][1];
+  s_part[warp][gid + 8][2 * tig] = acc[0][2] + acc[1][2];
+  s_part[warp][gid + 8][2 * tig + 1] = acc[0][3] + acc[1][3];
+  // norms: sum over the 4 tig lanes of each row (the whole d of this warp's chunks)
+#pragma unroll
+  for (int off = 1; off < 4; off <<= 1) {
+    xx0 += __shfl_xor_sync(0xffffffffu, xx0, off);
+    xx1 += __shfl_xor_sync(0xffffffffu, xx1, off);
+    ww += __shfl_xor_sync(0xffffffffu, ww, off);
+  }
+  if (tig == 0) {
+    s_xx[warp][gid] = xx0;
+    s_xx[warp][gid + 8] = xx1;
+    s_ww[warp][gid] = ww;
+  }
+  __syncthreads();
+  if (warp != 0) return;
+  // lanes 0..15: one token each
+  if (lane < 16 && tok0 + lane < N) {
+    const int t = lane;
+    double xn = 0.0;
+#pragma unroll
+    for (int w = 0; w < W; ++w) xn += s_xx[w][t];
+    uint32_t code = 0;
+    for (int j = 0; j < bits; ++j) {
+      double S = 0.0, wn = 0.0;
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        S += s_part[w][t][j];
+        wn += s_ww[w][j];
+      }
+      const double thr = 8.0 * double(d) * 0x1p-53 * sqrt(xn) * sqrt(wn) + 0x1p-1000;
+      bool bit;
+      if (xn == 0.0) {
+        bit = true;  // all products are +-0: the chain stays +0, and +0 >= 0
+      } else if (!force_exact && fabs(S) > thr) {
+        bit = S > 0.0;
+      } else {  // ambiguous, NaN or Inf: the reference's sequential chain
+        const T* xr = x + (tok0 + t) * int64_t(d);
+        const double* wr = proj + size_t(j) * d;
+        double dot = 0.0;
+        for (int i = 0; i < d; ++i)
+          dot = __dadd_rn(dot, __dmul_rn(double(load_as_f32(xr, i)), wr[i]));
+        bit = dot >= 0.0;
+      }
+      if (bit) code |= 1u << j;
+    }
+    const int64_t tk = tok0 + t;
+    const int e = int(code % uint32_t(E));
+    if (codes) codes[tk] = code;
+    topk_idx[tk] = e;
+    topk_w[tk] = 1.0f;
+    atomicAdd(&counts[e], 1);
+  }
+}
+
+template <typename T>
+void lsh_mma_go(const void* x, int64_t N, int d, const double* proj, int bits, int E,
+                uint32_t* codes, int32_t* idx, float* w, int32_t* counts, cudaStream_t s) {
+  static const int force = lsh_env("INFMOE_LSH_FORCE_EXACT", 0);
+  gate_lsh_mma_kernel<T><<<unsigned((N + 15) / 16), kLshMmaWarps * 32, 0, s>>>(
+      reinterpret_cast<const T*>(x), N, d, proj, bits, E, force, codes, idx, w, counts);
+}
+
 template <typename T, int EB>
 void softmax_go(const void* x, int64_t N, int d, const float* wg, const float* bias, int E, int k,
                 int32_t* idx, float* w, int32_t* counts, cudaStream_t s) {
@@ -630,6 +781,15 @@ void launch_gate_lsh(const void* x, int dtype, int64_t N, int d, const double* p
   INFMOE_CUDA(cudaMemsetAsync(counts, 0, sizeof(int32_t) * size_t(E), stream));
   if (N == 0) return;
   static const int fast = lsh_env("INFMOE_LSH_FAST", 1);
+  static const int mma = lsh_env("INFMOE_LSH_MMA", 1);
+  if (fast && mma && bits <= 8 && d % 8 == 0) {  // certified fast path on fp64 MMA
+    if (dtype == kDtypeBf16)
+      lsh_mma_go<__nv_bfloat16>(x, N, d, proj, bits, E, codes, topk_idx, topk_w, counts, stream);
+    else
+      lsh_mma_go<float>(x, N, d, proj, bits, E, codes, topk_idx, topk_w, counts, stream);
+    INFMOE_LAUNCH_CHECK();
+    return;
+  }
   if (fast && bits <= 8) {
     const bool bf = dtype == kDtypeBf16;
     if (bits <= 4) {

@@ -8,8 +8,9 @@ whose exact dot is +-1e-20 while the sequential double sum is exactly +0, an
 exact cancellation, all-zero / -0 rows, NaN and Inf rows.  Expected codes come
 from a pure-Python left-to-right loop (CPython floats: IEEE binary64, no
 contraction) for the crafted rows, and from the reference's lsh_codes for the
-random rows.  Each path (fast, forced exact chain, the all-sequential ring
-kernel) runs in its own subprocess because the mode is read once per process.
+random rows.  Each path (the fp64-MMA fast kernel, the DFMA fast kernel, each
+with its exact chain forced, and the all-sequential ring kernel) runs in its
+own subprocess because the mode is read once per process.
 """
 import os
 import subprocess
@@ -75,7 +76,9 @@ def _case(bf16: bool):
 
 
 @pytest.mark.parametrize("bf16", [True, False])
-@pytest.mark.parametrize("mode", [{}, {"INFMOE_LSH_FORCE_EXACT": "1"}, {"INFMOE_LSH_FAST": "0"}])
+@pytest.mark.parametrize("mode", [{}, {"INFMOE_LSH_FORCE_EXACT": "1"}, {"INFMOE_LSH_MMA": "0"},
+                                  {"INFMOE_LSH_MMA": "0", "INFMOE_LSH_FORCE_EXACT": "1"},
+                                  {"INFMOE_LSH_FAST": "0"}])
 def test_lsh_paths_match_sequential_reference(tmp_path, bf16, mode):
     x, proj, E, expect = _case(bf16)
     inp = tmp_path / "in.npz"
