@@ -505,6 +505,14 @@ def main() -> None:
     costs = [im.compute_costs(info["local_rows"].astype(np.uint64), g_loc, hw_meas)
              for info in all_infos[-1]]
     _, sim_rep, _ = im.simulate_model(costs, cfg["K"])
+    # the measured timelines of the last step against replay_check's rules
+    # (verification.hpp:108-206: one lane per stream, causality, <= K+1 experts
+    # resident; durations are measured, so they are not compared to alpha/beta)
+    audit = {}
+    for info, cv in zip(all_infos[-1], costs):
+        for kind, n in im.replay_check(info["events"], [cv], cfg["K"] + 1,
+                                       check_durations=False, tol_s=2e-6).items():
+            audit[kind] = audit.get(kind, 0) + n
     if os.environ.get("BENCH_VERBOSE"):
         for l, info in enumerate(all_infos[-1]):
             ld = [(s1 - s0) for (st, _l, _e, s0, s1) in info["events"] if st == 0]
@@ -654,7 +662,8 @@ def main() -> None:
                 "per": "rank (each rank streams its own experts over its own host link)",
                 "exposed_copy_ms_per_layer": 1e3 * float(np.mean(exposed)),
                 "simulated_ms_per_step": sim_rep.makespan * 1e3,
-                "measured_over_simulated": t_in / (sim_rep.makespan * 1e3)},
+                "measured_over_simulated": t_in / (sim_rep.makespan * 1e3),
+                "replay_check_violations": audit},
         # dominant kernel of the path: the expert FFN (both tcgen05 projections in
         # one persistent launch), timed with CUDA events on its stream over the
         # resident 24-layer pass; bytes = weights of routed experts + activations
