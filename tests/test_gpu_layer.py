@@ -289,3 +289,32 @@ def test_layer_edge_token_counts(cuda, gate, k, offloaded):
     err = np.abs(y1.float().cpu().numpy() - ref)
     assert np.all(err <= ATOL + RTOL * np.abs(ref)), err.max()
     layer.close()
+
+
+def test_layer_error_paths(cuda):
+    """Misuse is reported through the status codes (Python exceptions here),
+    never a crash: too many tokens, device weights for an offloaded layer,
+    K < 1, an unknown EP transport, N = 0 with NULL buffers allowed."""
+    d, f, E = 128, 256, 4
+    wi = torch.zeros(E, f, d, dtype=torch.bfloat16, device=cuda)
+    wo = torch.zeros(E, d, f, dtype=torch.bfloat16, device=cuda)
+    lay = dv.MoELayer(d, f, E, 1, wi, wo, gate="lsh", lsh_bits=2, max_tokens=8)
+    with pytest.raises(ValueError):
+        lay.forward(torch.zeros(9, d, dtype=torch.bfloat16, device=cuda))  # > max_tokens
+    lay.close()
+    with pytest.raises(ValueError):  # offloaded weights must be host memory
+        dv.MoELayer(d, f, E, 1, wi, wo, gate="lsh", lsh_bits=2, offloaded=True, K=2)
+    with pytest.raises(ValueError):
+        dv.MoELayer(d, f, E, 1, wi.cpu().pin_memory(), wo.cpu().pin_memory(), gate="lsh",
+                    lsh_bits=2, offloaded=True, K=0)
+    comm = im.ep_comm_init(im.ep_unique_id(), 1, 0)
+    try:
+        lay = dv.MoELayer(d, f, E, 1, wi, wo, gate="lsh", lsh_bits=2, ep_size=1, ep_rank=0,
+                          ep_comm=comm)
+        lay.desc.ep_transport = 7  # the struct is copied at create: rebuild through the C-ABI
+        h = C.c_void_p()
+        assert im._lib.infmoe_layer_create(C.byref(lay.desc), C.byref(h)) == 6
+        assert b"ep_transport" in im._lib.infmoe_last_error()
+        lay.close()
+    finally:
+        im.ep_comm_destroy(comm)
