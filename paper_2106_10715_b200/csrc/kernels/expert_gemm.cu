@@ -104,6 +104,15 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+// 0 evict_first, 1 evict_normal, 2 evict_last
+__device__ __forceinline__ uint64_t policy_of(int kind) {
+  return kind == 0 ? policy_evict_first() : kind == 1 ? policy_evict_normal() : policy_evict_last();
+}
 __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 }
@@ -482,12 +491,15 @@ struct FusedParams {
   // ret[r].x's y_back at row ret[r].y (peer_y = every rank's y_back)
   const int2* ret;
   void* peer_y[kMaxPeers];
+  int64_t band_bytes;  // L2 budget for one band of token rows (0: one band per expert)
+  int32_t pol_w, pol_x;  // L2 policies of the weight / token-row loads (policy_of; w -1: by chunks)
   int32_t experts[kMaxGroups];
   int32_t slots[kMaxGroups];
 };
 
 struct FusedTable {
   int32_t n_groups, fb1, fb2, total1;
+  int32_t band1, band2;  // token chunks per band (phase 1 / phase 2), see band_split
   int32_t start1[kMaxGroups + 1];
   int32_t start2[kMaxGroups + 1];
   int32_t chunks[kMaxGroups];
@@ -502,14 +514,61 @@ struct FTile {
   int32_t row0, ntok, w_row0, f0;
 };
 
+// The tiles of one expert are walked in bands of `band` token chunks, the token
+// chunk fastest inside a band.  The tiles in flight at once (one per CTA/pair)
+// then share a few weight blocks, and the band's token rows (x_perm or H) stay
+// L2-resident across all the expert's weight blocks: an expert with C chunks
+// reads its weights ceil(C / band) times instead of once per wave and its token
+// rows once instead of once per weight block.  band >= C (every balanced top-1
+// layer: one chunk per expert) is the plain chunk-fastest order.
+__device__ __forceinline__ void band_split(int32_t local, int32_t chunks, int32_t nfb,
+                                           int32_t band, int32_t& tc, int32_t& fb) {
+  band = min(band, chunks);
+  const int32_t per = band * nfb;
+  const int32_t b = local / per;
+  const int32_t rem = local - b * per;
+  const int32_t w = min(band, chunks - b * band);
+  tc = b * band + rem % w;
+  fb = rem / w;
+}
+
+__device__ __forceinline__ int32_t band_size(int64_t budget, int64_t chunk_bytes) {
+  if (budget <= 0) return 1 << 30;
+  const int64_t b = budget / chunk_bytes;
+  return b < 1 ? 1 : (b > (1 << 30) ? (1 << 30) : int32_t(b));
+}
+
+// L2 budget of one band of token rows; INFMOE_FFN_BAND_MB overrides (0 = one band)
+static int64_t ffn_band_bytes() {
+  static const int64_t v = [] {
+    const char* e = std::getenv("INFMOE_FFN_BAND_MB");
+    return int64_t(e ? std::atoi(e) : 64) << 20;
+  }();
+  return v;
+}
+
+// L2 policies of the fused FFN's loads.  Default (-1): token rows evict_last
+// (re-read once per weight block); weights evict_first when the expert is one
+// token chunk (read once) and evict_normal when it spans several (re-read once
+// per band, by the CTAs working on the band's other chunks).
+// INFMOE_FFN_POLICY="wx" (digits of policy_of) forces both.
+static void ffn_policies(int32_t& w, int32_t& x) {
+  static const int v = [] {
+    const char* e = std::getenv("INFMOE_FFN_POLICY");
+    return e ? std::atoi(e) : -1;
+  }();
+  w = v < 0 ? -1 : (v / 10) % 3;
+  x = v < 0 ? 2 : v % 10 % 3;
+}
+
 template <int TOK>
 __device__ __forceinline__ FTile fdecode(const FusedTable& tt, int32_t t, int32_t& c1,
                                          int32_t& c2, int32_t d, int32_t f) {
   FTile r;
   if (t < tt.total1) {
     while (t >= tt.start1[c1 + 1]) ++c1;
-    const int32_t local = t - tt.start1[c1];
-    const int32_t tc = local % tt.chunks[c1], fb = local / tt.chunks[c1];
+    int32_t tc, fb;
+    band_split(t - tt.start1[c1], tt.chunks[c1], tt.fb1, tt.band1, tc, fb);
     r.phase = 0;
     r.g = c1;
     r.row0 = tt.row0[c1] + tc * TOK;
@@ -519,8 +578,8 @@ __device__ __forceinline__ FTile fdecode(const FusedTable& tt, int32_t t, int32_
   } else {
     t -= tt.total1;
     while (t >= tt.start2[c2 + 1]) ++c2;
-    const int32_t local = t - tt.start2[c2];
-    const int32_t tc = local % tt.chunks[c2], fb = local / tt.chunks[c2];
+    int32_t tc, fb;
+    band_split(t - tt.start2[c2], tt.chunks[c2], tt.fb2, tt.band2, tc, fb);
     r.phase = 1;
     r.g = c2;
     r.row0 = tt.row0[c2] + tc * TOK;
@@ -568,6 +627,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     tt.n_groups = p.n_groups;
     tt.fb1 = p.f / BM;
     tt.fb2 = p.d / BM;
+    tt.band1 = band_size(p.band_bytes, int64_t(TOK) * p.d * 2);
+    tt.band2 = band_size(p.band_bytes, int64_t(TOK) * p.f * 2);
     int32_t a1 = 0, a2 = 0;
     for (int g = 0; g < p.n_groups; ++g) {
       const int e = p.experts[g];
@@ -613,8 +674,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (warp == 0) {
     // ================= TMA producer =================
     if (lane == 0) {
-      const uint64_t pol_w = policy_evict_first();
-      const uint64_t pol_x = policy_evict_last();
+      const uint64_t pol_w1 = policy_of(p.pol_w < 0 ? 0 : p.pol_w);  // single-chunk experts
+      const uint64_t pol_wn = policy_of(p.pol_w < 0 ? 1 : p.pol_w);  // multi-chunk experts
+      const uint64_t pol_x = policy_of(p.pol_x);
       int stage = 0;
       uint32_t phase = 0;
       int32_t c1 = 0, c2 = 0, ready_g = -1;
@@ -633,6 +695,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         const CUtensorMap* ta = tile.phase ? &tmap_h : &tmap_x;
         const CUtensorMap* tb = tile.phase ? &tmap_w2 : &tmap_w1;
+        const uint64_t pol_w = tt.chunks[tile.g] > 1 ? pol_wn : pol_w1;
         const int32_t kblocks = (tile.phase ? p.f : p.d) / bk;
         const int boxes = (tile.ntok + TOK_BOX - 1) / TOK_BOX;
         const uint32_t bytes = W_TILE + boxes * (TOK_BOX * ROW_BYTES);
@@ -796,6 +859,8 @@ void fused_launch(const FusedFfnArgs& a, cudaStream_t stream) {
   p.perm = a.perm;
   p.topk_w = a.topk_w;
   p.ret = a.ret;
+  p.band_bytes = ffn_band_bytes();
+  ffn_policies(p.pol_w, p.pol_x);
   for (int r = 0; r < a.n_peers && r < kMaxPeers; ++r) p.peer_y[r] = a.peer_y[r];
   for (int g = 0; g < a.n_groups; ++g) {
     p.experts[g] = a.experts[g];
@@ -927,6 +992,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     tt.n_groups = p.n_groups;
     tt.fb1 = p.f / (2 * BM);
     tt.fb2 = p.d / (2 * BM);
+    tt.band1 = band_size(p.band_bytes, int64_t(TOK) * p.d * 2);
+    tt.band2 = band_size(p.band_bytes, int64_t(TOK) * p.f * 2);
     int32_t a1 = 0, a2 = 0;
     for (int g = 0; g < p.n_groups; ++g) {
       const int e = p.experts[g];
@@ -973,8 +1040,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   if (warp == 0) {
     // ================= TMA producer (both CTAs) =================
     if (lane == 0) {
-      const uint64_t pol_w = policy_evict_first();
-      const uint64_t pol_x = policy_evict_last();
+      const uint64_t pol_w1 = policy_of(p.pol_w < 0 ? 0 : p.pol_w);  // single-chunk experts
+      const uint64_t pol_wn = policy_of(p.pol_w < 0 ? 1 : p.pol_w);  // multi-chunk experts
+      const uint64_t pol_x = policy_of(p.pol_x);
       int stage = 0;
       uint32_t phase = 0;
       int32_t c1 = 0, c2 = 0, ready_g = -1;
@@ -997,6 +1065,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         const uint32_t bytes_pair = 2u * (W_TILE + boxes * (TOK_BOX * ROW_BYTES));
         const CUtensorMap* ta = tile.phase ? &tmap_h : &tmap_x;
         const CUtensorMap* tb = tile.phase ? &tmap_w2 : &tmap_w1;
+        const uint64_t pol_w = tt.chunks[tile.g] > 1 ? pol_wn : pol_w1;
         const int32_t kblocks = (tile.phase ? p.f : p.d) / bk;
         for (int32_t kb = 0; kb < kblocks; ++kb) {
           mbar_wait_guarded(empty_bar(stage), phase ^ 1);
@@ -1160,6 +1229,8 @@ void fused_pair_launch(const FusedFfnArgs& a, cudaStream_t stream) {
   p.perm = a.perm;
   p.topk_w = a.topk_w;
   p.ret = a.ret;
+  p.band_bytes = ffn_band_bytes();
+  ffn_policies(p.pol_w, p.pol_x);
   for (int r = 0; r < a.n_peers && r < kMaxPeers; ++r) p.peer_y[r] = a.peer_y[r];
   for (int g = 0; g < a.n_groups; ++g) {
     p.experts[g] = a.experts[g];

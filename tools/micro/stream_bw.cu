@@ -6,6 +6,8 @@
 //   mode 1: 2D TMA, two 128-B boxes per row back to back (256 B per row/stage)
 //   mode 2: 1D bulk copies of 16 KB contiguous (a pre-tiled weight layout)
 //   mode 3: 2D TMA boxes 128 rows x 128 B with no L2 promotion
+//   l2rows > 0: the tiles cycle over the first l2rows weight rows only (an
+//   L2-resident working set): the L2 -> shared-memory TMA ceiling
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -133,9 +135,12 @@ int main() {
   CK(cudaFuncSetAttribute(stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           STAGES * STAGE + 1024));
   const int tiles = int(rows / 128);
-  int runs[][2] = {{0, 0}, {1, 0}, {2, 0}, {3, 0}, {0, 3}, {0, 4}, {0, 5}, {0, 6}, {0, 8}, {0, 10}};
+  int runs[][3] = {{0, 0, 0}, {1, 0, 0}, {2, 0, 0}, {3, 0, 0}, {0, 3, 0}, {0, 4, 0}, {0, 5, 0},
+                   {0, 6, 0}, {0, 8, 0}, {0, 10, 0}, {0, 6, 2048}, {0, 8, 2048}, {0, 12, 2048},
+                   {1, 6, 2048}, {0, 12, 4096}, {0, 12, 8192}};
   for (auto& rr : runs) {
     const int mode = rr[0], nst = rr[1];
+    const int l2rows = rr[2];
     CUtensorMap m;
     memset(&m, 0, sizeof(m));
     cuuint64_t dims[2] = {cuuint64_t(d), cuuint64_t(rows)};
@@ -151,7 +156,8 @@ int main() {
     float best = 1e30f;
     for (int it = 0; it < 5; ++it) {
       cudaEventRecord(a);
-      stream_kernel<<<sms, 64, STAGES * STAGE + 1024>>>(m, w, mode, tiles, int(rows), d, nst);
+      stream_kernel<<<sms, 64, STAGES * STAGE + 1024>>>(m, w, mode, tiles,
+                                                         l2rows ? l2rows : int(rows), d, nst);
       cudaEventRecord(b);
       CK(cudaEventSynchronize(b));
       float ms;
@@ -159,7 +165,12 @@ int main() {
       if (it > 0 && ms < best) best = ms;
     }
     CK(cudaGetLastError());
-    printf("mode %d stages %d: %.3f ms  %.1f GB/s\n", mode, nst, best, bytes / (best * 1e-3) / 1e9);
+    int clk_khz = 0;
+    cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, 0);
+    const double gbs = bytes / (best * 1e-3) / 1e9;
+    printf("mode %d stages %d l2rows %d (%s): %.3f ms  %.1f GB/s  %.1f B/clk/SM at %d MHz\n", mode,
+           nst, l2rows, l2rows ? "L2-resident" : "HBM", best, gbs,
+           gbs * 1e9 / (double(clk_khz) * 1e3) / sms, clk_khz / 1000);
   }
   return 0;
 }
