@@ -398,10 +398,10 @@ def measure_c5(torch, im, dv, dev, local, stream, peaks, h2d_peak, reps: int = 3
     wg_dev, b_dev = torch.from_numpy(gw).to(dev), torch.from_numpy(bias).to(dev)
     t_gate = timed(lambda: dv.gate_softmax_topk(x, wg_dev, k, bias=b_dev))
     t_disp = timed(lambda: dv.dispatch(idx, E))
-    t_gath = timed(lambda: dv.gather_rows(x, perm, k))
+    t_gath = timed(lambda: dv.gather_rows_by_token(x, inv, k))  # the layer's k > 1 path
     t_comb = timed(lambda: dv.combine(xp, inv, w, N, k))
     hbm = float(peaks["hbm_gbs"])
-    gath_b = N * d * 2 + N * k * d * 2 + N * k * 4       # x once, x_perm, perm
+    gath_b = N * d * 2 + N * k * d * 2 + N * k * 4       # x once, x_perm, inv
     comb_b = N * k * d * 2 + N * d * 2 + N * k * 8       # y_perm, y, inv + weights
     gate_b = N * d * 2 + E * d * 4 + N * k * 8            # x, W_g, idx + weights
     mv = {"config": "C5 sizes: 16384 tokens x 4096, top-2, E=64, bf16; median of 5 launches, "
@@ -412,7 +412,9 @@ def measure_c5(torch, im, dv, dev, local, stream, peaks, h2d_peak, reps: int = 3
           "dispatch_counting_sort": {"us": t_disp * 1e6, "assignments": N * k},
           "gather_rows": {"us": t_gath * 1e6, "gbs": gath_b / t_gath / 1e9,
                           "frac": gath_b / t_gath / 1e9 / hbm, "bytes": gath_b,
-                          "bytes_formula": "x read once + x_perm written + perm"},
+                          "kernel": "gather_rows_by_token (warp per token: row read once, "
+                                    "written to its k positions)",
+                          "bytes_formula": "x read once + x_perm written + inv"},
           "combine": {"us": t_comb * 1e6, "gbs": comb_b / t_comb / 1e9,
                       "frac": comb_b / t_comb / 1e9 / hbm, "bytes": comb_b,
                       "bytes_formula": "y_perm read + y written + inv/weights"},

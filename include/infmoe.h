@@ -201,6 +201,10 @@ int infmoe_dispatch(const int32_t* topk_idx, int64_t N, int32_t k, int32_t E,
 /* N2 gather: x_perm[p] = x[perm[p] / k] for p < N*k (row-vectorised) */
 int infmoe_gather_rows(const void* x, int32_t dtype, int64_t N, int32_t d, int32_t k,
                        const int32_t* perm, void* x_perm, void* stream);
+/* N2 gather, token-major: x_perm[inv[t*k+j]] = x[t] (the same x_perm as
+ * infmoe_gather_rows; each token row is read once — the layer's path for k > 1) */
+int infmoe_gather_rows_by_token(const void* x, int32_t dtype, int64_t N, int32_t d, int32_t k,
+                                const int32_t* inv, void* x_perm, void* stream);
 /* N3+N4 grouped expert FFN on tcgen05: for each listed expert e with rows
  * [offsets[e], offsets[e+1]) of x_perm:  h = GeLU(x_perm . w_in[slot]^T) (bf16 into h),
  * y_perm = h . w_out[slot]^T.  w_in is [n_slots, d_ff, d_model], w_out is

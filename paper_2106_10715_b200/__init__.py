@@ -175,6 +175,7 @@ _lib.infmoe_gate_lsh.argtypes = [_vp, _i32, C.c_int64, _i32, _vp, _i32, _i32, _v
                                  _vp, _vp]
 _lib.infmoe_dispatch.argtypes = [_vp, C.c_int64, _i32, _i32, _vp, _vp, _vp, _vp, _vp]
 _lib.infmoe_gather_rows.argtypes = [_vp, _i32, C.c_int64, _i32, _i32, _vp, _vp, _vp]
+_lib.infmoe_gather_rows_by_token.argtypes = [_vp, _i32, C.c_int64, _i32, _i32, _vp, _vp, _vp]
 _lib.infmoe_expert_ffn.argtypes = [_vp, C.c_int64, _i32, _i32, _i32, _vp, _i32, _vp, _vp, _i32,
                                    _vp, _vp, _i32, _vp, _vp, _vp]
 _lib.infmoe_combine.argtypes = [_vp, _i32, _vp, _vp, C.c_int64, _i32, _i32, _vp, _vp]

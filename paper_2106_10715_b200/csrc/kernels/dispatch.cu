@@ -171,7 +171,48 @@ __global__ void gather_rows_kernel(const uint4* __restrict__ x, int64_t rows_out
     const int64_t src = perm[p] / k;
     const uint4* s = x + src * vec_per_row;
     uint4* d = xp + p * vec_per_row;
-    for (int v = lane; v < vec_per_row; v += 32) d[v] = __ldg(s + v);
+    // 4 independent 16-byte loads in flight per lane before the stores (the
+    // row copy is latency-bound at 1 load per lane: ~32 KB in flight per SM)
+    int v = lane;
+    for (; v + 96 < vec_per_row; v += 128) {
+      uint4 r[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) r[u] = __ldg(s + v + 32 * u);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) d[v + 32 * u] = r[u];
+    }
+    for (; v < vec_per_row; v += 32) d[v] = __ldg(s + v);
+  }
+}
+
+// token-major form of the same gather: warp per token, the row is read ONCE and
+// written to its k positions x_perm[inv[t*k+j]] (the perm-driven form reads a
+// token row k times, which misses L2 when x is larger than L2)
+__global__ void gather_rows_by_token_kernel(const uint4* __restrict__ x, int64_t N,
+                                            int vec_per_row, int k,
+                                            const int32_t* __restrict__ inv,
+                                            uint4* __restrict__ xp) {
+  const int warps = blockDim.x / 32;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  for (int64_t t = int64_t(blockIdx.x) * warps + warp; t < N; t += int64_t(gridDim.x) * warps) {
+    int32_t dst[8];
+    for (int j = 0; j < k; ++j) dst[j] = inv[t * k + j];
+    const uint4* s = x + t * vec_per_row;
+    int v = lane;
+    for (; v + 96 < vec_per_row; v += 128) {
+      uint4 r[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) r[u] = __ldg(s + v + 32 * u);
+      for (int j = 0; j < k; ++j) {
+        uint4* d = xp + int64_t(dst[j]) * vec_per_row;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) d[v + 32 * u] = r[u];
+      }
+    }
+    for (; v < vec_per_row; v += 32) {
+      const uint4 r = __ldg(s + v);
+      for (int j = 0; j < k; ++j) xp[int64_t(dst[j]) * vec_per_row + v] = r;
+    }
   }
 }
 
@@ -202,24 +243,40 @@ __global__ void combine_kernel(const T* __restrict__ yp, const int32_t* __restri
       rows[j] = inv[t * k + j];
       ws[j] = w[t * k + j];
     }
-    for (int v = lane; v < nvec; v += 32) {
-      float acc[V];
+    // U vectors per lane per step: the k*U row loads of a step are issued
+    // before any arithmetic (same fmaf chain per element, slot order 0..k-1)
+    constexpr int U = 4;
+    for (int v0 = lane; v0 < nvec; v0 += 32 * U) {
+      float acc[U][V];
 #pragma unroll
-      for (int i = 0; i < V; ++i) acc[i] = 0.0f;
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int i = 0; i < V; ++i) acc[u][i] = 0.0f;
       for (int j = 0; j < k; ++j) {
-        const uint4 raw = __ldg(reinterpret_cast<const uint4*>(yp + size_t(rows[j]) * d) + v);
-        const T* e = reinterpret_cast<const T*>(&raw);
+        const uint4* src = reinterpret_cast<const uint4*>(yp + size_t(rows[j]) * d);
+        uint4 raw[U];
 #pragma unroll
-        for (int i = 0; i < V; ++i) acc[i] = fmaf(ws[j], load_as_f32(e, i), acc[i]);
-      }
-      uint4 out;
-      T* o = reinterpret_cast<T*>(&out);
+        for (int u = 0; u < U; ++u)
+          if (v0 + 32 * u < nvec) raw[u] = __ldg(src + v0 + 32 * u);
 #pragma unroll
-      for (int i = 0; i < V; ++i) {
-        if constexpr (sizeof(T) == 2) o[i] = __float2bfloat16_rn(acc[i]);
-        else o[i] = acc[i];
+        for (int u = 0; u < U; ++u) {
+          const T* e = reinterpret_cast<const T*>(&raw[u]);
+#pragma unroll
+          for (int i = 0; i < V; ++i) acc[u][i] = fmaf(ws[j], load_as_f32(e, i), acc[u][i]);
+        }
       }
-      reinterpret_cast<uint4*>(y + size_t(t) * d)[v] = out;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (v0 + 32 * u >= nvec) break;
+        uint4 out;
+        T* o = reinterpret_cast<T*>(&out);
+#pragma unroll
+        for (int i = 0; i < V; ++i) {
+          if constexpr (sizeof(T) == 2) o[i] = __float2bfloat16_rn(acc[u][i]);
+          else o[i] = acc[u][i];
+        }
+        reinterpret_cast<uint4*>(y + size_t(t) * d)[v0 + 32 * u] = out;
+      }
     }
   }
 }
@@ -266,6 +323,18 @@ void launch_gather_rows(const void* x, int dtype, int64_t N, int d, int k, const
   if (rows == 0) return;
   gather_rows_kernel<<<grid_for_rows(rows, 8), 256, 0, s>>>(
       reinterpret_cast<const uint4*>(x), rows, int(row_bytes / 16), k, perm,
+      reinterpret_cast<uint4*>(x_perm));
+  INFMOE_LAUNCH_CHECK();
+}
+
+void launch_gather_rows_by_token(const void* x, int dtype, int64_t N, int d, int k,
+                                 const int32_t* inv, void* x_perm, cudaStream_t s) {
+  const size_t row_bytes = size_t(d) * dtype_bytes(dtype);
+  require(row_bytes % 16 == 0, "gather: row bytes must be a multiple of 16");
+  require(k >= 1 && k <= 8, "gather: top_k must be in [1, 8]");
+  if (N == 0) return;
+  gather_rows_by_token_kernel<<<grid_for_rows(N, 8), 256, 0, s>>>(
+      reinterpret_cast<const uint4*>(x), N, int(row_bytes / 16), k, inv,
       reinterpret_cast<uint4*>(x_perm));
   INFMOE_LAUNCH_CHECK();
 }

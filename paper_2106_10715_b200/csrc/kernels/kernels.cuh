@@ -27,6 +27,9 @@ void launch_dispatch(const int32_t* topk_idx, int64_t n_assign, int E, int32_t* 
                      int32_t* perm, int32_t* inv, void* workspace, cudaStream_t stream);
 void launch_gather_rows(const void* x, int dtype, int64_t N, int d, int k, const int32_t* perm,
                         void* x_perm, cudaStream_t stream);
+// x_perm[inv[t*k+j]] = x[t]: the same x_perm, each token row read once
+void launch_gather_rows_by_token(const void* x, int dtype, int64_t N, int d, int k,
+                                 const int32_t* inv, void* x_perm, cudaStream_t s);
 void launch_scatter_rows(const void* src, int dtype, int64_t rows, int d, const int32_t* index,
                          void* dst, cudaStream_t stream);
 // N7 expert parallelism over peer memory (ep_peer.cu)

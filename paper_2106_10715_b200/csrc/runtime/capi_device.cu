@@ -69,6 +69,14 @@ int infmoe_gather_rows(const void* x, int32_t dtype, int64_t N, int32_t d, int32
   });
 }
 
+int infmoe_gather_rows_by_token(const void* x, int32_t dtype, int64_t N, int32_t d, int32_t k,
+                                const int32_t* inv, void* x_perm, void* stream) {
+  return guarded([&] {
+    require(x && inv && x_perm, "gather: NULL pointer");
+    launch_gather_rows_by_token(x, dtype, N, d, k, inv, x_perm, as_stream(stream));
+  });
+}
+
 int infmoe_expert_ffn(const void* x_perm, int64_t n_rows, int32_t d_model, int32_t d_ff,
                       int32_t dtype, const int32_t* offsets, int32_t E, const void* w_in,
                       const void* w_out, int32_t n_slots, const int32_t* experts,

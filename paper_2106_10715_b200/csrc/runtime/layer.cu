@@ -216,7 +216,10 @@ void Layer::route(const void* x, int64_t N, cudaStream_t s) {
                         s);
   launch_dispatch(idx, N * k, E, offsets, perm, inv, dws, s);
   // the PEER transport pushes token rows straight from x (no x_perm)
-  if (!ep_peer) launch_gather_rows(x, desc.dtype, N, desc.d_model, k, perm, xp, s);
+  if (!ep_peer) {
+    if (k > 1) launch_gather_rows_by_token(x, desc.dtype, N, desc.d_model, k, inv, xp, s);
+    else launch_gather_rows(x, desc.dtype, N, desc.d_model, k, perm, xp, s);
+  }
 }
 
 void Layer::ffn(const Rows& r, const int32_t* experts, const int32_t* slots, int n,

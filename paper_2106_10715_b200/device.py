@@ -102,6 +102,16 @@ def gather_rows(x, perm, k: int):
     return xp
 
 
+def gather_rows_by_token(x, inv, k: int):
+    """x_perm[inv[t*k+j]] = x[t]: gather_rows' output, each token row read once."""
+    torch = _torch()
+    N, d = x.shape
+    xp = torch.empty((N * k, d), dtype=x.dtype, device=x.device)
+    _check(_lib.infmoe_gather_rows_by_token(_p(x), _dtype_code(x), N, d, k, _p(inv), _p(xp),
+                                            _stream_ptr()))
+    return xp
+
+
 def expert_ffn(x_perm, offsets, w_in, w_out, experts: Optional[Sequence[int]] = None,
                slots: Optional[Sequence[int]] = None, h=None, y_perm=None):
     """h = GeLU(x_perm . w_in[slot]^T), y = h . w_out[slot]^T per expert segment.

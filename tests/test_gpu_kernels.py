@@ -209,9 +209,10 @@ def test_expert_ffn_vs_torch_fp32(cuda):
     assert (err <= BF16_ATOL + BF16_RTOL * ref.abs()).all(), err.max().item()
 
 
+@pytest.mark.parametrize("d", [256, 1160])
 @pytest.mark.parametrize("k,dtype", [(1, "bf16"), (2, "bf16"), (2, "f32")])
-def test_combine_bitexact(cuda, k, dtype):
-    N, d, E = 300, 256, 9
+def test_combine_bitexact(cuda, k, dtype, d):
+    N, E = 300, 9
     rng = np.random.default_rng(k)
     idx = np.stack([rng.permutation(E)[:k] for _ in range(N)]).astype(np.int32)
     w = rng.random((N, k)).astype(np.float32)
@@ -262,3 +263,21 @@ def test_fused_ffn_equals_two_launch_path(cuda, counts):
     ref = dv.combine(y2, inv, w, R, 1)
     torch.cuda.synchronize()
     assert torch.equal(yc.view(torch.int16), ref.view(torch.int16))
+
+
+@pytest.mark.parametrize("d", [256, 1160, 4096])
+@pytest.mark.parametrize("k", [1, 2, 3])
+def test_gather_rows_both_forms(cuda, k, d):
+    """x_perm[p] = x[perm[p] / k]: the perm-driven and the token-major
+    (inv-driven, one read per token row) gathers are bit-identical to numpy."""
+    N, E = 777, 13
+    rng = np.random.default_rng(100 + k)
+    idx = np.stack([rng.permutation(E)[:k] for _ in range(N)]).astype(np.int32)
+    off, perm, inv = dv.dispatch(torch.from_numpy(idx).to(cuda), E)
+    xb = fill_bf16(7 + k, N * d, 1.0)
+    x = _bf16_tensor(xb, (N, d), cuda)
+    a = dv.gather_rows(x, perm, k)
+    b = dv.gather_rows_by_token(x, inv, k)
+    ref = xb.reshape(N, d)[perm.cpu().numpy() // k]
+    assert np.array_equal(a.view(torch.int16).cpu().numpy().view(np.uint16), ref)
+    assert np.array_equal(b.view(torch.int16).cpu().numpy().view(np.uint16), ref)
