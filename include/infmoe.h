@@ -318,6 +318,15 @@ int infmoe_layer_forward(infmoe_layer* layer, const void* x, int64_t N, void* y,
                          infmoe_forward_out* out, void* stream);
 /* point an offloaded layer at another host weight set of the same shape */
 int infmoe_layer_set_host_weights(infmoe_layer* layer, const void* w_in, const void* w_out);
+/* SURVEY 8(f)-4, NOT in the reference (its eviction is immediate):
+ * hot-expert pinning for an offloaded layer.  The n listed local experts are
+ * copied to device memory once and stay there across forwards (n = 0 unpins);
+ * a forward then computes the pinned experts first, in one grouped launch with
+ * no load, while the first streamed copy is in flight, and streams only the
+ * others, in the InfMoE order over their own costs through the K+1 slots.
+ * Outputs are bit-identical to the unpinned layer.  Returns 3 (CapacityError)
+ * when the device copies do not fit, 6 for a resident layer or a bad list. */
+int infmoe_layer_pin_experts(infmoe_layer* layer, const int32_t* experts, int32_t n);
 int infmoe_layer_destroy(infmoe_layer* layer);
 
 #ifdef __cplusplus

@@ -281,6 +281,13 @@ int infmoe_layer_set_host_weights(infmoe_layer* layer, const void* w_in, const v
   });
 }
 
+int infmoe_layer_pin_experts(infmoe_layer* layer, const int32_t* experts, int32_t n) {
+  return guarded([&] {
+    require(layer && layer->impl, "pin_experts: NULL layer");
+    layer->impl->pin_experts(experts, n);
+  });
+}
+
 int infmoe_layer_destroy(infmoe_layer* layer) {
   return guarded([&] {
     if (!layer) return;

@@ -167,6 +167,9 @@ Layer::Layer(const infmoe_layer_desc& d) : desc(d) {
     INFMOE_CUDA(cudaEventCreate(&t_comp1[0]));
   }
   INFMOE_CUDA(cudaEventCreate(&t_start));
+  INFMOE_CUDA(cudaEventCreate(&t_pin0));
+  INFMOE_CUDA(cudaEventCreate(&t_pin1));
+  pin_slot.assign(size_t(n_local), -1);
 }
 
 void Layer::set_host_weights(const void* w_in, const void* w_out) {
@@ -186,6 +189,57 @@ void Layer::set_host_weights(const void* w_in, const void* w_out) {
   }
   host_in = reinterpret_cast<const uint8_t*>(w_in);
   host_out = reinterpret_cast<const uint8_t*>(w_out);
+  if (n_pinned) copy_pinned();  // pinned copies follow the new host weights
+}
+
+void Layer::copy_pinned() {
+  INFMOE_CUDA(cudaStreamSynchronize(copy_stream));
+  for (int i = 0; i < n_pinned; ++i) {
+    const size_t e = size_t(pin_list[size_t(i)]);
+    INFMOE_CUDA(cudaMemcpyAsync(pin_in + size_t(i) * expert_in_bytes,
+                                host_in + e * expert_in_bytes, expert_in_bytes,
+                                cudaMemcpyHostToDevice, copy_stream));
+    INFMOE_CUDA(cudaMemcpyAsync(pin_out + size_t(i) * expert_in_bytes,
+                                host_out + e * expert_in_bytes, expert_in_bytes,
+                                cudaMemcpyHostToDevice, copy_stream));
+  }
+  INFMOE_CUDA(cudaStreamSynchronize(copy_stream));
+}
+
+void Layer::pin_experts(const int32_t* experts, int n) {
+  require(desc.residency == INFMOE_OFFLOADED, "pin_experts: layer is resident");
+  require(n >= 0 && n <= n_local, "pin_experts: n must be in [0, local experts]");
+  require(n == 0 || experts, "pin_experts: NULL experts");
+  std::vector<int32_t> slot(size_t(n_local), -1), list;
+  for (int i = 0; i < n; ++i) {
+    const int e = experts[i];
+    require(e >= 0 && e < n_local, "pin_experts: expert out of range");
+    require(slot[size_t(e)] < 0, "pin_experts: expert listed twice");
+    slot[size_t(e)] = i;
+    list.push_back(e);
+  }
+  INFMOE_CUDA(cudaSetDevice(desc.device));
+  INFMOE_CUDA(cudaStreamSynchronize(copy_stream));
+  INFMOE_CUDA(cudaDeviceSynchronize());  // no forward may still read the old copies
+  if (pin_in) cudaFree(pin_in);
+  if (pin_out) cudaFree(pin_out);
+  pin_in = pin_out = nullptr;
+  n_pinned = 0;
+  pin_slot.assign(size_t(n_local), -1);
+  pin_list.clear();
+  if (n == 0) return;
+  const size_t bytes = size_t(n) * expert_in_bytes;
+  if (cudaMalloc(&pin_in, bytes) != cudaSuccess || cudaMalloc(&pin_out, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    if (pin_in) cudaFree(pin_in);
+    pin_in = nullptr;
+    fail(kCapacity, "pin_experts: not enough device memory for " + std::to_string(n) +
+                        " pinned experts");
+  }
+  pin_slot = slot;
+  pin_list = list;
+  n_pinned = n;
+  copy_pinned();
 }
 
 Layer::~Layer() {
@@ -195,6 +249,10 @@ Layer::~Layer() {
   for (auto* v : {&load_done, &compute_done, &t_load0, &t_load1, &t_comp0, &t_comp1})
     for (cudaEvent_t e : *v) cudaEventDestroy(e);
   if (t_start) cudaEventDestroy(t_start);
+  if (t_pin0) cudaEventDestroy(t_pin0);
+  if (t_pin1) cudaEventDestroy(t_pin1);
+  if (pin_in) cudaFree(pin_in);
+  if (pin_out) cudaFree(pin_out);
   if (copy_stream) cudaStreamDestroy(copy_stream);
   for (void* p : registered) cudaHostUnregister(p);
   if (counts_host) cudaFreeHost(counts_host);
@@ -317,12 +375,35 @@ void Layer::compute_offloaded(const Rows& r, bool timed, infmoe_forward_out* out
                               cudaStream_t s) {
   // experts taking part: all of them (reference default), or only those that
   // received rows when skip_empty_experts is set
+  // pinned experts (pin_experts) need no load: they are computed first, in one
+  // grouped launch from their device copies, while the first copy is in flight
   std::vector<int> members;
-  for (int e = 0; e < n_local; ++e)
-    if (!desc.skip_empty_experts || r.counts[e] > 0) members.push_back(e);
+  std::vector<int32_t> pex, psl;
+  int pin_rows = 0;
+  for (int e = 0; e < n_local; ++e) {
+    if (pin_slot[size_t(e)] >= 0) {
+      if (r.counts[e] > 0) {
+        pex.push_back(e);
+        psl.push_back(pin_slot[size_t(e)]);
+        pin_rows = std::max(pin_rows, int(r.counts[e]));
+      }
+    } else if (!desc.skip_empty_experts || r.counts[e] > 0) {
+      members.push_back(e);
+    }
+  }
+  n_pinned_run = int(pex.size());
+  if (!pex.empty())
+    ffn(r, pex.data(), psl.data(), int(pex.size()), pin_in, pin_out, n_pinned, 0, pin_rows, s,
+        timed ? t_pin0 : nullptr, timed ? t_pin1 : nullptr);
+  pinned_run = pex;
   const int E = int(members.size());
   n_scheduled = E;
-  if (E == 0) return;
+  if (E == 0) {
+    if (out && out->order)
+      for (int j = 0; j < n_local; ++j) out->order[j] = -1;
+    if (out && out->feasible) *out->feasible = 1;
+    return;
+  }
   std::vector<uint64_t> cnt(static_cast<size_t>(E));
   for (int i = 0; i < E; ++i) cnt[size_t(i)] = uint64_t(r.counts[members[size_t(i)]]);
   Geometry geo{1, 1, 1, desc.d_model, desc.d_ff, E, int(esz)};
@@ -600,6 +681,17 @@ void Layer::forward(const void* x, int64_t N, void* y, infmoe_forward_out* out, 
   double busy = 0.0, makespan = 0.0;
   if (out->events)
     for (int j = 0; j < 2 * n_local; ++j) out->events[j] = {-1, 0, -1, 0.0, 0.0};
+  if (n_pinned_run > 0) {  // one grouped launch: a compute event per pinned expert, no load
+    float a = 0, b = 0;
+    INFMOE_CUDA(cudaEventElapsedTime(&a, t_start, t_pin0));
+    INFMOE_CUDA(cudaEventElapsedTime(&b, t_start, t_pin1));
+    if (out->events)
+      for (int i = 0; i < n_pinned_run; ++i)
+        out->events[2 * (n_scheduled + i) + 1] = {INFMOE_STREAM_COMPUTE, 0, pinned_run[size_t(i)],
+                                                  a * 1e-3, b * 1e-3};
+    busy += (b - a) * 1e-3;
+    makespan = std::max(makespan, double(b) * 1e-3);
+  }
   for (int j = 0; j < n_scheduled; ++j) {
     float a = 0, b = 0, c0 = 0, c1 = 0;
     INFMOE_CUDA(cudaEventElapsedTime(&a, t_start, t_load0[size_t(j)]));

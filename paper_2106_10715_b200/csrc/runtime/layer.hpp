@@ -28,6 +28,10 @@ struct Layer {
 
   void forward(const void* x, int64_t N, void* y, infmoe_forward_out* out, cudaStream_t s);
   void set_host_weights(const void* w_in, const void* w_out);
+  // SURVEY 8(f)-4 hot-expert pinning (not in the reference): keep these local
+  // experts on the device across forwards; n = 0 unpins
+  void pin_experts(const int32_t* experts, int n);
+  int n_pinned_experts() const { return n_pinned; }
 
  private:
   // the rows one expert-compute pass works on
@@ -86,6 +90,16 @@ struct Layer {
   std::vector<cudaEvent_t> load_done, compute_done;
   std::vector<cudaEvent_t> t_load0, t_load1, t_comp0, t_comp1;
   cudaEvent_t t_start = nullptr;
+  // pinned experts (pin_experts): pin_slot[e] = slot in pin_in/pin_out or -1
+  std::vector<int32_t> pin_slot;
+  std::vector<int32_t> pin_list;  // pinned experts, slot order
+  int n_pinned = 0;
+  int n_pinned_run = 0;               // pinned experts computed by the last forward
+  std::vector<int32_t> pinned_run;
+  uint8_t* pin_in = nullptr;
+  uint8_t* pin_out = nullptr;
+  cudaEvent_t t_pin0 = nullptr, t_pin1 = nullptr;
+  void copy_pinned();
   // expert parallelism
   void* comm = nullptr;
   bool use_ep = false;

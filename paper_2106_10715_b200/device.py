@@ -263,6 +263,14 @@ class MoELayer:
         _check(_lib.infmoe_layer_set_host_weights(self._h, C.c_void_p(w_in.data_ptr()),
                                                   C.c_void_p(w_out.data_ptr())))
 
+    def pin_experts(self, experts) -> None:
+        """Hot-expert pinning (not in the reference): keep these
+        local experts on the device across forwards.  [] unpins."""
+        ex = np.ascontiguousarray(np.asarray(list(experts), dtype=np.int32))
+        _check(_lib.infmoe_layer_pin_experts(self._h, ex.ctypes.data_as(C.c_void_p) if len(ex)
+                                             else None, len(ex)))
+        self.pinned = [int(e) for e in ex]
+
     def forward(self, x, y=None, *, want_timeline: bool = False, want_info: bool = True):
         """Run the layer on x [N, d_model] (device).  want_info=False passes no
         output struct: a resident layer then never synchronises with the host
@@ -287,7 +295,7 @@ class MoELayer:
                          local_rows.ctypes.data)
         _check(_lib.infmoe_layer_forward(self._h, _p(x), N, _p(y), C.byref(out), _stream_ptr()))
         info = {"counts": counts, "order": order, "feasible": bool(feas.value),
-                "local_rows": local_rows}
+                "local_rows": local_rows, "pinned": list(getattr(self, "pinned", []))}
         if want_timeline:
             info["events"] = [(e.stream, e.layer_id, e.expert_id, e.start, e.end)
                               for e in events if e.stream >= 0]
