@@ -476,6 +476,9 @@ def main() -> None:
     ap.add_argument("--resident-steps", type=int, default=20)
     ap.add_argument("--cpu-sample", type=int, default=4096)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--pin-frac", type=float, default=0.5,
+                    help="hot-expert pinning line (SURVEY 8(f)-4, not reference-faithful): "
+                         "fraction of each layer's experts kept on the device (0 skips it)")
     ap.add_argument("--no-c5", action="store_true",
                     help="skip the C5 (E64 top-2 skewed, offloaded) and data-movement lines")
     ap.add_argument("--ep-transport", default="nccl", choices=["nccl", "peer"],
@@ -862,6 +865,48 @@ def main() -> None:
     }
     if cpu is not None:
         line["cpu_baseline"] = cpu
+    # ---------------- hot-expert pinning (reported apart) -------
+    # the same offloaded stack with the hottest pin_frac of each layer's experts
+    # (by the last timed step's counts) kept on the device across steps: those
+    # need no H2D, the rest stream in the InfMoE order over their own costs
+    n_pin = int(round(args.pin_frac * El))
+    if n_pin > 0:
+        for lay, info in zip(off_layers, all_infos[-1]):
+            hot = np.argsort(-info["local_rows"], kind="stable")[:n_pin]
+            lay.pin_experts(sorted(int(e) for e in hot))
+        stack(off_layers, x_dev)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        pin_ms, pin_infos = [], []
+        for _ in range(args.steps):
+            a, b = ev(), ev()
+            a.record(stream)
+            y_pin, pinfos = stack(off_layers, x_dev, timeline=True)
+            b.record(stream)
+            b.synchronize()
+            pin_ms.append(a.elapsed_time(b))
+            pin_infos.append(pinfos)
+        t_pin = float(np.mean(pin_ms))
+        if world > 1:
+            tt = torch.tensor([t_pin], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t_pin = tt.item()
+        streamed = sum(len([e for e in i["events"] if e[0] == 0]) for i in pin_infos[-1])
+        line["pinned"] = {
+            "note": "NOT reference-faithful (moesim evicts every expert at compute end, "
+                    "SPEC.md:325): SURVEY 8(f)-4 hot-expert pinning, reported apart",
+            "tokens_per_s": N_glob / (t_pin * 1e-3), "ms_per_step": t_pin,
+            "pinned_per_layer": n_pin, "experts_per_layer": El,
+            "device_bytes_pinned": L * n_pin * wbytes,
+            "h2d_bytes_per_step": streamed * wbytes,
+            "h2d_gbs": streamed * wbytes / (t_pin * 1e-3) / 1e9,
+            "speedup_vs_offloaded": t_in / t_pin,
+            "bit_identical_to_offloaded": bool(torch.equal(y_pin.view(torch.int16),
+                                                           y_off.view(torch.int16))),
+            "policy": "hottest experts of each layer by the last timed step's routed rows"}
+        for lay in off_layers:
+            lay.pin_experts([])
     for lay in off_layers + res_layers:
         lay.close()
     pool.close()
