@@ -272,7 +272,7 @@ def run_reference_arm(args, cfg, rank: int) -> None:
     proj = np.ascontiguousarray(im.gating_projection(im.derive_seed(SEED, 100), cfg["bits"], d))
     times = []
     for i in range(args.warmup + args.steps):
-        s, cores = cpu_layer_sample(cfg, x_bits, w_in, w_out, proj, n_tok)
+        s, cores, _ = cpu_layer_sample(cfg, x_bits, w_in, w_out, proj, n_tok)
         if i >= args.warmup:
             times.append(s)
     t_layer = float(np.mean(times))

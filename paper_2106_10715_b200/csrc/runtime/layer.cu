@@ -417,6 +417,8 @@ void Layer::compute_offloaded(const Rows& r, bool timed, infmoe_forward_out* out
     case INFMOE_POLICY_EXACT: pl = plan_exact(c, desc.K, 12); break;
     default: pl = plan_auto(c, desc.K, 12); break;
   }
+  exec_order.resize(size_t(E));
+  for (int j = 0; j < E; ++j) exec_order[size_t(j)] = members[size_t(pl.order[size_t(j)])];
   // ---- copy lane / compute lane ----
   INFMOE_CUDA(cudaStreamWaitEvent(copy_stream, t_start, 0));  // drain: after previous layer
   for (int j = 0; j < E; ++j) {
@@ -698,7 +700,7 @@ void Layer::forward(const void* x, int64_t N, void* y, infmoe_forward_out* out, 
     INFMOE_CUDA(cudaEventElapsedTime(&b, t_start, t_load1[size_t(j)]));
     INFMOE_CUDA(cudaEventElapsedTime(&c0, t_start, t_comp0[size_t(j)]));
     INFMOE_CUDA(cudaEventElapsedTime(&c1, t_start, t_comp1[size_t(j)]));
-    const int e = out->order ? out->order[j] : j;
+    const int e = exec_order[size_t(j)];
     if (out->events) {
       out->events[2 * j] = {INFMOE_STREAM_LOAD, 0, e, a * 1e-3, b * 1e-3};
       out->events[2 * j + 1] = {INFMOE_STREAM_COMPUTE, 0, e, c0 * 1e-3, c1 * 1e-3};

@@ -60,6 +60,7 @@ struct Layer {
   size_t esz = 2;
   int n_local = 0;  // experts held by this rank (E / ep_size)
   int n_scheduled = 0;  // experts loaded by the last offloaded forward
+  std::vector<int32_t> exec_order;  // ... and their load order (local expert ids)
   std::vector<void*> owned;
   std::vector<void*> registered;
   // routing / dispatch buffers
