@@ -871,9 +871,8 @@ def main() -> None:
     # need no H2D, the rest stream in the InfMoE order over their own costs
     n_pin = int(round(args.pin_frac * El))
     if n_pin > 0:
-        for lay, info in zip(off_layers, all_infos[-1]):
-            hot = np.argsort(-info["local_rows"], kind="stable")[:n_pin]
-            lay.pin_experts(sorted(int(e) for e in hot))
+        for lay in off_layers:  # the layer's cache policy: EMA of routed rows over forwards
+            lay.pin_hottest(n_pin)
         stack(off_layers, x_dev)
         torch.cuda.synchronize()
         if world > 1:
@@ -904,7 +903,8 @@ def main() -> None:
             "speedup_vs_offloaded": t_in / t_pin,
             "bit_identical_to_offloaded": bool(torch.equal(y_pin.view(torch.int16),
                                                            y_off.view(torch.int16))),
-            "policy": "hottest experts of each layer by the last timed step's routed rows"}
+            "policy": "infmoe_layer_pin_hottest: the experts of each layer with the highest "
+                      "EMA (decay 0.5) of routed rows over the warm-up and timed steps"}
         for lay in off_layers:
             lay.pin_experts([])
     for lay in off_layers + res_layers:

@@ -327,6 +327,12 @@ int infmoe_layer_set_host_weights(infmoe_layer* layer, const void* w_in, const v
  * Outputs are bit-identical to the unpinned layer.  Returns 3 (CapacityError)
  * when the device copies do not fit, 6 for a resident layer or a bad list. */
 int infmoe_layer_pin_experts(infmoe_layer* layer, const int32_t* experts, int32_t n);
+/* The cross-batch cache policy over infmoe_layer_pin_experts: pin the n local
+ * experts with the highest running load estimate (an EMA of each expert's
+ * routed rows over this layer's offloaded forwards, decay 0.5; ties to the
+ * lower index), re-using the device copies of experts that stay pinned.
+ * pinned (optional, n entries) receives the chosen experts in ascending order. */
+int infmoe_layer_pin_hottest(infmoe_layer* layer, int32_t n, int32_t* pinned);
 int infmoe_layer_destroy(infmoe_layer* layer);
 
 #ifdef __cplusplus

@@ -192,6 +192,7 @@ _lib.infmoe_layer_create.argtypes = [_P(LayerDesc), _P(_vp)]
 _lib.infmoe_layer_forward.argtypes = [_vp, _vp, C.c_int64, _vp, _P(ForwardOut), _vp]
 _lib.infmoe_layer_set_host_weights.argtypes = [_vp, _vp, _vp]
 _lib.infmoe_layer_pin_experts.argtypes = [_vp, _vp, _i32]
+_lib.infmoe_layer_pin_hottest.argtypes = [_vp, _i32, _vp]
 _lib.infmoe_layer_destroy.argtypes = [_vp]
 _lib.infmoe_slot_pool_create.argtypes = [_i32, _i32, _u64, _P(_vp)]
 _lib.infmoe_slot_pool_destroy.argtypes = [_vp]

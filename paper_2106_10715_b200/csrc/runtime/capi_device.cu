@@ -288,6 +288,14 @@ int infmoe_layer_pin_experts(infmoe_layer* layer, const int32_t* experts, int32_
   });
 }
 
+int infmoe_layer_pin_hottest(infmoe_layer* layer, int32_t n, int32_t* pinned) {
+  return guarded([&] {
+    require(layer && layer->impl, "pin_hottest: NULL layer");
+    const std::vector<int32_t> got = layer->impl->pin_hottest(n);
+    if (pinned) std::copy(got.begin(), got.end(), pinned);
+  });
+}
+
 int infmoe_layer_destroy(infmoe_layer* layer) {
   return guarded([&] {
     if (!layer) return;

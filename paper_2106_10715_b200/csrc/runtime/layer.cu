@@ -170,6 +170,7 @@ Layer::Layer(const infmoe_layer_desc& d) : desc(d) {
   INFMOE_CUDA(cudaEventCreate(&t_pin0));
   INFMOE_CUDA(cudaEventCreate(&t_pin1));
   pin_slot.assign(size_t(n_local), -1);
+  load_ema.assign(size_t(n_local), 0.0);
 }
 
 void Layer::set_host_weights(const void* w_in, const void* w_out) {
@@ -219,27 +220,56 @@ void Layer::pin_experts(const int32_t* experts, int n) {
     list.push_back(e);
   }
   INFMOE_CUDA(cudaSetDevice(desc.device));
-  INFMOE_CUDA(cudaStreamSynchronize(copy_stream));
   INFMOE_CUDA(cudaDeviceSynchronize());  // no forward may still read the old copies
+  uint8_t *nin = nullptr, *nout = nullptr;
+  if (n > 0) {
+    const size_t bytes = size_t(n) * expert_in_bytes;
+    if (cudaMalloc(&nin, bytes) != cudaSuccess || cudaMalloc(&nout, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      if (nin) cudaFree(nin);
+      fail(kCapacity, "pin_experts: not enough device memory for " + std::to_string(n) +
+                          " pinned experts");
+    }
+    // experts that stay pinned are copied on the device; the others come over the link
+    for (int i = 0; i < n; ++i) {
+      const size_t e = size_t(list[size_t(i)]);
+      const int old = pin_slot.empty() ? -1 : pin_slot[e];
+      const size_t dst = size_t(i) * expert_in_bytes;
+      if (old >= 0) {
+        const size_t src = size_t(old) * expert_in_bytes;
+        INFMOE_CUDA(cudaMemcpyAsync(nin + dst, pin_in + src, expert_in_bytes,
+                                    cudaMemcpyDeviceToDevice, copy_stream));
+        INFMOE_CUDA(cudaMemcpyAsync(nout + dst, pin_out + src, expert_in_bytes,
+                                    cudaMemcpyDeviceToDevice, copy_stream));
+      } else {
+        INFMOE_CUDA(cudaMemcpyAsync(nin + dst, host_in + e * expert_in_bytes, expert_in_bytes,
+                                    cudaMemcpyHostToDevice, copy_stream));
+        INFMOE_CUDA(cudaMemcpyAsync(nout + dst, host_out + e * expert_in_bytes, expert_in_bytes,
+                                    cudaMemcpyHostToDevice, copy_stream));
+      }
+    }
+    INFMOE_CUDA(cudaStreamSynchronize(copy_stream));
+  }
   if (pin_in) cudaFree(pin_in);
   if (pin_out) cudaFree(pin_out);
-  pin_in = pin_out = nullptr;
-  n_pinned = 0;
-  pin_slot.assign(size_t(n_local), -1);
-  pin_list.clear();
-  if (n == 0) return;
-  const size_t bytes = size_t(n) * expert_in_bytes;
-  if (cudaMalloc(&pin_in, bytes) != cudaSuccess || cudaMalloc(&pin_out, bytes) != cudaSuccess) {
-    cudaGetLastError();
-    if (pin_in) cudaFree(pin_in);
-    pin_in = nullptr;
-    fail(kCapacity, "pin_experts: not enough device memory for " + std::to_string(n) +
-                        " pinned experts");
-  }
+  pin_in = nin;
+  pin_out = nout;
   pin_slot = slot;
   pin_list = list;
   n_pinned = n;
-  copy_pinned();
+}
+
+std::vector<int32_t> Layer::pin_hottest(int n) {
+  require(n >= 0 && n <= n_local, "pin_hottest: n must be in [0, local experts]");
+  std::vector<int32_t> idx(static_cast<size_t>(n_local));
+  for (int e = 0; e < n_local; ++e) idx[size_t(e)] = e;
+  std::stable_sort(idx.begin(), idx.end(), [&](int32_t a, int32_t b) {
+    return load_ema[size_t(a)] > load_ema[size_t(b)];
+  });
+  idx.resize(size_t(n));
+  std::sort(idx.begin(), idx.end());
+  pin_experts(idx.data(), n);
+  return idx;
 }
 
 Layer::~Layer() {
@@ -375,6 +405,11 @@ void Layer::compute_offloaded(const Rows& r, bool timed, infmoe_forward_out* out
                               cudaStream_t s) {
   // experts taking part: all of them (reference default), or only those that
   // received rows when skip_empty_experts is set
+  // running load estimate across forwards (pin_hottest's cache policy)
+  for (int e = 0; e < n_local; ++e)
+    load_ema[size_t(e)] = ema_seen ? 0.5 * load_ema[size_t(e)] + 0.5 * double(r.counts[e])
+                                   : double(r.counts[e]);
+  ema_seen = true;
   // pinned experts (pin_experts) need no load: they are computed first, in one
   // grouped launch from their device copies, while the first copy is in flight
   std::vector<int> members;

@@ -31,6 +31,9 @@ struct Layer {
   // SURVEY 8(f)-4 hot-expert pinning (not in the reference): keep these local
   // experts on the device across forwards; n = 0 unpins
   void pin_experts(const int32_t* experts, int n);
+  // cache policy: pin the n experts with the highest running load estimate
+  // (EMA of routed rows over offloaded forwards, decay 0.5; ties: lower index)
+  std::vector<int32_t> pin_hottest(int n);
   int n_pinned_experts() const { return n_pinned; }
 
  private:
@@ -97,6 +100,8 @@ struct Layer {
   int n_pinned = 0;
   int n_pinned_run = 0;               // pinned experts computed by the last forward
   std::vector<int32_t> pinned_run;
+  std::vector<double> load_ema;  // per local expert (pin_hottest)
+  bool ema_seen = false;
   uint8_t* pin_in = nullptr;
   uint8_t* pin_out = nullptr;
   cudaEvent_t t_pin0 = nullptr, t_pin1 = nullptr;

@@ -271,6 +271,14 @@ class MoELayer:
                                              else None, len(ex)))
         self.pinned = [int(e) for e in ex]
 
+    def pin_hottest(self, n: int) -> list:
+        """Cross-batch cache policy: pin the n local experts with the highest
+        running load estimate (EMA of routed rows, decay 0.5).  Returns them."""
+        out = np.zeros(max(n, 1), dtype=np.int32)
+        _check(_lib.infmoe_layer_pin_hottest(self._h, n, out.ctypes.data_as(C.c_void_p)))
+        self.pinned = [int(e) for e in out[:n]]
+        return self.pinned
+
     def forward(self, x, y=None, *, want_timeline: bool = False, want_info: bool = True):
         """Run the layer on x [N, d_model] (device).  want_info=False passes no
         output struct: a resident layer then never synchronises with the host

@@ -101,3 +101,37 @@ def test_pin_errors(cuda):
     assert len([ev for ev in info["events"] if ev[0] == 0]) == E
     res.close()
     off.close()
+
+
+def test_pin_hottest_cache_policy(cuda):
+    """pin_hottest picks the top-n experts by the EMA (decay 0.5) of routed rows
+    over the layer's offloaded forwards; re-pinning re-uses device copies; the
+    output stays bit-identical throughout."""
+    N, d, f, E, k = 512, 256, 512, 8, 2
+    x, wi, wo = _weights(N, d, f, E, 12)
+    x = x.to(cuda)
+    gw = (np.random.default_rng(3).standard_normal((E, d)) / np.sqrt(d)).astype(np.float32)
+    bias = (-0.7 * np.log(np.arange(1, E + 1))).astype(np.float32)
+    kw = dict(gate="softmax", gate_weight=gw, gate_bias=bias, max_tokens=N)
+    res = dv.MoELayer(d, f, E, k, wi.to(cuda), wo.to(cuda), **kw)
+    off = dv.MoELayer(d, f, E, k, wi, wo, offloaded=True, K=2, **kw)
+    ema = None
+    for xb in (x, -x, x.roll(1, dims=1)):  # three batches, three routings
+        _, info = off.forward(xb.contiguous())
+        c = info["counts"].astype(np.float64)
+        ema = c if ema is None else 0.5 * ema + 0.5 * c
+    want = sorted(int(e) for e in np.argsort(-ema, kind="stable")[:3])
+    assert off.pin_hottest(3) == want
+    y_res, _ = res.forward(x)
+    y, info = off.forward(x, want_timeline=True)
+    torch.cuda.synchronize()
+    assert torch.equal(_bits(y), _bits(y_res))
+    assert not any(ev[2] in want for ev in info["events"] if ev[0] == 0)
+    got5 = off.pin_hottest(5)  # grows the pinned set, re-using the kept device copies
+    assert len(got5) == 5 and len(set(got5)) == 5
+    y, _ = off.forward(x)
+    torch.cuda.synchronize()
+    assert torch.equal(_bits(y), _bits(y_res))
+    assert off.pin_hottest(0) == []
+    res.close()
+    off.close()
