@@ -279,8 +279,17 @@ typedef struct {
    * the expert FFN's epilogue, plan computed on the device; peers are mapped
    * with CUDA IPC at create; NCCL only for 1-int barriers) */
   int32_t ep_transport;
+  /* offloaded, bf16: how expert weights cross the host link.  INFMOE_CODEC_RAW
+   * (default; the reference's model: expert_param_bytes per load) or
+   * INFMOE_CODEC_EXP4 (lossless: the handle packs the host weights once into
+   * pinned exp4 packs -- 12 bits per value, exponents coded against a per-block
+   * base -- shared by every layer on the same host weights; each load copies
+   * the pack and a decoder kernel restores the bf16 slot bit for bit before the
+   * FFN).  Outputs are identical; the scheduler's costs stay the reference's. */
+  int32_t h2d_codec;
 } infmoe_layer_desc;
 enum { INFMOE_EP_NCCL = 0, INFMOE_EP_PEER = 1 };
+enum { INFMOE_CODEC_RAW = 0, INFMOE_CODEC_EXP4 = 1 };
 
 /* per-forward outputs (all optional; host pointers unless noted) */
 typedef struct {
@@ -334,6 +343,11 @@ int infmoe_layer_pin_experts(infmoe_layer* layer, const int32_t* experts, int32_
  * pinned (optional, n entries) receives the chosen experts in ascending order. */
 int infmoe_layer_pin_hottest(infmoe_layer* layer, int32_t n, int32_t* pinned);
 int infmoe_layer_destroy(infmoe_layer* layer);
+/* exp4 codec round trip (test hook): pack n bf16 values (host) on the host,
+ * decode them on the device, copy the result to out (host); pack_bytes (may be
+ * NULL) receives the pack size.  n must be a positive multiple of 16. */
+int infmoe_codec_exp4_roundtrip(const uint16_t* in, uint64_t n, uint16_t* out,
+                                uint64_t* pack_bytes, int32_t device);
 
 #ifdef __cplusplus
 }

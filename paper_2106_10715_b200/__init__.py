@@ -124,7 +124,7 @@ class LayerDesc(C.Structure):
                 ("w_in", C.c_void_p), ("w_out", C.c_void_p), ("hw", Hardware),
                 ("ep_size", C.c_int32), ("ep_rank", C.c_int32), ("ep_comm", C.c_void_p),
                 ("skip_empty_experts", C.c_int32), ("slot_pool", C.c_void_p),
-                ("ep_transport", C.c_int32)]
+                ("ep_transport", C.c_int32), ("h2d_codec", C.c_int32)]
 
 
 class ForwardOut(C.Structure):
@@ -194,6 +194,7 @@ _lib.infmoe_layer_set_host_weights.argtypes = [_vp, _vp, _vp]
 _lib.infmoe_layer_pin_experts.argtypes = [_vp, _vp, _i32]
 _lib.infmoe_layer_pin_hottest.argtypes = [_vp, _i32, _vp]
 _lib.infmoe_layer_destroy.argtypes = [_vp]
+_lib.infmoe_codec_exp4_roundtrip.argtypes = [_vp, _u64, _vp, _vp, _i32]
 _lib.infmoe_slot_pool_create.argtypes = [_i32, _i32, _u64, _P(_vp)]
 _lib.infmoe_slot_pool_destroy.argtypes = [_vp]
 

@@ -32,6 +32,7 @@ CU_SOURCES = [
     "kernels/dispatch.cu",
     "kernels/expert_gemm.cu",
     "kernels/ep_peer.cu",
+    "kernels/codec.cu",
     "runtime/layer.cu",
     "runtime/capi_device.cu",
 ]

@@ -1,0 +1,69 @@
+// codec.cuh — lossless "exp4" packing of bf16 expert weights for the host link.
+//
+// The offloaded executor is host-link-bound (C3/C5 stream every
+// expert over PCIe each pass), so the bytes per expert ARE the step time.  A
+// bf16 weight is sign | 8-bit exponent | 7-bit mantissa; the mantissa and sign
+// are near-incompressible, but the exponents of a weight matrix cluster just
+// below its largest one (entropy ~2 bits for the bench's weights).  exp4
+// stores, per block of 32768 values, the largest exponent (the base), and per
+// value one byte (sign << 7 | mantissa) plus a 4-bit code base - exponent;
+// code 15 escapes to an exception list (uint16 index in the block | exponent
+// << 16) for exponents more than 14 below the base (zeros, subnormals, rare
+// small values).  12 bits per value + exceptions: ~25% fewer bytes over the
+// link, decoded on the GPU into the bf16 slot (HBM-bound, ~25 us per matrix),
+// bit for bit.
+//
+// Pack layout for n values (n % 16 == 0), all offsets from the pack start:
+//   [0, n)                 sign/mantissa bytes
+//   [n, n + n/2)           codes, two per byte (even value in the low nibble)
+//   [off_base, +nblocks)   per-block base exponent
+//   [off_exc_off, ...)     uint32 exception offsets per block [nblocks + 1]
+//   [off_exc, ...)         uint32 exceptions (index in block | exponent << 16)
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+#include <vector>
+
+namespace infmoe {
+namespace codec {
+
+constexpr int kExp4Block = 32768;
+
+struct Exp4Layout {
+  uint64_t n = 0, nblocks = 0;
+  uint64_t off_base = 0, off_exc_off = 0, off_exc = 0;
+};
+
+inline uint64_t align16(uint64_t v) { return (v + 15) & ~uint64_t(15); }
+
+inline Exp4Layout exp4_layout(uint64_t n) {
+  Exp4Layout L;
+  L.n = n;
+  L.nblocks = (n + kExp4Block - 1) / kExp4Block;
+  L.off_base = n + n / 2;
+  L.off_exc_off = align16(L.off_base + L.nblocks);
+  L.off_exc = align16(L.off_exc_off + 4 * (L.nblocks + 1));
+  return L;
+}
+
+// host: per-block bases and exception counts of one matrix (parallel over blocks)
+struct Exp4Plan {
+  Exp4Layout L;
+  std::vector<uint8_t> base;
+  std::vector<uint32_t> exc_off;  // [nblocks + 1], prefix sum
+  uint64_t bytes = 0;             // total pack bytes (16-aligned)
+};
+Exp4Plan exp4_plan(const uint16_t* in, uint64_t n);
+// host: write the pack described by plan into out (plan.bytes bytes)
+void exp4_fill(const uint16_t* in, const Exp4Plan& plan, uint8_t* out);
+// host reference decoder (tests)
+void exp4_unpack_host(const uint8_t* pack, uint64_t n, uint16_t* out);
+
+// device: decode one pack (16-byte aligned) into n bf16 values
+void launch_exp4_unpack(const uint8_t* pack, uint64_t n, uint16_t* out, cudaStream_t s);
+
+}  // namespace codec
+}  // namespace infmoe

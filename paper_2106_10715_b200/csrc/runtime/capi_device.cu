@@ -1,8 +1,10 @@
 // capi_device.cu — extern "C" entry points of the device path (infmoe.h,
 // "Device path" section).  Every call is exception-guarded.
 #include <cstring>
+#include <vector>
 
 #include "../host/status.hpp"
+#include "../kernels/codec.cuh"
 #include "../kernels/common.cuh"
 #include "../kernels/expert_gemm.cuh"
 #include "../kernels/kernels.cuh"
@@ -253,6 +255,7 @@ int infmoe_slot_pool_destroy(infmoe_slot_pool* pool) {
     cudaDeviceSynchronize();  // no layer may still be copying into the slots
     cudaFree(p->slot_in);
     cudaFree(p->slot_out);
+    if (p->stage) cudaFree(p->stage);
     delete p;
   });
 }
@@ -293,6 +296,27 @@ int infmoe_layer_pin_hottest(infmoe_layer* layer, int32_t n, int32_t* pinned) {
     require(layer && layer->impl, "pin_hottest: NULL layer");
     const std::vector<int32_t> got = layer->impl->pin_hottest(n);
     if (pinned) std::copy(got.begin(), got.end(), pinned);
+  });
+}
+
+int infmoe_codec_exp4_roundtrip(const uint16_t* in, uint64_t n, uint16_t* out,
+                                uint64_t* pack_bytes, int32_t device) {
+  return guarded([&] {
+    require(in && out, "codec_exp4_roundtrip: NULL argument");
+    INFMOE_CUDA(cudaSetDevice(device));
+    const codec::Exp4Plan plan = codec::exp4_plan(in, n);
+    std::vector<uint8_t> pk(plan.bytes);
+    codec::exp4_fill(in, plan, pk.data());
+    if (pack_bytes) *pack_bytes = plan.bytes;
+    uint8_t* dp = nullptr;
+    uint16_t* dout = nullptr;
+    INFMOE_CUDA(cudaMalloc(&dp, plan.bytes));
+    INFMOE_CUDA(cudaMalloc(&dout, n * 2));
+    INFMOE_CUDA(cudaMemcpy(dp, pk.data(), plan.bytes, cudaMemcpyHostToDevice));
+    codec::launch_exp4_unpack(dp, n, dout, nullptr);
+    INFMOE_CUDA(cudaMemcpy(out, dout, n * 2, cudaMemcpyDeviceToHost));
+    cudaFree(dp);
+    cudaFree(dout);
   });
 }
 

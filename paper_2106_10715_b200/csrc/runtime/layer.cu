@@ -23,12 +23,16 @@
 // all-to-allv brings the results home for the combine.
 #include <algorithm>
 #include <cstring>
+#include <map>
 #include <memory>
+#include <mutex>
+#include <tuple>
 #include <vector>
 
 #include <unistd.h>
 
 #include "../host/planner.hpp"
+#include "../kernels/codec.cuh"
 #include "../kernels/common.cuh"
 #include "../kernels/expert_gemm.cuh"
 #include "../kernels/kernels.cuh"
@@ -135,8 +139,13 @@ Layer::Layer(const infmoe_layer_desc& d) : desc(d) {
   expert_in_bytes = size_t(d.d_ff) * d.d_model * esz;
   if (d.residency == INFMOE_OFFLOADED) {
     require(d.K >= 1, "layer: offloaded mode needs K >= 1");
+    require(d.h2d_codec == INFMOE_CODEC_RAW || d.h2d_codec == INFMOE_CODEC_EXP4,
+            "layer: unknown h2d_codec");
+    require(d.h2d_codec == INFMOE_CODEC_RAW || d.dtype == INFMOE_DTYPE_BF16,
+            "layer: the exp4 codec packs bf16 weights");
     if (d.slot_pool) {  // K+1 slots shared with the other layers of the stack
-      const auto* pool = reinterpret_cast<const SlotPool*>(d.slot_pool);
+      auto* pool = reinterpret_cast<SlotPool*>(d.slot_pool);
+      pool_ptr = pool;
       require(pool->device == d.device, "layer: slot pool lives on another device");
       require(pool->K == d.K, "layer: slot pool K differs from the layer's K");
       require(pool->matrix_bytes == expert_in_bytes,
@@ -148,6 +157,13 @@ Layer::Layer(const infmoe_layer_desc& d) : desc(d) {
       n_slots = std::min(d.K + 1, n_local + 1);
       slot_in = dalloc<uint8_t>(size_t(n_slots) * expert_in_bytes, owned);
       slot_out = dalloc<uint8_t>(size_t(n_slots) * expert_in_bytes, owned);
+      own_pool.device = d.device;
+      own_pool.K = d.K;
+      own_pool.n_slots = n_slots;
+      own_pool.matrix_bytes = expert_in_bytes;
+      own_pool.slot_in = slot_in;
+      own_pool.slot_out = slot_out;
+      pool_ptr = &own_pool;
     }
     INFMOE_CUDA(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
     const size_t E = size_t(n_local);
@@ -190,6 +206,17 @@ void Layer::set_host_weights(const void* w_in, const void* w_out) {
   }
   host_in = reinterpret_cast<const uint8_t*>(w_in);
   host_out = reinterpret_cast<const uint8_t*>(w_out);
+  if (desc.h2d_codec == INFMOE_CODEC_EXP4) {
+    pack = HostPack::acquire(w_in, w_out, n_local, uint64_t(desc.d_ff) * desc.d_model);
+    if (pool_ptr->stage_bytes < pack->max_size) {  // grow the shared staging buffers
+      INFMOE_CUDA(cudaDeviceSynchronize());
+      if (pool_ptr->stage) INFMOE_CUDA(cudaFree(pool_ptr->stage));
+      pool_ptr->stage = nullptr;
+      pool_ptr->stage_bytes = 0;
+      INFMOE_CUDA(cudaMalloc(&pool_ptr->stage, size_t(pool_ptr->n_slots) * pack->max_size));
+      pool_ptr->stage_bytes = pack->max_size;
+    }
+  }
   if (n_pinned) copy_pinned();  // pinned copies follow the new host weights
 }
 
@@ -283,6 +310,7 @@ Layer::~Layer() {
   if (t_pin1) cudaEventDestroy(t_pin1);
   if (pin_in) cudaFree(pin_in);
   if (pin_out) cudaFree(pin_out);
+  if (own_pool.stage) cudaFree(own_pool.stage);
   if (copy_stream) cudaStreamDestroy(copy_stream);
   for (void* p : registered) cudaHostUnregister(p);
   if (counts_host) cudaFreeHost(counts_host);
@@ -462,12 +490,17 @@ void Layer::compute_offloaded(const Rows& r, bool timed, infmoe_forward_out* out
     if (j >= n_slots)
       INFMOE_CUDA(cudaStreamWaitEvent(copy_stream, compute_done[size_t(j - n_slots)], 0));
     if (timed) INFMOE_CUDA(cudaEventRecord(t_load0[size_t(j)], copy_stream));
-    INFMOE_CUDA(cudaMemcpyAsync(slot_in + size_t(slot) * expert_in_bytes,
-                                host_in + size_t(e) * expert_in_bytes, expert_in_bytes,
-                                cudaMemcpyHostToDevice, copy_stream));
-    INFMOE_CUDA(cudaMemcpyAsync(slot_out + size_t(slot) * expert_in_bytes,
-                                host_out + size_t(e) * expert_in_bytes, expert_in_bytes,
-                                cudaMemcpyHostToDevice, copy_stream));
+    if (pack) {  // exp4: the expert's packed bytes into this slot's staging buffer
+      INFMOE_CUDA(cudaMemcpyAsync(stage_of(slot), pack->host + pack->off[size_t(e)],
+                                  pack->size[size_t(e)], cudaMemcpyHostToDevice, copy_stream));
+    } else {
+      INFMOE_CUDA(cudaMemcpyAsync(slot_in + size_t(slot) * expert_in_bytes,
+                                  host_in + size_t(e) * expert_in_bytes, expert_in_bytes,
+                                  cudaMemcpyHostToDevice, copy_stream));
+      INFMOE_CUDA(cudaMemcpyAsync(slot_out + size_t(slot) * expert_in_bytes,
+                                  host_out + size_t(e) * expert_in_bytes, expert_in_bytes,
+                                  cudaMemcpyHostToDevice, copy_stream));
+    }
     if (timed) INFMOE_CUDA(cudaEventRecord(t_load1[size_t(j)], copy_stream));
     INFMOE_CUDA(cudaEventRecord(load_done[size_t(j)], copy_stream));
 
@@ -477,6 +510,15 @@ void Layer::compute_offloaded(const Rows& r, bool timed, infmoe_forward_out* out
     cudaEvent_t e0 = timed ? t_comp0[size_t(j)] : nullptr;
     cudaEvent_t e1 = timed ? t_comp1[size_t(j)] : nullptr;
     if (n_e > 0) {
+      if (pack) {  // decode both matrices into the slot (counted as compute)
+        if (e0) INFMOE_CUDA(cudaEventRecord(e0, s));
+        const uint64_t elems = uint64_t(desc.d_ff) * desc.d_model;
+        codec::launch_exp4_unpack(stage_of(slot), elems,
+                                  reinterpret_cast<uint16_t*>(slot_in + size_t(slot) * expert_in_bytes), s);
+        codec::launch_exp4_unpack(stage_of(slot) + pack->in_size[size_t(e)], elems,
+                                  reinterpret_cast<uint16_t*>(slot_out + size_t(slot) * expert_in_bytes), s);
+        e0 = nullptr;
+      }
       const int tiles = int((n_e + 127) / 128) * (std::max(desc.d_ff, desc.d_model) / 128);
       ffn(r, &ex, &sl, 1, slot_in, slot_out, n_slots, tiles, int(n_e), s, e0, e1);
     } else if (timed) {
@@ -744,6 +786,61 @@ void Layer::forward(const void* x, int64_t N, void* y, infmoe_forward_out* out, 
     makespan = std::max(makespan, double(c1) * 1e-3);
   }
   if (out->exposed_copy_s) *out->exposed_copy_s = makespan - busy;
+}
+
+// ------------------------------------------------------- exp4 host packs --
+namespace {
+struct PackKey {
+  const void* a;
+  const void* b;
+  int n;
+  uint64_t elems;
+  bool operator<(const PackKey& o) const {
+    return std::tie(a, b, n, elems) < std::tie(o.a, o.b, o.n, o.elems);
+  }
+};
+std::mutex g_pack_mu;
+std::map<PackKey, std::weak_ptr<HostPack>> g_packs;
+}  // namespace
+
+std::shared_ptr<HostPack> HostPack::acquire(const void* w_in, const void* w_out, int n_experts,
+                                            uint64_t matrix_elems) {
+  std::lock_guard<std::mutex> lock(g_pack_mu);
+  const PackKey key{w_in, w_out, n_experts, matrix_elems};
+  auto it = g_packs.find(key);
+  if (it != g_packs.end())
+    if (auto sp = it->second.lock()) return sp;
+  auto p = std::make_shared<HostPack>();
+  const auto* in = static_cast<const uint16_t*>(w_in);
+  const auto* out = static_cast<const uint16_t*>(w_out);
+  std::vector<codec::Exp4Plan> plans;
+  plans.reserve(size_t(2 * n_experts));
+  for (int e = 0; e < n_experts; ++e) {
+    plans.push_back(codec::exp4_plan(in + uint64_t(e) * matrix_elems, matrix_elems));
+    plans.push_back(codec::exp4_plan(out + uint64_t(e) * matrix_elems, matrix_elems));
+  }
+  for (int e = 0; e < n_experts; ++e) {
+    const uint64_t a = plans[size_t(2 * e)].bytes, b = plans[size_t(2 * e + 1)].bytes;
+    p->off.push_back(p->total);
+    p->size.push_back(a + b);
+    p->in_size.push_back(a);
+    p->max_size = std::max(p->max_size, a + b);
+    p->total += a + b;
+  }
+  p->raw_bytes = uint64_t(n_experts) * matrix_elems * 2 * 2;
+  INFMOE_CUDA(cudaMallocHost(&p->host, p->total));
+  for (int e = 0; e < n_experts; ++e) {
+    codec::exp4_fill(in + uint64_t(e) * matrix_elems, plans[size_t(2 * e)],
+                     p->host + p->off[size_t(e)]);
+    codec::exp4_fill(out + uint64_t(e) * matrix_elems, plans[size_t(2 * e + 1)],
+                     p->host + p->off[size_t(e)] + p->in_size[size_t(e)]);
+  }
+  g_packs[key] = p;
+  return p;
+}
+
+HostPack::~HostPack() {
+  if (host) cudaFreeHost(host);
 }
 
 }  // namespace infmoe

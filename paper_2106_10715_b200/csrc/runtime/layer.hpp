@@ -5,6 +5,7 @@
 
 #include <cuda_runtime.h>
 
+#include <memory>
 #include <vector>
 
 #include "../host/ep_plan.hpp"
@@ -18,6 +19,21 @@ struct SlotPool {
   size_t matrix_bytes = 0;
   uint8_t* slot_in = nullptr;
   uint8_t* slot_out = nullptr;
+  // exp4 codec: one staging buffer per slot for the packed bytes (grown on demand)
+  uint8_t* stage = nullptr;
+  size_t stage_bytes = 0;
+};
+
+// exp4 packs of one host weight set (w_in, w_out of n experts), pinned, shared
+// by every layer that points at the same host weights (HostPack::acquire)
+struct HostPack {
+  uint8_t* host = nullptr;          // pinned
+  std::vector<uint64_t> off, size;  // per expert: [w_in pack | w_out pack], 16-aligned
+  std::vector<uint64_t> in_size;    // bytes of the w_in pack (w_out pack follows)
+  uint64_t max_size = 0, total = 0, raw_bytes = 0;
+  static std::shared_ptr<HostPack> acquire(const void* w_in, const void* w_out, int n_experts,
+                                           uint64_t matrix_elems);
+  ~HostPack();
 };
 
 struct Layer {
@@ -90,6 +106,10 @@ struct Layer {
   uint8_t* slot_out = nullptr;
   const uint8_t* host_in = nullptr;
   const uint8_t* host_out = nullptr;
+  std::shared_ptr<HostPack> pack;   // exp4 codec: packed host weights
+  SlotPool own_pool;                // staging when the layer owns its slots
+  SlotPool* pool_ptr = nullptr;     // where the staging buffers live
+  uint8_t* stage_of(int slot) const { return pool_ptr->stage + size_t(slot) * pool_ptr->stage_bytes; }
   cudaStream_t copy_stream = nullptr;
   std::vector<cudaEvent_t> load_done, compute_done;
   std::vector<cudaEvent_t> t_load0, t_load1, t_comp0, t_comp1;

@@ -191,6 +191,16 @@ def combine(y_perm, inv, topk_w, N: int, k: int):
     return y
 
 
+def codec_exp4_roundtrip(bits: np.ndarray, device: int = 0):
+    """exp4-pack bf16 bit patterns on the host, decode on the GPU: (decoded, pack bytes)."""
+    a = np.ascontiguousarray(bits, dtype=np.uint16)
+    out = np.empty_like(a)
+    nb = C.c_uint64(0)
+    _check(_lib.infmoe_codec_exp4_roundtrip(a.ctypes.data_as(C.c_void_p), a.size,
+                                            out.ctypes.data_as(C.c_void_p), C.byref(nb), device))
+    return out, nb.value
+
+
 class SlotPool:
     """K+1 device expert slots shared by the offloaded layers of a stack
     (infmoe_slot_pool: K experts resident on the GPU in total + one in flight)."""
@@ -226,7 +236,8 @@ class MoELayer:
                  policy: int = POLICY_AUTO, max_tokens: int = 4096, device: int = 0,
                  hw: Optional[Hardware] = None, ep_size: int = 1, ep_rank: int = 0,
                  ep_comm: Optional[int] = None, skip_empty_experts: bool = False,
-                 slot_pool: Optional["SlotPool"] = None, ep_transport: str = "nccl"):
+                 slot_pool: Optional["SlotPool"] = None, ep_transport: str = "nccl",
+                 h2d_codec: str = "raw"):
         d = LayerDesc()
         d.d_model, d.d_ff, d.n_experts, d.top_k = d_model, d_ff, n_experts, top_k
         d.dtype = DTYPE_BF16 if dtype == "bf16" else DTYPE_F32
@@ -249,6 +260,7 @@ class MoELayer:
         d.ep_size, d.ep_rank, d.ep_comm = ep_size, ep_rank, ep_comm
         d.skip_empty_experts = int(skip_empty_experts)
         d.ep_transport = {"nccl": 0, "peer": 1}[ep_transport]
+        d.h2d_codec = {"raw": 0, "exp4": 1}[h2d_codec]
         if slot_pool is not None:
             d.slot_pool = slot_pool.handle
             self._keep.append(slot_pool)  # the pool outlives the layer

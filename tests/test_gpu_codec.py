@@ -1,0 +1,76 @@
+"""exp4 lossless host-link codec (codec.cuh): packs decode bit for bit on the
+GPU for every bf16 pattern (zeros, subnormals, Inf, NaN, wide exponent
+ranges), and an offloaded layer streaming exp4 packs gives exactly the raw
+layer's output with ~25% fewer bytes per load."""
+import numpy as np
+import pytest
+import torch
+
+import paper_2106_10715_b200 as im
+from paper_2106_10715_b200 import device as dv
+from oracle_lib import fill_bf16
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("case", ["all_patterns", "weights", "zeros", "wide", "tail_block"])
+def test_exp4_roundtrip_bit_exact(cuda, case):
+    rng = np.random.default_rng(1)
+    if case == "all_patterns":
+        a = np.tile(np.arange(1 << 16, dtype=np.uint16), 3)
+        rng.shuffle(a)
+    elif case == "weights":
+        a = fill_bf16(5, 1 << 20, 1.7320508 / 64)
+    elif case == "zeros":
+        a = np.zeros(4096, np.uint16)
+        a[::7] = 0x8000  # -0.0
+    elif case == "wide":  # exponents spread over the whole range: mostly escapes
+        a = rng.integers(0, 1 << 16, size=200_000, dtype=np.uint16)
+    else:  # a last block shorter than 32768 values
+        a = fill_bf16(9, 32768 * 3 + 48, 2.0)
+    n = (a.size // 16) * 16
+    a = np.ascontiguousarray(a[:n])
+    out, nbytes = dv.codec_exp4_roundtrip(a)
+    assert np.array_equal(out, a)
+    if case == "weights":
+        assert nbytes < 0.76 * 2 * n  # 12 bits per value + block headers + rare escapes
+
+
+@pytest.mark.parametrize("gate,k,pins", [("lsh", 1, []), ("softmax", 2, [1])])
+def test_exp4_layer_bit_identical(cuda, gate, k, pins):
+    N, d, f, E, K = 512, 256, 512, 8, 2
+    t = lambda b, sh: torch.from_numpy(b.view(np.int16).reshape(sh)).view(torch.bfloat16)
+    x = t(fill_bf16(1, N * d, 1.7320508), (N, d)).to(cuda)
+    wi = t(fill_bf16(2, E * f * d, 1.7320508 / 16), (E, f, d)).pin_memory()
+    wo = t(fill_bf16(3, E * d * f, 1.534 * 1.7320508 / np.sqrt(f)), (E, d, f)).pin_memory()
+    wi[2].zero_()  # an all-zero expert matrix: every value escapes
+    gw = (np.random.default_rng(4).standard_normal((E, d)) / np.sqrt(d)).astype(np.float32)
+    kw = dict(gate=gate, gate_weight=gw, lsh_seed=5, lsh_bits=3, max_tokens=N, offloaded=True,
+              K=K)
+    raw = dv.MoELayer(d, f, E, k, wi, wo, **kw)
+    pool = dv.SlotPool(K, d, f)
+    ex1 = dv.MoELayer(d, f, E, k, wi, wo, h2d_codec="exp4", slot_pool=pool, **kw)
+    ex2 = dv.MoELayer(d, f, E, k, wi, wo, h2d_codec="exp4", slot_pool=pool, **kw)  # shared pack
+    if pins:
+        ex1.pin_experts(pins)
+    y0, info0 = raw.forward(x, want_timeline=True)
+    y1, info1 = ex1.forward(x, want_timeline=True)
+    y2, _ = ex2.forward(y1)
+    y2r, _ = raw.forward(y0)
+    torch.cuda.synchronize()
+    assert torch.equal(y1.view(torch.int16), y0.view(torch.int16))
+    assert torch.equal(y2.view(torch.int16), y2r.view(torch.int16))
+    assert list(info1["order"][:E - len(pins)]) == [e for e in info0["order"] if e not in pins]
+    assert len([ev for ev in info1["events"] if ev[0] == 0]) == E - len(pins)
+    for lay in (raw, ex1, ex2):
+        lay.close()
+    pool.close()
+
+
+def test_exp4_needs_bf16(cuda):
+    N, d, f, E = 64, 256, 512, 4
+    wi = torch.zeros((E, f, d), dtype=torch.float32).pin_memory()
+    wo = torch.zeros((E, d, f), dtype=torch.float32).pin_memory()
+    with pytest.raises(im.InvalidArgument):
+        dv.MoELayer(d, f, E, 1, wi, wo, dtype="f32", offloaded=True, K=1, lsh_bits=2,
+                    max_tokens=N, h2d_codec="exp4")
