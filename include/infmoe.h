@@ -343,6 +343,9 @@ int infmoe_layer_pin_experts(infmoe_layer* layer, const int32_t* experts, int32_
  * pinned (optional, n entries) receives the chosen experts in ascending order. */
 int infmoe_layer_pin_hottest(infmoe_layer* layer, int32_t n, int32_t* pinned);
 int infmoe_layer_destroy(infmoe_layer* layer);
+/* bytes one pass of an offloaded layer moves over the host link for its local
+ * experts with its codec (packed) and without (raw = n_local * expert_param_bytes) */
+int infmoe_layer_h2d_bytes(infmoe_layer* layer, uint64_t* packed, uint64_t* raw);
 /* exp4 codec round trip (test hook): pack n bf16 values (host) on the host,
  * decode them on the device, copy the result to out (host); pack_bytes (may be
  * NULL) receives the pack size.  n must be a positive multiple of 16. */

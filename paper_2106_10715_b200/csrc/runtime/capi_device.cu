@@ -299,6 +299,13 @@ int infmoe_layer_pin_hottest(infmoe_layer* layer, int32_t n, int32_t* pinned) {
   });
 }
 
+int infmoe_layer_h2d_bytes(infmoe_layer* layer, uint64_t* packed, uint64_t* raw) {
+  return guarded([&] {
+    require(layer && layer->impl, "h2d_bytes: NULL layer");
+    layer->impl->h2d_bytes(packed, raw);
+  });
+}
+
 int infmoe_codec_exp4_roundtrip(const uint16_t* in, uint64_t n, uint16_t* out,
                                 uint64_t* pack_bytes, int32_t device) {
   return guarded([&] {

@@ -51,6 +51,11 @@ struct Layer {
   // (EMA of routed rows over offloaded forwards, decay 0.5; ties: lower index)
   std::vector<int32_t> pin_hottest(int n);
   int n_pinned_experts() const { return n_pinned; }
+  void h2d_bytes(uint64_t* packed, uint64_t* raw) const {
+    const uint64_t r = uint64_t(n_local) * 2 * expert_in_bytes;
+    if (raw) *raw = r;
+    if (packed) *packed = pack ? pack->total : r;
+  }
 
  private:
   // the rows one expert-compute pass works on

@@ -283,6 +283,12 @@ class MoELayer:
                                              else None, len(ex)))
         self.pinned = [int(e) for e in ex]
 
+    def packed_bytes(self) -> int:
+        """Bytes one pass moves over the host link for this layer's experts (its codec)."""
+        pk, raw = C.c_uint64(0), C.c_uint64(0)
+        _check(_lib.infmoe_layer_h2d_bytes(self._h, C.byref(pk), C.byref(raw)))
+        return pk.value
+
     def pin_hottest(self, n: int) -> list:
         """Cross-batch cache policy: pin the n local experts with the highest
         running load estimate (EMA of routed rows, decay 0.5).  Returns them."""
