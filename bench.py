@@ -479,11 +479,12 @@ def main() -> None:
     ap.add_argument("--pin-frac", type=float, default=0.5,
                     help="hot-expert pinning line (SURVEY 8(f)-4, not reference-faithful): "
                          "fraction of each layer's experts kept on the device (0 skips it)")
-    ap.add_argument("--h2d-codec", default="exp4", choices=["exp4", "raw"],
-                    help="exp4 (default): the headline streams lossless exp4 packs (12 bits per "
-                         "weight, decoded on the GPU, bit-identical outputs) and the raw bf16 "
-                         "stream (the reference's expert_param_bytes) is reported beside it as "
-                         "raw_stream; raw: the raw stream only")
+    ap.add_argument("--h2d-codec", default="exph", choices=["exph", "exp4", "raw"],
+                    help="exph (default) / exp4: the headline streams lossless packs (Huffman-"
+                         "coded or 4-bit exponents, ~10.7 / 12 bits per weight, decoded on the "
+                         "GPU, bit-identical outputs) and the raw bf16 stream (the reference's "
+                         "expert_param_bytes) is reported beside it as raw_stream; raw: the raw "
+                         "stream only")
     ap.add_argument("--no-c5", action="store_true",
                     help="skip the C5 (E64 top-2 skewed, offloaded) and data-movement lines")
     ap.add_argument("--ep-transport", default="nccl", choices=["nccl", "peer"],
@@ -915,7 +916,7 @@ def main() -> None:
     # ---------------- exp4: the same stack with lossless packed host weights ----
     # each load copies the expert's exp4 pack (12 bits per weight) and a decoder
     # kernel restores the bf16 slot bit for bit before the FFN (codec.cuh)
-    if args.h2d_codec == "exp4":
+    if args.h2d_codec != "raw":
         t0 = time.perf_counter()
         exp_layers = []
         for l in range(L):
@@ -926,7 +927,7 @@ def main() -> None:
                                           max_tokens=N, device=local, hw=hw, ep_size=P,
                                           ep_rank=rank, ep_comm=comm,
                                           ep_transport=args.ep_transport, slot_pool=pool,
-                                          h2d_codec="exp4"))
+                                          h2d_codec=args.h2d_codec))
         pack_s = time.perf_counter() - t0
         for _ in range(args.warmup):
             stack(exp_layers, x_dev)
@@ -978,11 +979,18 @@ def main() -> None:
         line["ms_per_step"] = t_ex
         line["e2e"] = {"value": N_glob / (t_ex_out * 1e-3), "unit": "tokens/s",
                        "h2d_bytes_per_step": N * d * 2, "d2h_bytes_per_step": N * d * 2}
+        codec_desc = {
+            "exp4": "exp4 (lossless: the same bf16 weights packed once on the host -- a "
+                    "sign/mantissa byte and a 4-bit exponent code per value against a "
+                    "per-32768-value base, exceptions listed -- decoded on the GPU before "
+                    "each expert's FFN; outputs bit-identical to the raw stream)",
+            "exph": "exph (lossless: the same bf16 weights packed once on the host -- a "
+                    "sign/mantissa byte and a canonical Huffman code (<= 12 bits, one table "
+                    "per matrix) of the exponent's distance to a per-32768-value base, 64-value "
+                    "chunks with recorded start bits -- decoded on the GPU before each "
+                    "expert's FFN; outputs bit-identical to the raw stream)"}
         line["h2d"] = {
-            "codec": "exp4 (lossless: the same bf16 weights packed once on the host -- a "
-                     "sign/mantissa byte and a 4-bit exponent code per value against a "
-                     "per-32768-value base, exceptions listed -- decoded on the GPU before "
-                     "each expert's FFN; outputs bit-identical to the raw stream)",
+            "codec": codec_desc[args.h2d_codec],
             "achieved_gbs": link_bytes / (t_ex * 1e-3) / 1e9, "peak_gbs": h2d_peak,
             "frac": link_bytes / (t_ex * 1e-3) / 1e9 / h2d_peak,
             "bytes_per_step": link_bytes, "raw_bytes_per_step": h2d_bytes_step,
@@ -1002,7 +1010,7 @@ def main() -> None:
             "pack_seconds_host_once": pack_s}
         line["clocks"] = ex_clocks.summary()
         line["gpu_launches"] = line["gpu_launches"] + 2 * L * El  # two decodes per expert
-        line["config"]["h2d_codec"] = "exp4"
+        line["config"]["h2d_codec"] = args.h2d_codec
         line["speedup_vs_raw_stream"] = t_in / t_ex
         line["raw_stream"] = raw_stream
         for lay in exp_layers:

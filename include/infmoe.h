@@ -285,11 +285,14 @@ typedef struct {
    * pinned exp4 packs -- 12 bits per value, exponents coded against a per-block
    * base -- shared by every layer on the same host weights; each load copies
    * the pack and a decoder kernel restores the bf16 slot bit for bit before the
-   * FFN).  Outputs are identical; the scheduler's costs stay the reference's. */
+   * FFN).  INFMOE_CODEC_EXPH codes the exponent with a per-matrix canonical
+   * Huffman code instead (~10.7 bits per value on the bench's weights; one GPU
+   * thread decodes each 64-value chunk through a shared-memory table).
+   * Outputs are identical; the scheduler's costs stay the reference's. */
   int32_t h2d_codec;
 } infmoe_layer_desc;
 enum { INFMOE_EP_NCCL = 0, INFMOE_EP_PEER = 1 };
-enum { INFMOE_CODEC_RAW = 0, INFMOE_CODEC_EXP4 = 1 };
+enum { INFMOE_CODEC_RAW = 0, INFMOE_CODEC_EXP4 = 1, INFMOE_CODEC_EXPH = 2 };
 
 /* per-forward outputs (all optional; host pointers unless noted) */
 typedef struct {
@@ -346,11 +349,12 @@ int infmoe_layer_destroy(infmoe_layer* layer);
 /* bytes one pass of an offloaded layer moves over the host link for its local
  * experts with its codec (packed) and without (raw = n_local * expert_param_bytes) */
 int infmoe_layer_h2d_bytes(infmoe_layer* layer, uint64_t* packed, uint64_t* raw);
-/* exp4 codec round trip (test hook): pack n bf16 values (host) on the host,
- * decode them on the device, copy the result to out (host); pack_bytes (may be
- * NULL) receives the pack size.  n must be a positive multiple of 16. */
-int infmoe_codec_exp4_roundtrip(const uint16_t* in, uint64_t n, uint16_t* out,
-                                uint64_t* pack_bytes, int32_t device);
+/* codec round trip (test hook): pack n bf16 values (host) with codec
+ * (INFMOE_CODEC_EXP4 / EXPH) on the host, decode them on the device, copy the
+ * result to out (host); pack_bytes (may be NULL) receives the pack size.  n must
+ * be a positive multiple of 64. */
+int infmoe_codec_roundtrip(int32_t codec, const uint16_t* in, uint64_t n, uint16_t* out,
+                           uint64_t* pack_bytes, int32_t device);
 
 #ifdef __cplusplus
 }

@@ -194,7 +194,7 @@ _lib.infmoe_layer_set_host_weights.argtypes = [_vp, _vp, _vp]
 _lib.infmoe_layer_pin_experts.argtypes = [_vp, _vp, _i32]
 _lib.infmoe_layer_pin_hottest.argtypes = [_vp, _i32, _vp]
 _lib.infmoe_layer_destroy.argtypes = [_vp]
-_lib.infmoe_codec_exp4_roundtrip.argtypes = [_vp, _u64, _vp, _vp, _i32]
+_lib.infmoe_codec_roundtrip.argtypes = [_i32, _vp, _u64, _vp, _vp, _i32]
 _lib.infmoe_layer_h2d_bytes.argtypes = [_vp, _vp, _vp]
 _lib.infmoe_slot_pool_create.argtypes = [_i32, _i32, _u64, _P(_vp)]
 _lib.infmoe_slot_pool_destroy.argtypes = [_vp]

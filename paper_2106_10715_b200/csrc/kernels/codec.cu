@@ -4,6 +4,8 @@
 #include "codec.cuh"
 
 #include <algorithm>
+#include <atomic>
+#include <queue>
 #include <thread>
 
 #include "common.cuh"
@@ -142,6 +144,267 @@ void exp4_unpack_host(const uint8_t* pack, uint64_t n, uint16_t* out) {
 void launch_exp4_unpack(const uint8_t* pack, uint64_t n, uint16_t* out, cudaStream_t s) {
   const Exp4Layout L = exp4_layout(n);
   exp4_unpack_kernel<<<unsigned(L.nblocks), 256, 0, s>>>(pack, L, out);
+  INFMOE_LAUNCH_CHECK();
+}
+
+// ------------------------------------------------------------------ exph --
+namespace {
+
+inline uint32_t exph_sym(uint16_t v, uint32_t base) {
+  const uint32_t d = base - ((v >> 7) & 0xFFu);
+  return d >= uint32_t(kExphEsc) ? uint32_t(kExphEsc) : d;
+}
+
+// Huffman code lengths for <= 32 symbols, limited to kExphMaxLen bits (longer
+// codes are clamped and the Kraft sum restored by lengthening the longest
+// codes below the limit); canonical codes assigned by (length, symbol)
+void huffman_lengths(const uint64_t* freq, uint8_t* len) {
+  struct Node { uint64_t f; int id; };
+  auto cmp = [](const Node& a, const Node& b) { return a.f != b.f ? a.f > b.f : a.id > b.id; };
+  std::priority_queue<Node, std::vector<Node>, decltype(cmp)> q(cmp);
+  std::vector<int> parent(64, -1);
+  int next = 32, used = 0;
+  for (int i = 0; i < 32; ++i) {
+    len[i] = 0;
+    if (freq[i]) { q.push({freq[i], i}); ++used; }
+  }
+  if (used == 0) return;
+  if (used == 1) { len[q.top().id] = 1; return; }
+  while (q.size() > 1) {
+    Node a = q.top(); q.pop();
+    Node b = q.top(); q.pop();
+    parent[size_t(a.id)] = next;
+    parent[size_t(b.id)] = next;
+    q.push({a.f + b.f, next++});
+  }
+  for (int i = 0; i < 32; ++i) {
+    if (!freq[i]) continue;
+    int d = 0;
+    for (int j = i; parent[size_t(j)] >= 0; j = parent[size_t(j)]) ++d;
+    len[i] = uint8_t(d);
+  }
+  int64_t kraft = 0;
+  const int64_t one = int64_t(1) << kExphMaxLen;
+  for (int i = 0; i < 32; ++i)
+    if (len[i]) {
+      if (len[i] > kExphMaxLen) len[i] = kExphMaxLen;
+      kraft += one >> len[i];
+    }
+  while (kraft > one) {  // lengthen the longest code still below the limit
+    int best = -1;
+    for (int i = 0; i < 32; ++i)
+      if (len[i] && len[i] < kExphMaxLen && (best < 0 || len[i] > len[best] ||
+                                             (len[i] == len[best] && freq[i] < freq[best])))
+        best = i;
+    kraft -= one >> (len[best] + 1);
+    ++len[best];
+  }
+}
+
+void canonical_codes(const uint8_t* len, uint32_t* code) {
+  uint32_t c = 0;
+  int prev = 0;
+  for (int l = 1; l <= kExphMaxLen; ++l) {
+    for (int s = 0; s < 32; ++s)
+      if (len[s] == l) {
+        c <<= (l - prev);
+        prev = l;
+        code[s] = c++;
+      }
+  }
+}
+
+__global__ void __launch_bounds__(256) exph_unpack_kernel(const uint8_t* __restrict__ pack,
+                                                          ExphLayout L, uint16_t* __restrict__ out) {
+  __shared__ uint16_t lut[1 << kExphMaxLen];
+  const auto* glut = reinterpret_cast<const uint4*>(pack + L.off_lut);
+  for (int i = threadIdx.x; i < (1 << kExphMaxLen) / 8; i += blockDim.x)
+    reinterpret_cast<uint4*>(lut)[i] = __ldg(glut + i);
+  __syncthreads();
+  const auto* words = reinterpret_cast<const uint32_t*>(pack + L.off_bits);
+  const auto* cbit = reinterpret_cast<const uint32_t*>(pack + L.off_chunk);
+  for (uint64_t c = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; c < L.nchunks;
+       c += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t v0 = c * kExphChunk;
+    const uint32_t base = pack[L.off_base + v0 / kExp4Block];
+    const uint32_t p = __ldg(cbit + c);
+    const uint32_t* wp = words + (p >> 5);
+    uint64_t buf = ((uint64_t(__ldg(wp)) << 32) | __ldg(wp + 1)) << (p & 31);
+    int nbits = 64 - int(p & 31);
+    wp += 2;
+    const uint4* smv = reinterpret_cast<const uint4*>(pack + v0);
+    uint4* dst = reinterpret_cast<uint4*>(out + v0);
+#pragma unroll 1
+    for (int q = 0; q < kExphChunk / 16; ++q) {
+      const uint4 s4 = __ldg(smv + q);
+      const uint32_t sw[4] = {s4.x, s4.y, s4.z, s4.w};
+      uint32_t r[8];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        if (nbits < 32) {
+          buf |= uint64_t(__ldg(wp++)) << (32 - nbits);
+          nbits += 32;
+        }
+        const uint32_t ent = lut[uint32_t(buf >> (64 - kExphMaxLen))];
+        const uint32_t sym = ent >> 4, ln = ent & 15u;
+        buf <<= ln;
+        nbits -= int(ln);
+        uint32_t e;
+        if (sym == uint32_t(kExphEsc)) {
+          e = uint32_t(buf >> 56);
+          buf <<= 8;
+          nbits -= 8;
+        } else {
+          e = (base - sym) & 0xFFu;
+        }
+        const uint32_t smb = (sw[j / 4] >> (8 * (j % 4))) & 0xFFu;
+        const uint32_t v = ((smb & 0x80u) << 8) | (e << 7) | (smb & 0x7Fu);
+        if (j % 2 == 0) r[j / 2] = v;
+        else r[j / 2] |= v << 16;
+      }
+      dst[2 * q] = make_uint4(r[0], r[1], r[2], r[3]);
+      dst[2 * q + 1] = make_uint4(r[4], r[5], r[6], r[7]);
+    }
+  }
+}
+
+}  // namespace
+
+ExphPlan exph_plan(const uint16_t* in, uint64_t n) {
+  require(n > 0 && n % kExphChunk == 0, "exph: value count must be a positive multiple of 64");
+  ExphPlan p;
+  ExphLayout& L = p.L;
+  L.n = n;
+  L.nblocks = (n + kExp4Block - 1) / kExp4Block;
+  L.nchunks = n / kExphChunk;
+  p.base.assign(L.nblocks, 0);
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  std::vector<std::vector<uint64_t>> hist(hw, std::vector<uint64_t>(32, 0));
+  {
+    std::vector<std::thread> th;
+    for (unsigned t = 0; t < hw; ++t)
+      th.emplace_back([&, t] {
+        for (uint64_t b = t; b < L.nblocks; b += hw) {
+          const uint64_t v0 = b * kExp4Block, v1 = std::min(n, v0 + kExp4Block);
+          uint32_t mx = 0;
+          for (uint64_t i = v0; i < v1; ++i) mx = std::max<uint32_t>(mx, (in[i] >> 7) & 0xFFu);
+          p.base[b] = uint8_t(mx);
+          for (uint64_t i = v0; i < v1; ++i) ++hist[t][exph_sym(in[i], mx)];
+        }
+      });
+    for (auto& x : th) x.join();
+  }
+  uint64_t freq[32] = {};
+  for (auto& h : hist)
+    for (int i = 0; i < 32; ++i) freq[i] += h[size_t(i)];
+  huffman_lengths(freq, p.len);
+  canonical_codes(p.len, p.code);
+  std::vector<uint32_t> cb(L.nchunks, 0);
+  parallel_blocks(L.nchunks, [&](uint64_t c) {
+    uint32_t bits = 0;
+    const uint32_t base = p.base[c * kExphChunk / kExp4Block];
+    for (uint64_t i = c * kExphChunk; i < (c + 1) * kExphChunk; ++i) {
+      const uint32_t sym = exph_sym(in[i], base);
+      bits += p.len[sym] + (sym == uint32_t(kExphEsc) ? 8u : 0u);
+    }
+    cb[c] = bits;
+  });
+  p.chunk_bit.assign(L.nchunks + 1, 0);
+  uint64_t total = 0;
+  for (uint64_t c = 0; c < L.nchunks; ++c) {
+    p.chunk_bit[c] = uint32_t(total);
+    total += cb[c];
+  }
+  require(total < (uint64_t(1) << 32) - 64, "exph: bitstream exceeds 2^32 bits");
+  p.chunk_bit[L.nchunks] = uint32_t(total);
+  L.off_bits = align16(n);
+  L.off_chunk = align16(L.off_bits + (total + 31) / 32 * 4 + 8);
+  L.off_base = align16(L.off_chunk + 4 * L.nchunks);
+  L.off_lut = align16(L.off_base + L.nblocks);
+  L.bytes = align16(L.off_lut + 2 * (1 << kExphMaxLen));
+  return p;
+}
+
+void exph_fill(const uint16_t* in, const ExphPlan& p, uint8_t* out) {
+  const ExphLayout& L = p.L;
+  std::fill(out, out + L.bytes, uint8_t(0));
+  auto* words = reinterpret_cast<uint32_t*>(out + L.off_bits);
+  parallel_blocks(L.nchunks, [&](uint64_t c) {
+    // the chunk's bits go to a local buffer (<= 64 x 20 bits); only its first
+    // and last words can be shared with the neighbouring chunks
+    const uint32_t base = p.base[c * kExphChunk / kExp4Block];
+    const uint64_t start = p.chunk_bit[c];
+    uint32_t loc[48] = {};
+    uint64_t pos = start & 31;  // bit position inside loc
+    auto put = [&](uint32_t val, uint32_t nb) {  // MSB-first, may straddle words
+      while (nb) {
+        const uint32_t w = uint32_t(pos >> 5), off = uint32_t(pos & 31);
+        const uint32_t take = std::min(nb, 32 - off);
+        const uint32_t bits = (val >> (nb - take)) & ((take == 32) ? 0xFFFFFFFFu : ((1u << take) - 1));
+        loc[w] |= bits << (32 - off - take);
+        pos += take;
+        nb -= take;
+      }
+    };
+    for (uint64_t i = c * kExphChunk; i < (c + 1) * kExphChunk; ++i) {
+      const uint16_t v = in[i];
+      out[i] = uint8_t(((v >> 8) & 0x80u) | (v & 0x7Fu));
+      const uint32_t sym = exph_sym(v, base);
+      put(p.code[sym], p.len[sym]);
+      if (sym == uint32_t(kExphEsc)) put((v >> 7) & 0xFFu, 8);
+    }
+    if (pos == (start & 31)) return;  // empty chunk (cannot happen: lengths >= 1)
+    const uint64_t w0 = start >> 5;
+    const uint32_t nw = uint32_t((pos + 31) >> 5);
+    for (uint32_t k = 0; k < nw; ++k) {
+      if (k == 0 || k + 1 == nw)
+        std::atomic_ref<uint32_t>(words[w0 + k]).fetch_or(loc[k], std::memory_order_relaxed);
+      else
+        words[w0 + k] = loc[k];
+    }
+  });
+  std::copy(p.chunk_bit.begin(), p.chunk_bit.end() - 1,
+            reinterpret_cast<uint32_t*>(out + L.off_chunk));
+  std::copy(p.base.begin(), p.base.end(), out + L.off_base);
+  auto* lut = reinterpret_cast<uint16_t*>(out + L.off_lut);
+  for (int sym = 0; sym < 32; ++sym) {
+    const uint32_t l = p.len[sym];
+    if (!l) continue;
+    const uint32_t first = p.code[sym] << (kExphMaxLen - l);
+    for (uint32_t s = 0; s < (1u << (kExphMaxLen - l)); ++s)
+      lut[first | s] = uint16_t((sym << 4) | l);
+  }
+}
+
+void exph_unpack_host(const uint8_t* pack, const ExphLayout& L, uint16_t* out) {
+  const auto* words = reinterpret_cast<const uint32_t*>(pack + L.off_bits);
+  const auto* cbit = reinterpret_cast<const uint32_t*>(pack + L.off_chunk);
+  const auto* lut = reinterpret_cast<const uint16_t*>(pack + L.off_lut);
+  auto bit = [&](uint64_t q) { return (words[q >> 5] >> (31 - (q & 31))) & 1u; };
+  for (uint64_t c = 0; c < L.nchunks; ++c) {
+    uint64_t q = cbit[c];
+    const uint32_t base = pack[L.off_base + c * kExphChunk / kExp4Block];
+    for (uint64_t i = c * kExphChunk; i < (c + 1) * kExphChunk; ++i) {
+      uint32_t peek = 0;
+      for (int k = 0; k < kExphMaxLen; ++k) peek = (peek << 1) | bit(q + k);
+      const uint32_t sym = lut[peek] >> 4, ln = lut[peek] & 15u;
+      q += ln;
+      uint32_t e = (base - sym) & 0xFFu;
+      if (sym == uint32_t(kExphEsc)) {
+        e = 0;
+        for (int k = 0; k < 8; ++k) e = (e << 1) | bit(q + k);
+        q += 8;
+      }
+      const uint32_t smb = pack[i];
+      out[i] = uint16_t(((smb & 0x80u) << 8) | (e << 7) | (smb & 0x7Fu));
+    }
+  }
+}
+
+void launch_exph_unpack(const uint8_t* pack, const ExphLayout& L, uint16_t* out, cudaStream_t s) {
+  const uint64_t want = (L.nchunks + 255) / 256;
+  const unsigned grid = unsigned(std::min<uint64_t>(want, uint64_t(device_sm_count()) * 8));
+  exph_unpack_kernel<<<std::max(1u, grid), 256, 0, s>>>(pack, L, out);
   INFMOE_LAUNCH_CHECK();
 }
 

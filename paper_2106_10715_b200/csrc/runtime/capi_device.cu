@@ -306,21 +306,34 @@ int infmoe_layer_h2d_bytes(infmoe_layer* layer, uint64_t* packed, uint64_t* raw)
   });
 }
 
-int infmoe_codec_exp4_roundtrip(const uint16_t* in, uint64_t n, uint16_t* out,
-                                uint64_t* pack_bytes, int32_t device) {
+int infmoe_codec_roundtrip(int32_t codec_id, const uint16_t* in, uint64_t n, uint16_t* out,
+                           uint64_t* pack_bytes, int32_t device) {
   return guarded([&] {
-    require(in && out, "codec_exp4_roundtrip: NULL argument");
+    require(in && out, "codec_roundtrip: NULL argument");
+    require(codec_id == INFMOE_CODEC_EXP4 || codec_id == INFMOE_CODEC_EXPH,
+            "codec_roundtrip: unknown codec");
+    require(n > 0 && n % 64 == 0, "codec_roundtrip: n must be a positive multiple of 64");
     INFMOE_CUDA(cudaSetDevice(device));
-    const codec::Exp4Plan plan = codec::exp4_plan(in, n);
-    std::vector<uint8_t> pk(plan.bytes);
-    codec::exp4_fill(in, plan, pk.data());
-    if (pack_bytes) *pack_bytes = plan.bytes;
+    std::vector<uint8_t> pk;
+    codec::ExphLayout hl;
+    if (codec_id == INFMOE_CODEC_EXP4) {
+      const codec::Exp4Plan plan = codec::exp4_plan(in, n);
+      pk.resize(plan.bytes);
+      codec::exp4_fill(in, plan, pk.data());
+    } else {
+      const codec::ExphPlan plan = codec::exph_plan(in, n);
+      hl = plan.L;
+      pk.resize(plan.L.bytes);
+      codec::exph_fill(in, plan, pk.data());
+    }
+    if (pack_bytes) *pack_bytes = pk.size();
     uint8_t* dp = nullptr;
     uint16_t* dout = nullptr;
-    INFMOE_CUDA(cudaMalloc(&dp, plan.bytes));
+    INFMOE_CUDA(cudaMalloc(&dp, pk.size()));
     INFMOE_CUDA(cudaMalloc(&dout, n * 2));
-    INFMOE_CUDA(cudaMemcpy(dp, pk.data(), plan.bytes, cudaMemcpyHostToDevice));
-    codec::launch_exp4_unpack(dp, n, dout, nullptr);
+    INFMOE_CUDA(cudaMemcpy(dp, pk.data(), pk.size(), cudaMemcpyHostToDevice));
+    if (codec_id == INFMOE_CODEC_EXP4) codec::launch_exp4_unpack(dp, n, dout, nullptr);
+    else codec::launch_exph_unpack(dp, hl, dout, nullptr);
     INFMOE_CUDA(cudaMemcpy(out, dout, n * 2, cudaMemcpyDeviceToHost));
     cudaFree(dp);
     cudaFree(dout);

@@ -139,10 +139,11 @@ Layer::Layer(const infmoe_layer_desc& d) : desc(d) {
   expert_in_bytes = size_t(d.d_ff) * d.d_model * esz;
   if (d.residency == INFMOE_OFFLOADED) {
     require(d.K >= 1, "layer: offloaded mode needs K >= 1");
-    require(d.h2d_codec == INFMOE_CODEC_RAW || d.h2d_codec == INFMOE_CODEC_EXP4,
+    require(d.h2d_codec == INFMOE_CODEC_RAW || d.h2d_codec == INFMOE_CODEC_EXP4 ||
+                d.h2d_codec == INFMOE_CODEC_EXPH,
             "layer: unknown h2d_codec");
     require(d.h2d_codec == INFMOE_CODEC_RAW || d.dtype == INFMOE_DTYPE_BF16,
-            "layer: the exp4 codec packs bf16 weights");
+            "layer: the exp4 / exph codecs pack bf16 weights");
     if (d.slot_pool) {  // K+1 slots shared with the other layers of the stack
       auto* pool = reinterpret_cast<SlotPool*>(d.slot_pool);
       pool_ptr = pool;
@@ -206,8 +207,9 @@ void Layer::set_host_weights(const void* w_in, const void* w_out) {
   }
   host_in = reinterpret_cast<const uint8_t*>(w_in);
   host_out = reinterpret_cast<const uint8_t*>(w_out);
-  if (desc.h2d_codec == INFMOE_CODEC_EXP4) {
-    pack = HostPack::acquire(w_in, w_out, n_local, uint64_t(desc.d_ff) * desc.d_model);
+  if (desc.h2d_codec != INFMOE_CODEC_RAW) {
+    pack = HostPack::acquire(w_in, w_out, n_local, uint64_t(desc.d_ff) * desc.d_model,
+                             desc.h2d_codec);
     if (pool_ptr->stage_bytes < pack->max_size) {  // grow the shared staging buffers
       INFMOE_CUDA(cudaDeviceSynchronize());
       if (pool_ptr->stage) INFMOE_CUDA(cudaFree(pool_ptr->stage));
@@ -513,10 +515,17 @@ void Layer::compute_offloaded(const Rows& r, bool timed, infmoe_forward_out* out
       if (pack) {  // decode both matrices into the slot (counted as compute)
         if (e0) INFMOE_CUDA(cudaEventRecord(e0, s));
         const uint64_t elems = uint64_t(desc.d_ff) * desc.d_model;
-        codec::launch_exp4_unpack(stage_of(slot), elems,
-                                  reinterpret_cast<uint16_t*>(slot_in + size_t(slot) * expert_in_bytes), s);
-        codec::launch_exp4_unpack(stage_of(slot) + pack->in_size[size_t(e)], elems,
-                                  reinterpret_cast<uint16_t*>(slot_out + size_t(slot) * expert_in_bytes), s);
+        auto* w1 = reinterpret_cast<uint16_t*>(slot_in + size_t(slot) * expert_in_bytes);
+        auto* w2 = reinterpret_cast<uint16_t*>(slot_out + size_t(slot) * expert_in_bytes);
+        const uint8_t* p1 = stage_of(slot);
+        const uint8_t* p2 = p1 + pack->in_size[size_t(e)];
+        if (pack->codec_id == INFMOE_CODEC_EXPH) {
+          codec::launch_exph_unpack(p1, pack->lay_in[size_t(e)], w1, s);
+          codec::launch_exph_unpack(p2, pack->lay_out[size_t(e)], w2, s);
+        } else {
+          codec::launch_exp4_unpack(p1, elems, w1, s);
+          codec::launch_exp4_unpack(p2, elems, w2, s);
+        }
         e0 = nullptr;
       }
       const int tiles = int((n_e + 127) / 128) * (std::max(desc.d_ff, desc.d_model) / 128);
@@ -795,8 +804,9 @@ struct PackKey {
   const void* b;
   int n;
   uint64_t elems;
+  int codec_id;
   bool operator<(const PackKey& o) const {
-    return std::tie(a, b, n, elems) < std::tie(o.a, o.b, o.n, o.elems);
+    return std::tie(a, b, n, elems, codec_id) < std::tie(o.a, o.b, o.n, o.elems, o.codec_id);
   }
 };
 std::mutex g_pack_mu;
@@ -804,23 +814,32 @@ std::map<PackKey, std::weak_ptr<HostPack>> g_packs;
 }  // namespace
 
 std::shared_ptr<HostPack> HostPack::acquire(const void* w_in, const void* w_out, int n_experts,
-                                            uint64_t matrix_elems) {
+                                            uint64_t matrix_elems, int codec_id) {
   std::lock_guard<std::mutex> lock(g_pack_mu);
-  const PackKey key{w_in, w_out, n_experts, matrix_elems};
+  const PackKey key{w_in, w_out, n_experts, matrix_elems, codec_id};
   auto it = g_packs.find(key);
   if (it != g_packs.end())
     if (auto sp = it->second.lock()) return sp;
   auto p = std::make_shared<HostPack>();
+  p->codec_id = codec_id;
   const auto* in = static_cast<const uint16_t*>(w_in);
   const auto* out = static_cast<const uint16_t*>(w_out);
-  std::vector<codec::Exp4Plan> plans;
-  plans.reserve(size_t(2 * n_experts));
+  const bool h = codec_id == INFMOE_CODEC_EXPH;
+  std::vector<codec::Exp4Plan> p4;
+  std::vector<codec::ExphPlan> ph;
+  for (int e = 0; e < n_experts; ++e)
+    for (const uint16_t* m : {in + uint64_t(e) * matrix_elems, out + uint64_t(e) * matrix_elems}) {
+      if (h) ph.push_back(codec::exph_plan(m, matrix_elems));
+      else p4.push_back(codec::exp4_plan(m, matrix_elems));
+    }
   for (int e = 0; e < n_experts; ++e) {
-    plans.push_back(codec::exp4_plan(in + uint64_t(e) * matrix_elems, matrix_elems));
-    plans.push_back(codec::exp4_plan(out + uint64_t(e) * matrix_elems, matrix_elems));
-  }
-  for (int e = 0; e < n_experts; ++e) {
-    const uint64_t a = plans[size_t(2 * e)].bytes, b = plans[size_t(2 * e + 1)].bytes;
+    const size_t i1 = size_t(2 * e), i2 = i1 + 1;
+    const uint64_t a = h ? ph[i1].L.bytes : p4[i1].bytes;
+    const uint64_t b = h ? ph[i2].L.bytes : p4[i2].bytes;
+    if (h) {
+      p->lay_in.push_back(ph[i1].L);
+      p->lay_out.push_back(ph[i2].L);
+    }
     p->off.push_back(p->total);
     p->size.push_back(a + b);
     p->in_size.push_back(a);
@@ -830,10 +849,16 @@ std::shared_ptr<HostPack> HostPack::acquire(const void* w_in, const void* w_out,
   p->raw_bytes = uint64_t(n_experts) * matrix_elems * 2 * 2;
   INFMOE_CUDA(cudaMallocHost(&p->host, p->total));
   for (int e = 0; e < n_experts; ++e) {
-    codec::exp4_fill(in + uint64_t(e) * matrix_elems, plans[size_t(2 * e)],
-                     p->host + p->off[size_t(e)]);
-    codec::exp4_fill(out + uint64_t(e) * matrix_elems, plans[size_t(2 * e + 1)],
-                     p->host + p->off[size_t(e)] + p->in_size[size_t(e)]);
+    uint8_t* dst = p->host + p->off[size_t(e)];
+    const uint16_t* m1 = in + uint64_t(e) * matrix_elems;
+    const uint16_t* m2 = out + uint64_t(e) * matrix_elems;
+    if (h) {
+      codec::exph_fill(m1, ph[size_t(2 * e)], dst);
+      codec::exph_fill(m2, ph[size_t(2 * e + 1)], dst + p->in_size[size_t(e)]);
+    } else {
+      codec::exp4_fill(m1, p4[size_t(2 * e)], dst);
+      codec::exp4_fill(m2, p4[size_t(2 * e + 1)], dst + p->in_size[size_t(e)]);
+    }
   }
   g_packs[key] = p;
   return p;

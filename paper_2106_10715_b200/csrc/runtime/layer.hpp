@@ -9,6 +9,7 @@
 #include <vector>
 
 #include "../host/ep_plan.hpp"
+#include "../kernels/codec.cuh"
 #include "infmoe.h"
 
 namespace infmoe {
@@ -30,9 +31,11 @@ struct HostPack {
   uint8_t* host = nullptr;          // pinned
   std::vector<uint64_t> off, size;  // per expert: [w_in pack | w_out pack], 16-aligned
   std::vector<uint64_t> in_size;    // bytes of the w_in pack (w_out pack follows)
+  std::vector<codec::ExphLayout> lay_in, lay_out;  // exph: per-matrix layouts
+  int codec_id = 0;
   uint64_t max_size = 0, total = 0, raw_bytes = 0;
   static std::shared_ptr<HostPack> acquire(const void* w_in, const void* w_out, int n_experts,
-                                           uint64_t matrix_elems);
+                                           uint64_t matrix_elems, int codec_id);
   ~HostPack();
 };
 

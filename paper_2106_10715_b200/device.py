@@ -191,13 +191,17 @@ def combine(y_perm, inv, topk_w, N: int, k: int):
     return y
 
 
-def codec_exp4_roundtrip(bits: np.ndarray, device: int = 0):
-    """exp4-pack bf16 bit patterns on the host, decode on the GPU: (decoded, pack bytes)."""
+CODECS = {"raw": 0, "exp4": 1, "exph": 2}
+
+
+def codec_roundtrip(bits: np.ndarray, codec: str = "exp4", device: int = 0):
+    """Pack bf16 bit patterns on the host with codec, decode on the GPU:
+    (decoded, pack bytes)."""
     a = np.ascontiguousarray(bits, dtype=np.uint16)
     out = np.empty_like(a)
     nb = C.c_uint64(0)
-    _check(_lib.infmoe_codec_exp4_roundtrip(a.ctypes.data_as(C.c_void_p), a.size,
-                                            out.ctypes.data_as(C.c_void_p), C.byref(nb), device))
+    _check(_lib.infmoe_codec_roundtrip(CODECS[codec], a.ctypes.data_as(C.c_void_p), a.size,
+                                       out.ctypes.data_as(C.c_void_p), C.byref(nb), device))
     return out, nb.value
 
 
@@ -260,7 +264,7 @@ class MoELayer:
         d.ep_size, d.ep_rank, d.ep_comm = ep_size, ep_rank, ep_comm
         d.skip_empty_experts = int(skip_empty_experts)
         d.ep_transport = {"nccl": 0, "peer": 1}[ep_transport]
-        d.h2d_codec = {"raw": 0, "exp4": 1}[h2d_codec]
+        d.h2d_codec = CODECS[h2d_codec]
         if slot_pool is not None:
             d.slot_pool = slot_pool.handle
             self._keep.append(slot_pool)  # the pool outlives the layer

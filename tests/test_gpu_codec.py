@@ -13,8 +13,10 @@ from oracle_lib import fill_bf16
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("case", ["all_patterns", "weights", "zeros", "wide", "tail_block"])
-def test_exp4_roundtrip_bit_exact(cuda, case):
+@pytest.mark.parametrize("codec", ["exp4", "exph"])
+@pytest.mark.parametrize("case", ["all_patterns", "weights", "zeros", "wide", "tail_block",
+                                  "one_symbol", "long_codes"])
+def test_roundtrip_bit_exact(cuda, case, codec):
     rng = np.random.default_rng(1)
     if case == "all_patterns":
         a = np.tile(np.arange(1 << 16, dtype=np.uint16), 3)
@@ -26,18 +28,25 @@ def test_exp4_roundtrip_bit_exact(cuda, case):
         a[::7] = 0x8000  # -0.0
     elif case == "wide":  # exponents spread over the whole range: mostly escapes
         a = rng.integers(0, 1 << 16, size=200_000, dtype=np.uint16)
-    else:  # a last block shorter than 32768 values
-        a = fill_bf16(9, 32768 * 3 + 48, 2.0)
-    n = (a.size // 16) * 16
+    elif case == "tail_block":  # a last block shorter than 32768 values
+        a = fill_bf16(9, 32768 * 3 + 64, 2.0)
+    elif case == "one_symbol":  # one exponent everywhere: a 1-bit code
+        a = (np.full(8192, 0x3F80, np.uint16) | rng.integers(0, 128, 8192, dtype=np.uint16))
+    else:  # a skewed exponent histogram: Huffman lengths hit the 12-bit limit
+        e = np.minimum(rng.geometric(0.75, size=300_000) - 1, 40)
+        a = (((127 - e) & 0xFF) << 7).astype(np.uint16) | rng.integers(0, 128, 300_000,
+                                                                        dtype=np.uint16)
+    n = (a.size // 64) * 64
     a = np.ascontiguousarray(a[:n])
-    out, nbytes = dv.codec_exp4_roundtrip(a)
+    out, nbytes = dv.codec_roundtrip(a, codec)
     assert np.array_equal(out, a)
-    if case == "weights":
-        assert nbytes < 0.76 * 2 * n  # 12 bits per value + block headers + rare escapes
+    if case == "weights":  # exp4: 12 bits per value; exph: ~10.7 (exponent entropy 2.14)
+        assert nbytes < (0.76 if codec == "exp4" else 0.70) * 2 * n
 
 
+@pytest.mark.parametrize("codec", ["exp4", "exph"])
 @pytest.mark.parametrize("gate,k,pins", [("lsh", 1, []), ("softmax", 2, [1])])
-def test_exp4_layer_bit_identical(cuda, gate, k, pins):
+def test_codec_layer_bit_identical(cuda, gate, k, pins, codec):
     N, d, f, E, K = 512, 256, 512, 8, 2
     t = lambda b, sh: torch.from_numpy(b.view(np.int16).reshape(sh)).view(torch.bfloat16)
     x = t(fill_bf16(1, N * d, 1.7320508), (N, d)).to(cuda)
@@ -49,8 +58,8 @@ def test_exp4_layer_bit_identical(cuda, gate, k, pins):
               K=K)
     raw = dv.MoELayer(d, f, E, k, wi, wo, **kw)
     pool = dv.SlotPool(K, d, f)
-    ex1 = dv.MoELayer(d, f, E, k, wi, wo, h2d_codec="exp4", slot_pool=pool, **kw)
-    ex2 = dv.MoELayer(d, f, E, k, wi, wo, h2d_codec="exp4", slot_pool=pool, **kw)  # shared pack
+    ex1 = dv.MoELayer(d, f, E, k, wi, wo, h2d_codec=codec, slot_pool=pool, **kw)
+    ex2 = dv.MoELayer(d, f, E, k, wi, wo, h2d_codec=codec, slot_pool=pool, **kw)  # shared pack
     if pins:
         ex1.pin_experts(pins)
     y0, info0 = raw.forward(x, want_timeline=True)
