@@ -352,7 +352,7 @@ int infmoe_layer_h2d_bytes(infmoe_layer* layer, uint64_t* packed, uint64_t* raw)
 /* codec round trip (test hook): pack n bf16 values (host) with codec
  * (INFMOE_CODEC_EXP4 / EXPH) on the host, decode them on the device, copy the
  * result to out (host); pack_bytes (may be NULL) receives the pack size.  n must
- * be a positive multiple of 64. */
+ * be a positive multiple of 128. */
 int infmoe_codec_roundtrip(int32_t codec, const uint16_t* in, uint64_t n, uint16_t* out,
                            uint64_t* pack_bytes, int32_t device);
 

@@ -222,12 +222,13 @@ __global__ void __launch_bounds__(256) exph_unpack_kernel(const uint8_t* __restr
     reinterpret_cast<uint4*>(lut)[i] = __ldg(glut + i);
   __syncthreads();
   const auto* words = reinterpret_cast<const uint32_t*>(pack + L.off_bits);
-  const auto* cbit = reinterpret_cast<const uint32_t*>(pack + L.off_chunk);
+  const auto* gbit = reinterpret_cast<const uint32_t*>(pack + L.off_group);
+  const auto* cbit = reinterpret_cast<const uint16_t*>(pack + L.off_chunk);
   for (uint64_t c = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; c < L.nchunks;
        c += uint64_t(gridDim.x) * blockDim.x) {
     const uint64_t v0 = c * kExphChunk;
     const uint32_t base = pack[L.off_base + v0 / kExp4Block];
-    const uint32_t p = __ldg(cbit + c);
+    const uint32_t p = __ldg(gbit + c / kExphGroup) + __ldg(cbit + c);
     const uint32_t* wp = words + (p >> 5);
     uint64_t buf = ((uint64_t(__ldg(wp)) << 32) | __ldg(wp + 1)) << (p & 31);
     int nbits = 64 - int(p & 31);
@@ -271,12 +272,13 @@ __global__ void __launch_bounds__(256) exph_unpack_kernel(const uint8_t* __restr
 }  // namespace
 
 ExphPlan exph_plan(const uint16_t* in, uint64_t n) {
-  require(n > 0 && n % kExphChunk == 0, "exph: value count must be a positive multiple of 64");
+  require(n > 0 && n % kExphChunk == 0, "exph: value count must be a positive multiple of 128");
   ExphPlan p;
   ExphLayout& L = p.L;
   L.n = n;
   L.nblocks = (n + kExp4Block - 1) / kExp4Block;
   L.nchunks = n / kExphChunk;
+  L.ngroups = (L.nchunks + kExphGroup - 1) / kExphGroup;
   p.base.assign(L.nblocks, 0);
   const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
   std::vector<std::vector<uint64_t>> hist(hw, std::vector<uint64_t>(32, 0));
@@ -318,8 +320,9 @@ ExphPlan exph_plan(const uint16_t* in, uint64_t n) {
   require(total < (uint64_t(1) << 32) - 64, "exph: bitstream exceeds 2^32 bits");
   p.chunk_bit[L.nchunks] = uint32_t(total);
   L.off_bits = align16(n);
-  L.off_chunk = align16(L.off_bits + (total + 31) / 32 * 4 + 8);
-  L.off_base = align16(L.off_chunk + 4 * L.nchunks);
+  L.off_group = align16(L.off_bits + (total + 31) / 32 * 4 + 8);
+  L.off_chunk = align16(L.off_group + 4 * L.ngroups);
+  L.off_base = align16(L.off_chunk + 2 * L.nchunks);
   L.off_lut = align16(L.off_base + L.nblocks);
   L.bytes = align16(L.off_lut + 2 * (1 << kExphMaxLen));
   return p;
@@ -330,11 +333,11 @@ void exph_fill(const uint16_t* in, const ExphPlan& p, uint8_t* out) {
   std::fill(out, out + L.bytes, uint8_t(0));
   auto* words = reinterpret_cast<uint32_t*>(out + L.off_bits);
   parallel_blocks(L.nchunks, [&](uint64_t c) {
-    // the chunk's bits go to a local buffer (<= 64 x 20 bits); only its first
+    // the chunk's bits go to a local buffer (<= 128 x 20 bits); only its first
     // and last words can be shared with the neighbouring chunks
     const uint32_t base = p.base[c * kExphChunk / kExp4Block];
     const uint64_t start = p.chunk_bit[c];
-    uint32_t loc[48] = {};
+    uint32_t loc[kExphChunk * 20 / 32 + 2] = {};
     uint64_t pos = start & 31;  // bit position inside loc
     auto put = [&](uint32_t val, uint32_t nb) {  // MSB-first, may straddle words
       while (nb) {
@@ -363,8 +366,12 @@ void exph_fill(const uint16_t* in, const ExphPlan& p, uint8_t* out) {
         words[w0 + k] = loc[k];
     }
   });
-  std::copy(p.chunk_bit.begin(), p.chunk_bit.end() - 1,
-            reinterpret_cast<uint32_t*>(out + L.off_chunk));
+  auto* gb = reinterpret_cast<uint32_t*>(out + L.off_group);
+  auto* cb = reinterpret_cast<uint16_t*>(out + L.off_chunk);
+  for (uint64_t c = 0; c < L.nchunks; ++c) {
+    if (c % kExphGroup == 0) gb[c / kExphGroup] = p.chunk_bit[c];
+    cb[c] = uint16_t(p.chunk_bit[c] - p.chunk_bit[c - c % kExphGroup]);
+  }
   std::copy(p.base.begin(), p.base.end(), out + L.off_base);
   auto* lut = reinterpret_cast<uint16_t*>(out + L.off_lut);
   for (int sym = 0; sym < 32; ++sym) {
@@ -378,11 +385,12 @@ void exph_fill(const uint16_t* in, const ExphPlan& p, uint8_t* out) {
 
 void exph_unpack_host(const uint8_t* pack, const ExphLayout& L, uint16_t* out) {
   const auto* words = reinterpret_cast<const uint32_t*>(pack + L.off_bits);
-  const auto* cbit = reinterpret_cast<const uint32_t*>(pack + L.off_chunk);
+  const auto* gbit = reinterpret_cast<const uint32_t*>(pack + L.off_group);
+  const auto* cbit = reinterpret_cast<const uint16_t*>(pack + L.off_chunk);
   const auto* lut = reinterpret_cast<const uint16_t*>(pack + L.off_lut);
   auto bit = [&](uint64_t q) { return (words[q >> 5] >> (31 - (q & 31))) & 1u; };
   for (uint64_t c = 0; c < L.nchunks; ++c) {
-    uint64_t q = cbit[c];
+    uint64_t q = uint64_t(gbit[c / kExphGroup]) + cbit[c];
     const uint32_t base = pack[L.off_base + c * kExphChunk / kExp4Block];
     for (uint64_t i = c * kExphChunk; i < (c + 1) * kExphChunk; ++i) {
       uint32_t peek = 0;

@@ -69,21 +69,24 @@ void launch_exp4_unpack(const uint8_t* pack, uint64_t n, uint16_t* out, cudaStre
 // Entropy-coded exponents ("exph"): the same sign/mantissa bytes, and per value
 // a canonical Huffman code (<= 12 bits, one code table per matrix) of
 // min(base - exponent, 31) against the per-block base; symbol 31 is followed by
-// the raw 8-bit exponent.  Codes are concatenated MSB-first per 64-value
-// chunk, with each chunk's starting bit recorded, so one GPU thread decodes one
-// chunk through a 4096-entry lookup table in shared memory.  ~2.1 bits of
-// exponent for the bench's weights (entropy 2.14): ~10.7 bits per value.
+// the raw 8-bit exponent.  Codes are concatenated MSB-first per 128-value
+// chunk; a chunk's starting bit is a uint32 per group of 16 chunks plus a
+// uint16 offset inside the group (0.14 bits per value), so one GPU thread
+// decodes one chunk through a 4096-entry lookup table in shared memory.  ~2.1
+// bits of exponent for the bench's weights (entropy 2.14): ~10.3 bits/value.
 //
 // Layout: [0, n) sign/mantissa | [off_bits) bitstream (uint32 words, + 8 B
-// slack) | [off_chunk) uint32 start bit per chunk | [off_base) base per block
-// | [off_lut) uint16 LUT[4096] = symbol << 4 | code length
-constexpr int kExphChunk = 64;
+// slack) | [off_group) uint32 start bit per group | [off_chunk) uint16 offset
+// per chunk | [off_base) base per block | [off_lut) uint16 LUT[4096] =
+// symbol << 4 | code length
+constexpr int kExphChunk = 128;
+constexpr int kExphGroup = 16;  // chunks per group (<= 16 x 128 x 20 bits < 2^16)
 constexpr int kExphMaxLen = 12;
 constexpr int kExphEsc = 31;
 
 struct ExphLayout {
-  uint64_t n = 0, nblocks = 0, nchunks = 0;
-  uint64_t off_bits = 0, off_chunk = 0, off_base = 0, off_lut = 0, bytes = 0;
+  uint64_t n = 0, nblocks = 0, nchunks = 0, ngroups = 0;
+  uint64_t off_bits = 0, off_group = 0, off_chunk = 0, off_base = 0, off_lut = 0, bytes = 0;
 };
 struct ExphPlan {
   ExphLayout L;

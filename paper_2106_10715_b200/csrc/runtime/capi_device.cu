@@ -312,7 +312,7 @@ int infmoe_codec_roundtrip(int32_t codec_id, const uint16_t* in, uint64_t n, uin
     require(in && out, "codec_roundtrip: NULL argument");
     require(codec_id == INFMOE_CODEC_EXP4 || codec_id == INFMOE_CODEC_EXPH,
             "codec_roundtrip: unknown codec");
-    require(n > 0 && n % 64 == 0, "codec_roundtrip: n must be a positive multiple of 64");
+    require(n > 0 && n % 128 == 0, "codec_roundtrip: n must be a positive multiple of 128");
     INFMOE_CUDA(cudaSetDevice(device));
     std::vector<uint8_t> pk;
     codec::ExphLayout hl;
