@@ -143,6 +143,27 @@ int main() {
     std::fprintf(stderr, "replay_check: %d violations\n", violations);
     return 1;
   }
+  // the same layer streaming lossless exph packs (shares the slot pool): the
+  // same output bit for bit, fewer bytes over the host link
+  infmoe_layer_desc hdesc = odesc;
+  hdesc.h2d_codec = INFMOE_CODEC_EXPH;
+  infmoe_layer* packed;
+  CHECK(infmoe_layer_create(&hdesc, &packed));
+  CHECK(infmoe_layer_forward(packed, x_d, N, y_off, nullptr, s));
+  CUDA(cudaStreamSynchronize(s));
+  CUDA(cudaMemcpy(b.data(), y_off, b.size() * 2, cudaMemcpyDeviceToHost));
+  if (a != b) {
+    std::fprintf(stderr, "exph-packed output differs from resident output\n");
+    return 1;
+  }
+  uint64_t packed_bytes = 0, raw_bytes = 0;
+  CHECK(infmoe_layer_h2d_bytes(packed, &packed_bytes, &raw_bytes));
+  if (!(packed_bytes < raw_bytes)) {
+    std::fprintf(stderr, "exph pack is not smaller than the raw weights\n");
+    return 1;
+  }
+  CHECK(infmoe_layer_destroy(packed));
+  std::printf("exph: %.2f bits per weight\n", 16.0 * double(packed_bytes) / double(raw_bytes));
   std::printf("order:");
   for (int e = 0; e < E; ++e) std::printf(" %d", order[e]);
   std::printf("  exposed copy %.3f ms\nlayer plugin demo ok\n", exposed * 1e3);
