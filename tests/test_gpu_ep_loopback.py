@@ -27,7 +27,7 @@ sys.path.insert(0, "{root}")
 import paper_2106_10715_b200 as im
 from paper_2106_10715_b200 import device as dv
 cuda = torch.device("cuda:0")
-P, k, gate, offloaded, transport = {P}, {k}, "{gate}", {offloaded}, "{transport}"
+P, k, gate, offloaded, transport, codec = {P}, {k}, "{gate}", {offloaded}, "{transport}", "{codec}"
 N, d, f, E = 1024, 256, 384, 16
 g = torch.Generator().manual_seed(7)
 x = torch.randn(N, d, generator=g).to(torch.bfloat16).to(cuda)
@@ -49,7 +49,7 @@ def rank(r):
         w = (wi_r.contiguous().pin_memory(), wo_r.contiguous().pin_memory()) if offloaded \
             else (wi_r.to(cuda), wo_r.to(cuda))
         lay = dv.MoELayer(d, f, E, k, *w, offloaded=offloaded, K=2, ep_size=P, ep_rank=r,
-                          ep_comm=comm, ep_transport=transport, **kw)
+                          ep_comm=comm, ep_transport=transport, h2d_codec=codec, **kw)
         s = torch.cuda.Stream()
         with torch.cuda.stream(s):
             for _ in range(2):  # twice: buffers are reused across forwards
@@ -86,10 +86,12 @@ def loopback_lib(tmp_path_factory):
 
 @pytest.mark.parametrize("transport", ["nccl", "peer"])
 @pytest.mark.parametrize("P,k,gate", [(2, 1, "lsh"), (4, 2, "softmax")])
-@pytest.mark.parametrize("offloaded", [False, True])
-def test_layer_ep_ranks_as_threads_equal_single_gpu(loopback_lib, P, k, gate, offloaded, transport):
+@pytest.mark.parametrize("offloaded,codec", [(False, "raw"), (True, "raw"), (True, "exph")])
+def test_layer_ep_ranks_as_threads_equal_single_gpu(loopback_lib, P, k, gate, offloaded, codec,
+                                                    transport):
     env = dict(os.environ, INFMOE_NCCL_LIB=str(loopback_lib))
-    code = SCRIPT.format(root=ROOT, P=P, k=k, gate=gate, offloaded=offloaded, transport=transport)
+    code = SCRIPT.format(root=ROOT, P=P, k=k, gate=gate, offloaded=offloaded, transport=transport,
+                         codec=codec)
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
                        timeout=300)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
