@@ -355,6 +355,9 @@ int infmoe_layer_h2d_bytes(infmoe_layer* layer, uint64_t* packed, uint64_t* raw)
  * be a positive multiple of 128. */
 int infmoe_codec_roundtrip(int32_t codec, const uint16_t* in, uint64_t n, uint16_t* out,
                            uint64_t* pack_bytes, int32_t device);
+/* the same round trip decoded by the host reference decoder (no GPU needed) */
+int infmoe_codec_roundtrip_host(int32_t codec, const uint16_t* in, uint64_t n, uint16_t* out,
+                                uint64_t* pack_bytes);
 
 #ifdef __cplusplus
 }

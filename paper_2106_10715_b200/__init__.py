@@ -195,6 +195,19 @@ _lib.infmoe_layer_pin_experts.argtypes = [_vp, _vp, _i32]
 _lib.infmoe_layer_pin_hottest.argtypes = [_vp, _i32, _vp]
 _lib.infmoe_layer_destroy.argtypes = [_vp]
 _lib.infmoe_codec_roundtrip.argtypes = [_i32, _vp, _u64, _vp, _vp, _i32]
+_lib.infmoe_codec_roundtrip_host.argtypes = [_i32, _vp, _u64, _vp, _vp]
+
+
+def codec_roundtrip_host(bits, codec: str = "exph"):
+    """Pack bf16 bit patterns with codec ("exp4" / "exph") and decode them with
+    the host reference decoder (no GPU): (decoded, pack bytes)."""
+    a = np.ascontiguousarray(bits, dtype=np.uint16)
+    out = np.empty_like(a)
+    nb = C.c_uint64(0)
+    _check(_lib.infmoe_codec_roundtrip_host({"exp4": 1, "exph": 2}[codec],
+                                            a.ctypes.data_as(_vp), a.size,
+                                            out.ctypes.data_as(_vp), C.byref(nb)))
+    return out, nb.value
 _lib.infmoe_layer_h2d_bytes.argtypes = [_vp, _vp, _vp]
 _lib.infmoe_slot_pool_create.argtypes = [_i32, _i32, _u64, _P(_vp)]
 _lib.infmoe_slot_pool_destroy.argtypes = [_vp]

@@ -299,6 +299,29 @@ int infmoe_layer_pin_hottest(infmoe_layer* layer, int32_t n, int32_t* pinned) {
   });
 }
 
+int infmoe_codec_roundtrip_host(int32_t codec_id, const uint16_t* in, uint64_t n, uint16_t* out,
+                                uint64_t* pack_bytes) {
+  return guarded([&] {
+    require(in && out, "codec_roundtrip_host: NULL argument");
+    require(codec_id == INFMOE_CODEC_EXP4 || codec_id == INFMOE_CODEC_EXPH,
+            "codec_roundtrip_host: unknown codec");
+    require(n > 0 && n % 128 == 0, "codec_roundtrip_host: n must be a positive multiple of 128");
+    std::vector<uint8_t> pk;
+    if (codec_id == INFMOE_CODEC_EXP4) {
+      const codec::Exp4Plan plan = codec::exp4_plan(in, n);
+      pk.resize(plan.bytes);
+      codec::exp4_fill(in, plan, pk.data());
+      codec::exp4_unpack_host(pk.data(), n, out);
+    } else {
+      const codec::ExphPlan plan = codec::exph_plan(in, n);
+      pk.resize(plan.L.bytes);
+      codec::exph_fill(in, plan, pk.data());
+      codec::exph_unpack_host(pk.data(), plan.L, out);
+    }
+    if (pack_bytes) *pack_bytes = pk.size();
+  });
+}
+
 int infmoe_layer_h2d_bytes(infmoe_layer* layer, uint64_t* packed, uint64_t* raw) {
   return guarded([&] {
     require(layer && layer->impl, "h2d_bytes: NULL layer");

@@ -1,0 +1,28 @@
+"""The exp4 / exph pack formats round-trip bit for bit through the host
+packer and the host reference decoder (CPU; the GPU decoders are checked
+against the same inputs in tests/test_gpu_codec.py)."""
+import numpy as np
+import pytest
+
+import paper_2106_10715_b200 as im
+
+
+@pytest.mark.parametrize("codec", ["exp4", "exph"])
+def test_host_roundtrip_all_patterns_and_weights(codec):
+    rng = np.random.default_rng(3)
+    a = np.tile(np.arange(1 << 16, dtype=np.uint16), 2)
+    rng.shuffle(a)
+    out, nb = im.codec_roundtrip_host(a, codec)
+    assert np.array_equal(out, a)
+    # uniform weights (the bench's distribution): 12 / ~10.3 bits per value
+    w = (rng.uniform(-0.027, 0.027, 1 << 18).astype(np.float32).view(np.uint32) >> 16
+         ).astype(np.uint16)
+    out, nb = im.codec_roundtrip_host(w, codec)
+    assert np.array_equal(out, w)
+    bits = 8.0 * nb / w.size
+    assert (11.9 < bits < 12.1) if codec == "exp4" else (10.0 < bits < 10.6), bits
+
+
+def test_host_roundtrip_rejects_bad_sizes():
+    with pytest.raises(im.InvalidArgument):
+        im.codec_roundtrip_host(np.zeros(100, np.uint16), "exph")
