@@ -5,7 +5,8 @@ size-independent properties plus a sampled oracle check:
   gating.hpp:87-104, compiled in oracle/_ref) for the C3 LSH layer, and against
   the oracle softmax/top-k gate for C5 (E=64, top-2, Zipf-skewed by a logit
   bias);
-* offloaded (K=4, InfMoE order) output bit-identical to the resident output;
+* offloaded (K=4, InfMoE order) output bit-identical to the resident output,
+  with the raw bf16 stream and with exph-packed weights;
 * executed order == the reference `auto_order` (scheduler.hpp:243) for the
   realised counts;
 * a sample of tokens (those routed to a few experts) against the fp64 oracle
@@ -91,10 +92,18 @@ def test_c3_layer_fullsize(cuda):
     res = dv.MoELayer(d, f, E, 1, wi, wo, gate="lsh", lsh_seed=seed, lsh_bits=5, max_tokens=N)
     off = dv.MoELayer(d, f, E, 1, hi, ho, gate="lsh", lsh_seed=seed, lsh_bits=5, offloaded=True,
                       K=K, max_tokens=N, hw=hw)
+    offh = dv.MoELayer(d, f, E, 1, hi, ho, gate="lsh", lsh_seed=seed, lsh_bits=5,
+                       offloaded=True, K=K, max_tokens=N, hw=hw, h2d_codec="exph")
     y_res, info_r = res.forward(x)
     y_off, info = off.forward(x)
+    y_offh, info_h = offh.forward(x)
     torch.cuda.synchronize()
     assert torch.equal(y_res.view(torch.int16), y_off.view(torch.int16))
+    # the exph-packed stream: same output bit for bit, same order, ~10.3 bits per weight
+    assert torch.equal(y_res.view(torch.int16), y_offh.view(torch.int16))
+    assert list(info_h["order"]) == list(info["order"])
+    assert offh.packed_bytes() < 0.66 * E * 2 * d * f * 2
+    offh.close()
     # routing counts == the reference's route_tokens on the fp64 promotion of x
     x_host = x.cpu()
     xd = bf16_bits_to_f32(_bits(x_host).reshape(-1)).astype(np.float64)
