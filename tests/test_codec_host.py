@@ -26,3 +26,21 @@ def test_host_roundtrip_all_patterns_and_weights(codec):
 def test_host_roundtrip_rejects_bad_sizes():
     with pytest.raises(im.InvalidArgument):
         im.codec_roundtrip_host(np.zeros(100, np.uint16), "exph")
+
+
+def test_exph_length_limit_fibonacci_histogram():
+    """Fibonacci symbol counts give the deepest Huffman tree (a 30-bit code
+    for 31 symbols); the encoder must clamp to 12 bits and keep the code
+    prefix-free, so the round trip stays exact."""
+    rng = np.random.default_rng(5)
+    fib = [1, 1]
+    while len(fib) < 31:
+        fib.append(fib[-1] + fib[-2])
+    deltas = np.concatenate([np.full(c, i) for i, c in enumerate(fib[::-1][:26])])
+    rng.shuffle(deltas)
+    n = (deltas.size // 128) * 128
+    exps = (200 - deltas[:n]).astype(np.uint16)
+    a = (exps << 7) | rng.integers(0, 128, n, dtype=np.uint16) | \
+        (rng.integers(0, 2, n, dtype=np.uint16) << 15)
+    out, nb = im.codec_roundtrip_host(a, "exph")
+    assert np.array_equal(out, a)
