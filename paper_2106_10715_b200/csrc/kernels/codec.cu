@@ -410,9 +410,10 @@ void exph_unpack_host(const uint8_t* pack, const ExphLayout& L, uint16_t* out) {
 }
 
 void launch_exph_unpack(const uint8_t* pack, const ExphLayout& L, uint16_t* out, cudaStream_t s) {
+  // one chunk per thread in a single wave of blocks (a capped grid left ~8% of
+  // the threads a second chunk, doubling the kernel time)
   const uint64_t want = (L.nchunks + 255) / 256;
-  const unsigned grid = unsigned(std::min<uint64_t>(want, uint64_t(device_sm_count()) * 8));
-  exph_unpack_kernel<<<std::max(1u, grid), 256, 0, s>>>(pack, L, out);
+  exph_unpack_kernel<<<unsigned(std::max<uint64_t>(want, 1)), 256, 0, s>>>(pack, L, out);
   INFMOE_LAUNCH_CHECK();
 }
 
