@@ -21,6 +21,7 @@ from paper_2106_10715_b200 import device as dv  # noqa: E402
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--layers", type=int, default=4)
+    ap.add_argument("--codec", default="raw", choices=["raw", "exp4", "exph"])
     a = ap.parse_args()
     d, f, E, N = 4096, 10240, 32, 4096
     bf = torch.bfloat16
@@ -37,7 +38,8 @@ def main():
     x = torch.empty((N, d), dtype=bf, device=dev)
     dv.fill_uniform(x, 3, math.sqrt(3.0))
     layers = [dv.MoELayer(d, f, E, 1, hi, ho, gate="lsh", lsh_seed=100 + l, lsh_bits=5,
-                          offloaded=True, K=4, max_tokens=N) for l in range(a.layers)]
+                          offloaded=True, K=4, max_tokens=N, h2d_codec=a.codec)
+              for l in range(a.layers)]
     bufs = [torch.empty_like(x) for _ in range(2)]
     for rep in range(2):
         cur = x
@@ -52,7 +54,7 @@ def main():
         t1.record()
         torch.cuda.synchronize()
     total = t0.elapsed_time(t1)
-    nbytes = 2 * d * f * 2
+    nbytes = layers[0].packed_bytes() / E  # bytes per expert load over the link
     for l, info in enumerate(infos):
         loads = sorted([(s0, s1) for st, _, _, s0, s1 in info["events"] if st == 0])
         comps = [(s0, s1) for st, _, _, s0, s1 in info["events"] if st == 1]
