@@ -221,7 +221,10 @@ __global__ void __launch_bounds__(256) exph_unpack_kernel(const uint8_t* __restr
   for (int i = threadIdx.x; i < (1 << kExphMaxLen) / 8; i += blockDim.x)
     reinterpret_cast<uint4*>(lut)[i] = __ldg(glut + i);
   __syncthreads();
-  const auto* words = reinterpret_cast<const uint32_t*>(pack + L.off_bits);
+  // the bitstream is read 16 bytes at a time with the next 16 bytes already in
+  // flight (a thread's chunk is ~300 bits; word-at-a-time loads missed L1 and
+  // left every refill waiting on L2), the sign/mantissa bytes one step ahead
+  const auto* bw = reinterpret_cast<const uint4*>(pack + L.off_bits);
   const auto* gbit = reinterpret_cast<const uint32_t*>(pack + L.off_group);
   const auto* cbit = reinterpret_cast<const uint16_t*>(pack + L.off_chunk);
   for (uint64_t c = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; c < L.nchunks;
@@ -229,21 +232,34 @@ __global__ void __launch_bounds__(256) exph_unpack_kernel(const uint8_t* __restr
     const uint64_t v0 = c * kExphChunk;
     const uint32_t base = pack[L.off_base + v0 / kExp4Block];
     const uint32_t p = __ldg(gbit + c / kExphGroup) + __ldg(cbit + c);
-    const uint32_t* wp = words + (p >> 5);
-    uint64_t buf = ((uint64_t(__ldg(wp)) << 32) | __ldg(wp + 1)) << (p & 31);
+    uint32_t bi = p >> 7;
+    uint4 cur = __ldg(bw + bi), nxt = __ldg(bw + bi + 1);
+    int qi = int(p >> 5) & 3;
+    auto take = [&]() -> uint32_t {
+      const uint32_t w = qi == 0 ? cur.x : qi == 1 ? cur.y : qi == 2 ? cur.z : cur.w;
+      if (++qi == 4) {
+        qi = 0;
+        cur = nxt;
+        nxt = __ldg(bw + (++bi) + 1);
+      }
+      return w;
+    };
+    uint64_t buf = uint64_t(take()) << 32;
+    buf = (buf | take()) << (p & 31);
     int nbits = 64 - int(p & 31);
-    wp += 2;
     const uint4* smv = reinterpret_cast<const uint4*>(pack + v0);
     uint4* dst = reinterpret_cast<uint4*>(out + v0);
+    uint4 s_next = __ldg(smv);
 #pragma unroll 1
     for (int q = 0; q < kExphChunk / 16; ++q) {
-      const uint4 s4 = __ldg(smv + q);
+      const uint4 s4 = s_next;
+      if (q + 1 < kExphChunk / 16) s_next = __ldg(smv + q + 1);
       const uint32_t sw[4] = {s4.x, s4.y, s4.z, s4.w};
       uint32_t r[8];
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         if (nbits < 32) {
-          buf |= uint64_t(__ldg(wp++)) << (32 - nbits);
+          buf |= uint64_t(take()) << (32 - nbits);
           nbits += 32;
         }
         const uint32_t ent = lut[uint32_t(buf >> (64 - kExphMaxLen))];
@@ -320,7 +336,7 @@ ExphPlan exph_plan(const uint16_t* in, uint64_t n) {
   require(total < (uint64_t(1) << 32) - 64, "exph: bitstream exceeds 2^32 bits");
   p.chunk_bit[L.nchunks] = uint32_t(total);
   L.off_bits = align16(n);
-  L.off_group = align16(L.off_bits + (total + 31) / 32 * 4 + 8);
+  L.off_group = align16(L.off_bits + (total + 31) / 32 * 4 + 32);  // reader runs 32 B ahead
   L.off_chunk = align16(L.off_group + 4 * L.ngroups);
   L.off_base = align16(L.off_chunk + 2 * L.nchunks);
   L.off_lut = align16(L.off_base + L.nblocks);
