@@ -216,9 +216,9 @@ void canonical_codes(const uint8_t* len, uint32_t* code) {
 
 __global__ void __launch_bounds__(256) exph_unpack_kernel(const uint8_t* __restrict__ pack,
                                                           ExphLayout L, uint16_t* __restrict__ out) {
-  __shared__ uint16_t lut[1 << kExphMaxLen];
+  __shared__ uint32_t lut[1 << kExphMaxLen];
   const auto* glut = reinterpret_cast<const uint4*>(pack + L.off_lut);
-  for (int i = threadIdx.x; i < (1 << kExphMaxLen) / 8; i += blockDim.x)
+  for (int i = threadIdx.x; i < (1 << kExphMaxLen) / 4; i += blockDim.x)
     reinterpret_cast<uint4*>(lut)[i] = __ldg(glut + i);
   __syncthreads();
   // the bitstream is read 16 bytes at a time with the next 16 bytes already in
@@ -256,28 +256,45 @@ __global__ void __launch_bounds__(256) exph_unpack_kernel(const uint8_t* __restr
       if (q + 1 < kExphChunk / 16) s_next = __ldg(smv + q + 1);
       const uint32_t sw[4] = {s4.x, s4.y, s4.z, s4.w};
       uint32_t r[8];
+      // one symbol: its code (+ 8 raw exponent bits for the escape)
+      auto one = [&](uint32_t ent) -> uint32_t {
+        const uint32_t sym = (ent >> 4) & 31u, ln = ent & 15u;
+        buf <<= ln;
+        nbits -= int(ln);
+        if (sym == uint32_t(kExphEsc)) {
+          const uint32_t e = uint32_t(buf >> 56);
+          buf <<= 8;
+          nbits -= 8;
+          return e;
+        }
+        return (base - sym) & 0xFFu;
+      };
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
+      for (int jp = 0; jp < 8; ++jp) {  // values in pairs: one table lookup per pair
         if (nbits < 32) {
           buf |= uint64_t(take()) << (32 - nbits);
           nbits += 32;
         }
         const uint32_t ent = lut[uint32_t(buf >> (64 - kExphMaxLen))];
-        const uint32_t sym = ent >> 4, ln = ent & 15u;
-        buf <<= ln;
-        nbits -= int(ln);
-        uint32_t e;
-        if (sym == uint32_t(kExphEsc)) {
-          e = uint32_t(buf >> 56);
-          buf <<= 8;
-          nbits -= 8;
-        } else {
-          e = (base - sym) & 0xFFu;
+        uint32_t e0, e1;
+        if (ent & (1u << 19)) {  // both codes inside the 12-bit window
+          const uint32_t ln = (ent >> 14) & 31u;
+          buf <<= ln;
+          nbits -= int(ln);
+          e0 = (base - ((ent >> 4) & 31u)) & 0xFFu;
+          e1 = (base - ((ent >> 9) & 31u)) & 0xFFu;
+        } else {  // a long code or an escape: the two values one at a time
+          e0 = one(ent);
+          if (nbits < 32) {
+            buf |= uint64_t(take()) << (32 - nbits);
+            nbits += 32;
+          }
+          e1 = one(lut[uint32_t(buf >> (64 - kExphMaxLen))]);
         }
-        const uint32_t smb = (sw[j / 4] >> (8 * (j % 4))) & 0xFFu;
-        const uint32_t v = ((smb & 0x80u) << 8) | (e << 7) | (smb & 0x7Fu);
-        if (j % 2 == 0) r[j / 2] = v;
-        else r[j / 2] |= v << 16;
+        const uint32_t s0 = (sw[jp / 2] >> (16 * (jp % 2))) & 0xFFu;
+        const uint32_t s1 = (sw[jp / 2] >> (16 * (jp % 2) + 8)) & 0xFFu;
+        r[jp] = (((s0 & 0x80u) << 8) | (e0 << 7) | (s0 & 0x7Fu)) |
+                ((((s1 & 0x80u) << 8) | (e1 << 7) | (s1 & 0x7Fu)) << 16);
       }
       dst[2 * q] = make_uint4(r[0], r[1], r[2], r[3]);
       dst[2 * q + 1] = make_uint4(r[4], r[5], r[6], r[7]);
@@ -340,7 +357,7 @@ ExphPlan exph_plan(const uint16_t* in, uint64_t n) {
   L.off_chunk = align16(L.off_group + 4 * L.ngroups);
   L.off_base = align16(L.off_chunk + 2 * L.nchunks);
   L.off_lut = align16(L.off_base + L.nblocks);
-  L.bytes = align16(L.off_lut + 2 * (1 << kExphMaxLen));
+  L.bytes = align16(L.off_lut + 4 * (1 << kExphMaxLen));
   return p;
 }
 
@@ -389,13 +406,27 @@ void exph_fill(const uint16_t* in, const ExphPlan& p, uint8_t* out) {
     cb[c] = uint16_t(p.chunk_bit[c] - p.chunk_bit[c - c % kExphGroup]);
   }
   std::copy(p.base.begin(), p.base.end(), out + L.off_base);
-  auto* lut = reinterpret_cast<uint16_t*>(out + L.off_lut);
+  // LUT entry per 12-bit window: len0 | sym0 << 4 | sym1 << 9 | (len0 + len1) << 14 |
+  // two << 19; "two" when a second non-escape code also fits inside the window
+  std::vector<uint32_t> one(1u << kExphMaxLen, 0);
   for (int sym = 0; sym < 32; ++sym) {
     const uint32_t l = p.len[sym];
     if (!l) continue;
     const uint32_t first = p.code[sym] << (kExphMaxLen - l);
-    for (uint32_t s = 0; s < (1u << (kExphMaxLen - l)); ++s)
-      lut[first | s] = uint16_t((sym << 4) | l);
+    for (uint32_t s = 0; s < (1u << (kExphMaxLen - l)); ++s) one[first | s] = (uint32_t(sym) << 4) | l;
+  }
+  auto* lut = reinterpret_cast<uint32_t*>(out + L.off_lut);
+  const uint32_t mask = (1u << kExphMaxLen) - 1;
+  for (uint32_t w = 0; w <= mask; ++w) {
+    uint32_t ent = one[w];
+    const uint32_t l0 = ent & 15u, s0 = (ent >> 4) & 31u;
+    if (l0 && l0 < uint32_t(kExphMaxLen) && s0 != uint32_t(kExphEsc)) {
+      const uint32_t e1 = one[(w << l0) & mask];
+      const uint32_t l1 = e1 & 15u, s1 = (e1 >> 4) & 31u;
+      if (l1 && l0 + l1 <= uint32_t(kExphMaxLen) && s1 != uint32_t(kExphEsc))
+        ent |= (s1 << 9) | ((l0 + l1) << 14) | (1u << 19);
+    }
+    lut[w] = ent;
   }
 }
 
@@ -403,7 +434,7 @@ void exph_unpack_host(const uint8_t* pack, const ExphLayout& L, uint16_t* out) {
   const auto* words = reinterpret_cast<const uint32_t*>(pack + L.off_bits);
   const auto* gbit = reinterpret_cast<const uint32_t*>(pack + L.off_group);
   const auto* cbit = reinterpret_cast<const uint16_t*>(pack + L.off_chunk);
-  const auto* lut = reinterpret_cast<const uint16_t*>(pack + L.off_lut);
+  const auto* lut = reinterpret_cast<const uint32_t*>(pack + L.off_lut);
   auto bit = [&](uint64_t q) { return (words[q >> 5] >> (31 - (q & 31))) & 1u; };
   for (uint64_t c = 0; c < L.nchunks; ++c) {
     uint64_t q = uint64_t(gbit[c / kExphGroup]) + cbit[c];
@@ -411,7 +442,7 @@ void exph_unpack_host(const uint8_t* pack, const ExphLayout& L, uint16_t* out) {
     for (uint64_t i = c * kExphChunk; i < (c + 1) * kExphChunk; ++i) {
       uint32_t peek = 0;
       for (int k = 0; k < kExphMaxLen; ++k) peek = (peek << 1) | bit(q + k);
-      const uint32_t sym = lut[peek] >> 4, ln = lut[peek] & 15u;
+      const uint32_t sym = (lut[peek] >> 4) & 31u, ln = lut[peek] & 15u;
       q += ln;
       uint32_t e = (base - sym) & 0xFFu;
       if (sym == uint32_t(kExphEsc)) {

@@ -77,8 +77,9 @@ void launch_exp4_unpack(const uint8_t* pack, uint64_t n, uint16_t* out, cudaStre
 //
 // Layout: [0, n) sign/mantissa | [off_bits) bitstream (uint32 words, + 8 B
 // slack) | [off_group) uint32 start bit per group | [off_chunk) uint16 offset
-// per chunk | [off_base) base per block | [off_lut) uint16 LUT[4096] =
-// symbol << 4 | code length
+// per chunk | [off_base) base per block | [off_lut) uint32 LUT[4096] = len0 |
+// sym0 << 4 | sym1 << 9 | (len0 + len1) << 14 | two << 19 (the decoder takes two
+// values per lookup when both codes fit in the 12-bit window)
 constexpr int kExphChunk = 128;
 constexpr int kExphGroup = 16;  // chunks per group (<= 16 x 128 x 20 bits < 2^16)
 constexpr int kExphMaxLen = 12;

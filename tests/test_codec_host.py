@@ -15,7 +15,7 @@ def test_host_roundtrip_all_patterns_and_weights(codec):
     out, nb = im.codec_roundtrip_host(a, codec)
     assert np.array_equal(out, a)
     # uniform weights (the bench's distribution): 12 / ~10.3 bits per value
-    w = (rng.uniform(-0.027, 0.027, 1 << 18).astype(np.float32).view(np.uint32) >> 16
+    w = (rng.uniform(-0.027, 0.027, 1 << 21).astype(np.float32).view(np.uint32) >> 16
          ).astype(np.uint16)
     out, nb = im.codec_roundtrip_host(w, codec)
     assert np.array_equal(out, w)
