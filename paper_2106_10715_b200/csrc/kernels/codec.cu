@@ -221,9 +221,9 @@ __global__ void __launch_bounds__(256) exph_unpack_kernel(const uint8_t* __restr
   for (int i = threadIdx.x; i < (1 << kExphMaxLen) / 4; i += blockDim.x)
     reinterpret_cast<uint4*>(lut)[i] = __ldg(glut + i);
   __syncthreads();
-  // the bitstream is read 16 bytes at a time with the next 16 bytes already in
-  // flight (a thread's chunk is ~300 bits; word-at-a-time loads missed L1 and
-  // left every refill waiting on L2), the sign/mantissa bytes one step ahead
+  // a thread's chunk is ~300 bits that L1 does not keep between refills, so
+  // the next bitstream word and the next 16 sign/mantissa bytes are always in
+  // flight before they are needed
   const auto* bw = reinterpret_cast<const uint4*>(pack + L.off_bits);
   const auto* gbit = reinterpret_cast<const uint32_t*>(pack + L.off_group);
   const auto* cbit = reinterpret_cast<const uint16_t*>(pack + L.off_chunk);
@@ -232,21 +232,18 @@ __global__ void __launch_bounds__(256) exph_unpack_kernel(const uint8_t* __restr
     const uint64_t v0 = c * kExphChunk;
     const uint32_t base = pack[L.off_base + v0 / kExp4Block];
     const uint32_t p = __ldg(gbit + c / kExphGroup) + __ldg(cbit + c);
-    uint32_t bi = p >> 7;
-    uint4 cur = __ldg(bw + bi), nxt = __ldg(bw + bi + 1);
-    int qi = int(p >> 5) & 3;
+    // 32-bit refills with the next word always in flight (one refill ahead:
+    // ~14 values of decode cover its L2 latency; no dynamic register select)
+    const uint32_t* wp = reinterpret_cast<const uint32_t*>(bw) + (p >> 5);
+    uint64_t buf = ((uint64_t(__ldg(wp)) << 32) | __ldg(wp + 1)) << (p & 31);
+    int nbits = 64 - int(p & 31);
+    wp += 2;
+    uint32_t nw = __ldg(wp);
     auto take = [&]() -> uint32_t {
-      const uint32_t w = qi == 0 ? cur.x : qi == 1 ? cur.y : qi == 2 ? cur.z : cur.w;
-      if (++qi == 4) {
-        qi = 0;
-        cur = nxt;
-        nxt = __ldg(bw + (++bi) + 1);
-      }
+      const uint32_t w = nw;
+      nw = __ldg(++wp);
       return w;
     };
-    uint64_t buf = uint64_t(take()) << 32;
-    buf = (buf | take()) << (p & 31);
-    int nbits = 64 - int(p & 31);
     const uint4* smv = reinterpret_cast<const uint4*>(pack + v0);
     uint4* dst = reinterpret_cast<uint4*>(out + v0);
     uint4 s_next = __ldg(smv);
