@@ -214,46 +214,49 @@ void canonical_codes(const uint8_t* len, uint32_t* code) {
   }
 }
 
-__global__ void __launch_bounds__(256) exph_unpack_kernel(const uint8_t* __restrict__ pack,
-                                                          ExphLayout L, uint16_t* __restrict__ out) {
+// One warp decodes 32 consecutive chunks, one per lane (Huffman codes are
+// sequential within a chunk).  The sign/mantissa bytes are stored
+// lane-interleaved per 16-value group (exph_sm_offset), so each group load is
+// one contiguous 512-byte warp access; each half of a lane's 256 output bytes
+// is staged in shared memory (16-byte slots XOR-swizzled by row) and written
+// back as full 128-byte lines.  Only the bitstream refills stay per lane (one
+// word ahead).
+constexpr int kExphWarps = 8;
+__global__ void __launch_bounds__(kExphWarps * 32) exph_unpack_kernel(const uint8_t* __restrict__ pack,
+                                                                      ExphLayout L,
+                                                                      uint16_t* __restrict__ out) {
   __shared__ uint32_t lut[1 << kExphMaxLen];
+  extern __shared__ uint4 stage[];  // [kExphWarps][kExphWarpChunks * 8]: 4 KB per warp
   const auto* glut = reinterpret_cast<const uint4*>(pack + L.off_lut);
   for (int i = threadIdx.x; i < (1 << kExphMaxLen) / 4; i += blockDim.x)
     reinterpret_cast<uint4*>(lut)[i] = __ldg(glut + i);
   __syncthreads();
-  // a thread's chunk is ~300 bits that L1 does not keep between refills, so
-  // the next bitstream word and the next 16 sign/mantissa bytes are always in
-  // flight before they are needed
-  const auto* bw = reinterpret_cast<const uint4*>(pack + L.off_bits);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  uint4* st = stage + warp * (kExphWarpChunks * 8);
+  const auto* bw = reinterpret_cast<const uint32_t*>(pack + L.off_bits);
   const auto* gbit = reinterpret_cast<const uint32_t*>(pack + L.off_group);
   const auto* cbit = reinterpret_cast<const uint16_t*>(pack + L.off_chunk);
-  for (uint64_t c = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; c < L.nchunks;
-       c += uint64_t(gridDim.x) * blockDim.x) {
-    const uint64_t v0 = c * kExphChunk;
-    const uint32_t base = pack[L.off_base + v0 / kExp4Block];
-    const uint32_t p = __ldg(gbit + c / kExphGroup) + __ldg(cbit + c);
-    // 32-bit refills with the next word always in flight (one refill ahead:
-    // ~14 values of decode cover its L2 latency; no dynamic register select)
-    const uint32_t* wp = reinterpret_cast<const uint32_t*>(bw) + (p >> 5);
-    uint64_t buf = ((uint64_t(__ldg(wp)) << 32) | __ldg(wp + 1)) << (p & 31);
-    int nbits = 64 - int(p & 31);
-    wp += 2;
-    uint32_t nw = __ldg(wp);
-    auto take = [&]() -> uint32_t {
-      const uint32_t w = nw;
-      nw = __ldg(++wp);
-      return w;
-    };
-    const uint4* smv = reinterpret_cast<const uint4*>(pack + v0);
-    uint4* dst = reinterpret_cast<uint4*>(out + v0);
-    uint4 s_next = __ldg(smv);
-#pragma unroll 1
-    for (int q = 0; q < kExphChunk / 16; ++q) {
-      const uint4 s4 = s_next;
-      if (q + 1 < kExphChunk / 16) s_next = __ldg(smv + q + 1);
-      const uint32_t sw[4] = {s4.x, s4.y, s4.z, s4.w};
-      uint32_t r[8];
-      // one symbol: its code (+ 8 raw exponent bits for the escape)
+  const uint64_t ngroups = (L.nchunks + kExphWarpChunks - 1) / kExphWarpChunks;
+  for (uint64_t g = uint64_t(blockIdx.x) * kExphWarps + warp; g < ngroups;
+       g += uint64_t(gridDim.x) * kExphWarps) {
+    const uint64_t c0 = g * kExphWarpChunks;
+    const int nch = int(min(uint64_t(kExphWarpChunks), L.nchunks - c0));
+    const unsigned active = nch == 32 ? 0xffffffffu : ((1u << nch) - 1u);
+    if (lane < nch) {
+      const uint64_t c = c0 + lane;
+      const uint64_t v0 = c * kExphChunk;
+      const uint32_t base = pack[L.off_base + v0 / kExp4Block];
+      const uint32_t p = __ldg(gbit + c / kExphGroup) + __ldg(cbit + c);
+      const uint32_t* wp = bw + (p >> 5);
+      uint64_t buf = ((uint64_t(__ldg(wp)) << 32) | __ldg(wp + 1)) << (p & 31);
+      int nbits = 64 - int(p & 31);
+      wp += 2;
+      uint32_t nw = __ldg(wp);
+      auto take = [&]() -> uint32_t {
+        const uint32_t w = nw;
+        nw = __ldg(++wp);
+        return w;
+      };
       auto one = [&](uint32_t ent) -> uint32_t {
         const uint32_t sym = (ent >> 4) & 31u, ln = ent & 15u;
         buf <<= ln;
@@ -266,35 +269,57 @@ __global__ void __launch_bounds__(256) exph_unpack_kernel(const uint8_t* __restr
         }
         return (base - sym) & 0xFFu;
       };
+      const uint8_t* smg = pack + c0 * kExphChunk + uint64_t(lane) * 16;
+      const uint64_t qstride = uint64_t(nch) * 16;
+      uint4 s_next = __ldg(reinterpret_cast<const uint4*>(smg));
+#pragma unroll 1
+      for (int q = 0; q < kExphChunk / 16; ++q) {
+        const uint4 s4 = s_next;
+        if (q + 1 < kExphChunk / 16)
+          s_next = __ldg(reinterpret_cast<const uint4*>(smg + uint64_t(q + 1) * qstride));
+        const uint32_t sw[4] = {s4.x, s4.y, s4.z, s4.w};
+        uint32_t r[8];
 #pragma unroll
-      for (int jp = 0; jp < 8; ++jp) {  // values in pairs: one table lookup per pair
-        if (nbits < 32) {
-          buf |= uint64_t(take()) << (32 - nbits);
-          nbits += 32;
-        }
-        const uint32_t ent = lut[uint32_t(buf >> (64 - kExphMaxLen))];
-        uint32_t e0, e1;
-        if (ent & (1u << 19)) {  // both codes inside the 12-bit window
-          const uint32_t ln = (ent >> 14) & 31u;
-          buf <<= ln;
-          nbits -= int(ln);
-          e0 = (base - ((ent >> 4) & 31u)) & 0xFFu;
-          e1 = (base - ((ent >> 9) & 31u)) & 0xFFu;
-        } else {  // a long code or an escape: the two values one at a time
-          e0 = one(ent);
+        for (int jp = 0; jp < 8; ++jp) {  // values in pairs: one table lookup per pair
           if (nbits < 32) {
             buf |= uint64_t(take()) << (32 - nbits);
             nbits += 32;
           }
-          e1 = one(lut[uint32_t(buf >> (64 - kExphMaxLen))]);
+          const uint32_t ent = lut[uint32_t(buf >> (64 - kExphMaxLen))];
+          uint32_t e0, e1;
+          if (ent & (1u << 19)) {  // both codes inside the 12-bit window
+            const uint32_t ln = (ent >> 14) & 31u;
+            buf <<= ln;
+            nbits -= int(ln);
+            e0 = (base - ((ent >> 4) & 31u)) & 0xFFu;
+            e1 = (base - ((ent >> 9) & 31u)) & 0xFFu;
+          } else {  // a long code or an escape: the two values one at a time
+            e0 = one(ent);
+            if (nbits < 32) {
+              buf |= uint64_t(take()) << (32 - nbits);
+              nbits += 32;
+            }
+            e1 = one(lut[uint32_t(buf >> (64 - kExphMaxLen))]);
+          }
+          const uint32_t s0 = (sw[jp / 2] >> (16 * (jp % 2))) & 0xFFu;
+          const uint32_t s1 = (sw[jp / 2] >> (16 * (jp % 2) + 8)) & 0xFFu;
+          r[jp] = (((s0 & 0x80u) << 8) | (e0 << 7) | (s0 & 0x7Fu)) |
+                  ((((s1 & 0x80u) << 8) | (e1 << 7) | (s1 & 0x7Fu)) << 16);
         }
-        const uint32_t s0 = (sw[jp / 2] >> (16 * (jp % 2))) & 0xFFu;
-        const uint32_t s1 = (sw[jp / 2] >> (16 * (jp % 2) + 8)) & 0xFFu;
-        r[jp] = (((s0 & 0x80u) << 8) | (e0 << 7) | (s0 & 0x7Fu)) |
-                ((((s1 & 0x80u) << 8) | (e1 << 7) | (s1 & 0x7Fu)) << 16);
+        // row = lane (the current half of its chunk: 8 16-byte slots), swizzled
+        const int sl = 2 * (q % 4);
+        st[lane * 8 + (sl ^ (lane & 7))] = make_uint4(r[0], r[1], r[2], r[3]);
+        st[lane * 8 + ((sl + 1) ^ (lane & 7))] = make_uint4(r[4], r[5], r[6], r[7]);
+        if (q % 4 == 3) {  // flush this half: 4 full 128-byte lines per warp store
+          __syncwarp(active);
+          uint4* dst = reinterpret_cast<uint4*>(out + c0 * kExphChunk);
+          for (int u = lane; u < nch * 8; u += nch) {
+            const int row = u / 8, slot = u % 8;
+            dst[row * 16 + (q / 4) * 8 + slot] = st[row * 8 + (slot ^ (row & 7))];
+          }
+          __syncwarp(active);
+        }
       }
-      dst[2 * q] = make_uint4(r[0], r[1], r[2], r[3]);
-      dst[2 * q + 1] = make_uint4(r[4], r[5], r[6], r[7]);
     }
   }
 }
@@ -381,7 +406,8 @@ void exph_fill(const uint16_t* in, const ExphPlan& p, uint8_t* out) {
     };
     for (uint64_t i = c * kExphChunk; i < (c + 1) * kExphChunk; ++i) {
       const uint16_t v = in[i];
-      out[i] = uint8_t(((v >> 8) & 0x80u) | (v & 0x7Fu));
+      const uint32_t k = uint32_t(i - c * kExphChunk);
+      out[exph_sm_offset(c, k / 16, L.nchunks) + k % 16] = uint8_t(((v >> 8) & 0x80u) | (v & 0x7Fu));
       const uint32_t sym = exph_sym(v, base);
       put(p.code[sym], p.len[sym]);
       if (sym == uint32_t(kExphEsc)) put((v >> 7) & 0xFFu, 8);
@@ -447,17 +473,26 @@ void exph_unpack_host(const uint8_t* pack, const ExphLayout& L, uint16_t* out) {
         for (int k = 0; k < 8; ++k) e = (e << 1) | bit(q + k);
         q += 8;
       }
-      const uint32_t smb = pack[i];
+      const uint32_t k = uint32_t(i - c * kExphChunk);
+      const uint32_t smb = pack[exph_sm_offset(c, k / 16, L.nchunks) + k % 16];
       out[i] = uint16_t(((smb & 0x80u) << 8) | (e << 7) | (smb & 0x7Fu));
     }
   }
 }
 
 void launch_exph_unpack(const uint8_t* pack, const ExphLayout& L, uint16_t* out, cudaStream_t s) {
-  // one chunk per thread in a single wave of blocks (a capped grid left ~8% of
-  // the threads a second chunk, doubling the kernel time)
-  const uint64_t want = (L.nchunks + 255) / 256;
-  exph_unpack_kernel<<<unsigned(std::max<uint64_t>(want, 1)), 256, 0, s>>>(pack, L, out);
+  const uint64_t groups = (L.nchunks + kExphWarpChunks - 1) / kExphWarpChunks;
+  const uint64_t want = (groups + kExphWarps - 1) / kExphWarps;
+  const uint64_t cap = uint64_t(device_sm_count()) * 4;  // 4 CTAs (48 KB smem each) per SM
+  constexpr int kStage = kExphWarps * kExphWarpChunks * 8 * 16;
+  static bool configured = false;
+  if (!configured) {
+    INFMOE_CUDA(cudaFuncSetAttribute(exph_unpack_kernel,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, kStage));
+    configured = true;
+  }
+  exph_unpack_kernel<<<unsigned(std::max<uint64_t>(std::min(want, cap), 1)), kExphWarps * 32,
+                       kStage, s>>>(pack, L, out);
   INFMOE_LAUNCH_CHECK();
 }
 

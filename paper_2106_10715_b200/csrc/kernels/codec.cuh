@@ -75,12 +75,24 @@ void launch_exp4_unpack(const uint8_t* pack, uint64_t n, uint16_t* out, cudaStre
 // decodes one chunk through a 4096-entry lookup table in shared memory.  ~2.1
 // bits of exponent for the bench's weights (entropy 2.14): ~10.3 bits/value.
 //
-// Layout: [0, n) sign/mantissa | [off_bits) bitstream (uint32 words, + 8 B
+// Layout: [0, n) sign/mantissa (lane-interleaved, exph_sm_offset) | [off_bits) bitstream (uint32 words, + 8 B
 // slack) | [off_group) uint32 start bit per group | [off_chunk) uint16 offset
 // per chunk | [off_base) base per block | [off_lut) uint32 LUT[4096] = len0 |
 // sym0 << 4 | sym1 << 9 | (len0 + len1) << 14 | two << 19 (the decoder takes two
 // values per lookup when both codes fit in the 12-bit window)
 constexpr int kExphChunk = 128;
+constexpr int kExphWarpChunks = 32;  // chunks decoded together by one warp (one per lane)
+
+// byte offset of the 16 sign/mantissa bytes of chunk c's 16-value group q: the
+// chunks of a warp group are interleaved per 16-byte group, so one warp-wide
+// load of group q reads contiguous memory
+__host__ __device__ inline uint64_t exph_sm_offset(uint64_t c, uint32_t q, uint64_t nchunks) {
+  const uint64_t g = c / kExphWarpChunks, lane = c % kExphWarpChunks;
+  const uint64_t first = g * kExphWarpChunks;
+  const uint64_t nch = (nchunks - first) < uint64_t(kExphWarpChunks) ? (nchunks - first)
+                                                                      : uint64_t(kExphWarpChunks);
+  return first * kExphChunk + uint64_t(q) * nch * 16 + lane * 16;
+}
 constexpr int kExphGroup = 16;  // chunks per group (<= 16 x 128 x 20 bits < 2^16)
 constexpr int kExphMaxLen = 12;
 constexpr int kExphEsc = 31;
