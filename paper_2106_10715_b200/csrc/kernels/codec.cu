@@ -321,6 +321,7 @@ __global__ void __launch_bounds__(kExphWarps * 32) exph_unpack_kernel(const uint
         }
       }
     }
+    __syncwarp();  // every lane is done with st before the next group reuses it
   }
 }
 
