@@ -1,6 +1,8 @@
-// codec.cu — exp4 lossless bf16 packing: host packer (threads over blocks) and
-// the device decoder the offload executor runs between an expert's H2D copy
-// and its FFN.  Format: codec.cuh.
+// codec.cu — lossless bf16 weight packing for the host link (exp4: 4-bit
+// exponent codes; exph: canonical-Huffman exponent codes): host packers
+// (threads over blocks / chunks), host reference decoders (tests), and the
+// device decoders the offload executor runs between an expert's H2D copy and
+// its FFN.  Formats: codec.cuh.
 #include "codec.cuh"
 
 #include <algorithm>

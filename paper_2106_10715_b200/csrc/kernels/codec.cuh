@@ -1,4 +1,5 @@
-// codec.cuh — lossless "exp4" packing of bf16 expert weights for the host link.
+// codec.cuh — lossless packing of bf16 expert weights for the host link
+// ("exp4" below, and the entropy-coded "exph" further down).
 //
 // The offloaded executor is host-link-bound (C3/C5 stream every
 // expert over PCIe each pass), so the bytes per expert ARE the step time.  A
