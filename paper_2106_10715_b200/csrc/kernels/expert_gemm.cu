@@ -23,6 +23,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -426,7 +427,7 @@ template <bool kTF32, bool kGelu, int TOK, int STAGES>
 void launch_impl(const GroupedGemmArgs& a, cudaStream_t stream) {
   using C = Cfg<TOK, STAGES>;
   auto kern = grouped_gemm_kernel<kTF32, kGelu, TOK, STAGES>;
-  static bool configured = false;
+  static std::atomic<bool> configured{false};  // idempotent, race-free flag
   if (!configured) {
     INFMOE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      int(C::SMEM_BYTES)));
@@ -834,7 +835,7 @@ template <int TOK, int STAGES>
 void fused_launch(const FusedFfnArgs& a, cudaStream_t stream) {
   using C = Cfg<TOK, STAGES>;
   auto kern = fused_ffn_kernel<TOK, STAGES>;
-  static bool configured = false;
+  static std::atomic<bool> configured{false};  // idempotent, race-free flag
   if (!configured) {
     INFMOE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      int(C::SMEM_BYTES)));
@@ -1204,7 +1205,7 @@ template <int TOK, int STAGES>
 void fused_pair_launch(const FusedFfnArgs& a, cudaStream_t stream) {
   using C = PairCfg<TOK, STAGES>;
   auto kern = fused_ffn_pair_kernel<TOK, STAGES>;
-  static bool configured = false;
+  static std::atomic<bool> configured{false};  // idempotent, race-free flag
   if (!configured) {
     INFMOE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      int(C::SMEM_BYTES)));

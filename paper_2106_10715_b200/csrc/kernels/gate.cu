@@ -10,6 +10,7 @@
 // x and the gate weights are staged through shared memory in d-chunks so the
 // weight matrix is read once per CTA of tokens, not once per token.
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdlib>
 
@@ -560,7 +561,7 @@ void lsh_fast_go(const void* x, int64_t N, int d, const double* proj, int bits, 
   static const int force = lsh_env("INFMOE_LSH_FORCE_EXACT", 0);
   using C = LshFastCfg<T, BMAX>;
   auto kern = gate_lsh_fast_kernel<T, BMAX>;
-  static bool configured = false;
+  static std::atomic<bool> configured{false};  // idempotent, race-free flag
   if (!configured) {
     INFMOE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM)));
     configured = true;
@@ -727,7 +728,7 @@ void softmax_go(const void* x, int64_t N, int d, const float* wg, const float* b
   using C = SoftCfg<T, EB>;
   auto kern = gate_softmax_kernel<T, EB>;
   const size_t smem = C::smem(E);
-  static size_t configured = 0;  // opt in to > 48 KiB dynamic smem once per size
+  static std::atomic<size_t> configured{0};  // opt in to > 48 KiB dynamic smem once per size
   if (smem > configured) {
     INFMOE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     configured = smem;
@@ -809,7 +810,7 @@ void launch_gate_lsh(const void* x, int dtype, int64_t N, int d, const double* p
                                      size_t(bits) * (kLshChunk + 2) * sizeof(double));
   if (dtype == kDtypeBf16) {
     auto kern = gate_lsh_kernel<__nv_bfloat16>;
-    static size_t configured = 0;  // opt in to >48 KiB dynamic smem once per size
+    static std::atomic<size_t> configured{0};  // opt in to >48 KiB dynamic smem once per size
     if (smem > configured) {
       INFMOE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
       configured = smem;
@@ -819,7 +820,7 @@ void launch_gate_lsh(const void* x, int dtype, int64_t N, int d, const double* p
         counts);
   } else {
     auto kern = gate_lsh_kernel<float>;
-    static size_t configured = 0;
+    static std::atomic<size_t> configured{0};
     if (smem > configured) {
       INFMOE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
       configured = smem;
