@@ -70,6 +70,8 @@ def test_codec_layer_bit_identical(cuda, gate, k, pins, codec):
     assert torch.equal(y1.view(torch.int16), y0.view(torch.int16))
     assert torch.equal(y2.view(torch.int16), y2r.view(torch.int16))
     assert list(info1["order"][:E - len(pins)]) == [e for e in info0["order"] if e not in pins]
+    assert raw.packed_bytes() == E * 2 * d * f * 2  # raw stream: expert_param_bytes per expert
+    assert ex1.packed_bytes() == ex2.packed_bytes() < raw.packed_bytes()
     assert len([ev for ev in info1["events"] if ev[0] == 0]) == E - len(pins)
     for lay in (raw, ex1, ex2):
         lay.close()
