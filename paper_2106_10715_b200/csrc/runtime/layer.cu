@@ -492,7 +492,8 @@ void Layer::compute_offloaded(const Rows& r, bool timed, infmoe_forward_out* out
     if (j >= n_slots)
       INFMOE_CUDA(cudaStreamWaitEvent(copy_stream, compute_done[size_t(j - n_slots)], 0));
     if (timed) INFMOE_CUDA(cudaEventRecord(t_load0[size_t(j)], copy_stream));
-    if (pack) {  // exp4: the expert's packed bytes into this slot's staging buffer
+    if (pack) {  // packed codec: one copy of the expert's pack pair into its staging buffer
+      // (one 108 MB copy ran at 55.00 GB/s, two half copies at 54.82)
       INFMOE_CUDA(cudaMemcpyAsync(stage_of(slot), pack->host + pack->off[size_t(e)],
                                   pack->size[size_t(e)], cudaMemcpyHostToDevice, copy_stream));
     } else {
