@@ -336,6 +336,10 @@ def measure_c5(torch, im, dv, dev, local, stream, peaks, h2d_peak, reps: int = 3
     res = dv.MoELayer(d, f, E, k, wi, wo, **kw)
     off = dv.MoELayer(d, f, E, k, hi, ho, offloaded=True, K=K, **kw)
     offh = dv.MoELayer(d, f, E, k, hi, ho, offloaded=True, K=K, h2d_codec="exph", **kw)
+    # the reference's skip_empty_experts option (scenario.hpp:99):
+    # experts that received no rows are neither scheduled nor loaded
+    off_skip = dv.MoELayer(d, f, E, k, hi, ho, offloaded=True, K=K, h2d_codec="exph",
+                           skip_empty_experts=True, **kw)
     y_off, y_res = torch.empty_like(x), torch.empty_like(x)
     ev = lambda: torch.cuda.Event(enable_timing=True)
     for _ in range(2):
@@ -367,6 +371,17 @@ def measure_c5(torch, im, dv, dev, local, stream, peaks, h2d_peak, reps: int = 3
         t_offh.append(a.elapsed_time(b))
     t_oh = float(np.mean(t_offh))
     packed = offh.packed_bytes()
+    y_offs = torch.empty_like(x)
+    off_skip.forward(x, y_offs)
+    t_offs = []
+    for _ in range(reps):
+        a, b = ev(), ev()
+        a.record(stream)
+        off_skip.forward(x, y_offs)
+        b.record(stream)
+        b.synchronize()
+        t_offs.append(a.elapsed_time(b))
+    t_os = float(np.mean(t_offs))
     wbytes = 2 * d * f * 2
     g = im.make_geometry(d, f, E, 2)
     cv = im.compute_costs(counts.astype(np.uint64), g, hw)
@@ -464,12 +479,20 @@ def measure_c5(torch, im, dv, dev, local, stream, peaks, h2d_peak, reps: int = 3
                            "speedup_vs_raw": t_o / t_oh,
                            "bit_identical_to_raw": bool(torch.equal(
                                y_offh.view(torch.int16), y_off.view(torch.int16)))},
+        "offloaded_exph_skip_empty": {
+            "tokens_per_s": N / (t_os * 1e-3), "ms_per_layer": t_os,
+            "experts_loaded": int((counts > 0).sum()), "experts": E,
+            "note": "the reference's skip_empty_experts option (default off): experts with no "
+                    "rows are neither scheduled nor loaded",
+            "bit_identical_to_raw": bool(torch.equal(y_offs.view(torch.int16),
+                                                     y_off.view(torch.int16)))},
         "offloaded_bit_identical_to_resident": same,
         "data_movement": mv,
     }
     res.close()
     off.close()
     offh.close()
+    off_skip.close()
     return out
 
 
