@@ -636,6 +636,22 @@ def main() -> None:
 
     off_layers = make_layers(True)
     res_layers = make_layers(False)
+    # the packed-stream layers (headline) are built here, so the one-time host
+    # packing and its 16 GB of pinned packs settle before any timed step
+    exp_layers = []
+    pack_s = 0.0
+    if args.h2d_codec != "raw":
+        t0 = time.perf_counter()
+        for l in range(L):
+            wi, wo = w_host[l % n_sets]
+            exp_layers.append(dv.MoELayer(d, f, E, k, wi, wo, gate="lsh",
+                                          lsh_seed=im.derive_seed(SEED, 100 + l),
+                                          lsh_bits=cfg["bits"], offloaded=True, K=cfg["K"],
+                                          max_tokens=N, device=local, hw=hw, ep_size=P,
+                                          ep_rank=rank, ep_comm=comm,
+                                          ep_transport=args.ep_transport, slot_pool=pool,
+                                          h2d_codec=args.h2d_codec))
+        pack_s = time.perf_counter() - t0
 
     bufs = [torch.empty((N, d), dtype=bf, device=dev) for _ in range(2)]
 
@@ -742,20 +758,7 @@ def main() -> None:
     # decoder kernels restore the bf16 slot bit for bit before the FFN
     # (codec.cuh); measured right after the raw stream, before the heavier
     # phases below (resident soak, 64 GB of pinned experts, C5)
-    exp_layers = []
     if args.h2d_codec != "raw":
-        t0 = time.perf_counter()
-        exp_layers = []
-        for l in range(L):
-            wi, wo = w_host[l % n_sets]
-            exp_layers.append(dv.MoELayer(d, f, E, k, wi, wo, gate="lsh",
-                                          lsh_seed=im.derive_seed(SEED, 100 + l),
-                                          lsh_bits=cfg["bits"], offloaded=True, K=cfg["K"],
-                                          max_tokens=N, device=local, hw=hw, ep_size=P,
-                                          ep_rank=rank, ep_comm=comm,
-                                          ep_transport=args.ep_transport, slot_pool=pool,
-                                          h2d_codec=args.h2d_codec))
-        pack_s = time.perf_counter() - t0
         for _ in range(args.warmup):
             stack(exp_layers, x_dev)
         torch.cuda.synchronize()
