@@ -737,11 +737,11 @@ def main() -> None:
              for info in all_infos[-1]]
     _, sim_rep, _ = im.simulate_model(costs, cfg["K"])
     # the measured timelines of the last step against replay_check's rules
-    # (verification.hpp:108-206: one lane per stream, causality, <= K+1 experts
+    # (verification.hpp:108-206: one lane per stream, causality, <= K experts
     # resident; durations are measured, so they are not compared to alpha/beta)
     audit = {}
     for info, cv in zip(all_infos[-1], costs):
-        for kind, n in im.replay_check(info["events"], [cv], cfg["K"] + 1,
+        for kind, n in im.replay_check(info["events"], [cv], cfg["K"],
                                        check_durations=False, tol_s=2e-6).items():
             audit[kind] = audit.get(kind, 0) + n
     if os.environ.get("BENCH_VERBOSE"):
@@ -791,7 +791,7 @@ def main() -> None:
         link_bytes = L * El * wbytes * packed / raw  # packed bytes moved per step
         audit_ex = {}
         for info, cv in zip(ex_infos[-1], costs):
-            for kind, nv in im.replay_check(info["events"], [cv], cfg["K"] + 1,
+            for kind, nv in im.replay_check(info["events"], [cv], cfg["K"],
                                             check_durations=False, tol_s=2e-6).items():
                 audit_ex[kind] = audit_ex.get(kind, 0) + nv
         # the reference simulator with the link's effective weight bandwidth

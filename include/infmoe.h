@@ -182,6 +182,16 @@ enum { INFMOE_RESIDENT = 0, INFMOE_OFFLOADED = 1 };
 int infmoe_fill_uniform(void* out, int32_t dtype, uint64_t n, uint64_t seed, float scale,
                         void* stream);
 
+/* test hooks: n_ctas spinning CTAs holding smem_bytes of shared memory each
+ * (one per SM at ~200 KB; an even n_ctas launches clusters of 2, i.e. whole
+ * TPCs) until *release != 0 (device int) or timeout_ns;
+ * *timed_out (device int) is set to 1 if any gave up.  infmoe_debug_set_flag
+ * stores 1 to *flag in stream order.  Used to check that the persistent FFN
+ * makes progress when part of the GPU is taken by a concurrent kernel. */
+int infmoe_debug_occupy_sms(int32_t n_ctas, int32_t smem_bytes, const int32_t* release,
+                            uint64_t timeout_ns, int32_t* timed_out, void* stream);
+int infmoe_debug_set_flag(int32_t* flag, void* stream);
+
 /* N1a softmax/top-k gate: x[N,d] (dtype), wg[E,d] f32, bias[E] f32 or NULL.
  * Outputs topk_idx[N,k] i32, topk_w[N,k] f32, counts[E] i32 (device). */
 int infmoe_gate_softmax_topk(const void* x, int32_t dtype, int64_t N, int32_t d,
@@ -217,7 +227,8 @@ int infmoe_expert_ffn(const void* x_perm, int64_t n_rows, int32_t d_model, int32
                       void* h, void* y_perm, void* stream);
 /* N3+N4 in ONE persistent launch (phase-2 tiles of an expert start once its
  * H rows are complete; see csrc/kernels/expert_gemm.cuh).  bf16 only.
- * done: >= n_groups int32 of device scratch.  perm/topk_w (top-1 only, or
+ * done: >= n_groups + 1 int32 of device scratch (per-expert completion counters
+ * and the tile-claim counter of the persistent launch).  perm/topk_w (top-1 only, or
  * NULL): fuse the combine, y[perm[r]] = bf16(fmaf(topk_w[perm[r]], bf16(acc_r), 0)),
  * in which case y is [N, d_model]; otherwise y is y_perm [n_rows, d_model]. */
 int infmoe_expert_ffn_fused(const void* x_perm, int64_t n_rows, int32_t d_model, int32_t d_ff,
@@ -285,9 +296,16 @@ typedef struct {
    * pinned exp4 packs -- 12 bits per value, exponents coded against a per-block
    * base -- shared by every layer on the same host weights; each load copies
    * the pack and a decoder kernel restores the bf16 slot bit for bit before the
-   * FFN).  INFMOE_CODEC_EXPH codes the exponent with a per-matrix canonical
-   * Huffman code instead (~10.7 bits per value on the bench's weights; one GPU
-   * thread decodes each 64-value chunk through a shared-memory table).
+   * FFN).  INFMOE_CODEC_EXPH codes the exponent's distance to its block base
+   * with a per-matrix canonical Huffman code (<= 12 bits) instead: 128-value
+   * chunks with recorded start bits, decoded one warp per 32 chunks (one lane
+   * per chunk) through a shared-memory table, sign/mantissa bytes
+   * lane-interleaved; ~10.3-10.8 bits per value (uniform / Gaussian weights).
+   * Packs are SNAPSHOTS of the host weights taken at create and at every
+   * infmoe_layer_set_host_weights call (which always re-packs); layers created
+   * on the same host buffers share one pack only while its content digest
+   * matches the buffers.  Refilling host weights in place without calling
+   * infmoe_layer_set_host_weights leaves a codec layer on the old snapshot.
    * Outputs are identical; the scheduler's costs stay the reference's. */
   int32_t h2d_codec;
 } infmoe_layer_desc;

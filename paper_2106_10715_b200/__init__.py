@@ -169,6 +169,8 @@ _lib.infmoe_simulate.argtypes = [_vp, _vp, _i32, _f64, _i32, _i32, _vp, _P(_SimR
 _lib.infmoe_simulate_model.argtypes = [_i32, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32,
                                        _vp, _vp, _P(_SimReport), _vp]
 _lib.infmoe_fill_uniform.argtypes = [_vp, _i32, _u64, _u64, C.c_float, _vp]
+_lib.infmoe_debug_occupy_sms.argtypes = [_i32, _i32, _vp, _u64, _vp, _vp]
+_lib.infmoe_debug_set_flag.argtypes = [_vp, _vp]
 _lib.infmoe_gate_softmax_topk.argtypes = [_vp, _i32, C.c_int64, _i32, _vp, _vp, _i32, _i32,
                                           _vp, _vp, _vp, _vp]
 _lib.infmoe_gate_lsh.argtypes = [_vp, _i32, C.c_int64, _i32, _vp, _i32, _i32, _vp, _vp, _vp,

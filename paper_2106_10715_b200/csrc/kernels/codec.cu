@@ -488,12 +488,7 @@ void launch_exph_unpack(const uint8_t* pack, const ExphLayout& L, uint16_t* out,
   const uint64_t want = (groups + kExphWarps - 1) / kExphWarps;
   const uint64_t cap = uint64_t(device_sm_count()) * 4;  // 4 CTAs (48 KB smem each) per SM
   constexpr int kStage = kExphWarps * kExphWarpChunks * 8 * 16;
-  static std::atomic<bool> configured{false};  // idempotent, race-free flag
-  if (!configured) {
-    INFMOE_CUDA(cudaFuncSetAttribute(exph_unpack_kernel,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, kStage));
-    configured = true;
-  }
+  ensure_dyn_smem(reinterpret_cast<const void*>(exph_unpack_kernel), size_t(kStage));
   exph_unpack_kernel<<<unsigned(std::max<uint64_t>(std::min(want, cap), 1)), kExphWarps * 32,
                        kStage, s>>>(pack, L, out);
   INFMOE_LAUNCH_CHECK();

@@ -5,7 +5,10 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <map>
+#include <mutex>
 #include <string>
+#include <utility>
 
 #include "../host/status.hpp"
 
@@ -43,6 +46,24 @@ inline int device_sm_count() {
   INFMOE_CUDA(cudaGetDevice(&dev));
   INFMOE_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
   return n;
+}
+
+// Opt a kernel in to `bytes` of dynamic shared memory on the CURRENT device.
+// The attribute is per (device, function), so the record is keyed on both and
+// only ever grows; a mutex makes concurrent launchers (EP ranks as threads,
+// layers on several GPUs) safe.  Cheap enough to call on every launch.
+inline void ensure_dyn_smem(const void* func, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> configured;
+  int dev = 0;
+  INFMOE_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& cur = configured[{dev, func}];
+  if (bytes > cur) {
+    INFMOE_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(bytes)));
+    cur = bytes;
+  }
 }
 
 }  // namespace infmoe

@@ -427,12 +427,7 @@ template <bool kTF32, bool kGelu, int TOK, int STAGES>
 void launch_impl(const GroupedGemmArgs& a, cudaStream_t stream) {
   using C = Cfg<TOK, STAGES>;
   auto kern = grouped_gemm_kernel<kTF32, kGelu, TOK, STAGES>;
-  static std::atomic<bool> configured{false};  // idempotent, race-free flag
-  if (!configured) {
-    INFMOE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     int(C::SMEM_BYTES)));
-    configured = true;
-  }
+  ensure_dyn_smem(reinterpret_cast<const void*>(kern), size_t(int(C::SMEM_BYTES)));
   const CUtensorMap tx = make_tmap(a.a, uint64_t(std::max<int64_t>(a.a_rows, 1)), uint64_t(a.K),
                                    kTF32, TOK_BOX);
   const CUtensorMap tw = make_tmap(a.b, uint64_t(a.n_slots) * uint64_t(a.N), uint64_t(a.K),
@@ -476,9 +471,12 @@ void dispatch_tok(const GroupedGemmArgs& a, cudaStream_t s) {
 
 // =================================================================== fused
 // Two-phase persistent kernel (see FusedFfnArgs).  Tiles are numbered phase-1
-// first (expert-major), then phase 2; every CTA walks its tiles in increasing
-// order, so all phase-1 tiles are issued before any phase-2 tile and the
-// per-group waits always make progress (grid <= #SMs, 1 CTA per SM).
+// first (expert-major), then phase 2, and claimed in that order from a global
+// counter (claim_tile), so every phase-1 tile is owned by a running CTA before
+// any phase-2 tile is handed out and the per-group waits always make progress,
+// whether or not the whole grid is resident (concurrent kernels, MPS / green
+// contexts, EP ranks sharing a GPU).  Dynamic claiming also balances the 2.5x
+// longer phase-2 tiles across CTAs (greedy list scheduling).
 struct FusedParams {
   int32_t d, f;
   int32_t n_groups;
@@ -603,6 +601,59 @@ __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
+// ---- dynamic tile claim (forward progress without co-residency) ----------
+// The persistent FFN kernels do not assume that their whole grid is resident.
+// One thread per CTA (per pair) claims tiles in global order from a counter
+// (done[n_groups]); all phase-1 tiles precede all phase-2 tiles in that order,
+// so when a phase-2 tile of expert g is claimed every phase-1 tile of g is
+// already owned by a RUNNING CTA whose pipeline drains without further claims.
+// A CTA that is never scheduled simply claims nothing.  The claimed index is
+// handed to the CTA's other roles through a small ring in shared memory
+// (full/empty mbarriers); in the pair kernel the leader also writes it into
+// the follower's ring over DSMEM.  The claim for tile i+1 is issued while
+// tile i's loads are being issued, so its latency is hidden.
+constexpr int kTileRing = 4;
+__device__ __forceinline__ void mbar_wait_cl(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ uint32_t map_rank(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_cluster_s32(uint32_t caddr, int32_t v) {
+  asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(caddr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void arrive_cluster(uint32_t caddr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(caddr)
+               : "memory");
+}
+__device__ __forceinline__ int32_t claim_tile(int32_t* ctr, int32_t n_tiles) {
+  const int32_t t = atomicAdd(ctr, 1);
+  return t < n_tiles ? t : -1;
+}
+// consumer side: the next claimed tile (-1 = no more), slot released at once
+struct TileRing {
+  uint32_t full0, empty0;  // barrier arrays (8 B apart)
+  volatile int32_t* idx;
+  int slot = 0;
+  uint32_t phase = 0;
+  __device__ __forceinline__ int32_t next(int lane, uint32_t empty_addr_of_slot0) {
+    mbar_wait_cl(full0 + 8u * slot, phase);
+    const int32_t t = idx[slot];
+    __syncwarp(__activemask());  // a whole role warp, or the single producer lane
+    if (lane == 0) arrive_cluster(empty_addr_of_slot0 + 8u * slot);
+    if (++slot == kTileRing) { slot = 0; phase ^= 1; }
+    return t;
+  }
+};
+
 template <int TOK, int STAGES>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     fused_ffn_kernel(const __grid_constant__ CUtensorMap tmap_x,
@@ -613,6 +664,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   extern __shared__ uint8_t smem_raw[];
   __shared__ FusedTable tt;
   __shared__ uint32_t tmem_base_slot;
+  __shared__ int32_t tile_idx[kTileRing];
+  __shared__ __align__(8) uint64_t tile_bar[2 * kTileRing];  // full[kTileRing] | empty[kTileRing]
 
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
@@ -655,6 +708,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_init(accf_bar(a), 1);
       mbar_init(acce_bar(a), 4);
     }
+    for (int i = 0; i < kTileRing; ++i) {
+      mbar_init(smem_u32(&tile_bar[i]), 1);              // the claiming producer
+      mbar_init(smem_u32(&tile_bar[kTileRing + i]), 5);  // MMA warp + 4 epilogue warps
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
@@ -671,6 +728,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const uint32_t tmem_base = tmem_base_slot;
   const int32_t n_tiles = tt.total1 + tt.start2[tt.n_groups];
   constexpr int32_t bk = ROW_BYTES / 2;  // bf16 elements per K-block
+  int32_t* const tile_ctr = p.done + p.n_groups;
+  TileRing ring{smem_u32(&tile_bar[0]), smem_u32(&tile_bar[kTileRing]), tile_idx};
 
   if (warp == 0) {
     // ================= TMA producer =================
@@ -681,7 +740,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       int32_t c1 = 0, c2 = 0, ready_g = -1;
-      for (int32_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      int ts = 0;
+      uint32_t tph = 0;
+      int32_t t = claim_tile(tile_ctr, n_tiles);
+      for (;;) {
+        mbar_wait_cl(ring.empty0 + 8u * ts, tph ^ 1);  // publish t to the MMA / epilogue warps
+        tile_idx[ts] = t;
+        mbar_arrive(ring.full0 + 8u * ts);
+        if (++ts == kTileRing) { ts = 0; tph ^= 1; }
+        if (t < 0) break;
+        const int32_t t_next = claim_tile(tile_ctr, n_tiles);  // latency hidden by this tile
         const FTile tile = fdecode<TOK>(tt, t, c1, c2, p.d, p.f);
         if (tile.phase == 1 && tile.g != ready_g) {
           // every phase-1 tile of this group has published its H rows
@@ -711,6 +779,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         tile.row0 + b * TOK_BOX, pol_x);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
+        t = t_next;
       }
     }
   } else if (warp == 1) {
@@ -720,7 +789,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     int32_t c1 = 0, c2 = 0;
-    for (int32_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+    for (int32_t t = ring.next(lane, ring.empty0); t >= 0; t = ring.next(lane, ring.empty0)) {
       const FTile tile = fdecode<TOK>(tt, t, c1, c2, p.d, p.f);
       const uint32_t n_mma = uint32_t((tile.ntok + 15) & ~15);
       const uint32_t idesc = make_idesc<false>(n_mma);
@@ -753,7 +822,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     int32_t c1 = 0, c2 = 0;
-    for (int32_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+    for (int32_t t = ring.next(lane, ring.empty0); t >= 0; t = ring.next(lane, ring.empty0)) {
       const FTile tile = fdecode<TOK>(tt, t, c1, c2, p.d, p.f);
       mbar_wait(accf_bar(acc), acc_phase);
       tc_fence_after();
@@ -835,12 +904,7 @@ template <int TOK, int STAGES>
 void fused_launch(const FusedFfnArgs& a, cudaStream_t stream) {
   using C = Cfg<TOK, STAGES>;
   auto kern = fused_ffn_kernel<TOK, STAGES>;
-  static std::atomic<bool> configured{false};  // idempotent, race-free flag
-  if (!configured) {
-    INFMOE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     int(C::SMEM_BYTES)));
-    configured = true;
-  }
+  ensure_dyn_smem(reinterpret_cast<const void*>(kern), size_t(int(C::SMEM_BYTES)));
   const uint64_t rows = uint64_t(std::max<int64_t>(a.rows, 1));
   const CUtensorMap tx = make_tmap(a.x, rows, uint64_t(a.d_model), false, TOK_BOX);
   const CUtensorMap tw1 = make_tmap(a.w_in, uint64_t(a.n_slots) * a.d_ff, uint64_t(a.d_model),
@@ -870,7 +934,7 @@ void fused_launch(const FusedFfnArgs& a, cudaStream_t stream) {
   int grid = device_sm_count();
   if (a.max_ctas > 0) grid = std::min(grid, a.max_ctas);
   if (a.ev_begin) INFMOE_CUDA(cudaEventRecord(a.ev_begin, stream));
-  INFMOE_CUDA(cudaMemsetAsync(a.done, 0, sizeof(int32_t) * size_t(a.n_groups), stream));
+  INFMOE_CUDA(cudaMemsetAsync(a.done, 0, sizeof(int32_t) * size_t(a.n_groups + 1), stream));
   kern<<<grid, NUM_THREADS, C::SMEM_BYTES, stream>>>(tx, tw1, th, tw2, p);
   INFMOE_LAUNCH_CHECK();
   if (a.ev_end) INFMOE_CUDA(cudaEventRecord(a.ev_end, stream));
@@ -975,6 +1039,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   extern __shared__ uint8_t smem_raw[];
   __shared__ FusedTable tt;
   __shared__ uint32_t tmem_base_slot;
+  __shared__ int32_t tile_idx[kTileRing];
+  __shared__ __align__(8) uint64_t tile_bar[2 * kTileRing];  // full[kTileRing] | empty[kTileRing]
 
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
@@ -987,7 +1053,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   const int lane = threadIdx.x % 32;
   const uint32_t rank = cluster_rank();
   const bool leader = rank == 0;
-  const int32_t pair = int32_t(blockIdx.x / 2), n_pairs = int32_t(gridDim.x / 2);
 
   if (threadIdx.x == 0) {
     tt.n_groups = p.n_groups;
@@ -1020,6 +1085,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       mbar_init(accf_bar(a), 1);   // one multicast commit per tile
       mbar_init(acce_bar(a), 8);   // 4 epilogue warps x 2 CTAs (the leader's copy is used)
     }
+    for (int i = 0; i < kTileRing; ++i) {
+      // full: the leader's producer publishes into both CTAs' rings; empty (the
+      // leader's copy is used): leader MMA + 4 leader epilogue warps + the
+      // follower's producer + 4 follower epilogue warps
+      mbar_init(smem_u32(&tile_bar[i]), 1);
+      mbar_init(smem_u32(&tile_bar[kTileRing + i]), 10);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
@@ -1037,6 +1109,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   const uint32_t tmem_base = tmem_base_slot;
   const int32_t n_tiles = tt.total1 + tt.start2[tt.n_groups];
   constexpr int32_t bk = ROW_BYTES / 2;
+  int32_t* const tile_ctr = p.done + p.n_groups;
+  TileRing ring{smem_u32(&tile_bar[0]), smem_u32(&tile_bar[kTileRing]), tile_idx};
+  const uint32_t leader_empty0 = map_rank(ring.empty0, 0);  // consumers release the leader's slot
 
   if (warp == 0) {
     // ================= TMA producer (both CTAs) =================
@@ -1047,7 +1122,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       int32_t c1 = 0, c2 = 0, ready_g = -1;
-      for (int32_t t = pair; t < n_tiles; t += n_pairs) {
+      int ts = 0;
+      uint32_t tph = 0;
+      const uint32_t peer_idx0 = map_rank(smem_u32(&tile_idx[0]), 1);
+      const uint32_t peer_full0 = map_rank(ring.full0, 1);
+      int32_t t = leader ? claim_tile(tile_ctr, n_tiles) : -1;
+      for (;;) {
+        int32_t t_next = -1;
+        if (leader) {  // claim and publish to both CTAs
+          mbar_wait_cl(ring.empty0 + 8u * ts, tph ^ 1);
+          tile_idx[ts] = t;
+          st_cluster_s32(peer_idx0 + 4u * ts, t);
+          arrive_cluster(peer_full0 + 8u * ts);
+          mbar_arrive(ring.full0 + 8u * ts);
+          if (++ts == kTileRing) { ts = 0; tph ^= 1; }
+          if (t < 0) break;
+          t_next = claim_tile(tile_ctr, n_tiles);  // latency hidden by this tile
+        } else {
+          t = ring.next(0, leader_empty0);
+          if (t < 0) break;
+        }
         const FTile tile = pdecode<TOK>(tt, t, c1, c2, p.d, p.f, rank);
         if (tile.phase == 1 && tile.g != ready_g) {
           const int32_t target = tt.chunks[tile.g] * tt.fb1 * 2;  // both halves of every tile
@@ -1079,6 +1173,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                              xrow0 + b * TOK_BOX, pol_x);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
+        t = t_next;
       }
     }
   } else if (warp == 1) {
@@ -1089,7 +1184,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       int acc = 0;
       uint32_t acc_phase = 0;
       int32_t c1 = 0, c2 = 0;
-      for (int32_t t = pair; t < n_tiles; t += n_pairs) {
+      for (int32_t t = ring.next(lane, ring.empty0); t >= 0; t = ring.next(lane, ring.empty0)) {
         const FTile tile = pdecode<TOK>(tt, t, c1, c2, p.d, p.f, rank);
         const uint32_t n_mma = uint32_t((tile.ntok + 15) & ~15);
         const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((n_mma >> 3) << 17) |
@@ -1124,7 +1219,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     int32_t c1 = 0, c2 = 0;
-    for (int32_t t = pair; t < n_tiles; t += n_pairs) {
+    for (int32_t t = ring.next(lane, leader_empty0); t >= 0; t = ring.next(lane, leader_empty0)) {
       const FTile tile = pdecode<TOK>(tt, t, c1, c2, p.d, p.f, rank);
       mbar_wait_guarded(accf_bar(acc), acc_phase);
       tc_fence_after();
@@ -1205,12 +1300,7 @@ template <int TOK, int STAGES>
 void fused_pair_launch(const FusedFfnArgs& a, cudaStream_t stream) {
   using C = PairCfg<TOK, STAGES>;
   auto kern = fused_ffn_pair_kernel<TOK, STAGES>;
-  static std::atomic<bool> configured{false};  // idempotent, race-free flag
-  if (!configured) {
-    INFMOE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     int(C::SMEM_BYTES)));
-    configured = true;
-  }
+  ensure_dyn_smem(reinterpret_cast<const void*>(kern), size_t(int(C::SMEM_BYTES)));
   const uint64_t rows = uint64_t(std::max<int64_t>(a.rows, 1));
   const CUtensorMap tx = make_tmap(a.x, rows, uint64_t(a.d_model), false, TOK_BOX);
   const CUtensorMap tw1 = make_tmap(a.w_in, uint64_t(a.n_slots) * a.d_ff, uint64_t(a.d_model),
@@ -1241,7 +1331,7 @@ void fused_pair_launch(const FusedFfnArgs& a, cudaStream_t stream) {
   if (a.max_ctas > 0) grid = std::min(grid, (a.max_ctas + 1) & ~1);
   grid = std::max(grid, 2);
   if (a.ev_begin) INFMOE_CUDA(cudaEventRecord(a.ev_begin, stream));
-  INFMOE_CUDA(cudaMemsetAsync(a.done, 0, sizeof(int32_t) * size_t(a.n_groups), stream));
+  INFMOE_CUDA(cudaMemsetAsync(a.done, 0, sizeof(int32_t) * size_t(a.n_groups + 1), stream));
   kern<<<grid, NUM_THREADS, C::SMEM_BYTES, stream>>>(tx, tw1, th, tw2, p);
   INFMOE_LAUNCH_CHECK();
   if (a.ev_end) INFMOE_CUDA(cudaEventRecord(a.ev_end, stream));

@@ -62,7 +62,8 @@ struct FusedFfnArgs {
   const int2* ret;
   void* peer_y[kMaxPeers];
   int32_t n_peers;
-  int32_t* done;        // >= n_groups counters in device memory (zeroed by the launcher)
+  int32_t* done;        // >= n_groups + 1 counters in device memory (zeroed by the launcher):
+                        // per-group phase-1 completion, then the tile-claim counter
   int32_t max_ctas;
   int32_t max_rows_hint;
   // optional events recorded right around the kernel, after all host-side

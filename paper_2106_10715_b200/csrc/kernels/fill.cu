@@ -34,4 +34,61 @@ void launch_fill_uniform(void* out, int dtype, uint64_t n, uint64_t seed, float 
   INFMOE_LAUNCH_CHECK();
 }
 
+
+// ---------------------------------------------------------------- test hooks
+// n_ctas CTAs, each holding `smem` bytes of shared memory (so one per SM),
+// spin until *release != 0 or timeout_ns elapsed (globaltimer); *timed_out is
+// set if any CTA gave up.  Used to take SMs away from a concurrent launch.
+__global__ void occupy_kernel(const volatile int32_t* release, uint64_t timeout_ns,
+                              int32_t* timed_out) {
+  extern __shared__ uint8_t pad[];
+  if (threadIdx.x != 0) return;
+  pad[0] = 0;
+  uint64_t t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  while (*release == 0) {
+    __nanosleep(1000);
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > timeout_ns) {
+      atomicExch(timed_out, 1);
+      return;
+    }
+  }
+}
+// the same spinner in clusters of two: it takes whole TPCs, so the SMs left
+// free come in pairs a cta_group::2 kernel can use
+__global__ void __cluster_dims__(2, 1, 1)
+    occupy_pair_kernel(const volatile int32_t* release, uint64_t timeout_ns, int32_t* timed_out) {
+  extern __shared__ uint8_t pad2[];
+  if (threadIdx.x != 0) return;
+  pad2[0] = 0;
+  uint64_t t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  while (*release == 0) {
+    __nanosleep(1000);
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > timeout_ns) {
+      atomicExch(timed_out, 1);
+      return;
+    }
+  }
+}
+__global__ void set_flag_kernel(int32_t* flag) { *reinterpret_cast<volatile int32_t*>(flag) = 1; }
+
+void launch_occupy(int n_ctas, size_t smem, const int32_t* release, uint64_t timeout_ns,
+                   int32_t* timed_out, cudaStream_t s) {
+  if (n_ctas % 2 == 0) {  // whole TPCs
+    ensure_dyn_smem(reinterpret_cast<const void*>(occupy_pair_kernel), smem);
+    occupy_pair_kernel<<<n_ctas, 32, smem, s>>>(release, timeout_ns, timed_out);
+  } else {
+    ensure_dyn_smem(reinterpret_cast<const void*>(occupy_kernel), smem);
+    occupy_kernel<<<n_ctas, 32, smem, s>>>(release, timeout_ns, timed_out);
+  }
+  INFMOE_LAUNCH_CHECK();
+}
+void launch_set_flag(int32_t* flag, cudaStream_t s) {
+  set_flag_kernel<<<1, 1, 0, s>>>(flag);
+  INFMOE_LAUNCH_CHECK();
+}
+
 }  // namespace infmoe

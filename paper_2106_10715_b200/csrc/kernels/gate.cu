@@ -561,11 +561,7 @@ void lsh_fast_go(const void* x, int64_t N, int d, const double* proj, int bits, 
   static const int force = lsh_env("INFMOE_LSH_FORCE_EXACT", 0);
   using C = LshFastCfg<T, BMAX>;
   auto kern = gate_lsh_fast_kernel<T, BMAX>;
-  static std::atomic<bool> configured{false};  // idempotent, race-free flag
-  if (!configured) {
-    INFMOE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM)));
-    configured = true;
-  }
+  ensure_dyn_smem(reinterpret_cast<const void*>(kern), size_t(int(C::SMEM)));
   const unsigned blocks = unsigned((N + C::TB - 1) / C::TB);
   kern<<<blocks, kLshFastWarps * 32, C::smem_bytes(bits), s>>>(
       reinterpret_cast<const T*>(x), N, d, proj, bits, E, force, codes, idx, w, counts);
@@ -728,11 +724,7 @@ void softmax_go(const void* x, int64_t N, int d, const float* wg, const float* b
   using C = SoftCfg<T, EB>;
   auto kern = gate_softmax_kernel<T, EB>;
   const size_t smem = C::smem(E);
-  static std::atomic<size_t> configured{0};  // opt in to > 48 KiB dynamic smem once per size
-  if (smem > configured) {
-    INFMOE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    configured = smem;
-  }
+  ensure_dyn_smem(reinterpret_cast<const void*>(kern), smem);
   const int warps = (E + EB - 1) / EB;
   kern<<<unsigned((N + C::TT - 1) / C::TT), warps * 32, smem, s>>>(
       reinterpret_cast<const T*>(x), N, d, wg, bias, E, k, idx, w, counts);
@@ -810,21 +802,13 @@ void launch_gate_lsh(const void* x, int dtype, int64_t N, int d, const double* p
                                      size_t(bits) * (kLshChunk + 2) * sizeof(double));
   if (dtype == kDtypeBf16) {
     auto kern = gate_lsh_kernel<__nv_bfloat16>;
-    static std::atomic<size_t> configured{0};  // opt in to >48 KiB dynamic smem once per size
-    if (smem > configured) {
-      INFMOE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-      configured = smem;
-    }
+    ensure_dyn_smem(reinterpret_cast<const void*>(kern), smem);
     kern<<<unsigned(blocks), kLshWarps * 32, smem, stream>>>(
         reinterpret_cast<const __nv_bfloat16*>(x), N, d, proj, bits, E, codes, topk_idx, topk_w,
         counts);
   } else {
     auto kern = gate_lsh_kernel<float>;
-    static std::atomic<size_t> configured{0};
-    if (smem > configured) {
-      INFMOE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-      configured = smem;
-    }
+    ensure_dyn_smem(reinterpret_cast<const void*>(kern), smem);
     kern<<<unsigned(blocks), kLshWarps * 32, smem, stream>>>(reinterpret_cast<const float*>(x), N, d,
                                                              proj, bits, E, codes, topk_idx,
                                                              topk_w, counts);

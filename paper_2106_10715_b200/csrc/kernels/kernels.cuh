@@ -9,6 +9,10 @@ namespace infmoe {
 
 void launch_fill_uniform(void* out, int dtype, uint64_t n, uint64_t seed, float scale,
                          cudaStream_t stream);
+// test hooks (fill.cu): SM-occupying spinners and the flag that releases them
+void launch_occupy(int n_ctas, size_t smem, const int32_t* release, uint64_t timeout_ns,
+                   int32_t* timed_out, cudaStream_t s);
+void launch_set_flag(int32_t* flag, cudaStream_t s);
 
 // N1a: logits by a sequential fmaf chain per (token, expert), top-k by strict
 // argmax (ties -> lower index), softmax weights.  counts must be zeroed by the

@@ -31,6 +31,21 @@ int infmoe_fill_uniform(void* out, int32_t dtype, uint64_t n, uint64_t seed, flo
   });
 }
 
+int infmoe_debug_occupy_sms(int32_t n_ctas, int32_t smem_bytes, const int32_t* release,
+                            uint64_t timeout_ns, int32_t* timed_out, void* stream) {
+  return guarded([&] {
+    require(n_ctas >= 1 && smem_bytes >= 0 && release && timed_out, "occupy: bad arguments");
+    launch_occupy(n_ctas, size_t(smem_bytes), release, timeout_ns, timed_out, as_stream(stream));
+  });
+}
+
+int infmoe_debug_set_flag(int32_t* flag, void* stream) {
+  return guarded([&] {
+    require(flag != nullptr, "set_flag: NULL flag");
+    launch_set_flag(flag, as_stream(stream));
+  });
+}
+
 int infmoe_gate_softmax_topk(const void* x, int32_t dtype, int64_t N, int32_t d,
                              const float* wg, const float* bias, int32_t E, int32_t k,
                              int32_t* topk_idx, float* topk_w, int32_t* counts, void* stream) {

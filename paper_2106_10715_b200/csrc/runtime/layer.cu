@@ -25,7 +25,9 @@
 #include <cstring>
 #include <map>
 #include <memory>
+#include <atomic>
 #include <mutex>
+#include <thread>
 #include <tuple>
 #include <vector>
 
@@ -90,7 +92,7 @@ Layer::Layer(const infmoe_layer_desc& d) : desc(d) {
   perm = dalloc<int32_t>(size_t(A), owned);
   inv = dalloc<int32_t>(size_t(A), owned);
   dws = dalloc<uint8_t>(dispatch_workspace_bytes(A, d.n_experts), owned);
-  done_ctr = dalloc<int32_t>(size_t(d.n_experts), owned);
+  done_ctr = dalloc<int32_t>(size_t(d.n_experts) + 1, owned);  // + the tile-claim counter
   xp = dalloc<uint8_t>(size_t(A) * d.d_model * esz, owned);
   yp = dalloc<uint8_t>(size_t(A) * d.d_model * esz, owned);
   // the exchange path runs whenever a communicator is given (ep_size == 1 then
@@ -176,7 +178,7 @@ Layer::Layer(const infmoe_layer_desc& d) : desc(d) {
       v->resize(E);
       for (auto& e : *v) INFMOE_CUDA(cudaEventCreate(&e));
     }
-    set_host_weights(d.w_in, d.w_out);
+    set_host_weights(d.w_in, d.w_out, /*fresh_pack=*/false);
   } else {
     t_comp0.resize(1);
     t_comp1.resize(1);
@@ -190,7 +192,7 @@ Layer::Layer(const infmoe_layer_desc& d) : desc(d) {
   load_ema.assign(size_t(n_local), 0.0);
 }
 
-void Layer::set_host_weights(const void* w_in, const void* w_out) {
+void Layer::set_host_weights(const void* w_in, const void* w_out, bool fresh_pack) {
   require(desc.residency == INFMOE_OFFLOADED, "set_host_weights: layer is resident");
   require(w_in && w_out, "set_host_weights: NULL weights");
   const size_t bytes = expert_in_bytes * size_t(n_local);
@@ -208,8 +210,12 @@ void Layer::set_host_weights(const void* w_in, const void* w_out) {
   host_in = reinterpret_cast<const uint8_t*>(w_in);
   host_out = reinterpret_cast<const uint8_t*>(w_out);
   if (desc.h2d_codec != INFMOE_CODEC_RAW) {
+    // packs are SNAPSHOTS of the host weights: an explicit set_host_weights
+    // always re-packs (the caller may have refilled the buffer in place); at
+    // create a cached pack of the same buffer is shared only if its content
+    // digest still matches (HostPack::acquire)
     pack = HostPack::acquire(w_in, w_out, n_local, uint64_t(desc.d_ff) * desc.d_model,
-                             desc.h2d_codec);
+                             desc.h2d_codec, fresh_pack);
     if (pool_ptr->stage_bytes < pack->max_size) {  // grow the shared staging buffers
       INFMOE_CUDA(cudaDeviceSynchronize());
       if (pool_ptr->stage) INFMOE_CUDA(cudaFree(pool_ptr->stage));
@@ -504,6 +510,13 @@ void Layer::compute_offloaded(const Rows& r, bool timed, infmoe_forward_out* out
                                   host_out + size_t(e) * expert_in_bytes, expert_in_bytes,
                                   cudaMemcpyHostToDevice, copy_stream));
     }
+    // the reference's residency gate (simulator.hpp:147-155): load j COMPLETES
+    // -- expert j becomes resident -- only once expert j-K has finished
+    // computing, so at most K experts are resident at any time; the copy in
+    // flight meanwhile occupies the (K+1)-th physical slot.  Like
+    // the simulator's single load lane, the next copy starts after this point.
+    if (j >= desc.K)
+      INFMOE_CUDA(cudaStreamWaitEvent(copy_stream, compute_done[size_t(j - desc.K)], 0));
     if (timed) INFMOE_CUDA(cudaEventRecord(t_load1[size_t(j)], copy_stream));
     INFMOE_CUDA(cudaEventRecord(load_done[size_t(j)], copy_stream));
 
@@ -814,15 +827,51 @@ std::mutex g_pack_mu;
 std::map<PackKey, std::weak_ptr<HostPack>> g_packs;
 }  // namespace
 
+// 64-bit content digest of both host matrices of every expert (threads over
+// 1 MiB blocks, combined in block order): a cached pack is reused only for
+// identical bytes
+static uint64_t host_digest(const void* w_in, const void* w_out, uint64_t bytes_each) {
+  constexpr uint64_t kBlock = 1 << 20;
+  const uint64_t nb = (bytes_each + kBlock - 1) / kBlock;
+  std::vector<uint64_t> part(size_t(2 * nb), 0);
+  const unsigned nt = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+  std::atomic<uint64_t> next{0};
+  auto work = [&] {
+    for (uint64_t b = next++; b < 2 * nb; b = next++) {
+      const auto* base = static_cast<const uint8_t*>(b < nb ? w_in : w_out);
+      const uint64_t off = (b % nb) * kBlock, len = std::min(kBlock, bytes_each - off);
+      uint64_t h = 0x9e3779b97f4a7c15ull ^ b, w = 0;
+      const uint8_t* q = base + off;
+      uint64_t i = 0;
+      for (; i + 8 <= len; i += 8) {
+        std::memcpy(&w, q + i, 8);
+        h = (h ^ w) * 0x100000001b3ull + (h >> 29);
+      }
+      for (; i < len; ++i) h = (h ^ q[i]) * 0x100000001b3ull;
+      part[size_t(b)] = h;
+    }
+  };
+  std::vector<std::thread> th;
+  for (unsigned t = 1; t < nt; ++t) th.emplace_back(work);
+  work();
+  for (auto& t : th) t.join();
+  uint64_t h = bytes_each;
+  for (uint64_t v : part) h = dev_mix64(h ^ v);
+  return h;
+}
+
 std::shared_ptr<HostPack> HostPack::acquire(const void* w_in, const void* w_out, int n_experts,
-                                            uint64_t matrix_elems, int codec_id) {
+                                            uint64_t matrix_elems, int codec_id, bool fresh) {
   std::lock_guard<std::mutex> lock(g_pack_mu);
   const PackKey key{w_in, w_out, n_experts, matrix_elems, codec_id};
+  const uint64_t digest = host_digest(w_in, w_out, uint64_t(n_experts) * matrix_elems * 2);
   auto it = g_packs.find(key);
-  if (it != g_packs.end())
-    if (auto sp = it->second.lock()) return sp;
+  if (!fresh && it != g_packs.end())
+    if (auto sp = it->second.lock())
+      if (sp->digest == digest) return sp;
   auto p = std::make_shared<HostPack>();
   p->codec_id = codec_id;
+  p->digest = digest;
   const auto* in = static_cast<const uint16_t*>(w_in);
   const auto* out = static_cast<const uint16_t*>(w_out);
   const bool h = codec_id == INFMOE_CODEC_EXPH;

@@ -34,8 +34,11 @@ struct HostPack {
   std::vector<codec::ExphLayout> lay_in, lay_out;  // exph: per-matrix layouts
   int codec_id = 0;
   uint64_t max_size = 0, total = 0, raw_bytes = 0;
+  uint64_t digest = 0;              // content digest of the host weights packed
+  // the pack of (w_in, w_out): a live cached pack of the same buffers and the
+  // same content digest is shared, unless `fresh` (always re-pack)
   static std::shared_ptr<HostPack> acquire(const void* w_in, const void* w_out, int n_experts,
-                                           uint64_t matrix_elems, int codec_id);
+                                           uint64_t matrix_elems, int codec_id, bool fresh);
   ~HostPack();
 };
 
@@ -46,7 +49,9 @@ struct Layer {
   Layer& operator=(const Layer&) = delete;
 
   void forward(const void* x, int64_t N, void* y, infmoe_forward_out* out, cudaStream_t s);
-  void set_host_weights(const void* w_in, const void* w_out);
+  // fresh_pack: re-pack the host weights for the h2d codec even if a pack of
+  // the same buffers is cached (explicit infmoe_layer_set_host_weights calls)
+  void set_host_weights(const void* w_in, const void* w_out, bool fresh_pack = true);
   // SURVEY 8(f)-4 hot-expert pinning (not in the reference): keep these local
   // experts on the device across forwards; n = 0 unpins
   void pin_experts(const int32_t* experts, int n);

@@ -51,6 +51,24 @@ def fill_uniform(t, seed: int, scale: float) -> None:
                                     _stream_ptr()))
 
 
+def occupy_sms(n_ctas: int, release, timed_out, smem_bytes: int = 200 * 1024,
+               timeout_s: float = 20.0, stream=None) -> None:
+    """Test hook: n_ctas spinning CTAs (one per SM at ~200 KB of shared memory)
+    until release[0] != 0 or the timeout; timed_out[0] = 1 if any gave up."""
+    torch = _torch()
+    _need_cuda(release, timed_out)
+    s = C.c_void_p((stream or torch.cuda.current_stream()).cuda_stream)
+    _check(_lib.infmoe_debug_occupy_sms(n_ctas, smem_bytes, _p(release), int(timeout_s * 1e9),
+                                        _p(timed_out), s))
+
+
+def set_flag(flag, stream=None) -> None:
+    torch = _torch()
+    _need_cuda(flag)
+    s = C.c_void_p((stream or torch.cuda.current_stream()).cuda_stream)
+    _check(_lib.infmoe_debug_set_flag(_p(flag), s))
+
+
 def gate_softmax_topk(x, wg, k: int, bias=None):
     torch = _torch()
     _need_cuda(x, wg, bias)
@@ -154,7 +172,7 @@ def expert_ffn_fused(x_perm, offsets, w_in, w_out, experts=None, slots=None, per
     h = torch.empty((R, f), dtype=x_perm.dtype, device=x_perm.device)
     rows_out = n_tokens if perm is not None else R
     y = torch.empty((rows_out, d), dtype=x_perm.dtype, device=x_perm.device)
-    done = torch.empty(max(E, 1), dtype=torch.int32, device=x_perm.device)
+    done = torch.empty(max(E, 1) + 1, dtype=torch.int32, device=x_perm.device)
     if experts is None:
         ex = sl = None
         n = E

@@ -137,7 +137,7 @@ int main() {
   int32_t Ts[1] = {E};
   double betas[1] = {beta};
   int32_t violations = -1;
-  CHECK(infmoe_replay_check(events.data(), 2 * E, 1, Ts, alphas.data(), betas, K + 1, 0, 2e-6,
+  CHECK(infmoe_replay_check(events.data(), 2 * E, 1, Ts, alphas.data(), betas, K, 0, 2e-6,
                             &violations, kinds));
   if (violations != 0) {
     std::fprintf(stderr, "replay_check: %d violations\n", violations);

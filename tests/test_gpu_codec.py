@@ -85,3 +85,40 @@ def test_exp4_needs_bf16(cuda):
     with pytest.raises(im.InvalidArgument):
         dv.MoELayer(d, f, E, 1, wi, wo, dtype="f32", offloaded=True, K=1, lsh_bits=2,
                     max_tokens=N, h2d_codec="exp4")
+
+
+def test_codec_packs_are_snapshots_that_follow_set_host_weights(cuda):
+    """exph packs are snapshots of the host weights (include/infmoe.h): after
+    the host buffers are refilled IN PLACE, a new codec layer created on them
+    while an old one is alive re-packs (content digest mismatch) and matches the
+    raw stream, the old layer keeps its snapshot until set_host_weights, which
+    always re-packs -- after which it matches the raw stream again."""
+    N, d, f, E, K = 256, 256, 512, 4, 1
+    t = lambda b, sh: torch.from_numpy(b.view(np.int16).reshape(sh)).view(torch.bfloat16)
+    x = t(fill_bf16(31, N * d, 1.7320508), (N, d)).to(cuda)
+    wi = t(fill_bf16(32, E * f * d, 1.7320508 / 16), (E, f, d)).pin_memory()
+    wo = t(fill_bf16(33, E * d * f, 1.534 * 1.7320508 / np.sqrt(f)), (E, d, f)).pin_memory()
+    kw = dict(gate="lsh", lsh_seed=7, lsh_bits=2, max_tokens=N, offloaded=True, K=K)
+    raw = dv.MoELayer(d, f, E, 1, wi, wo, **kw)
+    old = dv.MoELayer(d, f, E, 1, wi, wo, h2d_codec="exph", **kw)
+    y_raw0, _ = raw.forward(x)
+    y_old0, _ = old.forward(x)
+    torch.cuda.synchronize()
+    assert torch.equal(y_old0.view(torch.int16), y_raw0.view(torch.int16))
+    # refill the host weights in place (same pointers)
+    wi.copy_(t(fill_bf16(34, E * f * d, 1.7320508 / 16), (E, f, d)))
+    wo.copy_(t(fill_bf16(35, E * d * f, 1.534 * 1.7320508 / np.sqrt(f)), (E, d, f)))
+    new = dv.MoELayer(d, f, E, 1, wi, wo, h2d_codec="exph", **kw)  # old is alive: cache hit?
+    y_raw1, _ = raw.forward(x)   # the raw stream reads the host buffers live
+    y_new1, _ = new.forward(x)
+    y_old1, _ = old.forward(x)   # still the snapshot taken at create
+    torch.cuda.synchronize()
+    assert not torch.equal(y_raw1.view(torch.int16), y_raw0.view(torch.int16))
+    assert torch.equal(y_new1.view(torch.int16), y_raw1.view(torch.int16))
+    assert torch.equal(y_old1.view(torch.int16), y_raw0.view(torch.int16))
+    old.set_host_weights(wi, wo)  # re-packs
+    y_old2, _ = old.forward(x)
+    torch.cuda.synchronize()
+    assert torch.equal(y_old2.view(torch.int16), y_raw1.view(torch.int16))
+    for lay in (raw, old, new):
+        lay.close()
