@@ -65,10 +65,40 @@ uint64_t infmoe_derive_seed(uint64_t seed, uint64_t tag); /* prng.hpp:27-29 */
 /* n consecutive draws of GaussianStream(seed).next() (prng.hpp:49-71) */
 int infmoe_gaussian_fill(uint64_t seed, double* out, uint64_t n);
 
+/* The synthetic tensors of SURVEY 8(d), host side: n_mats independent
+ * GaussianStream(seeds[m]) sequences (prng.hpp:49-71, the generator of
+ * gaussian_tokens gating.hpp:108-114), each value times scales[m], rounded to
+ * dtype (INFMOE_DTYPE_BF16: double -> f32 round-to-nearest -> bf16 RNE;
+ * INFMOE_DTYPE_F32: double -> f32), n_each values into outs[m] (host memory).
+ * threads <= 0 uses every hardware thread; values do not depend on it. */
+int infmoe_gaussian_fill_typed(int32_t dtype, int32_t n_mats, const uint64_t* seeds,
+                               const double* scales, uint64_t n_each, void* const* outs,
+                               int32_t threads);
+
 /* ---- gating.hpp (host side) ------------------------------------------- */
 /* gating_projection gating.hpp:47-56: bits*hidden doubles, bit-major */
 int infmoe_gating_projection(uint64_t seed, int32_t n_hash_bits, int32_t hidden_dim,
                              double* out);
+/* lsh_codes gating.hpp:61-82 on HOST fp64 rows x[n_tokens, hidden]
+ * (GatingModel{seed, bits, hidden}): bit-identical codes (sequential fp64 dot,
+ * no contraction).  Errors as the reference: bits outside [1, 31] or hidden < 1
+ * -> 2 (ConfigError).  The device gate for bf16/f32 rows is infmoe_gate_lsh. */
+int infmoe_lsh_codes(uint64_t seed, int32_t n_hash_bits, int32_t hidden_dim, const double* x,
+                     uint64_t n_tokens, uint32_t* codes);
+/* route_tokens gating.hpp:87-104: counts[n_experts] of code mod n_experts.
+ * n_experts < 1 -> 6 (std::invalid_argument); 2^bits < n_experts -> 2 */
+int infmoe_route_tokens(uint64_t seed, int32_t n_hash_bits, int32_t hidden_dim,
+                        const double* x, uint64_t n_tokens, int32_t n_experts,
+                        uint64_t* counts);
+/* explicit_workload gating.hpp:167-175 (+ validate :25-33): *total = sum of
+ * counts; no experts -> 2 */
+int infmoe_explicit_workload(const uint64_t* counts, int32_t n_experts, uint64_t* total);
+/* workload_from_csv gating.hpp:180-219: "expert_id,token_count" rows, optional
+ * header line, ids in any order (missing ids count 0, duplicates -> 2).
+ * *n_experts = max id + 1; counts (capacity entries, may be NULL to query the
+ * size first) receives the per-expert counts; *total (may be NULL) their sum. */
+int infmoe_workload_from_csv(const char* path, uint64_t* counts, int32_t capacity,
+                             int32_t* n_experts, uint64_t* total);
 /* synthetic_workload gating.hpp:122-165; kind 0 uniform, 1 zipf, 2 balanced */
 int infmoe_synthetic_workload(int32_t kind, uint64_t total_tokens, int32_t n_experts,
                               uint64_t seed, double zipf_s, uint64_t* counts);
@@ -147,6 +177,14 @@ typedef struct {
 /* simulate(order, costs, K, mode) simulator.hpp:209-220; events[2T] */
 int infmoe_simulate(const int32_t* order, const double* alphas, int32_t T, double beta,
                     int32_t K, int32_t mode, infmoe_event* events, infmoe_sim_report* rep);
+/* run_layers (simulator.hpp:102-194) on GIVEN per-layer orders: simulate(schedule,
+ * costs, K, mode) and simulate(order, costs, K, mode) (simulator.hpp:199-220) for
+ * one layer, or a stack of layers with fixed orders (drain, or
+ * continuous_load_stream != 0).  Orders are checked as permutations. */
+int infmoe_simulate_orders(int32_t n_layers, const int32_t* T, const int32_t* orders,
+                           const double* alphas, const double* betas, int32_t K, int32_t mode,
+                           int32_t continuous_load_stream, infmoe_event* events,
+                           infmoe_sim_report* rep, infmoe_layer_report* per_layer);
 /* simulate_model(costs, K, opt) simulator.hpp:241-255.  Layer l has T[l] experts,
  * alphas concatenated, betas[l].  policy: INFMOE_POLICY_AUTO (= OrderPolicy::Greedy),
  * _NAIVE or _EXACT.  orders_out[sum T], events[2 sum T], per_layer[n_layers] (may be NULL). */
@@ -320,6 +358,15 @@ typedef struct {
   infmoe_event* events;  /* [2E] measured timeline (seconds from layer start) */
   double* exposed_copy_s;/* makespan - compute_busy on the measured timeline */
   int32_t* local_rows;   /* [E/ep_size] rows this rank computed per local expert */
+  /* per-token routing (SURVEY 8(b) infmoe_routing_out), DEVICE pointers filled
+   * in stream order (no host sync): topk_idx[N*k] expert of (token t, slot j)
+   * at t*k+j, topk_w[N*k] its gate weight, perm[N*k] the dispatch permutation
+   * (perm[pos] = t*k+j, grouped by expert, token order inside an expert),
+   * offsets[E+1] each expert's first position in perm.  Each may be NULL. */
+  int32_t* topk_idx;
+  float* topk_w;
+  int32_t* perm;
+  int32_t* offsets;
 } infmoe_forward_out;
 
 /* ---- expert parallelism (N7) ------------------------------------------ */

@@ -10,8 +10,13 @@
 // bit-identical (tests/test_planner_parity.py, tests/cpp/test_moesim_compat.cpp).
 #pragma once
 
+#include <cmath>
 #include <cstdint>
+#include <filesystem>
+#include <numbers>
 #include <optional>
+#include <random>
+#include <string_view>
 #include <span>
 #include <stdexcept>
 #include <string>
@@ -86,12 +91,106 @@ inline std::uint64_t expert_flops(const ModelGeometry& g, std::uint64_t n_tokens
   return infmoe_expert_flops(&cg, n_tokens);
 }
 
-// ---- gating.hpp (workload) ------------------------------------------------
+// ---- prng.hpp -------------------------------------------------------------
+inline constexpr std::string_view kPrngName = "mt19937_64/box-muller/v1";
+inline std::uint64_t splitmix64(std::uint64_t x) { return infmoe_splitmix64(x); }
+inline std::uint64_t derive_seed(std::uint64_t seed, std::uint64_t tag) {
+  return infmoe_derive_seed(seed, tag);
+}
+// The stream contract itself (prng.hpp:32-71): 53-bit uniforms and Box-Muller
+// with a cached spare over std::mt19937_64, whose output sequence is
+// standardised -- the library's generators produce the same values.
+inline double uniform01(std::mt19937_64& rng) {
+  return static_cast<double>(rng() >> 11) * 0x1.0p-53;
+}
+inline double uniform01_open0(std::mt19937_64& rng) {
+  return (static_cast<double>(rng() >> 11) + 1.0) * 0x1.0p-53;
+}
+inline std::uint64_t uniform_below(std::mt19937_64& rng, std::uint64_t n) {
+  return static_cast<std::uint64_t>(uniform01(rng) * static_cast<double>(n)) % n;
+}
+class GaussianStream {
+ public:
+  explicit GaussianStream(std::uint64_t seed) : rng_(seed) {}
+  double next() {
+    if (has_spare_) {
+      has_spare_ = false;
+      return spare_;
+    }
+    const double u1 = uniform01_open0(rng_);
+    const double u2 = uniform01(rng_);
+    const double r = std::sqrt(-2.0 * std::log(u1));
+    const double theta = 2.0 * std::numbers::pi * u2;
+    spare_ = r * std::sin(theta);
+    has_spare_ = true;
+    return r * std::cos(theta);
+  }
+
+ private:
+  std::mt19937_64 rng_;
+  double spare_ = 0.0;
+  bool has_spare_ = false;
+};
+
+// ---- gating.hpp -----------------------------------------------------------
 struct ExpertWorkload {
   int layer_id = 0;
   std::vector<std::uint64_t> token_counts;
   std::uint64_t total_tokens = 0;
 };
+inline void validate(const ExpertWorkload& w) {
+  std::uint64_t sum = 0;
+  for (std::uint64_t c : w.token_counts) sum += c;
+  if (sum != w.total_tokens)
+    throw ConfigError("workload: token_counts sum to " + std::to_string(sum) +
+                      ", expected total_tokens = " + std::to_string(w.total_tokens));
+  if (w.token_counts.empty()) throw ConfigError("workload: no experts");
+}
+struct GatingModel {
+  std::uint64_t projection_seed = 0;
+  int n_hash_bits = 5;
+  int hidden_dim = 0;
+};
+inline std::vector<double> gating_projection(const GatingModel& m) {
+  std::vector<double> p(m.n_hash_bits > 0 && m.hidden_dim > 0
+                            ? std::size_t(m.n_hash_bits) * std::size_t(m.hidden_dim)
+                            : 0);
+  detail::check(infmoe_gating_projection(m.projection_seed, m.n_hash_bits, m.hidden_dim,
+                                         p.data()));
+  return p;
+}
+inline std::vector<std::uint32_t> lsh_codes(const GatingModel& m,
+                                            std::span<const double> hidden_states,
+                                            std::size_t n_tokens) {
+  if (hidden_states.size() != n_tokens * static_cast<std::size_t>(m.hidden_dim))
+    throw std::invalid_argument("lsh_codes: hidden_states size != n_tokens * hidden_dim");
+  std::vector<std::uint32_t> codes(n_tokens, 0);
+  detail::check(infmoe_lsh_codes(m.projection_seed, m.n_hash_bits, m.hidden_dim,
+                                 hidden_states.data(), n_tokens, codes.data()));
+  return codes;
+}
+inline ExpertWorkload route_tokens(const GatingModel& m, std::span<const double> hidden_states,
+                                   std::size_t n_tokens, int n_experts, int layer_id = 0) {
+  if (n_experts < 1) throw std::invalid_argument("route_tokens: n_experts must be >= 1");
+  if (m.n_hash_bits >= 0 &&
+      (1u << std::min(m.n_hash_bits, 31)) < static_cast<std::uint32_t>(n_experts))
+    throw ConfigError("gating: 2^n_hash_bits must be >= n_experts");
+  if (hidden_states.size() != n_tokens * static_cast<std::size_t>(m.hidden_dim))
+    throw std::invalid_argument("lsh_codes: hidden_states size != n_tokens * hidden_dim");
+  ExpertWorkload w;
+  w.layer_id = layer_id;
+  w.token_counts.assign(std::size_t(n_experts), 0);
+  detail::check(infmoe_route_tokens(m.projection_seed, m.n_hash_bits, m.hidden_dim,
+                                    hidden_states.data(), n_tokens, n_experts,
+                                    w.token_counts.data()));
+  w.total_tokens = n_tokens;
+  return w;
+}
+inline std::vector<double> gaussian_tokens(std::uint64_t seed, std::size_t n_tokens, int dim) {
+  std::vector<double> out(n_tokens * static_cast<std::size_t>(dim));
+  detail::check(infmoe_gaussian_fill(seed, out.data(), out.size()));
+  return out;
+}
 enum class SyntheticKind { Uniform, Zipf, Balanced };
 inline ExpertWorkload synthetic_workload(SyntheticKind kind, std::uint64_t total_tokens,
                                          int n_experts, std::uint64_t seed,
@@ -104,6 +203,23 @@ inline ExpertWorkload synthetic_workload(SyntheticKind kind, std::uint64_t total
   detail::check(infmoe_synthetic_workload(k, total_tokens, n_experts, seed, zipf_s,
                                           w.token_counts.data()));
   return w;
+}
+inline ExpertWorkload explicit_workload(std::vector<std::uint64_t> counts, int layer_id = 0) {
+  ExpertWorkload w;
+  w.layer_id = layer_id;
+  detail::check(infmoe_explicit_workload(counts.data(), int32_t(counts.size()),
+                                         &w.total_tokens));
+  w.token_counts = std::move(counts);
+  return w;
+}
+inline ExpertWorkload workload_from_csv(const std::filesystem::path& path, int layer_id = 0) {
+  int32_t n = 0;
+  uint64_t total = 0;
+  const std::string p = path.string();
+  detail::check(infmoe_workload_from_csv(p.c_str(), nullptr, 0, &n, &total));
+  std::vector<std::uint64_t> counts(std::size_t(n), 0);
+  detail::check(infmoe_workload_from_csv(p.c_str(), counts.data(), n, &n, &total));
+  return explicit_workload(std::move(counts), layer_id);
 }
 
 // ---- cost_model.hpp -------------------------------------------------------
@@ -233,10 +349,23 @@ struct TimelineEvent {
   double start = 0.0;
   double end = 0.0;
 };
+struct LayerReport {
+  int layer_id = 0;
+  int n_experts = 0;
+  double start = 0.0;
+  double end = 0.0;
+  double compute_busy = 0.0;
+  double load_busy = 0.0;
+  double compute_stall = 0.0;
+  int peak_resident = 0;
+  double lower_bound = 0.0;
+  Schedule schedule;
+};
 struct SimReport {
   double makespan = 0.0, compute_busy = 0.0, load_busy = 0.0, compute_stall = 0.0;
   int peak_resident_experts = 0;
   double overlap_efficiency = 0.0;
+  std::vector<LayerReport> per_layer;
 };
 struct ModelSimOptions {
   SimMode mode = SimMode::Overlapped;
@@ -244,59 +373,93 @@ struct ModelSimOptions {
   bool continuous_load_stream = false;
   int exact_max_T = 12;
 };
+inline double lower_bound(const CostVector& c) {
+  return infmoe_lower_bound(c.alphas.data(), c.size(), c.beta);
+}
+inline Schedule order_for_policy(const CostVector& costs, int K, OrderPolicy policy,
+                                 int exact_max_T = 12) {
+  switch (policy) {
+    case OrderPolicy::Greedy: return auto_order(costs, K, exact_max_T);
+    case OrderPolicy::Naive: return naive_order(costs, K);
+    case OrderPolicy::Exact: return exact_order(costs, K, exact_max_T);
+  }
+  throw std::invalid_argument("unknown policy");
+}
 namespace detail {
-inline std::pair<std::vector<TimelineEvent>, SimReport> unpack(
-    const std::vector<infmoe_event>& ev, const infmoe_sim_report& r) {
+// the recurrence of simulator.hpp:102-194 on fixed schedules (one per layer)
+inline std::pair<std::vector<TimelineEvent>, SimReport> run(
+    std::span<const Schedule> schedules, std::span<const CostVector> costs, int K, SimMode mode,
+    bool continuous) {
+  std::vector<int32_t> T, orders;
+  std::vector<double> alphas, betas;
+  for (std::size_t l = 0; l < costs.size(); ++l) {
+    T.push_back(costs[l].size());
+    alphas.insert(alphas.end(), costs[l].alphas.begin(), costs[l].alphas.end());
+    betas.push_back(costs[l].beta);
+    if (int(schedules[l].order.size()) != costs[l].size())
+      throw std::invalid_argument("order size " + std::to_string(schedules[l].order.size()) +
+                                  " != expert count " + std::to_string(costs[l].size()));
+    orders.insert(orders.end(), schedules[l].order.begin(), schedules[l].order.end());
+  }
+  std::vector<infmoe_event> ev(2 * alphas.size());
+  std::vector<infmoe_layer_report> pl(costs.size());
+  infmoe_sim_report r;
+  check(infmoe_simulate_orders(int32_t(T.size()), T.data(), orders.data(), alphas.data(),
+                               betas.data(), K,
+                               mode == SimMode::Overlapped ? INFMOE_MODE_OVERLAPPED
+                                                           : INFMOE_MODE_SERIAL,
+                               continuous ? 1 : 0, ev.data(), &r, pl.data()));
   std::vector<TimelineEvent> out;
   out.reserve(ev.size());
   for (const auto& e : ev)
     out.push_back({e.stream == INFMOE_STREAM_LOAD ? StreamKind::Load : StreamKind::Compute,
                    e.layer_id, e.expert_id, e.start, e.end});
-  return {std::move(out), SimReport{r.makespan, r.compute_busy, r.load_busy, r.compute_stall,
-                                    r.peak_resident_experts, r.overlap_efficiency}};
+  SimReport rep{r.makespan, r.compute_busy, r.load_busy, r.compute_stall,
+                r.peak_resident_experts, r.overlap_efficiency, {}};
+  for (std::size_t l = 0; l < pl.size(); ++l)
+    rep.per_layer.push_back({pl[l].layer_id, pl[l].n_experts, pl[l].start, pl[l].end,
+                             pl[l].compute_busy, pl[l].load_busy, pl[l].compute_stall,
+                             pl[l].peak_resident, pl[l].lower_bound, schedules[l]});
+  return {std::move(out), std::move(rep)};
 }
 }  // namespace detail
 inline std::pair<std::vector<TimelineEvent>, SimReport> simulate(
-    std::span<const int> order, const CostVector& costs, int K,
+    const Schedule& schedule, const CostVector& costs, int K,
     SimMode mode = SimMode::Overlapped) {
-  std::vector<int32_t> o(order.begin(), order.end());
-  std::vector<infmoe_event> ev(2 * o.size());
-  infmoe_sim_report r;
-  detail::check(infmoe_simulate(o.data(), costs.alphas.data(), costs.size(), costs.beta, K,
-                                mode == SimMode::Overlapped ? INFMOE_MODE_OVERLAPPED
-                                                            : INFMOE_MODE_SERIAL,
-                                ev.data(), &r));
-  return detail::unpack(ev, r);
+  return detail::run(std::span<const Schedule>(&schedule, 1),
+                     std::span<const CostVector>(&costs, 1), K, mode, false);
 }
 inline std::pair<std::vector<TimelineEvent>, SimReport> simulate(
-    const Schedule& s, const CostVector& costs, int K, SimMode mode = SimMode::Overlapped) {
-  return simulate(std::span<const int>(s.order), costs, K, mode);
+    std::span<const int> order, const CostVector& costs, int K,
+    SimMode mode = SimMode::Overlapped) {
+  ConstraintReport chk = check_constraints(order, costs, K);
+  Schedule s;
+  s.order.assign(order.begin(), order.end());
+  s.feasible = chk.feasible;
+  s.slack = std::move(chk.slack);
+  s.method = ScheduleMethod::Naive;
+  return simulate(s, costs, K, mode);
 }
 inline std::pair<std::vector<TimelineEvent>, SimReport> simulate_model(
     std::span<const CostVector> layer_costs, int K, const ModelSimOptions& opt) {
-  std::vector<int32_t> T;
-  std::vector<double> alphas, betas;
-  for (const auto& c : layer_costs) {
-    T.push_back(c.size());
-    alphas.insert(alphas.end(), c.alphas.begin(), c.alphas.end());
-    betas.push_back(c.beta);
-  }
-  std::vector<int32_t> orders(alphas.size());
-  std::vector<infmoe_event> ev(2 * alphas.size());
-  infmoe_sim_report r;
-  const int pol = opt.policy == OrderPolicy::Greedy
-                      ? INFMOE_POLICY_AUTO
-                      : (opt.policy == OrderPolicy::Naive ? INFMOE_POLICY_NAIVE
-                                                          : INFMOE_POLICY_EXACT);
-  detail::check(infmoe_simulate_model(
-      int32_t(T.size()), T.data(), alphas.data(), betas.data(), K,
-      opt.mode == SimMode::Overlapped ? INFMOE_MODE_OVERLAPPED : INFMOE_MODE_SERIAL, pol,
-      opt.continuous_load_stream ? 1 : 0, opt.exact_max_T, orders.data(), ev.data(), &r,
-      nullptr));
-  return detail::unpack(ev, r);
+  if (layer_costs.empty()) throw std::invalid_argument("simulate_model: no layers");
+  std::vector<Schedule> schedules;
+  schedules.reserve(layer_costs.size());
+  for (const CostVector& c : layer_costs)
+    schedules.push_back(order_for_policy(c, K, opt.policy, opt.exact_max_T));
+  return detail::run(schedules, layer_costs, K, opt.mode, opt.continuous_load_stream);
 }
-inline double lower_bound(const CostVector& c) {
-  return infmoe_lower_bound(c.alphas.data(), c.size(), c.beta);
+inline std::pair<std::vector<TimelineEvent>, SimReport> simulate_model(
+    std::span<const ExpertWorkload> workloads, const ModelGeometry& geometry,
+    const HardwareProfile& hw, int K, const ModelSimOptions& opt) {
+  std::vector<CostVector> costs;
+  costs.reserve(workloads.size());
+  for (const ExpertWorkload& w : workloads) costs.push_back(compute_costs(w, geometry, hw));
+  return simulate_model(costs, K, opt);
+}
+inline std::string to_string(StreamKind s) { return s == StreamKind::Load ? "load" : "compute"; }
+inline std::string to_string(SimMode m) {
+  return m == SimMode::Overlapped ? "overlapped" : "serial";
 }
 
 }  // namespace infmoe::moesim

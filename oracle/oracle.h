@@ -129,6 +129,14 @@ void or_dispatch(const int32_t* topk_idx, uint64_t N, int k, int E, int32_t* off
  * it, output fp32 (caller rounds).  Threads: OpenMP over rows when available. */
 void or_expert_ffn(const float* x, uint64_t n, int d, int f, const float* w_in,
                    const float* w_out, int round_h, float* y);
+/* cpu_ffn.c — the CPU BASELINE's FFN (bench.py only; not a parity oracle):
+ * bf16 rows x [n, d], W_in [f, d], W_out [d, f] read in place, fp32
+ * accumulation (AVX512-BF16 dot products when the host has them), h [n, f]
+ * bf16 scratch = bf16(gelu_erf(.)), y [n, d] fp32. */
+void or_expert_ffn_bf16(const uint16_t* x, uint64_t n, int d, int f, const uint16_t* w_in,
+                        const uint16_t* w_out, uint16_t* h, float* y);
+/* 1 when or_expert_ffn_bf16 runs on AVX512-BF16 (vdpbf16ps), 0 generic fp32 */
+int or_cpu_ffn_isa(void);
 /* full layer in one call (gate -> dispatch -> FFN -> combine) */
 void or_combine(const float* y_perm, const int32_t* inv, const float* topk_w,
                 uint64_t N, int k, int d, float* y);

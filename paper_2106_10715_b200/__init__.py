@@ -130,7 +130,8 @@ class LayerDesc(C.Structure):
 class ForwardOut(C.Structure):
     _fields_ = [("counts", C.c_void_p), ("order", C.c_void_p), ("feasible", C.c_void_p),
                 ("events", C.c_void_p), ("exposed_copy_s", C.c_void_p),
-                ("local_rows", C.c_void_p)]
+                ("local_rows", C.c_void_p), ("topk_idx", C.c_void_p), ("topk_w", C.c_void_p),
+                ("perm", C.c_void_p), ("offsets", C.c_void_p)]
 
 
 DTYPE_BF16, DTYPE_F32 = 0, 1
@@ -157,7 +158,13 @@ _lib.infmoe_lower_bound.argtypes = [_vp, _i32, _f64]
 _lib.infmoe_dispatch_workspace_bytes.restype = C.c_size_t
 _lib.infmoe_dispatch_workspace_bytes.argtypes = [C.c_int64, _i32]
 _lib.infmoe_gaussian_fill.argtypes = [_u64, _vp, _u64]
+_lib.infmoe_gaussian_fill_typed.argtypes = [_i32, _i32, _vp, _vp, _u64, _vp, _i32]
 _lib.infmoe_gating_projection.argtypes = [_u64, _i32, _i32, _vp]
+_lib.infmoe_lsh_codes.argtypes = [_u64, _i32, _i32, _vp, _u64, _vp]
+_lib.infmoe_route_tokens.argtypes = [_u64, _i32, _i32, _vp, _u64, _i32, _vp]
+_lib.infmoe_explicit_workload.argtypes = [_vp, _i32, _vp]
+_lib.infmoe_workload_from_csv.argtypes = [C.c_char_p, _vp, _i32, _vp, _vp]
+_lib.infmoe_simulate_orders.argtypes = [_i32, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _vp, _vp, _vp]
 _lib.infmoe_synthetic_workload.argtypes = [_i32, _u64, _i32, _u64, _f64, _vp]
 _lib.infmoe_compute_costs.argtypes = [_P(Geometry), _P(Hardware), _vp, _i32, _vp, _vp]
 _lib.infmoe_check_constraints.argtypes = [_vp, _vp, _i32, _f64, _i32, _vp,
@@ -275,10 +282,74 @@ def gaussian_stream(seed: int, n: int) -> np.ndarray:
     return out
 
 
+def gaussian_fill_typed(dtype: str, seeds, scales, n_each: int, outs, threads: int = 0) -> None:
+    """SURVEY 8(d) synthetic tensors: outs[m][i] = round_dtype(GaussianStream(seeds[m])_i *
+    scales[m]) (prng.hpp:49-71).  outs: host numpy arrays or raw addresses (ints, e.g. the
+    data_ptr() of pinned torch tensors) of n_each elements each."""
+    sd = np.ascontiguousarray(np.asarray(seeds, dtype=np.uint64))
+    sc = np.ascontiguousarray(np.asarray(scales, dtype=np.float64))
+    if sd.size != sc.size or sd.size != len(outs):
+        raise ValueError("seeds, scales and outs must have one entry per matrix")
+    addr = np.array([o if isinstance(o, int) else o.ctypes.data for o in outs], dtype=np.uint64)
+    code = {"bf16": DTYPE_BF16, "f32": DTYPE_F32}[dtype]
+    _check(_lib.infmoe_gaussian_fill_typed(code, sd.size, _ptr(sd), _ptr(sc), n_each,
+                                           _ptr(addr), threads))
+
+
+def gaussian_bf16(seed: int, n: int, scale: float = 1.0) -> np.ndarray:
+    """uint16 bf16 bits of GaussianStream(seed) x scale (gaussian_tokens, gating.hpp:108-114)."""
+    out = np.empty(n, dtype=np.uint16)
+    gaussian_fill_typed("bf16", [seed], [scale], n, [out])
+    return out
+
+
 def gating_projection(seed: int, n_hash_bits: int, hidden_dim: int) -> np.ndarray:
     out = np.empty(max(n_hash_bits, 0) * max(hidden_dim, 0), dtype=np.float64)
     _check(_lib.infmoe_gating_projection(seed, n_hash_bits, hidden_dim, _ptr(out)))
     return out.reshape(n_hash_bits, hidden_dim)
+
+
+def lsh_codes(seed: int, n_hash_bits: int, hidden_dim: int, hidden_states) -> np.ndarray:
+    """lsh_codes (gating.hpp:61-82) on host fp64 rows [n_tokens, hidden_dim]: bit-exact."""
+    x = np.ascontiguousarray(np.asarray(hidden_states, dtype=np.float64))
+    n = x.size // max(hidden_dim, 1)
+    if x.size != n * hidden_dim:
+        raise InvalidArgument("lsh_codes: hidden_states size != n_tokens * hidden_dim")
+    codes = np.zeros(n, dtype=np.uint32)
+    _check(_lib.infmoe_lsh_codes(seed, n_hash_bits, hidden_dim, _ptr(x), n, _ptr(codes)))
+    return codes
+
+
+def route_tokens(seed: int, n_hash_bits: int, hidden_dim: int, hidden_states,
+                 n_experts: int) -> np.ndarray:
+    """route_tokens (gating.hpp:87-104): per-expert counts of code mod n_experts."""
+    x = np.ascontiguousarray(np.asarray(hidden_states, dtype=np.float64))
+    n = x.size // max(hidden_dim, 1)
+    if x.size != n * hidden_dim:
+        raise InvalidArgument("lsh_codes: hidden_states size != n_tokens * hidden_dim")
+    counts = np.zeros(max(n_experts, 1), dtype=np.uint64)
+    _check(_lib.infmoe_route_tokens(seed, n_hash_bits, hidden_dim, _ptr(x), n, n_experts,
+                                    _ptr(counts)))
+    return counts
+
+
+def explicit_workload(counts) -> tuple:
+    """explicit_workload (gating.hpp:167-175): (counts, total); ConfigError when empty."""
+    c = np.ascontiguousarray(np.asarray(counts, dtype=np.uint64))
+    total = C.c_uint64(0)
+    _check(_lib.infmoe_explicit_workload(_ptr(c) if c.size else None, c.size, C.byref(total)))
+    return c, int(total.value)
+
+
+def workload_from_csv(path) -> tuple:
+    """workload_from_csv (gating.hpp:180-219): (counts, total)."""
+    n = C.c_int32(0)
+    total = C.c_uint64(0)
+    p = str(path).encode()
+    _check(_lib.infmoe_workload_from_csv(p, None, 0, C.byref(n), C.byref(total)))
+    c = np.zeros(n.value, dtype=np.uint64)
+    _check(_lib.infmoe_workload_from_csv(p, _ptr(c), n.value, C.byref(n), C.byref(total)))
+    return c, int(total.value)
 
 
 WORKLOAD_KINDS = {"uniform": 0, "zipf": 1, "balanced": 2}

@@ -1,5 +1,7 @@
 // capi_host.cpp — extern "C" entry points of the planning layer (infmoe.h,
 // model_config / prng / gating / cost_model / scheduler / simulator sections).
+#include <algorithm>
+#include <climits>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -79,6 +81,61 @@ int infmoe_gaussian_fill(uint64_t seed, double* out, uint64_t n) {
   return guarded([&] {
     require(out != nullptr || n == 0, "out is NULL");
     normal_draws(seed, out, n);
+  });
+}
+int infmoe_gaussian_fill_typed(int32_t dtype, int32_t n_mats, const uint64_t* seeds,
+                               const double* scales, uint64_t n_each, void* const* outs,
+                               int32_t threads) {
+  return guarded([&] {
+    require(dtype == INFMOE_DTYPE_BF16 || dtype == INFMOE_DTYPE_F32, "gaussian fill: bad dtype");
+    require(n_mats >= 0 && (n_mats == 0 || (seeds && scales && outs)), "gaussian fill: NULL");
+    for (int m = 0; m < n_mats; ++m) require(outs[m] != nullptr || n_each == 0, "out is NULL");
+    normal_fill_typed(dtype, n_mats, seeds, scales, n_each, outs, threads);
+  });
+}
+int infmoe_lsh_codes(uint64_t seed, int32_t bits, int32_t hidden, const double* x,
+                     uint64_t n_tokens, uint32_t* codes) {
+  return guarded([&] {
+    if (bits < 1 || bits > 31) fail(kConfig, "gating: n_hash_bits must be in [1, 31]");
+    if (hidden < 1) fail(kConfig, "gating: hidden_dim must be >= 1");
+    require((x && codes) || n_tokens == 0, "lsh_codes: NULL argument");
+    lsh_codes_host(seed, bits, hidden, x, n_tokens, codes);
+  });
+}
+int infmoe_route_tokens(uint64_t seed, int32_t bits, int32_t hidden, const double* x,
+                        uint64_t n_tokens, int32_t n_experts, uint64_t* counts) {
+  return guarded([&] {
+    if (n_experts < 1) fail(kArgument, "route_tokens: n_experts must be >= 1");
+    if (bits >= 0 && (1u << std::min(bits, 31)) < uint32_t(n_experts))
+      fail(kConfig, "gating: 2^n_hash_bits must be >= n_experts");
+    if (bits < 1 || bits > 31) fail(kConfig, "gating: n_hash_bits must be in [1, 31]");
+    if (hidden < 1) fail(kConfig, "gating: hidden_dim must be >= 1");
+    require(counts && (x || n_tokens == 0), "route_tokens: NULL argument");
+    std::vector<uint32_t> codes(n_tokens);
+    lsh_codes_host(seed, bits, hidden, x, n_tokens, codes.data());
+    std::memset(counts, 0, sizeof(uint64_t) * size_t(n_experts));
+    for (uint32_t c : codes) ++counts[c % uint32_t(n_experts)];
+  });
+}
+int infmoe_explicit_workload(const uint64_t* counts, int32_t n_experts, uint64_t* total) {
+  return guarded([&] {
+    require(counts || n_experts <= 0, "explicit_workload: counts is NULL");
+    const uint64_t t = explicit_total(counts, n_experts);
+    if (total) *total = t;
+  });
+}
+int infmoe_workload_from_csv(const char* path, uint64_t* counts, int32_t capacity,
+                             int32_t* n_experts, uint64_t* total) {
+  return guarded([&] {
+    require(path && n_experts, "workload_from_csv: NULL argument");
+    const std::vector<uint64_t> c = workload_csv(path);
+    if (c.size() > size_t(INT32_MAX)) fail(kConfig, "workload csv: expert id too large");
+    *n_experts = int32_t(c.size());
+    if (total) *total = explicit_total(c.data(), int(c.size()));
+    if (counts) {
+      require(capacity >= int32_t(c.size()), "workload_from_csv: counts buffer too small");
+      std::memcpy(counts, c.data(), sizeof(uint64_t) * c.size());
+    }
   });
 }
 int infmoe_gating_projection(uint64_t seed, int32_t bits, int32_t hidden, double* out) {
@@ -196,6 +253,31 @@ int infmoe_simulate(const int32_t* order, const double* alphas, int32_t T, doubl
     std::vector<Event> ev;
     TimelineStats st = run_timeline(orders, cs, K, mode == INFMOE_MODE_SERIAL, false, &ev);
     emit_timeline(st, ev, events, rep, nullptr);
+  });
+}
+
+int infmoe_simulate_orders(int32_t n_layers, const int32_t* T, const int32_t* orders,
+                           const double* alphas, const double* betas, int32_t K, int32_t mode,
+                           int32_t continuous, infmoe_event* events, infmoe_sim_report* rep,
+                           infmoe_layer_report* per_layer) {
+  return guarded([&] {
+    if (n_layers < 1) fail(kArgument, "simulate: no layers");
+    require(T && orders && alphas && betas, "NULL argument");
+    std::vector<Costs> cs;
+    std::vector<std::vector<int>> ords;
+    std::size_t off = 0;
+    for (int32_t l = 0; l < n_layers; ++l) {
+      Costs c = to_costs(alphas + off, T[l], betas[l]);
+      check_costs(c);
+      band_check(std::span<const int>(orders + off, std::size_t(T[l])), c, K);  // validates
+      ords.emplace_back(orders + off, orders + off + T[l]);
+      cs.push_back(std::move(c));
+      off += std::size_t(T[l]);
+    }
+    std::vector<Event> ev;
+    TimelineStats st =
+        run_timeline(ords, cs, K, mode == INFMOE_MODE_SERIAL, continuous != 0, &ev);
+    emit_timeline(st, ev, events, rep, per_layer);
   });
 }
 

@@ -4,7 +4,11 @@
 #include "planner.hpp"
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
+#include <cstring>
+#include <fstream>
+#include <thread>
 #include <map>
 #include <numbers>
 #include <random>
@@ -47,6 +51,73 @@ void normal_draws(std::uint64_t seed, double* out, std::uint64_t n) {
     const double angle = 2.0 * std::numbers::pi * b;
     out[i++] = radius * std::cos(angle);
     if (i < n) out[i++] = radius * std::sin(angle);
+  }
+}
+
+// Rounding of a synthetic draw to the config dtype: double -> f32 (RN), then
+// f32 -> bf16 (RNE, the same bit trick as __float2bfloat16_rn) for bf16.
+static inline uint16_t f32_to_bf16_rne(float f) {
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  if ((u & 0x7F800000u) == 0x7F800000u && (u & 0x7FFFFFu)) return uint16_t((u >> 16) | 0x40);
+  return uint16_t((u + 0x7FFFu + ((u >> 16) & 1u)) >> 16);
+}
+
+void normal_fill_typed(int dtype, int n_mats, const std::uint64_t* seeds, const double* scales,
+                       std::uint64_t n_each, void* const* outs, int threads) {
+  const int nt = std::max(1, threads > 0 ? threads
+                                         : int(std::max(1u, std::thread::hardware_concurrency())));
+  auto store = [&](int m, std::uint64_t i, double g) {
+    const float v = static_cast<float>(g * scales[m]);
+    if (dtype == 0) static_cast<uint16_t*>(outs[m])[i] = f32_to_bf16_rne(v);
+    else static_cast<float*>(outs[m])[i] = v;
+  };
+  auto run = [&](auto&& body, std::uint64_t n_items) {  // body(item), items claimed in order
+    std::atomic<std::uint64_t> next{0};
+    auto worker = [&] {
+      for (std::uint64_t it = next++; it < n_items; it = next++) body(it);
+    };
+    std::vector<std::thread> th;
+    for (int t = 1; t < nt; ++t) th.emplace_back(worker);
+    worker();
+    for (auto& t : th) t.join();
+  };
+  if (n_mats >= nt) {  // one stream per thread, streamed straight into the output
+    run([&](std::uint64_t m) {
+          std::mt19937_64 g(seeds[m]);
+          for (std::uint64_t i = 0; i < n_each;) {
+            const double a = unit_open0(g);
+            const double b = unit_closed0(g);
+            const double radius = std::sqrt(-2.0 * std::log(a));
+            const double angle = 2.0 * std::numbers::pi * b;
+            store(int(m), i++, radius * std::cos(angle));
+            if (i < n_each) store(int(m), i++, radius * std::sin(angle));
+          }
+        },
+        std::uint64_t(n_mats));
+    return;
+  }
+  // few long streams: the engine's raw outputs sequentially (two per pair),
+  // then the Box-Muller pairs in parallel chunks (each pair depends only on
+  // its own two outputs, so the values are those of the sequential stream)
+  const std::uint64_t pairs = (n_each + 1) / 2;
+  std::vector<std::uint64_t> raw(2 * pairs);
+  for (int m = 0; m < n_mats; ++m) {
+    std::mt19937_64 g(seeds[m]);
+    for (auto& r : raw) r = g();
+    constexpr std::uint64_t kChunk = 1 << 16;  // pairs per work item
+    run([&](std::uint64_t c) {
+          const std::uint64_t p1 = std::min(pairs, (c + 1) * kChunk);
+          for (std::uint64_t p = c * kChunk; p < p1; ++p) {
+            const double a = (static_cast<double>(raw[2 * p] >> 11) + 1.0) * 0x1.0p-53;
+            const double b = static_cast<double>(raw[2 * p + 1] >> 11) * 0x1.0p-53;
+            const double radius = std::sqrt(-2.0 * std::log(a));
+            const double angle = 2.0 * std::numbers::pi * b;
+            store(m, 2 * p, radius * std::cos(angle));
+            if (2 * p + 1 < n_each) store(m, 2 * p + 1, radius * std::sin(angle));
+          }
+        },
+        (pairs + kChunk - 1) / kChunk);
   }
 }
 
@@ -96,6 +167,89 @@ std::vector<double> lsh_hyperplanes(std::uint64_t seed, int bits, int hidden) {
   std::vector<double> p(std::size_t(bits) * std::size_t(hidden));
   normal_draws(seed, p.data(), p.size());  // bit-major: plane j = p[j*hidden ...]
   return p;
+}
+
+// lsh_codes (gating.hpp:61-82): per token, bit j = (sum_d x[t,d] * P[j,d] >= 0)
+// with the products and the running sum rounded separately in ascending d
+// (this translation unit is built with -ffp-contract=off, like the reference),
+// so the codes are bit-identical.  Tokens are independent: split over threads.
+void lsh_codes_host(std::uint64_t seed, int bits, int hidden, const double* x,
+                    std::uint64_t n_tokens, std::uint32_t* codes) {
+  const std::vector<double> proj = lsh_hyperplanes(seed, bits, hidden);
+  auto rows = [&](std::uint64_t t0, std::uint64_t t1) {
+    for (std::uint64_t t = t0; t < t1; ++t) {
+      const double* row = x + t * std::uint64_t(hidden);
+      std::uint32_t code = 0;
+      for (int j = 0; j < bits; ++j) {
+        const double* hp = proj.data() + std::size_t(j) * std::size_t(hidden);
+        double dot = 0.0;
+        for (int d = 0; d < hidden; ++d) dot += row[d] * hp[d];
+        if (dot >= 0.0) code |= (1u << j);
+      }
+      codes[t] = code;
+    }
+  };
+  const std::uint64_t work = n_tokens * std::uint64_t(bits) * std::uint64_t(hidden);
+  const unsigned nt = work < (1u << 22) ? 1u
+                                        : std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+  if (nt == 1) {
+    rows(0, n_tokens);
+    return;
+  }
+  std::vector<std::thread> th;
+  const std::uint64_t per = (n_tokens + nt - 1) / nt;
+  for (unsigned i = 0; i < nt; ++i) {
+    const std::uint64_t a = std::min(n_tokens, i * per), b = std::min(n_tokens, a + per);
+    if (a < b) th.emplace_back(rows, a, b);
+  }
+  for (auto& t : th) t.join();
+}
+
+// explicit_workload + validate(ExpertWorkload) (gating.hpp:25-33, :167-175)
+std::uint64_t explicit_total(const std::uint64_t* counts, int n) {
+  if (n < 1) fail(kConfig, "workload: no experts");
+  std::uint64_t s = 0;
+  for (int e = 0; e < n; ++e) s += counts[e];
+  return s;
+}
+
+// workload_from_csv (gating.hpp:180-219): "expert_id,token_count" rows, an
+// optional header (first line only, non-numeric id), ids in any order, an id
+// listed twice is an error; expert count = max id + 1 (missing ids count 0).
+std::vector<std::uint64_t> workload_csv(const std::string& path) {
+  std::ifstream in(path);
+  if (!in) fail(kConfig, "workload csv: cannot open " + path);
+  std::vector<std::pair<std::uint64_t, std::uint64_t>> rows;
+  std::string line;
+  int lineno = 0;
+  while (std::getline(in, line)) {
+    ++lineno;
+    while (!line.empty() && (line.back() == '\r' || line.back() == '\n')) line.pop_back();
+    if (line.empty()) continue;
+    const std::size_t comma = line.find(',');
+    // both fields must be non-empty up to the end of the line
+    if (comma == std::string::npos || comma + 1 >= line.size())
+      fail(kConfig, "workload csv: line " + std::to_string(lineno) +
+                        ": expected expert_id,token_count");
+    const std::string a = line.substr(0, comma), b = line.substr(comma + 1);
+    if (lineno == 1 && a.find_first_not_of("0123456789 ") != std::string::npos) continue;
+    try {
+      rows.emplace_back(std::stoull(a), std::stoull(b));
+    } catch (const std::exception&) {
+      fail(kConfig, "workload csv: line " + std::to_string(lineno) + ": not a number: " + line);
+    }
+  }
+  if (rows.empty()) fail(kConfig, "workload csv: no rows in " + path);
+  std::uint64_t max_id = 0;
+  for (const auto& r : rows) max_id = std::max(max_id, r.first);
+  std::vector<std::uint64_t> counts(max_id + 1, 0);
+  std::vector<bool> seen(max_id + 1, false);
+  for (const auto& [id, n] : rows) {
+    if (seen[id]) fail(kConfig, "workload csv: duplicate expert_id " + std::to_string(id));
+    seen[id] = true;
+    counts[id] = n;
+  }
+  return counts;
 }
 
 std::vector<std::uint64_t> workload_counts(int kind, std::uint64_t total, int experts,

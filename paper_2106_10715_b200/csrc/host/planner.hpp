@@ -19,6 +19,11 @@ namespace infmoe {
 std::uint64_t mix64(std::uint64_t x);                       // splitmix64
 std::uint64_t child_seed(std::uint64_t seed, std::uint64_t tag);  // derive_seed
 void normal_draws(std::uint64_t seed, double* out, std::uint64_t n);
+// n_mats independent streams normal_draws(seeds[m]) x scales[m], rounded to
+// dtype (0 bf16: double -> f32 RN -> bf16 RNE; 1 f32: double -> f32 RN), n_each
+// values into outs[m]; `threads` host threads (<= 0: all)
+void normal_fill_typed(int dtype, int n_mats, const std::uint64_t* seeds, const double* scales,
+                       std::uint64_t n_each, void* const* outs, int threads);
 
 // ------------------------------------------------------------ geometry ----
 struct Geometry {  // model_config.hpp:14-22
@@ -37,6 +42,13 @@ bool preset(const std::string& name, Geometry* out);
 
 // --------------------------------------------------------------- gating ---
 std::vector<double> lsh_hyperplanes(std::uint64_t seed, int bits, int hidden);
+// lsh_codes gating.hpp:61-82 on host fp64 rows (bit-exact, threads over tokens)
+void lsh_codes_host(std::uint64_t seed, int bits, int hidden, const double* x,
+                    std::uint64_t n_tokens, std::uint32_t* codes);
+// explicit_workload's validation (gating.hpp:25-33): returns the total
+std::uint64_t explicit_total(const std::uint64_t* counts, int n);
+// workload_from_csv gating.hpp:180-219: per-expert counts
+std::vector<std::uint64_t> workload_csv(const std::string& path);
 std::vector<std::uint64_t> workload_counts(int kind, std::uint64_t total, int experts,
                                            std::uint64_t seed, double zipf_s);
 

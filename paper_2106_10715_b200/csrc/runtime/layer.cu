@@ -705,6 +705,18 @@ void Layer::forward(const void* x, int64_t N, void* y, infmoe_forward_out* out, 
   const bool timed = out && (out->events || out->exposed_copy_s);
   INFMOE_CUDA(cudaEventRecord(t_start, s));
   route(x, N, s);
+  if (out) {  // per-token routing outputs at the layer boundary (device to device)
+    const size_t A = size_t(N) * size_t(k);
+    if (out->topk_idx && A)
+      INFMOE_CUDA(cudaMemcpyAsync(out->topk_idx, idx, A * 4, cudaMemcpyDeviceToDevice, s));
+    if (out->topk_w && A)
+      INFMOE_CUDA(cudaMemcpyAsync(out->topk_w, wts, A * 4, cudaMemcpyDeviceToDevice, s));
+    if (out->perm && A)
+      INFMOE_CUDA(cudaMemcpyAsync(out->perm, perm, A * 4, cudaMemcpyDeviceToDevice, s));
+    if (out->offsets)
+      INFMOE_CUDA(cudaMemcpyAsync(out->offsets, offsets, size_t(E + 1) * 4,
+                                  cudaMemcpyDeviceToDevice, s));
+  }
 
   Rows r;
   std::vector<int32_t> local_counts;

@@ -288,6 +288,7 @@ class MoELayer:
             self._keep.append(slot_pool)  # the pool outlives the layer
         self.desc = d
         self.n_experts = n_experts
+        self.top_k = top_k
         self.n_local = n_experts // max(ep_size, 1)
         self._h = C.c_void_p()
         _check(_lib.infmoe_layer_create(C.byref(d), C.byref(self._h)))
@@ -319,10 +320,12 @@ class MoELayer:
         self.pinned = [int(e) for e in out[:n]]
         return self.pinned
 
-    def forward(self, x, y=None, *, want_timeline: bool = False, want_info: bool = True):
+    def forward(self, x, y=None, *, want_timeline: bool = False, want_info: bool = True,
+                want_routing: bool = False):
         """Run the layer on x [N, d_model] (device).  want_info=False passes no
         output struct: a resident layer then never synchronises with the host
-        (and can be captured in a CUDA graph)."""
+        (and can be captured in a CUDA graph).  want_routing adds the per-token
+        routing as device tensors: topk_idx / topk_w [N, k], perm [N*k], offsets [E+1]."""
         torch = _torch()
         N = x.shape[0]
         if y is None:
@@ -337,13 +340,24 @@ class MoELayer:
         exposed = C.c_double(0.0)
         events = (Event * (2 * El))()
         local_rows = np.zeros(El, dtype=np.int32)
+        rt = None
+        if want_routing:
+            k = self.top_k
+            rt = {"topk_idx": torch.empty((N, k), dtype=torch.int32, device=x.device),
+                  "topk_w": torch.empty((N, k), dtype=torch.float32, device=x.device),
+                  "perm": torch.empty(N * k, dtype=torch.int32, device=x.device),
+                  "offsets": torch.empty(E + 1, dtype=torch.int32, device=x.device)}
         out = ForwardOut(counts.ctypes.data, order.ctypes.data, C.addressof(feas),
                          C.addressof(events) if want_timeline else None,
                          C.addressof(exposed) if want_timeline else None,
-                         local_rows.ctypes.data)
+                         local_rows.ctypes.data,
+                         *([rt[n].data_ptr() for n in ("topk_idx", "topk_w", "perm", "offsets")]
+                           if rt else [None] * 4))
         _check(_lib.infmoe_layer_forward(self._h, _p(x), N, _p(y), C.byref(out), _stream_ptr()))
         info = {"counts": counts, "order": order, "feasible": bool(feas.value),
                 "local_rows": local_rows, "pinned": list(getattr(self, "pinned", []))}
+        if rt:
+            info.update(rt)
         if want_timeline:
             info["events"] = [(e.stream, e.layer_id, e.expert_id, e.start, e.end)
                               for e in events if e.stream >= 0]

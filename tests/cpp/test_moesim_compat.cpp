@@ -5,7 +5,9 @@
 // Both builds must print identical output (a differential test) and pass.
 #include <cstdio>
 #include <cstring>
+#include <fstream>
 #include <random>
+#include <string>
 #include <vector>
 
 #ifdef USE_INFMOE
@@ -13,6 +15,8 @@
 namespace ms = infmoe::moesim;
 #else
 #include "moesim/cost_model.hpp"
+#include "moesim/gating.hpp"
+#include "moesim/prng.hpp"
 #include "moesim/scheduler.hpp"
 #include "moesim/simulator.hpp"
 namespace ms = moesim;
@@ -107,6 +111,122 @@ int main() {
     unsigned long long bits;
     std::memcpy(&bits, &rep2.makespan, 8);
     mix(bits);
+  }
+  // ---- prng.hpp / gating.hpp: the LSH gate on host fp64 rows, workloads ----
+  auto mixd = [&](double v) {
+    unsigned long long b;
+    std::memcpy(&b, &v, 8);
+    mix(b);
+  };
+  mix(ms::derive_seed(1, 0));
+  {
+    ms::GaussianStream gs(0);
+    for (int i = 0; i < 5; ++i) mixd(gs.next());
+  }
+  const ms::GatingModel gm{ms::derive_seed(20261018, 2), 5, 256};
+  for (double v : ms::gating_projection(gm)) mixd(v);
+  const std::vector<double> hid = ms::gaussian_tokens(ms::derive_seed(20261018, 0), 700, 256);
+  mixd(hid.front());
+  mixd(hid.back());
+  const auto codes = ms::lsh_codes(gm, hid, 700);
+  for (auto c2 : codes) mix(c2);
+  const ms::ExpertWorkload rw = ms::route_tokens(gm, hid, 700, 24, 3);
+  CHECK(rw.total_tokens == 700 && rw.layer_id == 3 && rw.token_counts.size() == 24);
+  for (auto c2 : rw.token_counts) mix(c2);
+  threw = false;
+  try {
+    ms::route_tokens(ms::GatingModel{1, 3, 256}, hid, 700, 9);  // 2^3 < 9 experts
+  } catch (const ms::ConfigError&) {
+    threw = true;
+  }
+  CHECK(threw);
+  threw = false;
+  try {
+    ms::lsh_codes(gm, hid, 699);  // size mismatch
+  } catch (const std::invalid_argument&) {
+    threw = true;
+  }
+  CHECK(threw);
+  threw = false;
+  try {
+    ms::gating_projection(ms::GatingModel{1, 32, 8});
+  } catch (const ms::ConfigError&) {
+    threw = true;
+  }
+  CHECK(threw);
+  const ms::ExpertWorkload ew = ms::explicit_workload({5, 0, 7}, 2);
+  CHECK(ew.total_tokens == 12 && ew.layer_id == 2);
+  threw = false;
+  try {
+    ms::explicit_workload({});
+  } catch (const ms::ConfigError&) {
+    threw = true;
+  }
+  CHECK(threw);
+  const char* csv = "/tmp/infmoe_compat_workload.csv";
+  {
+    std::ofstream o(csv);
+    o << "expert_id,token_count\r\n3,10\n\n0,4\n1,2,9\n";
+  }
+  const ms::ExpertWorkload cw = ms::workload_from_csv(csv, 1);
+  CHECK((cw.token_counts == std::vector<std::uint64_t>{4, 2, 0, 10}) && cw.total_tokens == 16);
+  for (auto c2 : cw.token_counts) mix(c2);
+  for (const char* bad : {"0,1\n0,2\n", "0,\n", "x,1\n1,y\n", ""}) {
+    std::ofstream(csv) << bad;
+    threw = false;
+    try {
+      ms::workload_from_csv(csv);
+    } catch (const ms::ConfigError&) {
+      threw = true;
+    }
+    CHECK(threw);
+  }
+  // ---- simulate_model over workloads, per-layer reports, order_for_policy ----
+  ms::ModelGeometry small{2, 8, 64, 512, 2048, 24, 2};
+  ms::HardwareProfile hw2{2e12, 2e9, 8ull << 30, 1ull << 30};
+  std::vector<ms::ExpertWorkload> wls{rw, ms::synthetic_workload(ms::SyntheticKind::Zipf, 900,
+                                                                 24, 5, 1.0, 1)};
+  for (bool cont : {false, true}) {
+    for (ms::OrderPolicy pol : {ms::OrderPolicy::Greedy, ms::OrderPolicy::Naive}) {
+      ms::ModelSimOptions o2;
+      o2.policy = pol;
+      o2.continuous_load_stream = cont;
+      auto [evm, repm] = ms::simulate_model(wls, small, hw2, 3, o2);
+      CHECK(repm.per_layer.size() == 2);
+      mixd(repm.makespan);
+      mixd(repm.compute_stall);
+      mix(unsigned(repm.peak_resident_experts));
+      for (const auto& lr : repm.per_layer) {
+        mix(unsigned(lr.layer_id));
+        mix(unsigned(lr.n_experts));
+        mixd(lr.start);
+        mixd(lr.end);
+        mixd(lr.compute_busy);
+        mixd(lr.compute_stall);
+        mix(unsigned(lr.peak_resident));
+        mixd(lr.lower_bound);
+        for (int o : lr.schedule.order) mix(unsigned(o));
+        mix(lr.schedule.feasible);
+        mix(unsigned(lr.schedule.method));
+      }
+      for (const auto& e2 : evm) {
+        mix(unsigned(e2.stream == ms::StreamKind::Load));
+        mix(unsigned(e2.expert_id));
+        mixd(e2.end);
+      }
+      const ms::Schedule sp = ms::order_for_policy(ms::compute_costs(wls[1], small, hw2), 3, pol);
+      for (int o : sp.order) mix(unsigned(o));
+    }
+  }
+  {
+    auto [ev1, rep1] = ms::simulate(g, c, 2);
+    CHECK(rep1.per_layer.size() == 1 && rep1.per_layer[0].schedule.order == g.order);
+    mixd(rep1.per_layer[0].lower_bound);
+    std::vector<int> ord{3, 2, 1, 0};
+    auto [ev2, rep2] = ms::simulate(ord, c, 2);
+    CHECK(rep2.per_layer[0].schedule.method == ms::ScheduleMethod::Naive);
+    mixd(rep2.makespan);
+    mix(rep2.per_layer[0].schedule.feasible);
   }
   std::printf("digest %016llx failures %d\n", digest, failures);
   return failures == 0 ? 0 : 1;

@@ -10,7 +10,8 @@ ROOT = Path(__file__).resolve().parent.parent
 
 def test_reference_arm_prints_contract_line():
     r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference",
-                        "--cpu-sample", "8", "--steps", "1", "--warmup", "0"],
+                        "--cpu-sample", "8", "--steps", "1", "--warmup", "0",
+                        "--host-sets", "1"],
                        capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stderr[-2000:]
     line = json.loads(r.stdout.strip().splitlines()[-1])
@@ -20,6 +21,11 @@ def test_reference_arm_prints_contract_line():
         assert key in line, key
     assert line["value"] > 0 and line["cpu_baseline"]["cores"] >= 1
     assert line["e2e"]["h2d_bytes_per_step"] == 0
+    # the CPU path alone: the reference build and the oracle port, never the product
+    libs = line["native_libs_loaded"]
+    assert not any("libinfmoe" in p for p in libs), libs
+    assert "oracle/_ref/libmoesim_ref.so" in libs and "oracle/liboracle.so" in libs
+    assert line["config"]["layers"] == 24 and line["dtype"] == "bf16"
 
 
 def test_reference_arm_nonzero_rank_exits_quietly():

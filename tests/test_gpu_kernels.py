@@ -63,12 +63,21 @@ def _oracle_softmax(xf, wg, bias, E, k):
     (300, 512, 100, 8, "bf16", True),    # > 64 experts (16 per warp), k = 8
     (5, 8, 3, 3, "bf16", False),         # d = 8: one partial chunk, k = E
 ])
-def test_gate_softmax_topk_bitexact(cuda, N, d, E, k, dtype, use_bias):
+@pytest.mark.parametrize("inputs", ["uniform", "gaussian"])
+def test_gate_softmax_topk_bitexact(cuda, N, d, E, k, dtype, use_bias, inputs):
     seed = 99 + N
-    xb = fill_bf16(seed, N * d, 1.7320508)
-    xf = bf16_bits_to_f32(xb).reshape(N, d) if dtype == "bf16" else \
-        fill_f32(seed, N * d, 1.7320508).reshape(N, d)
-    wg = fill_f32(seed + 1, E * d, 1.7320508 / np.sqrt(d)).reshape(E, d)
+    if inputs == "gaussian":  # gaussian_tokens x, W_g = GaussianStream x d^-1/2
+        xb = im.gaussian_bf16(im.derive_seed(seed, 0), N * d)
+        xf32 = np.empty(N * d, np.float32)
+        im.gaussian_fill_typed("f32", [im.derive_seed(seed, 0)], [1.0], N * d, [xf32])
+        xf = bf16_bits_to_f32(xb).reshape(N, d) if dtype == "bf16" else xf32.reshape(N, d)
+        wg = np.ascontiguousarray((im.gaussian_stream(im.derive_seed(seed, 1), d * E) /
+                                   np.sqrt(d)).astype(np.float32).reshape(d, E).T)
+    else:
+        xb = fill_bf16(seed, N * d, 1.7320508)
+        xf = bf16_bits_to_f32(xb).reshape(N, d) if dtype == "bf16" else \
+            fill_f32(seed, N * d, 1.7320508).reshape(N, d)
+        wg = fill_f32(seed + 1, E * d, 1.7320508 / np.sqrt(d)).reshape(E, d)
     bias = (-0.8 * np.log(np.arange(1, E + 1))).astype(np.float32) if use_bias else None
     x = _bf16_tensor(xb, (N, d), cuda) if dtype == "bf16" else torch.from_numpy(xf).to(cuda)
     idx, w, cnt = dv.gate_softmax_topk(x, torch.from_numpy(wg).to(cuda), k,
@@ -101,9 +110,11 @@ def test_gate_softmax_ties_and_nan(cuda):
 
 @pytest.mark.parametrize("N,d,E,bits", [(512, 768, 8, 3), (4096, 4096, 32, 5),
                                         (3001, 1000, 64, 6), (100, 64, 3, 2)])
-def test_gate_lsh_matches_reference(cuda, N, d, E, bits):
+@pytest.mark.parametrize("inputs", ["uniform", "gaussian"])
+def test_gate_lsh_matches_reference(cuda, N, d, E, bits, inputs):
     seed = 7 + N
-    xb = fill_bf16(seed, N * d, 1.7320508)
+    xb = im.gaussian_bf16(im.derive_seed(seed, 0), N * d) if inputs == "gaussian" else \
+        fill_bf16(seed, N * d, 1.7320508)
     xf = bf16_bits_to_f32(xb).reshape(N, d)
     proj = im.gating_projection(im.derive_seed(seed, 2), bits, d)
     codes, idx, w, cnt = dv.gate_lsh(_bf16_tensor(xb, (N, d), cuda),

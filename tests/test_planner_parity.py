@@ -9,7 +9,7 @@ import numpy as np
 import pytest
 
 import paper_2106_10715_b200 as im
-from oracle_lib import REF, f64a, i32a, ptr, schedule
+from oracle_lib import REF, f32_to_bf16_bits, f64a, i32a, ptr, schedule
 
 G = json.loads((Path(__file__).parent / "golden" / "moesim_reference.json").read_text())
 DIAG_CODE = {None: -1, "feasible": 0, "too_little_compute": 1, "imbalanced": 2}
@@ -143,3 +143,25 @@ def test_random_instances_live_vs_reference():
             rc, order, feas, diag, meth = schedule("ref", cv.alphas, cv.beta, K, pol)
             assert got.order == order and got.feasible == feas
             assert DIAG_CODE[got.diagnosis] == diag and METH_CODE[got.method] == meth
+
+
+@pytest.mark.skipif(REF is None, reason="reference build (oracle/_ref) not present")
+@pytest.mark.parametrize("threads", [1, 3, 0])
+def test_gaussian_fill_typed_is_the_reference_stream(threads):
+    """infmoe_gaussian_fill_typed (the bench's and tests' synthetic tensors,
+    SURVEY 8(d)) == the reference's gaussian_tokens (prng.hpp GaussianStream) x
+    scale, rounded f32 RN -> bf16 RNE, for any thread count; one long stream
+    (parallel Box-Muller over the sequential engine outputs) and many short ones."""
+    for n_mats, n in ((1, 200_001), (7, 5_003)):
+        seeds = [im.derive_seed(77, t) for t in range(n_mats)]
+        scales = [1.0 / (t + 1.5) for t in range(n_mats)]
+        outs = [np.empty(n, np.uint16) for _ in range(n_mats)]
+        outs32 = [np.empty(n, np.float32) for _ in range(n_mats)]
+        im.gaussian_fill_typed("bf16", seeds, scales, n, outs, threads=threads)
+        im.gaussian_fill_typed("f32", seeds, scales, n, outs32, threads=threads)
+        for sd, sc, o, o32 in zip(seeds, scales, outs, outs32):
+            g = np.empty(n, np.float64)
+            REF.ref_gaussian_tokens(sd, n, 1, ptr(g))
+            v = (g * sc).astype(np.float32)
+            assert np.array_equal(o32.view(np.uint32), v.view(np.uint32))
+            assert np.array_equal(o, f32_to_bf16_bits(v))
