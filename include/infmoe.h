@@ -367,6 +367,10 @@ typedef struct {
   float* topk_w;
   int32_t* perm;
   int32_t* offsets;
+  /* input, optional: a cudaEvent_t recorded earlier on the stream; measured
+   * event times are then seconds from it (not from this forward's start), so
+   * the layers of a stack report on one time axis */
+  void* time_origin;
 } infmoe_forward_out;
 
 /* ---- expert parallelism (N7) ------------------------------------------ */
@@ -393,6 +397,13 @@ int infmoe_layer_create(const infmoe_layer_desc* desc, infmoe_layer** out);
 /* x, y: device [N, d_model] in dtype; stream: cudaStream_t or NULL. */
 int infmoe_layer_forward(infmoe_layer* layer, const void* x, int64_t N, void* y,
                          infmoe_forward_out* out, void* stream);
+/* infmoe_layer_forward with the caller's routing instead of the layer's gate:
+ * topk_idx[N*k] (device, every entry in [0, n_experts)) and topk_w[N*k]
+ * (device) -- e.g. a scenario's synthetic / explicit / CSV workload realised
+ * as token assignments.  Dispatch, executor and combine are unchanged. */
+int infmoe_layer_forward_routed(infmoe_layer* layer, const void* x, int64_t N,
+                                const int32_t* topk_idx, const float* topk_w, void* y,
+                                infmoe_forward_out* out, void* stream);
 /* point an offloaded layer at another host weight set of the same shape */
 int infmoe_layer_set_host_weights(infmoe_layer* layer, const void* w_in, const void* w_out);
 /* SURVEY 8(f)-4, NOT in the reference (its eviction is immediate):
@@ -423,6 +434,42 @@ int infmoe_codec_roundtrip(int32_t codec, const uint16_t* in, uint64_t n, uint16
 /* the same round trip decoded by the host reference decoder (no GPU needed) */
 int infmoe_codec_roundtrip_host(int32_t codec, const uint16_t* in, uint64_t n, uint16_t* out,
                                 uint64_t* pack_bytes);
+
+/* ---- scenario.hpp + the CLI front door ------------------ */
+/* parse_scenario (scenario.hpp:188-332: strict keys, presets from
+ * builtin_geometry_presets + $MOE_SIM_PRESETS, K = integer or "auto", seed from
+ * entropy when omitted) and to_json (scenario.hpp:350-406): the resolved
+ * self-contained scenario, indented JSON with sorted keys, into out (cap bytes,
+ * NUL-terminated; *len = bytes needed).  Errors 2 / 3 with the reference's
+ * messages. */
+int infmoe_scenario_resolve(const char* json_text, char* out, uint64_t cap, uint64_t* len);
+int infmoe_scenario_resolve_file(const char* path, char* out, uint64_t cap, uint64_t* len);
+typedef struct {
+  const char* out_dir;   /* NULL: the scenario's output_dir */
+  int32_t trace_format;  /* bit 0 Chrome trace JSON, bit 1 events CSV (0 = both) */
+  int32_t execute;       /* 1: also run the layers on the GPU through the offload executor
+                          * and write MEASURED timelines under <out>/measured/ */
+  int32_t device;
+  int32_t host_sets;     /* execute: distinct host weight sets aliased across layers */
+  int32_t repeats;       /* execute: stack passes per policy (the last is reported) */
+  int32_t jobs;          /* sweep: points simulated concurrently (results unchanged) */
+  int32_t has_seed;      /* 1: seed overrides the config's seed (--seed) */
+  uint64_t seed;
+} infmoe_run_options;
+/* run_scenario: per policy <out>/<policy>/{trace.json,
+ * events.csv, report.json}, <out>/summary.csv, <out>/resolved.json, and
+ * <out>/meta.json (the only file with timestamps: two runs of the same
+ * resolved scenario give byte-identical artefacts otherwise).
+ * The summary CSV is also returned in summary (cap bytes; *len needed). */
+int infmoe_scenario_run(const char* config_path, const infmoe_run_options* opt, char* summary,
+                        uint64_t cap, uint64_t* len);
+/* sweep over axis "K" | "total_tokens" | "zipf_s" |
+ * "bandwidth": one run per value under <out>/<axis>=<value>/ and
+ * <out>/sweep.csv (rows in value order, whatever opt->jobs); an axis the
+ * scenario cannot take -> 2. */
+int infmoe_scenario_sweep(const char* config_path, const char* axis, const double* values,
+                          int32_t n_values, const infmoe_run_options* opt, char* table,
+                          uint64_t cap, uint64_t* len);
 
 #ifdef __cplusplus
 }

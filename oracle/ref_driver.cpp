@@ -91,6 +91,23 @@ int ref_route_tokens(uint64_t seed, int bits, int hidden, const double* x, uint6
     std::memcpy(counts, w.token_counts.data(), sizeof(uint64_t) * E);
   });
 }
+// workload_from_csv / explicit_workload (gating.hpp:167-219); returns the
+// guard code (2 = ConfigError); counts receives up to cap entries
+int ref_workload_from_csv(const char* path, uint64_t* counts, int cap, int* n_experts,
+                          uint64_t* total) {
+  return guard([&] {
+    auto w = workload_from_csv(path);
+    *n_experts = int(w.token_counts.size());
+    *total = w.total_tokens;
+    for (int e = 0; e < *n_experts && e < cap; ++e) counts[e] = w.token_counts[size_t(e)];
+  });
+}
+int ref_explicit_workload(const uint64_t* counts, int n, uint64_t* total) {
+  return guard([&] {
+    auto w = explicit_workload(std::vector<uint64_t>(counts, counts + n));
+    *total = w.total_tokens;
+  });
+}
 int ref_synthetic_workload(int kind, uint64_t total, int E, uint64_t seed, double s,
                            uint64_t* counts) {
   return guard([&] {

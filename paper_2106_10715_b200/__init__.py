@@ -131,7 +131,7 @@ class ForwardOut(C.Structure):
     _fields_ = [("counts", C.c_void_p), ("order", C.c_void_p), ("feasible", C.c_void_p),
                 ("events", C.c_void_p), ("exposed_copy_s", C.c_void_p),
                 ("local_rows", C.c_void_p), ("topk_idx", C.c_void_p), ("topk_w", C.c_void_p),
-                ("perm", C.c_void_p), ("offsets", C.c_void_p)]
+                ("perm", C.c_void_p), ("offsets", C.c_void_p), ("time_origin", C.c_void_p)]
 
 
 DTYPE_BF16, DTYPE_F32 = 0, 1
@@ -199,6 +199,8 @@ _lib.infmoe_ep_comm_init.argtypes = [_vp, _i32, _i32, _P(_vp)]
 _lib.infmoe_ep_comm_destroy.argtypes = [_vp]
 _lib.infmoe_layer_create.argtypes = [_P(LayerDesc), _P(_vp)]
 _lib.infmoe_layer_forward.argtypes = [_vp, _vp, C.c_int64, _vp, _P(ForwardOut), _vp]
+_lib.infmoe_layer_forward_routed.argtypes = [_vp, _vp, C.c_int64, _vp, _vp, _vp,
+                                             _P(ForwardOut), _vp]
 _lib.infmoe_layer_set_host_weights.argtypes = [_vp, _vp, _vp]
 _lib.infmoe_layer_pin_experts.argtypes = [_vp, _vp, _i32]
 _lib.infmoe_layer_pin_hottest.argtypes = [_vp, _i32, _vp]

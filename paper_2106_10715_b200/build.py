@@ -40,8 +40,26 @@ CXX_SOURCES = [
     "host/planner.cpp",
     "host/capi_host.cpp",
     "host/ep_plan.cpp",
+    "host/scenario.cpp",
     "runtime/nccl_shim.cpp",
+    "runtime/scenario_run.cpp",
+    "runtime/capi_scenario.cpp",
 ]
+CLI = OUT_DIR / "infmoe"
+
+
+def _json_include() -> str:
+    """nlohmann json 3.11.3 (header-only; compile time only): the copy the image
+    ships with cudnn_frontend, the same release the reference vendors."""
+    import sysconfig
+    cands = [Path(sysconfig.get_paths()["purelib"]) / "include" / "cudnn_frontend" /
+             "thirdparty" / "nlohmann",
+             Path("/opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/"
+                  "thirdparty/nlohmann")]
+    for c in cands:
+        if (c / "json.hpp").exists():
+            return str(c)
+    raise RuntimeError("json.hpp (nlohmann 3.11.3) not found")
 
 
 def _headers_digest() -> str:
@@ -65,7 +83,8 @@ def _compile(src: str, digest: str, verbose: bool) -> Path:
                "--expt-relaxed-constexpr", *INCLUDES, "-c", str(path), "-o", str(obj)]
     else:
         cmd = [HOST_CXX, "-O2", "-std=c++20", "-fPIC", "-Wall", "-ffp-contract=off",
-               *INCLUDES, f"-I/usr/local/cuda/include", "-c", str(path), "-o", str(obj)]
+               *INCLUDES, f"-I/usr/local/cuda/include", f"-I{_json_include()}", "-c", str(path),
+               "-o", str(obj)]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"compile failed: {src}\n{' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
@@ -88,6 +107,7 @@ def build(verbose: bool = False) -> Path:
                               .encode()).hexdigest()
     link_stamp = OBJ_DIR / "libinfmoe.stamp"
     if LIB.exists() and link_stamp.exists() and link_stamp.read_text() == link_key:
+        _build_cli(link_key)
         return LIB
     cmd = [NVCC, *ARCH, "-shared", "-ccbin", HOST_CXX, "-o", str(LIB), *map(str, objs),
            "-lcudart", "-ldl", "-Xlinker", "-rpath,/usr/local/cuda/lib64"]
@@ -95,7 +115,24 @@ def build(verbose: bool = False) -> Path:
     if r.returncode != 0:
         raise RuntimeError(f"link failed\n{' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
     link_stamp.write_text(link_key)
+    _build_cli(link_key)
     return LIB
+
+
+def _build_cli(link_key: str) -> None:
+    """The scenario CLI (`infmoe run|sweep|resolve`), a thin C++ front end over
+    libinfmoe.so (loaded from its own directory)."""
+    src = CSRC / "cli" / "infmoe_cli.cpp"
+    key = hashlib.sha256(src.read_bytes() + link_key.encode()).hexdigest()
+    stamp = OBJ_DIR / "infmoe_cli.stamp"
+    if CLI.exists() and stamp.exists() and stamp.read_text() == key:
+        return
+    cmd = [HOST_CXX, "-O2", "-std=c++20", "-Wall", *INCLUDES, str(src), "-o", str(CLI),
+           f"-L{OUT_DIR}", "-linfmoe", "-Wl,-rpath,$ORIGIN"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"cli build failed\n{' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
+    stamp.write_text(key)
 
 
 if __name__ == "__main__":

@@ -68,6 +68,10 @@ void normal_fill_typed(int dtype, int n_mats, const std::uint64_t* seeds, const 
   const int nt = std::max(1, threads > 0 ? threads
                                          : int(std::max(1u, std::thread::hardware_concurrency())));
   auto store = [&](int m, std::uint64_t i, double g) {
+    if (dtype == 2) {  // f64: the draws themselves, times the scale
+      static_cast<double*>(outs[m])[i] = g * scales[m];
+      return;
+    }
     const float v = static_cast<float>(g * scales[m]);
     if (dtype == 0) static_cast<uint16_t*>(outs[m])[i] = f32_to_bf16_rne(v);
     else static_cast<float*>(outs[m])[i] = v;

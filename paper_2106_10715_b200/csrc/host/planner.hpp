@@ -20,7 +20,7 @@ std::uint64_t mix64(std::uint64_t x);                       // splitmix64
 std::uint64_t child_seed(std::uint64_t seed, std::uint64_t tag);  // derive_seed
 void normal_draws(std::uint64_t seed, double* out, std::uint64_t n);
 // n_mats independent streams normal_draws(seeds[m]) x scales[m], rounded to
-// dtype (0 bf16: double -> f32 RN -> bf16 RNE; 1 f32: double -> f32 RN), n_each
+// dtype (0 bf16: double -> f32 RN -> bf16 RNE; 1 f32: double -> f32 RN; 2 f64), n_each
 // values into outs[m]; `threads` host threads (<= 0: all)
 void normal_fill_typed(int dtype, int n_mats, const std::uint64_t* seeds, const double* scales,
                        std::uint64_t n_each, void* const* outs, int threads);

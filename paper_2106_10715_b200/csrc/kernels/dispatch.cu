@@ -288,6 +288,17 @@ int grid_for_rows(int64_t rows, int warps_per_block) {
 
 }  // namespace
 
+__global__ void counts_from_offsets_kernel(const int32_t* __restrict__ offsets, int E,
+                                           int32_t* __restrict__ counts) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x)
+    counts[e] = offsets[e + 1] - offsets[e];
+}
+
+void launch_counts_from_offsets(const int32_t* offsets, int E, int32_t* counts, cudaStream_t s) {
+  counts_from_offsets_kernel<<<(E + 255) / 256, 256, 0, s>>>(offsets, E, counts);
+  INFMOE_LAUNCH_CHECK();
+}
+
 size_t dispatch_workspace_bytes(int64_t n_assign, int E) {
   const int64_t chunks = std::max<int64_t>(1, (n_assign + kChunkAssign - 1) / kChunkAssign);
   return size_t(chunks) * size_t(E) * sizeof(int32_t);

@@ -29,6 +29,8 @@ void launch_gate_lsh(const void* x, int dtype, int64_t N, int d, const double* p
 size_t dispatch_workspace_bytes(int64_t n_assign, int E);
 void launch_dispatch(const int32_t* topk_idx, int64_t n_assign, int E, int32_t* offsets,
                      int32_t* perm, int32_t* inv, void* workspace, cudaStream_t stream);
+// counts[e] = offsets[e+1] - offsets[e] (routing given by the caller)
+void launch_counts_from_offsets(const int32_t* offsets, int E, int32_t* counts, cudaStream_t s);
 void launch_gather_rows(const void* x, int dtype, int64_t N, int d, int k, const int32_t* perm,
                         void* x_perm, cudaStream_t stream);
 // x_perm[inv[t*k+j]] = x[t]: the same x_perm, each token row read once

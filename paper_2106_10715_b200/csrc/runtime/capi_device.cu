@@ -284,6 +284,16 @@ int infmoe_layer_create(const infmoe_layer_desc* desc, infmoe_layer** out) {
   });
 }
 
+int infmoe_layer_forward_routed(infmoe_layer* layer, const void* x, int64_t N,
+                                const int32_t* topk_idx, const float* topk_w, void* y,
+                                infmoe_forward_out* out, void* stream) {
+  return guarded([&] {
+    require(layer && layer->impl && (N == 0 || (x && y && topk_idx && topk_w)),
+            "layer_forward_routed: NULL argument");
+    layer->impl->forward(x, N, y, out, as_stream(stream), topk_idx, topk_w);
+  });
+}
+
 int infmoe_layer_forward(infmoe_layer* layer, const void* x, int64_t N, void* y,
                          infmoe_forward_out* out, void* stream) {
   return guarded([&] {

@@ -330,15 +330,24 @@ Layer::~Layer() {
   for (void* p : owned) cudaFree(p);
 }
 
-void Layer::route(const void* x, int64_t N, cudaStream_t s) {
+void Layer::route(const void* x, int64_t N, cudaStream_t s, const int32_t* given_idx,
+                  const float* given_w) {
   const int E = desc.n_experts, k = desc.top_k;
-  if (desc.gate_kind == INFMOE_GATE_LSH)
+  if (given_idx) {  // the caller's routing: assignments and weights, no gate
+    const size_t A = size_t(N) * size_t(k);
+    if (A) {
+      INFMOE_CUDA(cudaMemcpyAsync(idx, given_idx, A * 4, cudaMemcpyDeviceToDevice, s));
+      INFMOE_CUDA(cudaMemcpyAsync(wts, given_w, A * 4, cudaMemcpyDeviceToDevice, s));
+    }
+  } else if (desc.gate_kind == INFMOE_GATE_LSH) {
     launch_gate_lsh(x, desc.dtype, N, desc.d_model, proj, desc.lsh_bits, E, nullptr, idx, wts,
                     counts, s);
-  else
+  } else {
     launch_gate_softmax(x, desc.dtype, N, desc.d_model, gate_w, gate_b, E, k, idx, wts, counts,
                         s);
+  }
   launch_dispatch(idx, N * k, E, offsets, perm, inv, dws, s);
+  if (given_idx) launch_counts_from_offsets(offsets, E, counts, s);
   // the PEER transport pushes token rows straight from x (no x_perm)
   if (!ep_peer) {
     if (k > 1) launch_gather_rows_by_token(x, desc.dtype, N, desc.d_model, k, inv, xp, s);
@@ -697,14 +706,15 @@ void Layer::ep_exchange_back(cudaStream_t s) {
   nccl::check(nc.GroupEnd(), "ncclGroupEnd");
 }
 
-void Layer::forward(const void* x, int64_t N, void* y, infmoe_forward_out* out, cudaStream_t s) {
+void Layer::forward(const void* x, int64_t N, void* y, infmoe_forward_out* out, cudaStream_t s,
+                    const int32_t* given_idx, const float* given_w) {
   require(N >= 0 && N <= desc.max_tokens, "forward: N exceeds max_tokens");
   INFMOE_CUDA(cudaSetDevice(desc.device));
   const int E = desc.n_experts, k = desc.top_k;
   const bool offloaded = desc.residency == INFMOE_OFFLOADED;
   const bool timed = out && (out->events || out->exposed_copy_s);
   INFMOE_CUDA(cudaEventRecord(t_start, s));
-  route(x, N, s);
+  route(x, N, s, given_idx, given_w);
   if (out) {  // per-token routing outputs at the layer boundary (device to device)
     const size_t A = size_t(N) * size_t(k);
     if (out->topk_idx && A)
@@ -784,11 +794,21 @@ void Layer::forward(const void* x, int64_t N, void* y, infmoe_forward_out* out, 
     else std::memcpy(out->local_rows, counts_host, sizeof(int32_t) * n_local);
   }
   if (!timed) return;
+  // event times are seconds from this forward's start, or from the caller's
+  // origin event (out->time_origin) so a stack's layers share one time axis
+  double base = 0.0;
+  if (out->time_origin) {
+    float o = 0;
+    INFMOE_CUDA(cudaEventElapsedTime(&o, reinterpret_cast<cudaEvent_t>(out->time_origin),
+                                     t_start));
+    base = double(o) * 1e-3;
+  }
   if (!offloaded) {
     float a = 0, b = 0;
     INFMOE_CUDA(cudaEventElapsedTime(&a, t_start, t_comp0[0]));
     INFMOE_CUDA(cudaEventElapsedTime(&b, t_start, t_comp1[0]));
-    if (out->events) out->events[0] = {INFMOE_STREAM_COMPUTE, 0, -1, a * 1e-3, b * 1e-3};
+    if (out->events)
+      out->events[0] = {INFMOE_STREAM_COMPUTE, 0, -1, base + a * 1e-3, base + b * 1e-3};
     if (out->exposed_copy_s) *out->exposed_copy_s = 0.0;
     return;
   }
@@ -802,7 +822,7 @@ void Layer::forward(const void* x, int64_t N, void* y, infmoe_forward_out* out, 
     if (out->events)
       for (int i = 0; i < n_pinned_run; ++i)
         out->events[2 * (n_scheduled + i) + 1] = {INFMOE_STREAM_COMPUTE, 0, pinned_run[size_t(i)],
-                                                  a * 1e-3, b * 1e-3};
+                                                  base + a * 1e-3, base + b * 1e-3};
     busy += (b - a) * 1e-3;
     makespan = std::max(makespan, double(b) * 1e-3);
   }
@@ -814,8 +834,8 @@ void Layer::forward(const void* x, int64_t N, void* y, infmoe_forward_out* out, 
     INFMOE_CUDA(cudaEventElapsedTime(&c1, t_start, t_comp1[size_t(j)]));
     const int e = exec_order[size_t(j)];
     if (out->events) {
-      out->events[2 * j] = {INFMOE_STREAM_LOAD, 0, e, a * 1e-3, b * 1e-3};
-      out->events[2 * j + 1] = {INFMOE_STREAM_COMPUTE, 0, e, c0 * 1e-3, c1 * 1e-3};
+      out->events[2 * j] = {INFMOE_STREAM_LOAD, 0, e, base + a * 1e-3, base + b * 1e-3};
+      out->events[2 * j + 1] = {INFMOE_STREAM_COMPUTE, 0, e, base + c0 * 1e-3, base + c1 * 1e-3};
     }
     busy += (c1 - c0) * 1e-3;
     makespan = std::max(makespan, double(c1) * 1e-3);

@@ -48,7 +48,10 @@ struct Layer {
   Layer(const Layer&) = delete;
   Layer& operator=(const Layer&) = delete;
 
-  void forward(const void* x, int64_t N, void* y, infmoe_forward_out* out, cudaStream_t s);
+  // given_idx / given_w (device [N*k], optional): the caller's routing instead
+  // of the layer's gate (infmoe_layer_forward_routed)
+  void forward(const void* x, int64_t N, void* y, infmoe_forward_out* out, cudaStream_t s,
+               const int32_t* given_idx = nullptr, const float* given_w = nullptr);
   // fresh_pack: re-pack the host weights for the h2d codec even if a pack of
   // the same buffers is cached (explicit infmoe_layer_set_host_weights calls)
   void set_host_weights(const void* w_in, const void* w_out, bool fresh_pack = true);
@@ -75,7 +78,8 @@ struct Layer {
     void* y;                  // [rows, d_model]
     const int32_t* counts;    // host [n_local] rows per local expert (may be NULL: resident)
   };
-  void route(const void* x, int64_t N, cudaStream_t s);
+  void route(const void* x, int64_t N, cudaStream_t s, const int32_t* given_idx,
+             const float* given_w);
   void compute_resident(const Rows& r, bool timed, cudaStream_t s);  // grouped GEMM pair
   void compute_offloaded(const Rows& r, bool timed, infmoe_forward_out* out, cudaStream_t s);
   void ffn(const Rows& r, const int32_t* experts, const int32_t* slots, int n, const void* w_in,

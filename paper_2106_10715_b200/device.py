@@ -321,17 +321,27 @@ class MoELayer:
         return self.pinned
 
     def forward(self, x, y=None, *, want_timeline: bool = False, want_info: bool = True,
-                want_routing: bool = False):
+                want_routing: bool = False, routing=None, time_origin=None):
         """Run the layer on x [N, d_model] (device).  want_info=False passes no
         output struct: a resident layer then never synchronises with the host
         (and can be captured in a CUDA graph).  want_routing adds the per-token
-        routing as device tensors: topk_idx / topk_w [N, k], perm [N*k], offsets [E+1]."""
+        routing as device tensors: topk_idx / topk_w [N, k], perm [N*k], offsets [E+1].
+        routing=(topk_idx, topk_w) (device int32 / f32 [N, k]) replaces the gate
+        (infmoe_layer_forward_routed); time_origin (a torch.cuda.Event recorded
+        earlier) puts the measured timeline on that event's time axis."""
         torch = _torch()
         N = x.shape[0]
         if y is None:
             y = torch.empty_like(x)
+        def call(out):
+            if routing is None:
+                return _lib.infmoe_layer_forward(self._h, _p(x), N, _p(y), out, _stream_ptr())
+            ti, tw = routing
+            _need_cuda(ti, tw)
+            return _lib.infmoe_layer_forward_routed(self._h, _p(x), N, _p(ti), _p(tw), _p(y), out,
+                                                    _stream_ptr())
         if not want_info and not want_timeline:
-            _check(_lib.infmoe_layer_forward(self._h, _p(x), N, _p(y), None, _stream_ptr()))
+            _check(call(None))
             return y, None
         E, El = self.n_experts, self.n_local
         counts = np.zeros(E, dtype=np.int32)
@@ -352,8 +362,9 @@ class MoELayer:
                          C.addressof(exposed) if want_timeline else None,
                          local_rows.ctypes.data,
                          *([rt[n].data_ptr() for n in ("topk_idx", "topk_w", "perm", "offsets")]
-                           if rt else [None] * 4))
-        _check(_lib.infmoe_layer_forward(self._h, _p(x), N, _p(y), C.byref(out), _stream_ptr()))
+                           if rt else [None] * 4),
+                         None if time_origin is None else time_origin.cuda_event)
+        _check(call(C.byref(out)))
         info = {"counts": counts, "order": order, "feasible": bool(feas.value),
                 "local_rows": local_rows, "pinned": list(getattr(self, "pinned", []))}
         if rt:

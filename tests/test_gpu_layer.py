@@ -320,3 +320,30 @@ def test_layer_error_paths(cuda):
         lay.close()
     finally:
         im.ep_comm_destroy(comm)
+
+
+@pytest.mark.parametrize("gate,k,offloaded", [("lsh", 1, False), ("softmax", 2, True)])
+def test_forward_routing_outputs(cuda, gate, k, offloaded):
+    """infmoe_forward_out's per-token routing (topk_idx, topk_w, perm, offsets;
+    device pointers filled in stream order) equals the standalone gate and
+    dispatch kernels on the same input."""
+    N, d, f, E = 300, 256, 384, 8
+    (_, _, _), (x, wi, wo) = _setup(cuda, N, d, f, E, seed=71)
+    gw = (np.random.default_rng(3).standard_normal((E, d)) / np.sqrt(d)).astype(np.float32)
+    w_in, w_out = (wi.pin_memory(), wo.pin_memory()) if offloaded else (wi.to(cuda), wo.to(cuda))
+    lay = dv.MoELayer(d, f, E, k, w_in, w_out, gate=gate, gate_weight=gw, lsh_seed=9,
+                      lsh_bits=3, max_tokens=N, offloaded=offloaded, K=2)
+    _, info = lay.forward(x, want_routing=True)
+    if gate == "lsh":
+        proj = torch.from_numpy(im.gating_projection(9, 3, d)).to(cuda)
+        _, idx, w, cnt = dv.gate_lsh(x, proj, E)
+    else:
+        idx, w, cnt = dv.gate_softmax_topk(x, torch.from_numpy(gw).to(cuda), k)
+    offs, perm, _ = dv.dispatch(idx, E)
+    torch.cuda.synchronize()
+    assert torch.equal(info["topk_idx"].view(-1), idx.view(-1))
+    assert torch.equal(info["topk_w"].view(-1), w.view(-1))
+    assert torch.equal(info["perm"], perm.view(-1))
+    assert torch.equal(info["offsets"], offs.view(-1))
+    assert np.array_equal(info["counts"], cnt.cpu().numpy())
+    lay.close()
