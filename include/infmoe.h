@@ -346,6 +346,19 @@ typedef struct {
    * infmoe_layer_set_host_weights leaves a codec layer on the old snapshot.
    * Outputs are identical; the scheduler's costs stay the reference's. */
   int32_t h2d_codec;
+  /* continuous_load_stream (simulator.hpp:99-101, :131-133; scenario.hpp:98;
+   * default 0 = the reference's drain mode).  A layer's loads depend on its
+   * routing, i.e. on the previous layer's output, so the executor realises the
+   * continuous lane SPECULATIVELY: once this layer's last load is issued, it
+   * streams the first prefetch_depth experts of the layer set with
+   * infmoe_layer_set_next, in the InfMoE order of that layer's predicted counts
+   * (an EMA of its routed rows), into that layer's own slots; the next forward
+   * reuses the leading positions whose expert matches its real order and loads
+   * the rest as usual.  Outputs are unchanged.  Layers sharing a slot pool
+   * need a pool with 2 slot sets (infmoe_slot_pool_create_ex): consecutive
+   * layers use alternate sets ("each layer has its own K slots"). */
+  int32_t continuous_load_stream;
+  int32_t prefetch_depth; /* 0: 1 position; at most K */
 } infmoe_layer_desc;
 enum { INFMOE_EP_NCCL = 0, INFMOE_EP_PEER = 1 };
 enum { INFMOE_CODEC_RAW = 0, INFMOE_CODEC_EXP4 = 1, INFMOE_CODEC_EXPH = 2 };
@@ -371,6 +384,9 @@ typedef struct {
    * event times are then seconds from it (not from this forward's start), so
    * the layers of a stack report on one time axis */
   void* time_origin;
+  /* output, optional: leading positions of this forward's load order whose
+   * copies the previous layer prefetched and that were reused (continuous) */
+  int32_t* prefetched;
 } infmoe_forward_out;
 
 /* ---- expert parallelism (N7) ------------------------------------------ */
@@ -391,6 +407,10 @@ int infmoe_ep_comm_destroy(void* comm);
 /* K+1 slots of expert_matrix_bytes (= d_ff * d_model * bytes/param) per matrix */
 int infmoe_slot_pool_create(int32_t device, int32_t K, uint64_t expert_matrix_bytes,
                             infmoe_slot_pool** out);
+/* the same with `sets` independent sets of K+1 slots (sets = 2 for stacks of
+ * continuous_load_stream layers: consecutive layers use alternate sets) */
+int infmoe_slot_pool_create_ex(int32_t device, int32_t K, uint64_t expert_matrix_bytes,
+                               int32_t sets, infmoe_slot_pool** out);
 int infmoe_slot_pool_destroy(infmoe_slot_pool* pool);
 
 int infmoe_layer_create(const infmoe_layer_desc* desc, infmoe_layer** out);
@@ -404,6 +424,12 @@ int infmoe_layer_forward(infmoe_layer* layer, const void* x, int64_t N, void* y,
 int infmoe_layer_forward_routed(infmoe_layer* layer, const void* x, int64_t N,
                                 const int32_t* topk_idx, const float* topk_w, void* y,
                                 infmoe_forward_out* out, void* stream);
+/* continuous_load_stream: `next` is the layer forwarded after `layer` (may be
+ * the first layer of the stack, closing the cycle for the next batch); both
+ * offloaded with continuous_load_stream, on one device.  Layers sharing a
+ * pool alternate slot sets along the chain (an odd cycle on one pool -> 6).
+ * next == NULL unlinks. */
+int infmoe_layer_set_next(infmoe_layer* layer, infmoe_layer* next);
 /* point an offloaded layer at another host weight set of the same shape */
 int infmoe_layer_set_host_weights(infmoe_layer* layer, const void* w_in, const void* w_out);
 /* SURVEY 8(f)-4, NOT in the reference (its eviction is immediate):

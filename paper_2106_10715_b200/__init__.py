@@ -124,14 +124,16 @@ class LayerDesc(C.Structure):
                 ("w_in", C.c_void_p), ("w_out", C.c_void_p), ("hw", Hardware),
                 ("ep_size", C.c_int32), ("ep_rank", C.c_int32), ("ep_comm", C.c_void_p),
                 ("skip_empty_experts", C.c_int32), ("slot_pool", C.c_void_p),
-                ("ep_transport", C.c_int32), ("h2d_codec", C.c_int32)]
+                ("ep_transport", C.c_int32), ("h2d_codec", C.c_int32),
+                ("continuous_load_stream", C.c_int32), ("prefetch_depth", C.c_int32)]
 
 
 class ForwardOut(C.Structure):
     _fields_ = [("counts", C.c_void_p), ("order", C.c_void_p), ("feasible", C.c_void_p),
                 ("events", C.c_void_p), ("exposed_copy_s", C.c_void_p),
                 ("local_rows", C.c_void_p), ("topk_idx", C.c_void_p), ("topk_w", C.c_void_p),
-                ("perm", C.c_void_p), ("offsets", C.c_void_p), ("time_origin", C.c_void_p)]
+                ("perm", C.c_void_p), ("offsets", C.c_void_p), ("time_origin", C.c_void_p),
+                ("prefetched", C.c_void_p)]
 
 
 DTYPE_BF16, DTYPE_F32 = 0, 1
@@ -221,6 +223,8 @@ def codec_roundtrip_host(bits, codec: str = "exph"):
     return out, nb.value
 _lib.infmoe_layer_h2d_bytes.argtypes = [_vp, _vp, _vp]
 _lib.infmoe_slot_pool_create.argtypes = [_i32, _i32, _u64, _P(_vp)]
+_lib.infmoe_slot_pool_create_ex.argtypes = [_i32, _i32, _u64, _i32, _P(_vp)]
+_lib.infmoe_layer_set_next.argtypes = [_vp, _vp]
 _lib.infmoe_slot_pool_destroy.argtypes = [_vp]
 
 

@@ -11,8 +11,10 @@
 //                  the owners of the experts (fused into the FFN epilogue).
 // The exchange plan is computed on the device from counts[P][E], so a
 // resident layer needs no host round trip between its kernels.  Three
-// stream-ordered barriers (a 1-int all-reduce, see layer.cu) separate
-// "counts pushed" / "rows pushed" / "results pushed" across ranks.
+// stream-ordered barriers separate "counts pushed" / "rows pushed" / "results
+// pushed" across ranks: device-side epoch flags in the symmetric flags[P]
+// buffers (ep_flag_barrier_kernel: no collective, no host), or a 1-int NCCL
+// all-reduce when the ranks share one process (layer.cu peer_barrier).
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -86,7 +88,42 @@ __global__ void ep_dispatch_push_kernel(const uint4* __restrict__ x, const int32
   __threadfence_system();
 }
 
+// Cross-rank barrier on epoch flags: rank `me` stores `epoch` into slot `me`
+// of every rank's flags[P] (release, system scope, after a system fence that
+// orders this rank's earlier peer stores), then waits until every slot of its
+// own flags[] reached `epoch` (acquire).  Epochs only grow (wrap-safe compare).
+// A rank that never arrives traps after `timeout_ns` instead of hanging.
+__global__ void ep_flag_barrier_kernel(uint32_t* const* __restrict__ peer_flags,
+                                       uint32_t* __restrict__ my_flags, int me, int P,
+                                       uint32_t epoch, uint64_t timeout_ns) {
+  const int t = threadIdx.x;
+  __threadfence_system();
+  __syncthreads();
+  if (t < P) {
+    uint32_t* dst = peer_flags[t] + me;
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(dst), "r"(epoch) : "memory");
+    uint64_t t0, now;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (;;) {
+      uint32_t v;
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(my_flags + t) : "memory");
+      if (int32_t(v - epoch) >= 0) break;
+      __nanosleep(200);
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+      if (now - t0 > timeout_ns) __trap();  // a peer never arrived
+    }
+  }
+  __syncthreads();
+  __threadfence_system();
+}
+
 }  // namespace
+
+void launch_ep_flag_barrier(uint32_t* const* peer_flags, uint32_t* my_flags, int me, int P,
+                            uint32_t epoch, uint64_t timeout_ns, cudaStream_t s) {
+  ep_flag_barrier_kernel<<<1, 32, 0, s>>>(peer_flags, my_flags, me, P, epoch, timeout_ns);
+  INFMOE_LAUNCH_CHECK();
+}
 
 void launch_ep_counts_push(const int32_t* counts, int E, int me, int P, int32_t* const* peer_counts,
                            cudaStream_t s) {

@@ -46,6 +46,9 @@ void launch_ep_plan(const int32_t* all_counts, int P, int E, int me, int32_t* de
 void launch_ep_dispatch_push(const void* x, const int32_t* perm, int k, int dtype, int64_t rows,
                              int d, const int32_t* offsets, int E, int P, const int32_t* dest_base,
                              int me, void* const* peer_x, int2* const* peer_ret, cudaStream_t s);
+// cross-rank barrier on epoch flags in symmetric buffers (P <= 32)
+void launch_ep_flag_barrier(uint32_t* const* peer_flags, uint32_t* my_flags, int me, int P,
+                            uint32_t epoch, uint64_t timeout_ns, cudaStream_t s);
 // N5
 void launch_combine(const void* y_perm, int dtype, const int32_t* inv, const float* topk_w,
                     int64_t N, int k, int d, void* y, cudaStream_t stream);

@@ -243,13 +243,20 @@ int infmoe_combine(const void* y_perm, int32_t dtype, const int32_t* inv, const 
 
 int infmoe_slot_pool_create(int32_t device, int32_t K, uint64_t expert_matrix_bytes,
                             infmoe_slot_pool** out) {
+  return infmoe_slot_pool_create_ex(device, K, expert_matrix_bytes, 1, out);
+}
+
+int infmoe_slot_pool_create_ex(int32_t device, int32_t K, uint64_t expert_matrix_bytes,
+                               int32_t sets, infmoe_slot_pool** out) {
   return guarded([&] {
     require(out != nullptr, "slot_pool_create: NULL argument");
     *out = nullptr;
     require(K >= 1, "slot_pool_create: K must be >= 1");
+    require(sets >= 1 && sets <= 2, "slot_pool_create: sets must be 1 or 2");
     require(expert_matrix_bytes > 0, "slot_pool_create: expert_matrix_bytes must be > 0");
     INFMOE_CUDA(cudaSetDevice(device));
-    auto* p = new SlotPool{device, K, K + 1, size_t(expert_matrix_bytes), nullptr, nullptr};
+    auto* p = new SlotPool{device, K, sets * (K + 1), sets, size_t(expert_matrix_bytes), nullptr,
+                           nullptr};
     const size_t n = size_t(p->n_slots) * p->matrix_bytes;
     cudaError_t e1 = cudaMalloc(&p->slot_in, n);
     cudaError_t e2 = e1 == cudaSuccess ? cudaMalloc(&p->slot_out, n) : e1;
@@ -281,6 +288,13 @@ int infmoe_layer_create(const infmoe_layer_desc* desc, infmoe_layer** out) {
     *out = nullptr;
     Layer* impl = new Layer(*desc);
     *out = new infmoe_layer{impl};
+  });
+}
+
+int infmoe_layer_set_next(infmoe_layer* layer, infmoe_layer* next) {
+  return guarded([&] {
+    require(layer && layer->impl, "set_next: NULL layer");
+    layer->impl->set_next(next ? next->impl : nullptr);
   });
 }
 

@@ -22,6 +22,8 @@
 // owner runs its local experts (resident or offloaded), and the reverse
 // all-to-allv brings the results home for the combine.
 #include <algorithm>
+#include <cstdlib>
+#include <string>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -114,6 +116,8 @@ Layer::Layer(const infmoe_layer_desc& d) : desc(d) {
     dest_base = dalloc<int32_t>(size_t(d.n_experts), owned);
     loc_offsets = dalloc<int32_t>(size_t(n_local) + 1, owned);
     bar_buf = dalloc<int32_t>(1, owned);
+    sym_flags = reinterpret_cast<uint32_t*>(dalloc<int32_t>(size_t(P), owned));
+    INFMOE_CUDA(cudaMemset(sym_flags, 0, sizeof(uint32_t) * size_t(P)));
     cap_h = size_t(cap_recv) * d.d_ff * esz;  // freed with the other exchange buffers
     INFMOE_CUDA(cudaMalloc(&loc_h, cap_h));
     peer_setup();
@@ -154,10 +158,15 @@ Layer::Layer(const infmoe_layer_desc& d) : desc(d) {
       require(pool->matrix_bytes == expert_in_bytes,
               "layer: slot pool expert size differs from the layer's");
       n_slots = pool->n_slots;
+      n_rot = pool->K + 1;
+      require(!d.continuous_load_stream || pool->sets >= 2,
+              "layer: continuous_load_stream on a shared pool needs 2 slot sets "
+              "(infmoe_slot_pool_create_ex)");
       slot_in = pool->slot_in;
       slot_out = pool->slot_out;
     } else {
       n_slots = std::min(d.K + 1, n_local + 1);
+      n_rot = n_slots;
       slot_in = dalloc<uint8_t>(size_t(n_slots) * expert_in_bytes, owned);
       slot_out = dalloc<uint8_t>(size_t(n_slots) * expert_in_bytes, owned);
       own_pool.device = d.device;
@@ -168,7 +177,9 @@ Layer::Layer(const infmoe_layer_desc& d) : desc(d) {
       own_pool.slot_out = slot_out;
       pool_ptr = &own_pool;
     }
+    require(d.prefetch_depth >= 0, "layer: prefetch_depth must be >= 0");
     INFMOE_CUDA(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
+    INFMOE_CUDA(cudaEventCreateWithFlags(&last_load, cudaEventDisableTiming));
     const size_t E = size_t(n_local);
     for (auto* v : {&load_done, &compute_done}) {
       v->resize(E);
@@ -209,6 +220,7 @@ void Layer::set_host_weights(const void* w_in, const void* w_out, bool fresh_pac
   }
   host_in = reinterpret_cast<const uint8_t*>(w_in);
   host_out = reinterpret_cast<const uint8_t*>(w_out);
+  pf.clear();  // a prefetched slot would hold the old weights
   if (desc.h2d_codec != INFMOE_CODEC_RAW) {
     // packs are SNAPSHOTS of the host weights: an explicit set_host_weights
     // always re-packs (the caller may have refilled the buffer in place); at
@@ -314,6 +326,7 @@ Layer::~Layer() {
   for (auto* v : {&load_done, &compute_done, &t_load0, &t_load1, &t_comp0, &t_comp1})
     for (cudaEvent_t e : *v) cudaEventDestroy(e);
   if (t_start) cudaEventDestroy(t_start);
+  if (last_load) cudaEventDestroy(last_load);
   if (t_pin0) cudaEventDestroy(t_pin0);
   if (t_pin1) cudaEventDestroy(t_pin1);
   if (pin_in) cudaFree(pin_in);
@@ -499,13 +512,28 @@ void Layer::compute_offloaded(const Rows& r, bool timed, infmoe_forward_out* out
   }
   exec_order.resize(size_t(E));
   for (int j = 0; j < E; ++j) exec_order[size_t(j)] = members[size_t(pl.order[size_t(j)])];
+  // continuous_load_stream: the leading positions the previous layer already
+  // streamed in (prefetch) are reused while their expert matches the real
+  // order; the first mismatch and everything after it load as usual (the
+  // slot is simply overwritten, in copy-stream order)
+  pf_reused = 0;
+  while (pf_reused < int(pf.size()) && pf_reused < E &&
+         pf[size_t(pf_reused)].expert == exec_order[size_t(pf_reused)])
+    ++pf_reused;
+  pf.clear();
   // ---- copy lane / compute lane ----
-  INFMOE_CUDA(cudaStreamWaitEvent(copy_stream, t_start, 0));  // drain: after previous layer
+  // drain (simulator.hpp:131-133): this layer's own loads start after the
+  // previous layer's computes (in either mode they also need this layer's
+  // routing, which the counts read-back above already waited for)
+  INFMOE_CUDA(cudaStreamWaitEvent(copy_stream, t_start, 0));
   for (int j = 0; j < E; ++j) {
     const int e = members[size_t(pl.order[size_t(j)])];
-    const int slot = j % n_slots;
-    if (j >= n_slots)
-      INFMOE_CUDA(cudaStreamWaitEvent(copy_stream, compute_done[size_t(j - n_slots)], 0));
+    const int slot = slot_of(j);
+    if (j < pf_reused) {  // streamed in by the previous layer: no copy
+      INFMOE_CUDA(cudaStreamWaitEvent(s, load_done[size_t(j)], 0));
+    } else {
+    if (j >= n_rot)
+      INFMOE_CUDA(cudaStreamWaitEvent(copy_stream, compute_done[size_t(j - n_rot)], 0));
     if (timed) INFMOE_CUDA(cudaEventRecord(t_load0[size_t(j)], copy_stream));
     if (pack) {  // packed codec: one copy of the expert's pack pair into its staging buffer
       // (one 108 MB copy ran at 55.00 GB/s, two half copies at 54.82)
@@ -530,6 +558,7 @@ void Layer::compute_offloaded(const Rows& r, bool timed, infmoe_forward_out* out
     INFMOE_CUDA(cudaEventRecord(load_done[size_t(j)], copy_stream));
 
     INFMOE_CUDA(cudaStreamWaitEvent(s, load_done[size_t(j)], 0));
+    }
     const int32_t ex = e, sl = slot;
     const int64_t n_e = int64_t(r.counts[e]);
     cudaEvent_t e0 = timed ? t_comp0[size_t(j)] : nullptr;
@@ -559,13 +588,111 @@ void Layer::compute_offloaded(const Rows& r, bool timed, infmoe_forward_out* out
     }
     INFMOE_CUDA(cudaEventRecord(compute_done[size_t(j)], s));
   }
+  // continuous_load_stream: keep the load lane flowing into the next layer
+  if (desc.continuous_load_stream && next) {
+    INFMOE_CUDA(cudaEventRecord(last_load, copy_stream));
+    next->prefetch(last_load, t_start);
+  }
   if (out) {
+    if (out->prefetched) *out->prefetched = pf_reused;
     if (out->order) {
       for (int j = 0; j < n_local; ++j) out->order[j] = -1;  // -1: not loaded (skipped)
       for (int j = 0; j < E; ++j) out->order[j] = members[size_t(pl.order[size_t(j)])];
     }
     if (out->feasible) *out->feasible = pl.feasible ? 1 : 0;
   }
+}
+
+// The InfMoE order of this layer's PREDICTED counts (the EMA of its routed
+// rows over its forwards, rounded): the same members rule and scheduler call
+// as compute_offloaded, so a stable routing predicts the real order exactly.
+std::vector<int> Layer::predicted_order(std::vector<int>* members_out) const {
+  std::vector<int> members;
+  std::vector<uint64_t> cnt;
+  for (int e = 0; e < n_local; ++e) {
+    const uint64_t c = uint64_t(std::llround(load_ema[size_t(e)]));
+    if (pin_slot[size_t(e)] >= 0) continue;
+    if (!desc.skip_empty_experts || c > 0) {
+      members.push_back(e);
+      cnt.push_back(c);
+    }
+  }
+  std::vector<int> order;
+  if (members.empty()) return order;
+  const int E = int(members.size());
+  Geometry geo{1, 1, 1, desc.d_model, desc.d_ff, E, int(esz)};
+  Hardware hw{desc.hw.peak_flops, desc.hw.h2d_bandwidth, desc.hw.device_memory,
+              desc.hw.reserved_memory};
+  Costs c = derive_costs(cnt.data(), E, geo, hw);
+  Plan pl;
+  switch (desc.policy) {
+    case INFMOE_POLICY_NAIVE: pl = plan_identity(c, desc.K); break;
+    case INFMOE_POLICY_GREEDY: pl = plan_greedy(c, desc.K); break;
+    case INFMOE_POLICY_EXACT: pl = plan_exact(c, desc.K, 12); break;
+    default: pl = plan_auto(c, desc.K, 12); break;
+  }
+  for (int j = 0; j < E; ++j) order.push_back(members[size_t(pl.order[size_t(j)])]);
+  if (members_out) *members_out = members;
+  return order;
+}
+
+// Called by the previous layer once its last load is issued: stream the first
+// prefetch_depth experts of this layer's predicted order into this layer's
+// own slots, on this layer's copy lane after the previous layer's loads (one
+// load lane) and after every compute that preceded the previous layer's
+// forward (the last users of this layer's slot set).  No residency gate is
+// needed for positions < K (simulator.hpp:147: the gate starts at j = K).
+void Layer::prefetch(cudaEvent_t after_loads, cudaEvent_t after_computes) {
+  pf.clear();
+  if (!ema_seen || n_scheduled < 0) return;
+  const std::vector<int> order = predicted_order(nullptr);
+  const int depth = std::max(1, desc.prefetch_depth);
+  const int m = std::min({depth, int(order.size()), desc.K, n_rot});
+  if (m <= 0) return;
+  INFMOE_CUDA(cudaStreamWaitEvent(copy_stream, after_loads, 0));
+  INFMOE_CUDA(cudaStreamWaitEvent(copy_stream, after_computes, 0));
+  for (int j = 0; j < m; ++j) {
+    const int e = order[size_t(j)];
+    const int slot = slot_of(j);
+    INFMOE_CUDA(cudaEventRecord(t_load0[size_t(j)], copy_stream));
+    if (pack) {
+      INFMOE_CUDA(cudaMemcpyAsync(stage_of(slot), pack->host + pack->off[size_t(e)],
+                                  pack->size[size_t(e)], cudaMemcpyHostToDevice, copy_stream));
+    } else {
+      INFMOE_CUDA(cudaMemcpyAsync(slot_in + size_t(slot) * expert_in_bytes,
+                                  host_in + size_t(e) * expert_in_bytes, expert_in_bytes,
+                                  cudaMemcpyHostToDevice, copy_stream));
+      INFMOE_CUDA(cudaMemcpyAsync(slot_out + size_t(slot) * expert_in_bytes,
+                                  host_out + size_t(e) * expert_in_bytes, expert_in_bytes,
+                                  cudaMemcpyHostToDevice, copy_stream));
+    }
+    INFMOE_CUDA(cudaEventRecord(t_load1[size_t(j)], copy_stream));
+    INFMOE_CUDA(cudaEventRecord(load_done[size_t(j)], copy_stream));
+    pf.push_back({e});
+  }
+}
+
+void Layer::set_next(Layer* nxt) {
+  require(desc.residency == INFMOE_OFFLOADED && desc.continuous_load_stream,
+          "set_next: the layer is not an offloaded continuous_load_stream layer");
+  if (!nxt) {
+    next = nullptr;
+    return;
+  }
+  require(nxt->desc.residency == INFMOE_OFFLOADED && nxt->desc.continuous_load_stream,
+          "set_next: the next layer is not an offloaded continuous_load_stream layer");
+  require(nxt->desc.device == desc.device, "set_next: layers on different devices");
+  if (pool_ptr == nxt->pool_ptr && pool_ptr != &own_pool) {
+    // one shared pool: consecutive layers use alternate slot sets
+    if (!set_assigned) set_assigned = true;
+    const int want = slot_base == 0 ? n_rot : 0;
+    if (nxt->set_assigned && nxt->slot_base != want)
+      fail(kArgument, "set_next: consecutive layers would share a slot set (odd cycle on one "
+                      "pool)");
+    nxt->slot_base = want;
+    nxt->set_assigned = true;
+  }
+  next = nxt;
 }
 
 // PEER transport: publish (pid, pointers, IPC handles) of the symmetric
@@ -575,14 +702,14 @@ void Layer::compute_offloaded(const Rows& r, bool timed, infmoe_forward_out* out
 void Layer::peer_setup() {
   struct Info {
     int64_t pid;
-    uint64_t ptr[4];
-    cudaIpcMemHandle_t h[4];
+    uint64_t ptr[5];
+    cudaIpcMemHandle_t h[5];
   };
   const int P = desc.ep_size, me = desc.ep_rank;
   Info mine{};
   mine.pid = int64_t(getpid());
-  void* bufs[4] = {sym_x, sym_ret, sym_y, sym_counts};
-  for (int i = 0; i < 4; ++i) {
+  void* bufs[5] = {sym_x, sym_ret, sym_y, sym_counts, sym_flags};
+  for (int i = 0; i < 5; ++i) {
     mine.ptr[i] = reinterpret_cast<uint64_t>(bufs[i]);
     INFMOE_CUDA(cudaIpcGetMemHandle(&mine.h[i], bufs[i]));
   }
@@ -601,11 +728,14 @@ void Layer::peer_setup() {
   std::vector<Info> all(static_cast<size_t>(P));
   INFMOE_CUDA(cudaMemcpy(all.data(), dev, sizeof(Info) * size_t(P), cudaMemcpyDeviceToHost));
   INFMOE_CUDA(cudaFree(dev));
-  std::vector<void*> px(static_cast<size_t>(P)), pr(static_cast<size_t>(P)), pc(static_cast<size_t>(P));
+  std::vector<void*> px(static_cast<size_t>(P)), pr(static_cast<size_t>(P)), pc(static_cast<size_t>(P)),
+      pf(static_cast<size_t>(P));
   peer_y.assign(size_t(P), nullptr);
+  bool all_remote = true;  // every peer lives in another process
   for (int r = 0; r < P; ++r) {
-    void* q[4];
-    for (int i = 0; i < 4; ++i) {
+    void* q[5];
+    if (r != me && all[size_t(r)].pid == mine.pid) all_remote = false;
+    for (int i = 0; i < 5; ++i) {
       if (r == me || all[size_t(r)].pid == mine.pid) {
         q[i] = reinterpret_cast<void*>(all[size_t(r)].ptr[i]);
       } else {
@@ -618,7 +748,20 @@ void Layer::peer_setup() {
     pr[size_t(r)] = q[1];
     peer_y[size_t(r)] = q[2];
     pc[size_t(r)] = q[3];
+    pf[size_t(r)] = q[4];
   }
+  // barriers: device epoch flags when the peers are other processes (one
+  // process per GPU: no collective and no host per barrier); a 1-int NCCL
+  // all-reduce when ranks share this process (threads: a spinning barrier
+  // kernel could stall another rank's first kernel launch, e.g. a lazy module
+  // load).  INFMOE_EP_BARRIER=device|nccl overrides.
+  dev_barrier = all_remote;
+  if (const char* m = std::getenv("INFMOE_EP_BARRIER")) {
+    if (std::string(m) == "device") dev_barrier = true;
+    else if (std::string(m) == "nccl") dev_barrier = false;
+  }
+  d_peer_flags = reinterpret_cast<uint32_t**>(dalloc<void*>(size_t(P), owned));
+  INFMOE_CUDA(cudaMemcpy(d_peer_flags, pf.data(), sizeof(void*) * P, cudaMemcpyHostToDevice));
   d_peer_x = dalloc<void*>(size_t(P), owned);
   d_peer_ret = dalloc<int2*>(size_t(P), owned);
   d_peer_counts = dalloc<int32_t*>(size_t(P), owned);
@@ -630,6 +773,15 @@ void Layer::peer_setup() {
 // every rank's work enqueued before this point has finished before any rank's
 // work after it starts: a 1-int all-reduce on the stream
 void Layer::peer_barrier(cudaStream_t s) {
+  if (dev_barrier) {
+    static const uint64_t timeout_ns = [] {
+      const char* t = std::getenv("INFMOE_EP_BARRIER_TIMEOUT_S");
+      return uint64_t(t ? std::atof(t) * 1e9 : 60e9);
+    }();
+    launch_ep_flag_barrier(d_peer_flags, sym_flags, desc.ep_rank, desc.ep_size, ++bar_epoch,
+                           timeout_ns, s);
+    return;
+  }
   const auto& nc = nccl::api();
   nccl::check(nc.AllReduce(bar_buf, bar_buf, 1, nccl::kInt32, nccl::kSum,
                            reinterpret_cast<nccl::Comm>(comm), s),

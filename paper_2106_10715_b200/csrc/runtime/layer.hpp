@@ -16,7 +16,8 @@ namespace infmoe {
 
 // K+1 shared expert slots (infmoe_slot_pool)
 struct SlotPool {
-  int device = 0, K = 0, n_slots = 0;
+  int device = 0, K = 0, n_slots = 0;  // n_slots = sets * (K + 1)
+  int sets = 1;
   size_t matrix_bytes = 0;
   uint8_t* slot_in = nullptr;
   uint8_t* slot_out = nullptr;
@@ -62,6 +63,8 @@ struct Layer {
   // (EMA of routed rows over offloaded forwards, decay 0.5; ties: lower index)
   std::vector<int32_t> pin_hottest(int n);
   int n_pinned_experts() const { return n_pinned; }
+  // continuous_load_stream: the layer forwarded after this one
+  void set_next(Layer* nxt);
   void h2d_bytes(uint64_t* packed, uint64_t* raw) const {
     const uint64_t r = uint64_t(n_local) * 2 * expert_in_bytes;
     if (raw) *raw = r;
@@ -118,7 +121,21 @@ struct Layer {
   void* fused_out = nullptr;       // y when the combine is fused into the GEMM2 epilogue
   // offload executor
   size_t expert_in_bytes = 0;  // = bytes of W_in = bytes of W_out of one expert
-  int n_slots = 0;
+  int n_slots = 0;   // slots in the weight tensors (all sets of the pool)
+  int n_rot = 0;     // slots this layer rotates through (K+1, or fewer experts + 1)
+  int slot_base = 0; // first slot of this layer's set
+  int slot_of(int j) const { return slot_base + j % n_rot; }
+  // continuous_load_stream: prefetched leading positions of the next forward
+  struct Prefetched {
+    int expert;
+  };
+  Layer* next = nullptr;
+  bool set_assigned = false;
+  std::vector<Prefetched> pf;
+  int pf_reused = 0;
+  cudaEvent_t last_load = nullptr;
+  void prefetch(cudaEvent_t after_loads, cudaEvent_t after_computes);
+  std::vector<int> predicted_order(std::vector<int>* members) const;
   uint8_t* slot_in = nullptr;
   uint8_t* slot_out = nullptr;
   const uint8_t* host_in = nullptr;
@@ -166,7 +183,11 @@ struct Layer {
   int32_t* sym_counts = nullptr;  // [P, E] every source's histogram
   int32_t* dest_base = nullptr;   // [E]
   int32_t* loc_offsets = nullptr; // [n_local + 1]
-  int32_t* bar_buf = nullptr;     // 1-int all-reduce of the barrier
+  int32_t* bar_buf = nullptr;     // 1-int all-reduce of the barrier (ranks in one process)
+  uint32_t* sym_flags = nullptr;  // [P] barrier epochs written by the peers
+  uint32_t** d_peer_flags = nullptr;
+  uint32_t bar_epoch = 0;
+  bool dev_barrier = false;       // device flag barrier (peers in other processes)
   void** d_peer_x = nullptr;      // device arrays of the peers' buffers
   int2** d_peer_ret = nullptr;
   int32_t** d_peer_counts = nullptr;

@@ -227,11 +227,14 @@ class SlotPool:
     """K+1 device expert slots shared by the offloaded layers of a stack
     (infmoe_slot_pool: K experts resident on the GPU in total + one in flight)."""
 
-    def __init__(self, K: int, d_model: int, d_ff: int, dtype: str = "bf16", device: int = 0):
+    def __init__(self, K: int, d_model: int, d_ff: int, dtype: str = "bf16", device: int = 0,
+                 sets: int = 1):
+        """sets=2: two slot sets, for stacks of continuous_load_stream layers."""
         esz = 2 if dtype == "bf16" else 4
         self.K = K
         self._h = C.c_void_p()
-        _check(_lib.infmoe_slot_pool_create(device, K, d_model * d_ff * esz, C.byref(self._h)))
+        _check(_lib.infmoe_slot_pool_create_ex(device, K, d_model * d_ff * esz, sets,
+                                               C.byref(self._h)))
 
     @property
     def handle(self):
@@ -259,7 +262,8 @@ class MoELayer:
                  hw: Optional[Hardware] = None, ep_size: int = 1, ep_rank: int = 0,
                  ep_comm: Optional[int] = None, skip_empty_experts: bool = False,
                  slot_pool: Optional["SlotPool"] = None, ep_transport: str = "nccl",
-                 h2d_codec: str = "raw"):
+                 h2d_codec: str = "raw", continuous_load_stream: bool = False,
+                 prefetch_depth: int = 0):
         d = LayerDesc()
         d.d_model, d.d_ff, d.n_experts, d.top_k = d_model, d_ff, n_experts, top_k
         d.dtype = DTYPE_BF16 if dtype == "bf16" else DTYPE_F32
@@ -283,6 +287,8 @@ class MoELayer:
         d.skip_empty_experts = int(skip_empty_experts)
         d.ep_transport = {"nccl": 0, "peer": 1}[ep_transport]
         d.h2d_codec = CODECS[h2d_codec]
+        d.continuous_load_stream = int(continuous_load_stream)
+        d.prefetch_depth = prefetch_depth
         if slot_pool is not None:
             d.slot_pool = slot_pool.handle
             self._keep.append(slot_pool)  # the pool outlives the layer
@@ -292,6 +298,10 @@ class MoELayer:
         self.n_local = n_experts // max(ep_size, 1)
         self._h = C.c_void_p()
         _check(_lib.infmoe_layer_create(C.byref(d), C.byref(self._h)))
+
+    def set_next(self, nxt: Optional["MoELayer"]) -> None:
+        """continuous_load_stream: the layer forwarded after this one."""
+        _check(_lib.infmoe_layer_set_next(self._h, None if nxt is None else nxt._h))
 
     def set_host_weights(self, w_in, w_out) -> None:
         self._keep += [w_in, w_out]
@@ -350,6 +360,7 @@ class MoELayer:
         exposed = C.c_double(0.0)
         events = (Event * (2 * El))()
         local_rows = np.zeros(El, dtype=np.int32)
+        prefetched = C.c_int32(0)
         rt = None
         if want_routing:
             k = self.top_k
@@ -363,10 +374,12 @@ class MoELayer:
                          local_rows.ctypes.data,
                          *([rt[n].data_ptr() for n in ("topk_idx", "topk_w", "perm", "offsets")]
                            if rt else [None] * 4),
-                         None if time_origin is None else time_origin.cuda_event)
+                         None if time_origin is None else time_origin.cuda_event,
+                         C.addressof(prefetched))
         _check(call(C.byref(out)))
         info = {"counts": counts, "order": order, "feasible": bool(feas.value),
-                "local_rows": local_rows, "pinned": list(getattr(self, "pinned", []))}
+                "local_rows": local_rows, "pinned": list(getattr(self, "pinned", [])),
+                "prefetched": int(prefetched.value)}
         if rt:
             info.update(rt)
         if want_timeline:

@@ -95,3 +95,21 @@ def test_layer_ep_ranks_as_threads_equal_single_gpu(loopback_lib, P, k, gate, of
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
                        timeout=300)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
+
+
+@pytest.mark.parametrize("P,k,gate,offloaded", [(2, 1, "lsh", False), (4, 2, "softmax", False),
+                                                (2, 1, "lsh", True)])
+def test_peer_device_flag_barrier(loopback_lib, P, k, gate, offloaded):
+    """The PEER transport's device-side epoch-flag barrier (ep_flag_barrier_kernel,
+    the default when ranks are separate processes): here forced on for ranks as
+    threads (INFMOE_EP_BARRIER=device), with every kernel module loaded up front
+    (CUDA_MODULE_LOADING=EAGER) so no first launch can wait behind a spinning
+    barrier; the barrier traps after 20 s rather than hang.  No collective runs
+    per layer; outputs equal the one-GPU layer bit for bit."""
+    env = dict(os.environ, INFMOE_NCCL_LIB=str(loopback_lib), INFMOE_EP_BARRIER="device",
+               CUDA_MODULE_LOADING="EAGER", INFMOE_EP_BARRIER_TIMEOUT_S="20")
+    code = SCRIPT.format(root=ROOT, P=P, k=k, gate=gate, offloaded=offloaded, transport="peer",
+                         codec="raw")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]

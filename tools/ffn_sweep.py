@@ -23,16 +23,28 @@ ap.add_argument("--E", type=int, default=32)
 ap.add_argument("--k", type=int, default=1)
 ap.add_argument("--N", type=int, default=4096)
 ap.add_argument("--skew", type=float, default=0.0)
+ap.add_argument("--c5", action="store_true",
+                help="bench.py's C5 layer: SURVEY 8(d) Gaussian inputs at S5 = SEED + 500, "
+                     "softmax top-2 over 64 experts, 16384 tokens, calibrated bias c = 0.6258")
 a = ap.parse_args()
+if a.c5:
+    a.gate, a.E, a.k, a.N, a.skew = "softmax", 64, 2, 16384, 0.6258
 d, f, E, N, k = 4096, 10240, a.E, a.N, a.k
 dev = torch.device("cuda:0")
-wi = torch.empty((E, f, d), dtype=torch.bfloat16, device=dev)
-wo = torch.empty((E, d, f), dtype=torch.bfloat16, device=dev)
-x = torch.empty((N, d), dtype=torch.bfloat16, device=dev)
-dv.fill_uniform(wi, 1, 3 ** 0.5 / d ** 0.5)
-dv.fill_uniform(wo, 2, 1.534 * 3 ** 0.5 / f ** 0.5)
-dv.fill_uniform(x, 3, 3 ** 0.5)
-gw = (np.random.default_rng(5).standard_normal((E, d)) / d ** 0.5).astype(np.float32)
+import paper_2106_10715_b200 as im  # noqa: E402
+S = 20261018 + 500
+hi = torch.empty((E, f, d), dtype=torch.bfloat16, pin_memory=True)
+ho = torch.empty((E, d, f), dtype=torch.bfloat16, pin_memory=True)
+seeds = [im.derive_seed(S, 1000 + 2 * e) for e in range(E)] + \
+        [im.derive_seed(S, 1001 + 2 * e) for e in range(E)]
+im.gaussian_fill_typed("bf16", seeds, [d ** -0.5] * E + [f ** -0.5] * E, f * d,
+                       [hi[e].data_ptr() for e in range(E)] + [ho[e].data_ptr() for e in range(E)])
+wi, wo = hi.to(dev), ho.to(dev)
+del hi, ho
+x = torch.from_numpy(im.gaussian_bf16(im.derive_seed(S, 0), N * d).view(np.int16)
+                     .reshape(N, d)).view(torch.bfloat16).to(dev)
+gw = np.ascontiguousarray((im.gaussian_stream(im.derive_seed(S, 1), d * E) * d ** -0.5)
+                          .astype(np.float32).reshape(d, E).T)
 bias = (-a.skew * np.log(np.arange(1, E + 1))).astype(np.float32)
 layer = dv.MoELayer(d, f, E, k, wi, wo, gate=a.gate, gate_weight=gw, gate_bias=bias, lsh_seed=7,
                     lsh_bits=5, max_tokens=N)
@@ -52,8 +64,11 @@ for _ in range(a.iters):
     _, info = layer.forward(x, y, want_timeline=True)
     ffn.append((info["events"][0][4] - info["events"][0][3]) * 1e3)
 flops = 4.0 * N * k * d * f
+hbm = (int((info["counts"] > 0).sum()) * 2 * d * f + N * k * (2 * d + 2 * f)) * 2
+t_bound = max(flops / 1643.6e12, hbm / 6549.1e9)
 print(json.dumps({"env": {kk: v for kk, v in os.environ.items() if kk.startswith("INFMOE_")},
                   "layer_ms": float(np.median(ts)), "ffn_ms": float(np.median(ffn)),
                   "ffn_tflops": flops / (float(np.median(ffn)) * 1e-3) / 1e12,
+                  "layer_over_t_bound": t_bound / (float(np.median(ts)) * 1e-3),
                   "max_rows": int(info["counts"].max()),
                   "y_sum": int(y.view(torch.int16).to(torch.int64).sum().item())}))
