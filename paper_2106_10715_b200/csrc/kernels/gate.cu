@@ -84,6 +84,72 @@ struct SoftCfg {
   }
 };
 
+// Selection from the logits tile lg_s [TT][E+1] (one warp per token): top-k by
+// logit (ties and NaN -> lower index), softmax weights (renormalised over the
+// picks for k > 1), per-CTA histogram merged into counts.
+__device__ __forceinline__ void softmax_select(const float* lg_s, int TT, int64_t tok0,
+                                               int64_t N, int E, int k, int warp, int nwarps,
+                                               int lane, int* hist, int32_t* __restrict__ topk_idx,
+                                               float* __restrict__ topk_w,
+                                               int32_t* __restrict__ counts) {
+  const int NT = nwarps * 32;
+  constexpr int SQ = 4;  // logits per lane during selection (E <= 128)
+  for (int row = warp; row < TT; row += nwarps) {
+    const int64_t tok = tok0 + row;
+    if (tok >= N) break;
+    float lg[SQ];
+    bool live[SQ];
+#pragma unroll
+    for (int q = 0; q < SQ; ++q) {
+      const int e = lane + 32 * q;
+      live[q] = e < E;
+      lg[q] = live[q] ? lg_s[row * (E + 1) + e] : 0.0f;
+    }
+    // softmax denominator over all experts (fp32; weights are tolerance-checked)
+    float mx = -INFINITY;
+#pragma unroll
+    for (int q = 0; q < SQ; ++q)
+      if (live[q] && !isnan(lg[q])) mx = fmaxf(mx, lg[q]);
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    float se = 0.0f;
+#pragma unroll
+    for (int q = 0; q < SQ; ++q)
+      if (live[q]) se += expf(lg[q] - mx);
+    for (int o = 16; o; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
+
+    float psum = 0.0f;
+    float pk_mine = 0.0f;
+    int ik_mine = 0;
+    for (int j = 0; j < k; ++j) {
+      Cand best{0.0f, -1};
+#pragma unroll
+      for (int q = 0; q < SQ; ++q) {
+        Cand c{lg[q], live[q] ? lane + 32 * q : -1};
+        if (better(c, best)) best = c;
+      }
+      for (int o = 16; o; o >>= 1) {
+        Cand other{__shfl_xor_sync(0xffffffffu, best.v, o),
+                   __shfl_xor_sync(0xffffffffu, best.i, o)};
+        if (better(other, best)) best = other;
+      }
+      const float pj = expf(best.v - mx) / se;
+      psum += pj;
+      if (lane == j) { pk_mine = pj; ik_mine = best.i; }  // lane j keeps pick j
+#pragma unroll
+      for (int q = 0; q < SQ; ++q)
+        if (lane + 32 * q == best.i) live[q] = false;  // exclude from the next pick
+    }
+    if (lane < k) {
+      topk_idx[tok * k + lane] = ik_mine;
+      topk_w[tok * k + lane] = k > 1 ? pk_mine / psum : pk_mine;
+      atomicAdd(&hist[ik_mine], 1);
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += NT)
+    if (hist[e]) atomicAdd(&counts[e], hist[e]);
+}
+
 template <typename T, int EB>
 __global__ void __launch_bounds__(SoftCfg<T, EB>::MAXW * 32) gate_softmax_kernel(
     const T* __restrict__ x, int64_t N, int d, const float* __restrict__ wg,
@@ -183,61 +249,7 @@ __global__ void __launch_bounds__(SoftCfg<T, EB>::MAXW * 32) gate_softmax_kernel
           lg_s[t * (E + 1) + e0 + e] = bias ? __fadd_rn(acc[t][e], bias[e0 + e]) : acc[t][e];
   __syncthreads();
 
-  constexpr int SQ = 4;  // logits per lane during selection (E <= 128)
-  for (int row = warp; row < TT; row += nwarps) {
-    const int64_t tok = tok0 + row;
-    if (tok >= N) break;
-    float lg[SQ];
-    bool live[SQ];
-#pragma unroll
-    for (int q = 0; q < SQ; ++q) {
-      const int e = lane + 32 * q;
-      live[q] = e < E;
-      lg[q] = live[q] ? lg_s[row * (E + 1) + e] : 0.0f;
-    }
-    // softmax denominator over all experts (fp32; weights are tolerance-checked)
-    float mx = -INFINITY;
-#pragma unroll
-    for (int q = 0; q < SQ; ++q)
-      if (live[q] && !isnan(lg[q])) mx = fmaxf(mx, lg[q]);
-    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    float se = 0.0f;
-#pragma unroll
-    for (int q = 0; q < SQ; ++q)
-      if (live[q]) se += expf(lg[q] - mx);
-    for (int o = 16; o; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
-
-    float psum = 0.0f;
-    float pk_mine = 0.0f;
-    int ik_mine = 0;
-    for (int j = 0; j < k; ++j) {
-      Cand best{0.0f, -1};
-#pragma unroll
-      for (int q = 0; q < SQ; ++q) {
-        Cand c{lg[q], live[q] ? lane + 32 * q : -1};
-        if (better(c, best)) best = c;
-      }
-      for (int o = 16; o; o >>= 1) {
-        Cand other{__shfl_xor_sync(0xffffffffu, best.v, o),
-                   __shfl_xor_sync(0xffffffffu, best.i, o)};
-        if (better(other, best)) best = other;
-      }
-      const float pj = expf(best.v - mx) / se;
-      psum += pj;
-      if (lane == j) { pk_mine = pj; ik_mine = best.i; }  // lane j keeps pick j
-#pragma unroll
-      for (int q = 0; q < SQ; ++q)
-        if (lane + 32 * q == best.i) live[q] = false;  // exclude from the next pick
-    }
-    if (lane < k) {
-      topk_idx[tok * k + lane] = ik_mine;
-      topk_w[tok * k + lane] = k > 1 ? pk_mine / psum : pk_mine;
-      atomicAdd(&hist[ik_mine], 1);
-    }
-  }
-  __syncthreads();
-  for (int e = threadIdx.x; e < E; e += NT)
-    if (hist[e]) atomicAdd(&counts[e], hist[e]);
+  softmax_select(lg_s, TT, tok0, N, E, k, warp, nwarps, lane, hist, topk_idx, topk_w, counts);
 }
 
 // ---------------------------------------------------------------- N1b ----
