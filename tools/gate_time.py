@@ -1,6 +1,6 @@
 """Softmax gate timing at C5 size (16384 x 4096, E = 64, top-2; Gaussian inputs,
 calibrated bias), CUDA events over 10 back-to-back launches after an L2 flush,
-plus a checksum of the routing so kernel variants (INFMOE_SOFTMAX_V1=1) can be
+plus a checksum of the routing so kernel variants can be
 compared for speed and identity (dev tool)."""
 import sys
 from pathlib import Path
