@@ -1198,7 +1198,7 @@ def main() -> None:
         # the same packed stack with the load lane flowing into the next layer:
         # each layer's predicted first expert is streamed while the previous
         # layer's tail (last decode + FFN, next gate / dispatch / plan) runs
-        if args.continuous:
+        if args.continuous and P == 1:  # (one GPU: the speculative lane is measured here)
             cpool = dv.SlotPool(cfg["K"], d, f, device=local, sets=2)
             cont = []
             for l in range(L):

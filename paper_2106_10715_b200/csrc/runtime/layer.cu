@@ -210,6 +210,10 @@ void Layer::set_host_weights(const void* w_in, const void* w_out, bool fresh_pac
   for (const void* p : {w_in, w_out}) {
     cudaPointerAttributes at;
     INFMOE_CUDA(cudaPointerGetAttributes(&at, p));
+    // a packed-codec layer streams its pinned packs, never the raw weights
+    // (they are only read by the host packer and by pin_experts' one-time
+    // copies), so pageable raw weights stay pageable: half the pinned memory
+    if (at.type == cudaMemoryTypeUnregistered && desc.h2d_codec != INFMOE_CODEC_RAW) continue;
     if (at.type == cudaMemoryTypeUnregistered) {
       INFMOE_CUDA(cudaHostRegister(const_cast<void*>(p), bytes, cudaHostRegisterDefault));
       registered.push_back(const_cast<void*>(p));

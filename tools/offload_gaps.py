@@ -5,7 +5,6 @@ reports, per layer: time to the first load, the sum of load durations, the
 gaps between consecutive loads, and the tail after the last load.
 """
 import argparse
-import math
 import os
 import sys
 
@@ -26,19 +25,15 @@ def main():
     d, f, E, N = 4096, 10240, 32, 4096
     bf = torch.bfloat16
     dev = torch.device("cuda:0")
-    wi = torch.empty((E, f, d), dtype=bf, device=dev)
-    wo = torch.empty((E, d, f), dtype=bf, device=dev)
-    dv.fill_uniform(wi, 11, bench.SQRT3 / d ** 0.5)
-    dv.fill_uniform(wo, 12, bench.GELU_GAIN * bench.SQRT3 / f ** 0.5)
-    hi = torch.empty(wi.shape, dtype=bf, pin_memory=True)
-    ho = torch.empty(wo.shape, dtype=bf, pin_memory=True)
-    hi.copy_(wi)
-    ho.copy_(wo)
-    del wi, wo
-    x = torch.empty((N, d), dtype=bf, device=dev)
-    dv.fill_uniform(x, 3, math.sqrt(3.0))
-    layers = [dv.MoELayer(d, f, E, 1, hi, ho, gate="lsh", lsh_seed=100 + l, lsh_bits=5,
-                          offloaded=True, K=4, max_tokens=N, h2d_codec=a.codec)
+    hi = torch.empty((E, f, d), dtype=bf, pin_memory=True)
+    ho = torch.empty((E, d, f), dtype=bf, pin_memory=True)
+    bench.fill_expert_weights(im, bench.SEED, 0, E, d, f, hi, ho)  # SURVEY 8(d) weights
+    x = torch.from_numpy(im.gaussian_bf16(im.derive_seed(bench.SEED, 0), N * d).view(np.int16)
+                         .reshape(N, d)).view(bf).to(dev)
+    pool = dv.SlotPool(4, d, f)
+    layers = [dv.MoELayer(d, f, E, 1, hi, ho, gate="lsh", lsh_seed=bench.lsh_seed(im, l),
+                          lsh_bits=5, offloaded=True, K=4, max_tokens=N, h2d_codec=a.codec,
+                          slot_pool=pool)
               for l in range(a.layers)]
     bufs = [torch.empty_like(x) for _ in range(2)]
     for rep in range(2):
@@ -47,7 +42,7 @@ def main():
         t0.record()
         infos = []
         for l, layer in enumerate(layers):
-            _, info = layer.forward(cur, bufs[l % 2], want_timeline=True)
+            _, info = layer.forward(cur, bufs[l % 2], want_timeline=True, time_origin=t0)
             infos.append(info)
             cur = bufs[l % 2]
         t1 = torch.cuda.Event(enable_timing=True)
@@ -55,16 +50,20 @@ def main():
         torch.cuda.synchronize()
     total = t0.elapsed_time(t1)
     nbytes = layers[0].packed_bytes() / E  # bytes per expert load over the link
-    for l, info in enumerate(infos):
+    prev_end = 0.0
+    for l, info in enumerate(infos):  # times on one axis: seconds from t0
         loads = sorted([(s0, s1) for st, _, _, s0, s1 in info["events"] if st == 0])
-        comps = [(s0, s1) for st, _, _, s0, s1 in info["events"] if st == 1]
+        comps = sorted([(s0, s1) for st, _, _, s0, s1 in info["events"] if st == 1])
         dur = [b - a for a, b in loads]
         gaps = [loads[i + 1][0] - loads[i][1] for i in range(len(loads) - 1)]
         end = max(c[1] for c in comps)
-        print(f"layer {l}: first load at {loads[0][0] * 1e3:.3f} ms, loads {sum(dur) * 1e3:.2f} ms "
-              f"(mean {np.mean(dur) * 1e3:.3f} ms = {nbytes / np.mean(dur) / 1e9:.2f} GB/s), "
-              f"gaps sum {sum(gaps) * 1e3:.3f} ms max {max(gaps) * 1e6:.1f} us, "
-              f"tail after last load {(end - loads[-1][1]) * 1e3:.3f} ms, layer {end * 1e3:.2f} ms")
+        print(f"layer {l}: head (prev layer end -> first load) {(loads[0][0] - prev_end) * 1e3:.3f} ms, "
+              f"loads {sum(dur) * 1e3:.2f} ms (mean {np.mean(dur) * 1e3:.3f} ms = "
+              f"{nbytes / np.mean(dur) / 1e9:.2f} GB/s), gaps sum {sum(gaps) * 1e3:.3f} ms max "
+              f"{max(gaps) * 1e6:.1f} us, tail (last load end -> last compute end) "
+              f"{(end - loads[-1][1]) * 1e3:.3f} ms [last compute {(comps[-1][1] - comps[-1][0]) * 1e3:.3f} ms "
+              f"started {(comps[-1][0] - loads[-1][1]) * 1e6:.1f} us after its load]")
+        prev_end = end
     print(f"stack {total:.2f} ms, ideal at per-load rate {a.layers * E * np.mean(dur) * 1e3:.2f} ms")
     for layer in layers:
         layer.close()
