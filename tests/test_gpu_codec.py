@@ -122,3 +122,25 @@ def test_codec_packs_are_snapshots_that_follow_set_host_weights(cuda):
     assert torch.equal(y_old2.view(torch.int16), y_raw1.view(torch.int16))
     for lay in (raw, old, new):
         lay.close()
+
+
+def test_codec_layer_from_pageable_weights(cuda):
+    """A packed-codec layer streams its pinned packs only, so pageable raw host
+    weights stay pageable (not registered); output equals the raw stream."""
+    N, d, f, E, K = 256, 256, 512, 4, 1
+    t = lambda b, sh: torch.from_numpy(b.view(np.int16).reshape(sh)).view(torch.bfloat16)
+    x = t(fill_bf16(41, N * d, 1.7320508), (N, d)).to(cuda)
+    wi = t(fill_bf16(42, E * f * d, 1.7320508 / 16), (E, f, d))        # pageable
+    wo = t(fill_bf16(43, E * d * f, 1.534 * 1.7320508 / np.sqrt(f)), (E, d, f))
+    assert not wi.is_pinned()
+    kw = dict(gate="lsh", lsh_seed=3, lsh_bits=2, max_tokens=N, offloaded=True, K=K)
+    raw = dv.MoELayer(d, f, E, 1, wi.pin_memory(), wo.pin_memory(), **kw)
+    ex = dv.MoELayer(d, f, E, 1, wi, wo, h2d_codec="exph", **kw)
+    ex.pin_experts([1])  # the one-time device copy reads the pageable weights
+    y0, _ = raw.forward(x)
+    y1, _ = ex.forward(x)
+    torch.cuda.synchronize()
+    assert torch.equal(y0.view(torch.int16), y1.view(torch.int16))
+    assert not wi.is_pinned()
+    raw.close()
+    ex.close()
