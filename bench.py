@@ -658,6 +658,39 @@ def main() -> None:
         e1.synchronize()
         h2d_peak = max(h2d_peak, (1 << 30) / (e0.elapsed_time(e1) * 1e-3) / 1e9)
     del probe_h, probe_d
+    ep_probe = None
+    if world > 1:
+        # SURVEY 8(d)'s multi-GPU probes: every rank's pinned H2D peak measured
+        # CONCURRENTLY (the copies above ran on all ranks at once), and the NCCL
+        # all-to-all at the C4 message size (each rank sends (N/P)*k*(P-1)/P rows
+        # of d bf16 in total, split evenly over its peers), median of 10
+        peaks_all = [None] * world
+        dist.all_gather_object(peaks_all, h2d_peak)
+        rows_pp = max(1, (N_glob // world) * k // world)
+        sbuf = torch.empty(world * rows_pp * d, dtype=torch.bfloat16, device=dev)
+        rbuf = torch.empty_like(sbuf)
+        for _ in range(3):
+            dist.all_to_all_single(rbuf, sbuf)
+        ts = []
+        for _ in range(10):
+            dist.barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            dist.all_to_all_single(rbuf, sbuf)
+            e1.record()
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1) * 1e-3)
+        t_a2a = float(np.median(ts))
+        tt = torch.tensor([t_a2a], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_a2a = tt.item()
+        sent = (world - 1) * rows_pp * d * 2  # bytes each rank sends to its peers
+        ep_probe = {"h2d_peak_gbs_per_rank_concurrent": peaks_all,
+                    "alltoall": {"bytes_sent_per_rank": sent, "us": t_a2a * 1e6,
+                                 "algbw_gbs_per_rank": sent / t_a2a / 1e9,
+                                 "how": "torch.distributed all_to_all_single (NCCL) of the C4 "
+                                        "dispatch size, max over ranks of the median of 10"}}
+        del sbuf, rbuf
 
     # --- weights: n_sets distinct sets of this rank's experts in
     # one pinned host pool, plus device copies.  Set s is the layer weights of
@@ -1079,6 +1112,7 @@ def main() -> None:
                      "bit_identical_to_offloaded": parity_equal,
                      "clocks": res_clocks.summary()},
         "gpu_launches": launches,
+        "ep_probe": ep_probe,
         "clocks": clocks.summary(),
     }
     if cpu is not None:
