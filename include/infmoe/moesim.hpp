@@ -10,9 +10,11 @@
 // bit-identical (tests/test_planner_parity.py, tests/cpp/test_moesim_compat.cpp).
 #pragma once
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <filesystem>
+#include <map>
 #include <numbers>
 #include <optional>
 #include <random>
@@ -50,6 +52,18 @@ inline void check(int rc) {
   }
 }
 }  // namespace detail
+
+// ---- tolerance.hpp ---------------------------------------------------------
+// the one comparison rule of the scheduler / simulator (tolerance.hpp:10-23)
+inline constexpr double kRelTol = 1e-9;
+inline constexpr double kAbsTol = 1e-15;
+inline double cmp_tol(double a, double b) {
+  return std::max(kAbsTol, kRelTol * std::max(std::fabs(a), std::fabs(b)));
+}
+inline bool approx_geq(double a, double b) { return a >= b - cmp_tol(a, b); }
+inline bool approx_leq(double a, double b) { return a <= b + cmp_tol(a, b); }
+inline bool approx_eq(double a, double b) { return std::fabs(a - b) <= cmp_tol(a, b); }
+inline bool definitely_lt(double a, double b) { return !approx_geq(a, b); }
 
 // ---- model_config.hpp ----------------------------------------------------
 struct ModelGeometry {
@@ -89,6 +103,19 @@ inline std::uint64_t expert_param_bytes(const ModelGeometry& g) {
 inline std::uint64_t expert_flops(const ModelGeometry& g, std::uint64_t n_tokens) {
   const infmoe_geometry cg = detail::c(g);
   return infmoe_expert_flops(&cg, n_tokens);
+}
+inline const std::map<std::string, ModelGeometry>& builtin_geometry_presets() {
+  static const std::map<std::string, ModelGeometry> presets = [] {
+    std::map<std::string, ModelGeometry> m;
+    for (const char* name : {"cpm2", "cpm-small"}) {
+      infmoe_geometry g;
+      detail::check(infmoe_geometry_preset(name, &g));
+      m[name] = ModelGeometry{g.n_layers, g.n_heads, g.d_head, g.d_model, g.d_ff,
+                              g.n_experts_per_layer, g.bytes_per_param};
+    }
+    return m;
+  }();
+  return presets;
 }
 
 // ---- prng.hpp -------------------------------------------------------------
@@ -460,6 +487,51 @@ inline std::pair<std::vector<TimelineEvent>, SimReport> simulate_model(
 inline std::string to_string(StreamKind s) { return s == StreamKind::Load ? "load" : "compute"; }
 inline std::string to_string(SimMode m) {
   return m == SimMode::Overlapped ? "overlapped" : "serial";
+}
+
+// ---- scenario.hpp + the CLI front door -------------------------------------
+// The reference's parse_scenario / to_json work on nlohmann::json objects; the
+// library exchanges the resolved scenario as JSON text (indent 2, sorted keys:
+// byte-identical to the reference's to_json(parse_scenario(...)).dump(2)).
+inline std::string resolve_scenario(const std::string& json_text) {
+  uint64_t len = 0;
+  detail::check(infmoe_scenario_resolve(json_text.c_str(), nullptr, 0, &len));
+  std::string out(len, '\0');
+  detail::check(infmoe_scenario_resolve(json_text.c_str(), out.data(), len, &len));
+  out.resize(len ? len - 1 : 0);
+  return out;
+}
+inline std::string resolve_scenario_file(const std::filesystem::path& path) {
+  uint64_t len = 0;
+  const std::string p = path.string();
+  detail::check(infmoe_scenario_resolve_file(p.c_str(), nullptr, 0, &len));
+  std::string out(len, '\0');
+  detail::check(infmoe_scenario_resolve_file(p.c_str(), out.data(), len, &len));
+  out.resize(len ? len - 1 : 0);
+  return out;
+}
+// run_scenario / sweep: artefacts under opt.out_dir (or the
+// scenario's output_dir); returns summary.csv / sweep.csv
+inline std::string run_scenario(const std::filesystem::path& path,
+                                const infmoe_run_options* opt = nullptr) {
+  std::string out(1 << 20, '\0');
+  uint64_t len = 0;
+  const std::string p = path.string();
+  detail::check(infmoe_scenario_run(p.c_str(), opt, out.data(), out.size(), &len));
+  out.resize(std::min<uint64_t>(len ? len - 1 : 0, out.size()));
+  return out;
+}
+inline std::string sweep_scenario(const std::filesystem::path& path, const std::string& axis,
+                                  const std::vector<double>& values,
+                                  const infmoe_run_options* opt = nullptr) {
+  std::string out(1 << 20, '\0');
+  uint64_t len = 0;
+  const std::string p = path.string();
+  detail::check(infmoe_scenario_sweep(p.c_str(), axis.c_str(), values.data(),
+                                      int32_t(values.size()), opt, out.data(), out.size(),
+                                      &len));
+  out.resize(std::min<uint64_t>(len ? len - 1 : 0, out.size()));
+  return out;
 }
 
 }  // namespace infmoe::moesim

@@ -16,6 +16,8 @@ namespace ms = infmoe::moesim;
 #else
 #include "moesim/cost_model.hpp"
 #include "moesim/gating.hpp"
+#include "moesim/model_config.hpp"
+#include "moesim/tolerance.hpp"
 #include "moesim/prng.hpp"
 #include "moesim/scheduler.hpp"
 #include "moesim/simulator.hpp"
@@ -111,6 +113,16 @@ int main() {
     unsigned long long bits;
     std::memcpy(&bits, &rep2.makespan, 8);
     mix(bits);
+  }
+  // ---- tolerance.hpp, builtin presets ----
+  CHECK(ms::approx_eq(1.0, 1.0 + 1e-10) && !ms::approx_eq(1.0, 1.0 + 1e-8));
+  CHECK(ms::approx_geq(1.0, 1.0 + 5e-10) && ms::definitely_lt(1.0, 1.0 + 1e-6));
+  CHECK(ms::approx_leq(0.0, 1e-16) && !ms::approx_leq(0.0, -1e-14));
+  mix(unsigned(ms::builtin_geometry_presets().size()));
+  for (const auto& [name, geo] : ms::builtin_geometry_presets()) {
+    mix(unsigned(name.size()));
+    mix(unsigned(geo.d_model) + unsigned(geo.d_ff) + unsigned(geo.n_experts_per_layer) +
+        unsigned(geo.bytes_per_param));
   }
   // ---- prng.hpp / gating.hpp: the LSH gate on host fp64 rows, workloads ----
   auto mixd = [&](double v) {

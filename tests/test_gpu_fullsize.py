@@ -160,6 +160,12 @@ def test_c3_layer_fullsize(cuda):
           f"frac(err > ulp) {float((err > ulp).mean()):.2e}")
     assert np.all(err <= ATOL + RTOL * np.abs(ref)), float(err.max())
     assert np.linalg.norm(err) / np.linalg.norm(ref) < 5e-3
+    # a tighter, structural bound: two bf16 ulps of the reference value plus a
+    # small multiple of rms(y) for elements near zero (cancellation)
+    ulp_ref = np.exp2(np.floor(np.log2(np.maximum(np.abs(ref), 1e-30))) - 7)
+    for c in (1e-3, 3e-3, 1e-2):
+        print(f"  max err / (2 ulp + {c} rms) = {float((err / (2 * ulp_ref + c * rms)).max()):.3f}")
+    assert np.all(err <= 2 * ulp_ref + 1e-2 * rms), float((err / (2 * ulp_ref + 1e-2 * rms)).max())
     res.close()
     off.close()
 

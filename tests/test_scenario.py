@@ -251,3 +251,24 @@ def test_cli_seed_override_and_resolve(tmp_path):
     assert json.loads((tmp_path / "a" / "resolved.json").read_text())["seed"] == 11
     assert (tmp_path / "a" / "greedy" / "events.csv").read_bytes() != \
         (tmp_path / "b" / "greedy" / "events.csv").read_bytes()
+
+
+def test_cpp_scenario_wrappers(tmp_path):
+    """The same front door from C++ through include/infmoe/moesim.hpp."""
+    exe = tmp_path / "scenario_demo"
+    lib_dir = Path(im.library_path()).parent
+    subprocess.run(["/usr/bin/g++", "-std=c++20", "-O2", str(ROOT / "tests" / "cpp" /
+                                                             "scenario_demo.cpp"),
+                    f"-I{ROOT / 'include'}", f"-L{lib_dir}", "-linfmoe",
+                    f"-Wl,-rpath,{lib_dir}", "-o", str(exe)], check=True, capture_output=True)
+    cfg = _write(tmp_path, variant(policies=["greedy", "serial"]))
+    r = subprocess.run([str(exe), str(cfg), str(tmp_path / "o")], capture_output=True,
+                       text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    summary, table, verdict = r.stdout.split("---\n")
+    assert summary.startswith("policy,makespan_s") and "greedy," in summary
+    rows = table.strip().splitlines()
+    assert len(rows) == 1 + 3 * 2 and all(r.startswith("K,") for r in rows[1:])  # 3 K x 2 policies
+    assert verdict.strip() == "ok"
+    assert (tmp_path / "o" / "run" / "greedy" / "events.csv").exists()
+    assert (tmp_path / "o" / "sweep" / "sweep.csv").exists()
