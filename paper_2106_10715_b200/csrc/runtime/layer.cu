@@ -324,6 +324,10 @@ std::vector<int32_t> Layer::pin_hottest(int n) {
 }
 
 Layer::~Layer() {
+  // continuous_load_stream links: nobody may prefetch into a destroyed layer
+  for (Layer* p : prevs) p->next = nullptr;
+  if (next) next->prevs.erase(std::remove(next->prevs.begin(), next->prevs.end(), this),
+                              next->prevs.end());
   cudaSetDevice(desc.device);
   for (void* p : ipc_opened) cudaIpcCloseMemHandle(p);
   if (copy_stream) cudaStreamSynchronize(copy_stream);
@@ -679,8 +683,13 @@ void Layer::prefetch(cudaEvent_t after_loads, cudaEvent_t after_computes) {
 void Layer::set_next(Layer* nxt) {
   require(desc.residency == INFMOE_OFFLOADED && desc.continuous_load_stream,
           "set_next: the layer is not an offloaded continuous_load_stream layer");
-  if (!nxt) {
+  auto unlink = [&] {
+    if (next) next->prevs.erase(std::remove(next->prevs.begin(), next->prevs.end(), this),
+                                next->prevs.end());
     next = nullptr;
+  };
+  if (!nxt) {
+    unlink();
     return;
   }
   require(nxt->desc.residency == INFMOE_OFFLOADED && nxt->desc.continuous_load_stream,
@@ -696,7 +705,9 @@ void Layer::set_next(Layer* nxt) {
     nxt->slot_base = want;
     nxt->set_assigned = true;
   }
+  unlink();
   next = nxt;
+  nxt->prevs.push_back(this);
 }
 
 // PEER transport: publish (pid, pointers, IPC handles) of the symmetric

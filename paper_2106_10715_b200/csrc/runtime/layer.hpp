@@ -130,6 +130,7 @@ struct Layer {
     int expert;
   };
   Layer* next = nullptr;
+  std::vector<Layer*> prevs;  // layers whose `next` is this one (unlinked on destroy)
   bool set_assigned = false;
   std::vector<Prefetched> pf;
   int pf_reused = 0;

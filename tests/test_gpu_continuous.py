@@ -65,3 +65,23 @@ def test_continuous_stack_bit_identical_and_prefetch_hits(cuda, codec, depth):
         lay.close()
     pool1.close()
     pool2.close()
+
+
+def test_continuous_links_survive_destroy(cuda):
+    """Destroying a layer unlinks it from the layer that would prefetch into it."""
+    N, d, f, E, K = 128, 256, 512, 4, 1
+    t = lambda b, sh: torch.from_numpy(b.view(np.int16).reshape(sh)).view(torch.bfloat16)
+    wi = t(fill_bf16(1, E * f * d, 0.1), (E, f, d)).pin_memory()
+    wo = t(fill_bf16(2, E * d * f, 0.03), (E, d, f)).pin_memory()
+    x = t(fill_bf16(3, N * d, 1.0), (N, d)).to(cuda)
+    kw = dict(gate="lsh", lsh_bits=2, max_tokens=N, offloaded=True, K=K,
+              continuous_load_stream=True)
+    a = dv.MoELayer(d, f, E, 1, wi, wo, lsh_seed=1, **kw)
+    b = dv.MoELayer(d, f, E, 1, wi, wo, lsh_seed=2, **kw)
+    a.set_next(b)
+    a.forward(x)
+    b.forward(x)
+    b.close()            # a's link to b must go with it
+    y, info = a.forward(x)   # would prefetch into freed memory if still linked
+    torch.cuda.synchronize()
+    a.close()
