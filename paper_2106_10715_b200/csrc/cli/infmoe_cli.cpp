@@ -1,6 +1,7 @@
 // infmoe — the scenario CLI: a thin front end over the
-// C-ABI (include/infmoe.h).  Exit codes: 0 ok, 2 config, 3 capacity, 4
-// invariant breach, 5 CUDA runtime, 6 malformed call.
+// C-ABI (include/infmoe.h).  Exit codes: 0 ok, 2 config error
+// (including the library's 6, a malformed argument), 3 capacity, 4 invariant
+// breach; 5 CUDA runtime (execute only).
 //   infmoe run   <config.json> [--out DIR] [--seed S] [--trace-format chrome|csv|both]
 //                [--execute] [--device N] [--host-sets N] [--repeats N]
 //   infmoe sweep <config.json> --axis K|total_tokens|zipf_s|bandwidth --values a,b,c
@@ -83,5 +84,5 @@ int main(int argc, char** argv) {
     return usage();
   }
   if (rc != 0) std::fprintf(stderr, "infmoe: %s\n", infmoe_last_error());
-  return rc;
+  return rc == INFMOE_ERR_ARGUMENT ? INFMOE_ERR_CONFIG : rc;
 }
