@@ -335,10 +335,10 @@ typedef struct {
    * base -- shared by every layer on the same host weights; each load copies
    * the pack and a decoder kernel restores the bf16 slot bit for bit before the
    * FFN).  INFMOE_CODEC_EXPH codes the exponent's distance to its block base
-   * with a per-matrix canonical Huffman code (<= 12 bits) instead: 128-value
+   * with a per-matrix canonical Huffman code (<= 12 bits) instead: 256-value
    * chunks with recorded start bits, decoded one warp per 32 chunks (one lane
    * per chunk) through a shared-memory table, sign/mantissa bytes
-   * lane-interleaved; ~10.3-10.8 bits per value (uniform / Gaussian weights).
+   * lane-interleaved; ~10.3-10.7 bits per value (uniform / Gaussian weights).
    * Packs are SNAPSHOTS of the host weights taken at create and at every
    * infmoe_layer_set_host_weights call (which always re-packs); layers created
    * on the same host buffers share one pack only while its content digest
@@ -454,7 +454,7 @@ int infmoe_layer_h2d_bytes(infmoe_layer* layer, uint64_t* packed, uint64_t* raw)
 /* codec round trip (test hook): pack n bf16 values (host) with codec
  * (INFMOE_CODEC_EXP4 / EXPH) on the host, decode them on the device, copy the
  * result to out (host); pack_bytes (may be NULL) receives the pack size.  n must
- * be a positive multiple of 128. */
+ * be a positive multiple of 256 (exph) or 128 (exp4). */
 int infmoe_codec_roundtrip(int32_t codec, const uint16_t* in, uint64_t n, uint16_t* out,
                            uint64_t* pack_bytes, int32_t device);
 /* the same round trip decoded by the host reference decoder (no GPU needed) */

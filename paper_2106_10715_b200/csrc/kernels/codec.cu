@@ -317,7 +317,7 @@ __global__ void __launch_bounds__(kExphWarps * 32) exph_unpack_kernel(const uint
           uint4* dst = reinterpret_cast<uint4*>(out + c0 * kExphChunk);
           for (int u = lane; u < nch * 8; u += nch) {
             const int row = u / 8, slot = u % 8;
-            dst[row * 16 + (q / 4) * 8 + slot] = st[row * 8 + (slot ^ (row & 7))];
+            dst[row * (kExphChunk / 8) + (q / 4) * 8 + slot] = st[row * 8 + (slot ^ (row & 7))];
           }
           __syncwarp(active);
         }
@@ -330,7 +330,7 @@ __global__ void __launch_bounds__(kExphWarps * 32) exph_unpack_kernel(const uint
 }  // namespace
 
 ExphPlan exph_plan(const uint16_t* in, uint64_t n) {
-  require(n > 0 && n % kExphChunk == 0, "exph: value count must be a positive multiple of 128");
+  require(n > 0 && n % kExphChunk == 0, "exph: value count must be a positive multiple of 256");
   ExphPlan p;
   ExphLayout& L = p.L;
   L.n = n;
@@ -339,25 +339,56 @@ ExphPlan exph_plan(const uint16_t* in, uint64_t n) {
   L.ngroups = (L.nchunks + kExphGroup - 1) / kExphGroup;
   p.base.assign(L.nblocks, 0);
   const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-  std::vector<std::vector<uint64_t>> hist(hw, std::vector<uint64_t>(32, 0));
-  {
+  auto run = [&](auto&& body) {  // body(thread, block) over all blocks
     std::vector<std::thread> th;
     for (unsigned t = 0; t < hw; ++t)
       th.emplace_back([&, t] {
-        for (uint64_t b = t; b < L.nblocks; b += hw) {
-          const uint64_t v0 = b * kExp4Block, v1 = std::min(n, v0 + kExp4Block);
-          uint32_t mx = 0;
-          for (uint64_t i = v0; i < v1; ++i) mx = std::max<uint32_t>(mx, (in[i] >> 7) & 0xFFu);
-          p.base[b] = uint8_t(mx);
-          for (uint64_t i = v0; i < v1; ++i) ++hist[t][exph_sym(in[i], mx)];
-        }
+        for (uint64_t b = t; b < L.nblocks; b += hw) body(t, b);
       });
     for (auto& x : th) x.join();
+  };
+  // exponent bases: each block's largest exponent, and the matrix's largest
+  run([&](unsigned, uint64_t b) {
+    const uint64_t v0 = b * kExp4Block, v1 = std::min(n, v0 + kExp4Block);
+    uint32_t mx = 0;
+    for (uint64_t i = v0; i < v1; ++i) mx = std::max<uint32_t>(mx, (in[i] >> 7) & 0xFFu);
+    p.base[b] = uint8_t(mx);
+  });
+  const uint32_t gmax = *std::max_element(p.base.begin(), p.base.end());
+  // histograms of the distance symbols against both choices of base
+  std::vector<std::vector<uint64_t>> hb(hw, std::vector<uint64_t>(32, 0)), hg = hb;
+  run([&](unsigned t, uint64_t b) {
+    const uint64_t v0 = b * kExp4Block, v1 = std::min(n, v0 + kExp4Block);
+    for (uint64_t i = v0; i < v1; ++i) {
+      ++hb[t][exph_sym(in[i], p.base[b])];
+      ++hg[t][exph_sym(in[i], gmax)];
+    }
+  });
+  // One base for the whole matrix codes the distance with the exponent's own
+  // entropy (i.i.d. weights: 2.55 bits for Gaussian bf16), block bases add the
+  // spread of the block maxima (2.62); blocks help when the magnitude drifts
+  // along the matrix.  The encoder keeps whichever costs fewer bits; the pack
+  // format (a base per block) and the decoder are the same either way.
+  uint64_t fb[32] = {}, fg[32] = {};
+  for (unsigned t = 0; t < hw; ++t)
+    for (int i = 0; i < 32; ++i) {
+      fb[i] += hb[t][size_t(i)];
+      fg[i] += hg[t][size_t(i)];
+    }
+  uint8_t lb[32], lg[32];
+  huffman_lengths(fb, lb);
+  huffman_lengths(fg, lg);
+  auto cost = [](const uint64_t* f, const uint8_t* l) {
+    uint64_t bits = 0;
+    for (int i = 0; i < 32; ++i) bits += f[i] * (l[i] + (i == kExphEsc ? 8u : 0u));
+    return bits;
+  };
+  if (cost(fg, lg) < cost(fb, lb)) {
+    std::fill(p.base.begin(), p.base.end(), uint8_t(gmax));
+    std::copy(lg, lg + 32, p.len);
+  } else {
+    std::copy(lb, lb + 32, p.len);
   }
-  uint64_t freq[32] = {};
-  for (auto& h : hist)
-    for (int i = 0; i < 32; ++i) freq[i] += h[size_t(i)];
-  huffman_lengths(freq, p.len);
   canonical_codes(p.len, p.code);
   std::vector<uint32_t> cb(L.nchunks, 0);
   parallel_blocks(L.nchunks, [&](uint64_t c) {

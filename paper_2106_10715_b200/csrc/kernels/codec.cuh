@@ -69,19 +69,20 @@ void launch_exp4_unpack(const uint8_t* pack, uint64_t n, uint16_t* out, cudaStre
 // ------------------------------------------------------------------ exph --
 // Entropy-coded exponents ("exph"): the same sign/mantissa bytes, and per value
 // a canonical Huffman code (<= 12 bits, one code table per matrix) of
-// min(base - exponent, 31) against the per-block base; symbol 31 is followed by
-// the raw 8-bit exponent.  Codes are concatenated MSB-first per 128-value
-// chunk; a chunk's starting bit is a uint32 per group of 16 chunks plus a
-// uint16 offset inside the group (0.14 bits per value), so one GPU thread
-// decodes one chunk through a 4096-entry lookup table in shared memory.  ~2.1
-// bits of exponent for the bench's weights (entropy 2.14): ~10.3 bits/value.
+// min(base - exponent, 31) against the per-block base (the encoder may give
+// every block the matrix's base when that codes shorter); symbol 31 is
+// followed by the raw 8-bit exponent.  Codes are concatenated MSB-first per
+// 256-value chunk; a chunk's starting bit is a uint32 per group of 8 chunks
+// plus a uint16 offset inside the group (0.078 bits per value), so one GPU
+// thread decodes one chunk through a 4096-entry lookup table in shared memory.
+// ~10.7 bits per value for Gaussian bf16 weights (entropy 10.46).
 //
 // Layout: [0, n) sign/mantissa (lane-interleaved, exph_sm_offset) | [off_bits) bitstream (uint32 words, + 8 B
 // slack) | [off_group) uint32 start bit per group | [off_chunk) uint16 offset
 // per chunk | [off_base) base per block | [off_lut) uint32 LUT[4096] = len0 |
 // sym0 << 4 | sym1 << 9 | (len0 + len1) << 14 | two << 19 (the decoder takes two
 // values per lookup when both codes fit in the 12-bit window)
-constexpr int kExphChunk = 128;
+constexpr int kExphChunk = 256;
 constexpr int kExphWarpChunks = 32;  // chunks decoded together by one warp (one per lane)
 
 // byte offset of the 16 sign/mantissa bytes of chunk c's 16-value group q: the
@@ -94,7 +95,7 @@ __host__ __device__ inline uint64_t exph_sm_offset(uint64_t c, uint32_t q, uint6
                                                                       : uint64_t(kExphWarpChunks);
   return first * kExphChunk + uint64_t(q) * nch * 16 + lane * 16;
 }
-constexpr int kExphGroup = 16;  // chunks per group (<= 16 x 128 x 20 bits < 2^16)
+constexpr int kExphGroup = 8;  // chunks per group (8 x 256 x 20 bits < 2^16: uint16 offsets)
 constexpr int kExphMaxLen = 12;
 constexpr int kExphEsc = 31;
 

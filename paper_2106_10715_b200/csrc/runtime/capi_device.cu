@@ -344,7 +344,8 @@ int infmoe_codec_roundtrip_host(int32_t codec_id, const uint16_t* in, uint64_t n
     require(in && out, "codec_roundtrip_host: NULL argument");
     require(codec_id == INFMOE_CODEC_EXP4 || codec_id == INFMOE_CODEC_EXPH,
             "codec_roundtrip_host: unknown codec");
-    require(n > 0 && n % 128 == 0, "codec_roundtrip_host: n must be a positive multiple of 128");
+    require(n > 0 && n % (codec_id == INFMOE_CODEC_EXPH ? 256 : 128) == 0,
+            "codec_roundtrip_host: n must be a positive multiple of 256 (exph) / 128 (exp4)");
     std::vector<uint8_t> pk;
     if (codec_id == INFMOE_CODEC_EXP4) {
       const codec::Exp4Plan plan = codec::exp4_plan(in, n);
@@ -374,7 +375,8 @@ int infmoe_codec_roundtrip(int32_t codec_id, const uint16_t* in, uint64_t n, uin
     require(in && out, "codec_roundtrip: NULL argument");
     require(codec_id == INFMOE_CODEC_EXP4 || codec_id == INFMOE_CODEC_EXPH,
             "codec_roundtrip: unknown codec");
-    require(n > 0 && n % 128 == 0, "codec_roundtrip: n must be a positive multiple of 128");
+    require(n > 0 && n % (codec_id == INFMOE_CODEC_EXPH ? 256 : 128) == 0,
+            "codec_roundtrip: n must be a positive multiple of 256 (exph) / 128 (exp4)");
     INFMOE_CUDA(cudaSetDevice(device));
     std::vector<uint8_t> pk;
     codec::ExphLayout hl;

@@ -38,7 +38,7 @@ def test_exph_length_limit_fibonacci_histogram():
         fib.append(fib[-1] + fib[-2])
     deltas = np.concatenate([np.full(c, i) for i, c in enumerate(fib[::-1][:26])])
     rng.shuffle(deltas)
-    n = (deltas.size // 128) * 128
+    n = (deltas.size // 256) * 256
     exps = (200 - deltas[:n]).astype(np.uint16)
     a = (exps << 7) | rng.integers(0, 128, n, dtype=np.uint16) | \
         (rng.integers(0, 2, n, dtype=np.uint16) << 15)
