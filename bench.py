@@ -1176,9 +1176,10 @@ def main() -> None:
                     "each expert's FFN; outputs bit-identical to the raw stream)",
             "exph": "exph (lossless: the same bf16 weights packed once on the host -- a "
                     "sign/mantissa byte and a canonical Huffman code (<= 12 bits, one table "
-                    "per matrix) of the exponent's distance to a per-32768-value base, 128-value "
-                    "chunks with recorded start bits -- decoded on the GPU before each "
-                    "expert's FFN; outputs bit-identical to the raw stream)"}
+                    "per matrix) of the exponent's distance to a per-32768-value or matrix-wide "
+                    "base (whichever codes shorter), 256-value chunks with recorded start bits "
+                    "-- decoded on the GPU before each expert's FFN, the last expert's W_in "
+                    "while its W_out is on the link; outputs bit-identical to the raw stream)"}
         line["h2d"] = {
             "codec": codec_desc[args.h2d_codec],
             "achieved_gbs": link_bytes / (t_ex * 1e-3) / 1e9, "peak_gbs": h2d_peak,

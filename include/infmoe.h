@@ -235,6 +235,16 @@ int infmoe_debug_set_flag(int32_t* flag, void* stream);
 int infmoe_gate_softmax_topk(const void* x, int32_t dtype, int64_t N, int32_t d,
                              const float* wg, const float* bias, int32_t E, int32_t k,
                              int32_t* topk_idx, float* topk_w, int32_t* counts, void* stream);
+/* Test hook of the same gate: also returns the tensor-core path's approximate
+ * logits (approx_logits[N,E] f32 device, may be NULL) and its counters
+ * (stats[4] u64 device: tokens certified from the tensor-core logits, tokens
+ * sent to the exact fallback, exact-chain logits the fallback computed, tokens
+ * that took every expert through the exact chain; all-ones when the call ran
+ * on the CUDA-core path: f32 x, top_k == 1 or > 8, E > 128, d % 64 != 0). */
+int infmoe_gate_softmax_debug(const void* x, int32_t dtype, int64_t N, int32_t d,
+                              const float* wg, const float* bias, int32_t E, int32_t k,
+                              int32_t* topk_idx, float* topk_w, int32_t* counts,
+                              float* approx_logits, uint64_t* stats, void* stream);
 /* N1b LSH gate (gating.hpp:61-104) on the fp64 promotion of x; proj[bits,d] f64 device.
  * Writes codes[N] u32 (may be NULL), topk_idx[N], topk_w[N]=1, counts[E]. */
 int infmoe_gate_lsh(const void* x, int32_t dtype, int64_t N, int32_t d, const double* proj,

@@ -14,8 +14,11 @@
 #include <cmath>
 #include <cstdlib>
 
+#include <cuda_bf16.h>
+
 #include "common.cuh"
 #include "kernels.cuh"
+#include "tc_ptx.cuh"
 
 namespace infmoe {
 namespace {
@@ -730,6 +733,703 @@ void lsh_mma_go(const void* x, int64_t N, int d, const double* proj, int bits, i
       reinterpret_cast<const T*>(x), N, d, proj, bits, E, force, codes, idx, w, counts);
 }
 
+// ------------------------------------------------- N1a on tensor cores ----
+// The CUDA-core gate above spends d FMAs per (token, expert) on the CUDA
+// cores and is issue-bound (C5: 16384 x 64 x 4096, ~350 us).  For bf16 token
+// rows and 2 <= top_k <= 8 the gate instead runs as
+//  0. gate_split_kernel (once per gate matrix; a layer does it at set-up):
+//     W_g (fp32) = hi + mid + lo, three bf16 matrices (3 x 8 significand bits
+//     cover fp32's 24; a residual only where a part underflows, measured), and
+//     the per-expert bound coefficient g_e (below).
+//  1. gate_tc_kernel: L~[t, e] = x_t . (hi_e + mid_e + lo_e) on tcgen05
+//     (kind::f16, 128-token tiles, the three parts against the same
+//     TMA-staged x tile).  The hi products go to S fp32 TMEM accumulators, one
+//     per K segment; mid and lo (<= 2^-8 of hi) share one more; the epilogue
+//     sums them in a fixed order.  The 4 epilogue warps also read every staged
+//     x tile (their row's 128 B) for ||x_t||_2, so x is streamed from HBM
+//     exactly once.  Epilogue thread = token:
+//       B_e = ||x_t|| g_e + 2^-22 |L~_e| + beta >= |L~_e - L_e|,
+//     L_e the exact fmaf-chain logit of the CUDA-core gate (its reduction
+//     order is the contract, oracle.c or_gate_softmax).  If the k largest
+//     L~ are separated by their bounds (L~_(j) - B_(j) > L~_(j+1) + B_(j+1))
+//     and from every other expert (L~_(k) - B_(k) > max_rest L~_e + B_e),
+//     the exact chain would pick the same experts in the same order: the
+//     token is CERTIFIED and its picks, softmax weights (from L~, renormalised
+//     over the picks) and counts are written right there.
+//  2. gate_tc_fallback_kernel (one warp per uncertified token, listed by
+//     step 1): every expert whose upper bound reaches the k-th largest lower
+//     bound is a candidate and gets its exact logit by the CUDA-core gate's
+//     fmaf chain and butterfly; top-k over those (ties and NaN -> lower
+//     index).  A token with a non-finite value or more than kTcCandMax
+//     candidates takes every expert through the exact chain.
+// So indices and counts equal the exact gate's by construction; the weights
+// carry the tensor-core logits' error (observed <= 1.5e-7 ||x|| ||w||).
+// g_e = gamma_hi ||hi_e|| + gamma_ml ||mid_e + lo_e|| + gamma_w ||w_e|| +
+// ||residual_e||, with gamma_hi/ml = 17 2^-23 (m + 1) for the m tcgen05.mma
+// accumulated into one hi / the mid-lo accumulator (each MMA, 16 products plus
+// the accumulator, is modelled as aligning its 17 addends to the largest and
+// truncating each at 2^-23 of it; a wider alignment only tightens this), and
+// gamma_w = (S + 1) 2^-24 (the epilogue's sum) + (dpad/32 + 8) 2^-23 (the
+// exact chain's own fmaf/butterfly rounding), all against sum |x_i v_i| <=
+// ||x|| ||v|| (Cauchy-Schwarz).  tests/test_gpu_gate_tc.py records the
+// observed |L~ - x.w| against the model.
+constexpr int kTcTok = 128;     // tokens per tile = UMMA M = TMEM lanes
+constexpr int kTcThreads = 192; // warp 0 TMA, warp 1 MMA, warps 2-5 epilogue
+constexpr int kTcMaxStages = 8;
+constexpr int kTcParts = 3;     // hi, mid, lo
+constexpr int kTcKMax = 8;
+constexpr int kTcCandMax = 24;
+constexpr int kTcSelWarps = 4;  // tokens per fallback CTA
+constexpr int kTcMaxD = 16384;  // the fallback stages d bf16 per warp in shared memory
+constexpr int kTcTmemCols = 512;
+constexpr int kTcSplitSeg = 16; // column segments per expert row in the split
+
+__global__ void __launch_bounds__(256) gate_split_kernel(const float* __restrict__ wg, int E,
+                                                         int Ep, int d,
+                                                         __nv_bfloat16* __restrict__ w3,
+                                                         double* __restrict__ sums) {
+  __shared__ double red[4][256];
+  const int e = blockIdx.x;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};  // w^2, hi^2, (mid + lo)^2, residual^2
+  for (int c = blockIdx.y * 256 + threadIdx.x; c < d; c += kTcSplitSeg * 256) {
+    const float w = e < E ? wg[size_t(e) * d + c] : 0.0f;
+    const __nv_bfloat16 hi = __float2bfloat16_rn(w);
+    const float r1 = w - __bfloat162float(hi);  // exact (Sterbenz)
+    const __nv_bfloat16 mid = __float2bfloat16_rn(r1);
+    const __nv_bfloat16 lo = __float2bfloat16_rn(r1 - __bfloat162float(mid));
+    w3[size_t(e) * d + c] = hi;
+    w3[(size_t(Ep) + e) * d + c] = mid;
+    w3[(size_t(2 * Ep) + e) * d + c] = lo;
+    // exact in fp64 (0 unless a part underflows bf16's normal range)
+    const double ml = double(__bfloat162float(mid)) + double(__bfloat162float(lo));
+    const double res = double(w) - double(__bfloat162float(hi)) - ml;
+    acc[0] += double(w) * double(w);
+    acc[1] += double(__bfloat162float(hi)) * double(__bfloat162float(hi));
+    acc[2] += ml * ml;
+    acc[3] += res * res;
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) red[q][threadIdx.x] = acc[q];
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (int(threadIdx.x) < o)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) red[q][threadIdx.x] += red[q][threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x < 4) atomicAdd(&sums[4 * e + threadIdx.x], red[threadIdx.x][0]);
+}
+
+// g_e = gamma_hi ||hi_e|| + gamma_ml ||mid_e + lo_e|| + gamma_w ||w_e|| + ||res_e||
+__global__ void gate_coef_kernel(const double* __restrict__ sums, int Ep, double gamma_hi,
+                                 double gamma_ml, double gamma_w, float* __restrict__ gcoef) {
+  for (int e = threadIdx.x; e < Ep; e += blockDim.x) {
+    const double* q = sums + 4 * e;
+    const double g = (gamma_hi * sqrt(q[1]) + gamma_ml * sqrt(q[2]) + gamma_w * sqrt(q[0]) +
+                      sqrt(q[3])) *
+                     (1.0 + 1e-6);
+    gcoef[e] = __double2float_ru(g);
+  }
+}
+
+struct TcGateArgs {
+  int64_t N;
+  int d, Ep, E, k, stages, seg_kb, n_seg, force_exact;  // n_seg hi segments (+1 mid/lo)
+  const float* gcoef;
+  const float* bias;
+  int32_t* topk_idx;
+  float* topk_w;
+  int32_t* counts;
+  int32_t* fb_list;    // uncertified tokens
+  int32_t* fb_count;
+  float* fb_logits;    // [fb slot][Ep] their L~ (no bias)
+  float* approx;       // optional [N][Ep] L~ of every token (test hook)
+  unsigned long long* stats;  // [2]: certified tokens
+};
+
+__device__ __forceinline__ float tc_bound(float nx, float g, float v) {
+  return __fadd_ru(__fmaf_ru(nx, g, 1e-30f), __fmul_ru(fabsf(v), 2.4e-7f));
+}
+
+template <int K>
+__global__ void __launch_bounds__(kTcThreads, 1) gate_tc_kernel(
+    const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_w,
+    const TcGateArgs a) {
+  using namespace gemm;
+  extern __shared__ uint8_t tc_smem[];
+  __shared__ uint32_t tmem_slot;
+  __shared__ int hist[128];
+  const uint32_t base = (smem_u32(tc_smem) + 1023u) & ~1023u;
+  const uint32_t A_BYTES = kTcTok * ROW_BYTES;
+  const uint32_t P_BYTES = uint32_t(a.Ep) * ROW_BYTES;
+  const uint32_t STAGE = A_BYTES + kTcParts * P_BYTES;
+  const int stages = a.stages;
+  const uint32_t bar0 = base + uint32_t(stages) * STAGE;
+  auto full_bar = [&](int s) { return bar0 + 8u * s; };
+  auto empty_bar = [&](int s) { return bar0 + 8u * (kTcMaxStages + s); };
+  const uint32_t accf_bar = bar0 + 8u * (2 * kTcMaxStages);
+  const uint32_t acce_bar = accf_bar + 8u;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  for (int i = threadIdx.x; i < 128; i += blockDim.x) hist[i] = 0;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(full_bar(s), 1);
+      mbar_init(empty_bar(s), 1 + 4);  // the MMA commit + the 4 norm/epilogue warps
+    }
+    mbar_init(accf_bar, 1);
+    mbar_init(acce_bar, 4);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&tmem_slot)),
+                 "n"(kTcTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+  const int64_t N = a.N;
+  const int Ep = a.Ep;
+  const int64_t n_tiles = (N + kTcTok - 1) / kTcTok;
+  const int kblocks = a.d / (ROW_BYTES / 2);
+
+  if (warp == 0) {  // ---- TMA producer: x tile + the W_g parts per K-block
+    if (lane == 0) {
+      const uint64_t pol_x = policy_evict_first(), pol_w = policy_evict_last();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x)
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(empty_bar(stage), phase ^ 1);
+          const uint32_t sA = base + uint32_t(stage) * STAGE;
+          mbar_expect_tx(full_bar(stage), STAGE);
+          tma_load_2d(sA, &tmap_x, full_bar(stage), kb * 64, int32_t(t * kTcTok), pol_x);
+          for (int p = 0; p < kTcParts; ++p)
+            tma_load_2d(sA + A_BYTES + p * P_BYTES, &tmap_w, full_bar(stage), kb * 64, p * Ep,
+                        pol_w);
+          if (++stage == stages) { stage = 0; phase ^= 1; }
+        }
+    }
+  } else if (warp == 1) {  // ---- MMA issuer (one elected lane)
+    const uint32_t idesc = make_idesc<false>(uint32_t(Ep));
+    int stage = 0;
+    uint32_t phase = 0, acc_phase = 0;
+    for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      mbar_wait(acce_bar, acc_phase ^ 1);  // the previous tile's epilogue has read TMEM
+      tc_fence_after();
+      for (int kb = 0; kb < kblocks; ++kb) {
+        mbar_wait(full_bar(stage), phase);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t sA = base + uint32_t(stage) * STAGE;
+          const uint64_t da = sdesc(sA);
+          // hi -> its K segment's accumulator; mid and lo -> one shared accumulator
+          const uint32_t d_hi = tmem + uint32_t((kb / a.seg_kb) * Ep);
+          const uint32_t d_ml = tmem + uint32_t(a.n_seg * Ep);
+          const bool first_hi = kb % a.seg_kb == 0;
+          const uint64_t db_hi = sdesc(sA + A_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            mma<false>(d_hi, da + 2 * kk, db_hi + 2 * kk, idesc, (first_hi && kk == 0) ? 0u : 1u);
+#pragma unroll
+          for (int p = 1; p < kTcParts; ++p) {
+            const uint64_t db = sdesc(sA + A_BYTES + p * P_BYTES);
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+              mma<false>(d_ml, da + 2 * kk, db + 2 * kk, idesc,
+                         (kb == 0 && p == 1 && kk == 0) ? 0u : 1u);
+          }
+          tc_commit(empty_bar(stage));
+        }
+        __syncwarp();
+        if (++stage == stages) { stage = 0; phase ^= 1; }
+      }
+      if (lane == 0) tc_commit(accf_bar);
+      __syncwarp();
+      acc_phase ^= 1;
+    }
+  } else {  // ---- norm + certification epilogue: thread = token row
+    const int quarter = warp & 3;  // TMEM lanes 32*quarter .. +31
+    const int r = quarter * 32 + lane;
+    int stage = 0;
+    uint32_t phase = 0, acc_phase = 0;
+    for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      // ||x_t||^2 from the staged tiles: row r's 8 16-byte chunks (SW128:
+      // chunk j of row r sits at j ^ (r & 7))
+      float ssj[8] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f};  // 8 short chains
+      for (int kb = 0; kb < kblocks; ++kb) {
+        mbar_wait(full_bar(stage), phase);
+        const uint8_t* row = tc_smem + (base - smem_u32(tc_smem)) + size_t(stage) * STAGE +
+                             size_t(r) * ROW_BYTES;
+        uint4 v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          v[j] = *reinterpret_cast<const uint4*>(row + ((j ^ (r & 7)) << 4));
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty_bar(stage));  // the row is in registers
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint32_t w4[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const float p = __uint_as_float(w4[i] << 16), q = __uint_as_float(w4[i] & 0xffff0000u);
+            ssj[j] = fmaf(p, p, ssj[j]);
+            ssj[j] = fmaf(q, q, ssj[j]);
+          }
+        }
+        if (++stage == stages) { stage = 0; phase ^= 1; }
+      }
+      float ss = 0.0f;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) ss += ssj[j];
+      // >= ||x_t||_2 (the fp32 sum of d squares is within (d/8 + 8) 2^-24 of exact)
+      const float nx = __fmul_ru(__fsqrt_ru(ss), 1.001f);
+      mbar_wait(accf_bar, acc_phase);
+      tc_fence_after();
+      const int64_t tok = t * kTcTok + r;
+      const uint32_t taddr = tmem + (uint32_t(quarter * 32) << 16);
+      // running top-K by L~ (ties -> lower index: experts arrive ascending)
+      float tv[K], tlo[K], tup[K];
+      int ti[K];
+#pragma unroll
+      for (int j = 0; j < K; ++j) { tv[j] = -INFINITY; tlo[j] = tup[j] = -INFINITY; ti[j] = -1; }
+      float rest_up = -INFINITY;
+      bool bad = !(nx <= 3.0e38f);
+      for (int cc = 0; cc < Ep / 32; ++cc) {
+        float acc[32];
+        uint32_t rr[32], r2[32];
+        tmem_ld32(taddr + cc * 32, rr);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) acc[i] = __uint_as_float(rr[i]);
+        int sg = 1;
+        for (; sg + 1 < a.n_seg; sg += 2) {  // two segment loads in flight
+          tmem_ld32_nowait(taddr + uint32_t(sg * Ep) + cc * 32, rr);
+          tmem_ld32_nowait(taddr + uint32_t((sg + 1) * Ep) + cc * 32, r2);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) acc[i] += __uint_as_float(rr[i]);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) acc[i] += __uint_as_float(r2[i]);
+        }
+        if (sg < a.n_seg) {
+          tmem_ld32(taddr + uint32_t(sg * Ep) + cc * 32, rr);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) acc[i] += __uint_as_float(rr[i]);
+        }
+        tmem_ld32(taddr + uint32_t(a.n_seg * Ep) + cc * 32, rr);  // + (mid + lo)
+#pragma unroll
+        for (int i = 0; i < 32; ++i) acc[i] += __uint_as_float(rr[i]);
+        if (a.approx && tok < N) {
+          float4* dst = reinterpret_cast<float4*>(a.approx + tok * Ep + cc * 32);
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            dst[i] = make_float4(acc[4 * i], acc[4 * i + 1], acc[4 * i + 2], acc[4 * i + 3]);
+        }
+        if (a.fb_logits && tok < N) {  // kept for the fallback in case the token is not certified
+          float4* dst = reinterpret_cast<float4*>(a.fb_logits + tok * Ep + cc * 32);
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            dst[i] = make_float4(acc[4 * i], acc[4 * i + 1], acc[4 * i + 2], acc[4 * i + 3]);
+        }
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const int e = cc * 32 + i;
+          if (e >= a.E) break;
+          const float v = a.bias ? __fadd_rn(acc[i], a.bias[e]) : acc[i];
+          const float B = tc_bound(nx, a.gcoef[e], v);
+          if (!(fabsf(v) <= 3.0e38f) || !(B <= 3.0e38f)) bad = true;
+          const float lo = __fsub_rd(v, B), up = __fadd_ru(v, B);
+          // insert (v, e) into the sorted top-K; whatever falls out joins the rest
+          float cv = v, clo = lo, cup = up;
+          int ci = e;
+#pragma unroll
+          for (int j = 0; j < K; ++j) {
+            if (cv > tv[j]) {
+              const float sv = tv[j], slo = tlo[j], sup = tup[j];
+              const int si = ti[j];
+              tv[j] = cv; tlo[j] = clo; tup[j] = cup; ti[j] = ci;
+              cv = sv; clo = slo; cup = sup; ci = si;
+            }
+          }
+          if (ci >= 0) rest_up = fmaxf(rest_up, cup);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(acce_bar);  // TMEM may be overwritten now
+      acc_phase ^= 1;
+      if (tok < N) {
+        bool ok = !bad && !a.force_exact && ti[K - 1] >= 0;
+#pragma unroll
+        for (int j = 0; j + 1 < K; ++j) ok = ok && tlo[j] > tup[j + 1];
+        ok = ok && tlo[K - 1] > rest_up;
+        if (ok) {  // certified: the exact chain picks the same experts in the same order
+          float ps = 0.0f, pj[K];
+#pragma unroll
+          for (int j = 0; j < K; ++j) { pj[j] = expf(tv[j] - tv[0]); ps += pj[j]; }
+#pragma unroll
+          for (int j = 0; j < K; ++j) {
+            a.topk_idx[tok * K + j] = ti[j];
+            a.topk_w[tok * K + j] = pj[j] / ps;
+            atomicAdd(&hist[ti[j]], 1);
+          }
+        } else {
+          const int pos = atomicAdd(a.fb_count, 1);
+          a.fb_list[pos] = int32_t(tok);
+        }
+        const unsigned m = __ballot_sync(__activemask(), ok);
+        if (a.stats && (lane == __ffs(__activemask()) - 1))
+          atomicAdd(&a.stats[0], static_cast<unsigned long long>(__popc(m)));
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  for (int e = threadIdx.x; e < a.E; e += blockDim.x)
+    if (hist[e]) atomicAdd(&a.counts[e], hist[e]);
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "n"(kTcTmemCols)
+                 : "memory");
+  }
+}
+
+// the CUDA-core gate's logit for one (token, expert), by one warp: lane l's
+// fmaf chain over columns 8l..8l+7 of every 256-column chunk (columns past d
+// contribute fmaf(0, 0, acc)), butterfly, + bias.  x row from shared memory;
+// the weight slices of 8 chunks are requested before the chain consumes them.
+__device__ __forceinline__ void fma8(float& acc, const uint4 raw, const float4 a,
+                                     const float4 b) {
+  acc = fmaf(__uint_as_float(raw.x << 16), a.x, acc);
+  acc = fmaf(__uint_as_float(raw.x & 0xffff0000u), a.y, acc);
+  acc = fmaf(__uint_as_float(raw.y << 16), a.z, acc);
+  acc = fmaf(__uint_as_float(raw.y & 0xffff0000u), a.w, acc);
+  acc = fmaf(__uint_as_float(raw.z << 16), b.x, acc);
+  acc = fmaf(__uint_as_float(raw.z & 0xffff0000u), b.y, acc);
+  acc = fmaf(__uint_as_float(raw.w << 16), b.z, acc);
+  acc = fmaf(__uint_as_float(raw.w & 0xffff0000u), b.w, acc);
+}
+
+__device__ __forceinline__ float exact_logit(const __nv_bfloat16* xs,
+                                             const float* __restrict__ wr, int d, int lane,
+                                             const float* bias, int e) {
+  constexpr int G = 8;
+  const int nch = (d + 255) / 256;
+  float acc = 0.0f;
+  for (int cb = 0; cb < nch; cb += G) {
+    float4 wa[G], wb[G];
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+      const int c = (cb + j) * 256 + lane * 8;
+      if (cb + j < nch && c < d) {
+        wa[j] = __ldg(reinterpret_cast<const float4*>(wr + c));
+        wb[j] = __ldg(reinterpret_cast<const float4*>(wr + c) + 1);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+      if (cb + j < nch) {
+        const int c = (cb + j) * 256 + lane * 8;
+        if (c < d) fma8(acc, *reinterpret_cast<const uint4*>(xs + c), wa[j], wb[j]);
+        else acc = __fadd_rn(acc, 0.0f);  // == fmaf(0, 0, acc), also for acc = -0
+      }
+    }
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  return bias ? __fadd_rn(acc, bias[e]) : acc;
+}
+
+// persistent over the uncertified tokens listed by gate_tc_kernel
+__global__ void __launch_bounds__(kTcSelWarps * 32) gate_tc_fallback_kernel(
+    const __nv_bfloat16* __restrict__ x, int d, const float* __restrict__ wg,
+    const float* __restrict__ bias, int E, int Ep, int k, const int32_t* __restrict__ fb_list,
+    const int32_t* __restrict__ fb_count, const float* __restrict__ logits,
+    const float* __restrict__ gcoef, int force_exact, int32_t* __restrict__ topk_idx,
+    float* __restrict__ topk_w, int32_t* __restrict__ counts,
+    unsigned long long* __restrict__ stats) {
+  constexpr int SQ = 4;  // experts per lane (E <= 128)
+  extern __shared__ __align__(16) uint8_t sel_smem[];
+  __shared__ int hist[128];
+  const int64_t n_fb = *fb_count;
+  if (int64_t(blockIdx.x) * kTcSelWarps >= n_fb) return;
+  for (int i = threadIdx.x; i < E; i += blockDim.x) hist[i] = 0;
+  __syncthreads();
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  __nv_bfloat16* xs = reinterpret_cast<__nv_bfloat16*>(sel_smem) + size_t(warp) * d;
+  const int64_t stride = int64_t(gridDim.x) * kTcSelWarps;
+  unsigned long long n_cand = 0, n_full = 0, n_tok = 0;
+  for (int64_t it = int64_t(blockIdx.x) * kTcSelWarps + warp; it < n_fb; it += stride) {
+    const int64_t tok = fb_list[it];
+    const __nv_bfloat16* xr = x + tok * d;
+    float ss = 0.0f;
+    constexpr int G = 8;  // 16-byte slices in flight per lane
+    __syncwarp();
+    for (int cb = 0; cb * 256 < d; cb += G) {
+      uint4 raw[G];
+#pragma unroll
+      for (int j = 0; j < G; ++j) {
+        const int c = (cb + j) * 256 + lane * 8;
+        if (c < d) raw[j] = __ldg(reinterpret_cast<const uint4*>(xr + c));
+      }
+#pragma unroll
+      for (int j = 0; j < G; ++j) {
+        const int c = (cb + j) * 256 + lane * 8;
+        if (c < d) {
+          *reinterpret_cast<uint4*>(xs + c) = raw[j];
+          const uint32_t wds[4] = {raw[j].x, raw[j].y, raw[j].z, raw[j].w};
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const float p = __uint_as_float(wds[i] << 16),
+                        q = __uint_as_float(wds[i] & 0xffff0000u);
+            ss = fmaf(p, p, ss);
+            ss = fmaf(q, q, ss);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
+    __syncwarp();
+    const float nx = __fmul_ru(__fsqrt_ru(ss), 1.001f);
+    float lo_b[SQ], hi_b[SQ];
+    bool live[SQ];
+    bool bad = !(nx <= 3.0e38f);
+#pragma unroll
+    for (int q = 0; q < SQ; ++q) {
+      const int e = lane + 32 * q;
+      live[q] = e < E;
+      lo_b[q] = hi_b[q] = 0.0f;
+      if (live[q]) {
+        float v = logits[tok * Ep + e];
+        if (bias) v = __fadd_rn(v, bias[e]);
+        const float B = tc_bound(nx, gcoef[e], v);
+        lo_b[q] = __fsub_rd(v, B);
+        hi_b[q] = __fadd_ru(v, B);
+        if (!(fabsf(v) <= 3.0e38f) || !(B <= 3.0e38f)) bad = true;
+      }
+    }
+    bad = __any_sync(0xffffffffu, bad);
+    // v_k: the k-th largest lower bound
+    float vk = 0.0f;
+    {
+      bool used[SQ] = {false, false, false, false};
+      for (int j = 0; j < k; ++j) {
+        float best = -INFINITY;
+        int bi = -1;
+#pragma unroll
+        for (int q = 0; q < SQ; ++q)
+          if (live[q] && !used[q] && (bi < 0 || lo_b[q] > best)) { best = lo_b[q]; bi = lane + 32 * q; }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+          const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+          if (oi >= 0 && (bi < 0 || ob > best || (ob == best && oi < bi))) { best = ob; bi = oi; }
+        }
+#pragma unroll
+        for (int q = 0; q < SQ; ++q)
+          if (lane + 32 * q == bi) used[q] = true;
+        vk = best;
+      }
+    }
+    bool cand[SQ];
+    int nc = 0;
+#pragma unroll
+    for (int q = 0; q < SQ; ++q) {
+      cand[q] = live[q] && hi_b[q] >= vk;
+      nc += __popc(__ballot_sync(0xffffffffu, cand[q]));
+    }
+    const bool full = bad || force_exact || nc > kTcCandMax;
+    if (full) {
+#pragma unroll
+      for (int q = 0; q < SQ; ++q) cand[q] = live[q];
+    }
+    float ex[SQ];
+#pragma unroll
+    for (int q = 0; q < SQ; ++q) {
+      ex[q] = 0.0f;
+      unsigned m = __ballot_sync(0xffffffffu, cand[q]);
+      while (m) {
+        const int b = __ffs(m) - 1;
+        m &= m - 1;
+        const int e = b + 32 * q;
+        const float L = exact_logit(xs, wg + size_t(e) * d, d, lane, bias, e);
+        if (lane == b) ex[q] = L;
+      }
+    }
+    // top-k over the exact candidate logits (ties and NaN -> lower index)
+    float mx = -INFINITY;
+#pragma unroll
+    for (int q = 0; q < SQ; ++q)
+      if (cand[q] && !isnan(ex[q])) mx = fmaxf(mx, ex[q]);
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    float psum = 0.0f, pk_mine = 0.0f;
+    int ik_mine = 0;
+    for (int j = 0; j < k; ++j) {
+      Cand best{0.0f, -1};
+#pragma unroll
+      for (int q = 0; q < SQ; ++q) {
+        Cand c{ex[q], cand[q] ? lane + 32 * q : -1};
+        if (better(c, best)) best = c;
+      }
+      for (int o = 16; o; o >>= 1) {
+        Cand other{__shfl_xor_sync(0xffffffffu, best.v, o),
+                   __shfl_xor_sync(0xffffffffu, best.i, o)};
+        if (better(other, best)) best = other;
+      }
+      const float pj = expf(best.v - mx);
+      psum += pj;
+      if (lane == j) { pk_mine = pj; ik_mine = best.i; }
+#pragma unroll
+      for (int q = 0; q < SQ; ++q)
+        if (lane + 32 * q == best.i) cand[q] = false;
+    }
+    if (lane < k) {
+      topk_idx[tok * k + lane] = ik_mine;
+      topk_w[tok * k + lane] = pk_mine / psum;
+      atomicAdd(&hist[ik_mine], 1);
+    }
+    n_cand += full ? unsigned(E) : unsigned(nc);
+    n_full += full ? 1u : 0u;
+    n_tok += 1;
+  }
+  if (stats && lane == 0 && n_tok) {
+    atomicAdd(&stats[1], n_tok);
+    atomicAdd(&stats[2], n_cand);
+    if (n_full) atomicAdd(&stats[3], n_full);
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += blockDim.x)
+    if (hist[e]) atomicAdd(&counts[e], hist[e]);
+}
+
+struct TcGateWs {
+  size_t w3, sums, gcoef, stats, fb_count, fb_list, fb_logits, total;
+};
+TcGateWs tc_gate_layout(int64_t N, int d, int Ep) {
+  auto up = [](size_t v) { return (v + 1023) & ~size_t(1023); };
+  const size_t n = size_t(std::max<int64_t>(N, 1));
+  TcGateWs L;
+  L.w3 = 0;
+  L.sums = up(size_t(kTcParts) * Ep * d * 2);
+  L.gcoef = up(L.sums + size_t(Ep) * 32);
+  L.stats = up(L.gcoef + size_t(Ep) * 4);
+  L.fb_count = L.stats + 32;
+  L.fb_list = up(L.fb_count + 4);
+  L.fb_logits = up(L.fb_list + n * 4);
+  L.total = up(L.fb_logits + n * Ep * 4);
+  return L;
+}
+
+int tc_gate_env(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v ? std::atoi(v) : dflt;
+}
+
+bool tc_gate_applies(int dtype, int64_t N, int d, int E, int k) {
+  return dtype == kDtypeBf16 && k >= 2 && k <= kTcKMax && E <= 128 && d % 64 == 0 && d > 0 &&
+         d <= kTcMaxD && N > 0 && tc_gate_env("INFMOE_GATE_TC", 1) != 0;
+}
+
+struct TcSeg {
+  int n_seg, seg_kb;
+};
+TcSeg tc_segments(int d, int Ep) {
+  const int kblocks = d / 64;
+  const int max_seg = kTcTmemCols / Ep - 1;  // the last accumulator takes mid + lo
+  TcSeg s;
+  s.seg_kb = (kblocks + max_seg - 1) / max_seg;
+  s.n_seg = (kblocks + s.seg_kb - 1) / s.seg_kb;
+  return s;
+}
+
+// step 0 into ws: the bf16 parts of W_g and the per-expert bound coefficients
+void tc_gate_prepare(const float* wg, int E, int d, uint8_t* ws, cudaStream_t s) {
+  const int Ep = (E + 31) / 32 * 32;
+  const TcGateWs L = tc_gate_layout(1, d, Ep);
+  auto* sums = reinterpret_cast<double*>(ws + L.sums);
+  INFMOE_CUDA(cudaMemsetAsync(sums, 0, size_t(Ep) * 32, s));
+  gate_split_kernel<<<dim3(unsigned(Ep), kTcSplitSeg), 256, 0, s>>>(
+      wg, E, Ep, d, reinterpret_cast<__nv_bfloat16*>(ws + L.w3), sums);
+  INFMOE_LAUNCH_CHECK();
+  const TcSeg sg = tc_segments(d, Ep);
+  const int m_hi = 4 * sg.seg_kb;                      // tcgen05.mma per hi accumulator
+  const int m_ml = 4 * (kTcParts - 1) * (d / 64);      // ... into the mid/lo accumulator
+  const int dpad = (d + 255) / 256 * 256;
+  const double gamma_hi = std::ldexp(17.0 * (m_hi + 1), -23);
+  const double gamma_ml = std::ldexp(17.0 * (m_ml + 1), -23);
+  const double gamma_w = std::ldexp(double(sg.n_seg + 1), -24) + std::ldexp(dpad / 32.0 + 8.0, -23);
+  gate_coef_kernel<<<1, 128, 0, s>>>(sums, Ep, gamma_hi, gamma_ml, gamma_w,
+                                     reinterpret_cast<float*>(ws + L.gcoef));
+  INFMOE_LAUNCH_CHECK();
+}
+
+void tc_gate_go(const void* x, int64_t N, int d, const float* wg, const float* bias, int E, int k,
+                int32_t* idx, float* w, int32_t* counts, uint8_t* ws, float* approx_out,
+                unsigned long long* stats_out, cudaStream_t s) {
+  const int Ep = (E + 31) / 32 * 32;
+  const TcGateWs L = tc_gate_layout(N, d, Ep);
+  const int force = tc_gate_env("INFMOE_GATE_TC_FORCE_EXACT", 0);
+  auto* stats = reinterpret_cast<unsigned long long*>(ws + L.stats);
+  auto* fb_count = reinterpret_cast<int32_t*>(ws + L.fb_count);
+  auto* fb_list = reinterpret_cast<int32_t*>(ws + L.fb_list);
+  auto* fb_logits = reinterpret_cast<float*>(ws + L.fb_logits);
+  INFMOE_CUDA(cudaMemsetAsync(stats, 0, 32 + 4, s));  // stats[4] + fb_count
+
+  const uint32_t stage_bytes = uint32_t(gemm::BM + kTcParts * Ep) * gemm::ROW_BYTES;
+  const int stages = std::min<int>(kTcMaxStages, int((200u * 1024u) / stage_bytes));
+  const size_t smem = size_t(stages) * stage_bytes + 1024 + 8 * (2 * kTcMaxStages + 2);
+  const void* kern = nullptr;
+  switch (k) {
+    case 2: kern = reinterpret_cast<const void*>(gate_tc_kernel<2>); break;
+    case 3: kern = reinterpret_cast<const void*>(gate_tc_kernel<3>); break;
+    case 4: kern = reinterpret_cast<const void*>(gate_tc_kernel<4>); break;
+    case 5: kern = reinterpret_cast<const void*>(gate_tc_kernel<5>); break;
+    case 6: kern = reinterpret_cast<const void*>(gate_tc_kernel<6>); break;
+    case 7: kern = reinterpret_cast<const void*>(gate_tc_kernel<7>); break;
+    default: kern = reinterpret_cast<const void*>(gate_tc_kernel<8>); break;
+  }
+  ensure_dyn_smem(kern, smem);
+  const CUtensorMap tx = gemm::make_tmap(x, uint64_t(N), uint64_t(d), false, kTcTok);
+  const CUtensorMap tw =
+      gemm::make_tmap(ws + L.w3, uint64_t(kTcParts * Ep), uint64_t(d), false, uint32_t(Ep));
+  const TcSeg sg = tc_segments(d, Ep);
+  TcGateArgs a;
+  a.N = N; a.d = d; a.Ep = Ep; a.E = E; a.k = k; a.stages = stages;
+  a.seg_kb = sg.seg_kb; a.n_seg = sg.n_seg; a.force_exact = force;
+  a.gcoef = reinterpret_cast<const float*>(ws + L.gcoef);
+  a.bias = bias; a.topk_idx = idx; a.topk_w = w; a.counts = counts;
+  a.fb_list = fb_list; a.fb_count = fb_count; a.fb_logits = fb_logits;
+  a.approx = nullptr; a.stats = stats;
+  const int64_t tiles = (N + kTcTok - 1) / kTcTok;
+  const int grid = int(std::min<int64_t>(tiles, device_sm_count()));
+  void* kargs[] = {const_cast<CUtensorMap*>(&tx), const_cast<CUtensorMap*>(&tw), &a};
+  INFMOE_CUDA(cudaLaunchKernel(kern, dim3(unsigned(grid)), dim3(kTcThreads), kargs, smem, s));
+  INFMOE_LAUNCH_CHECK();
+
+  const size_t sel_smem = size_t(kTcSelWarps) * d * 2;
+  ensure_dyn_smem(reinterpret_cast<const void*>(gate_tc_fallback_kernel), sel_smem);
+  int per_sm = 0;
+  INFMOE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      &per_sm, gate_tc_fallback_kernel, kTcSelWarps * 32, sel_smem));
+  const int64_t fb_grid = std::min<int64_t>((N + kTcSelWarps - 1) / kTcSelWarps,
+                                            int64_t(std::max(per_sm, 1)) * device_sm_count());
+  gate_tc_fallback_kernel<<<unsigned(fb_grid), kTcSelWarps * 32, sel_smem, s>>>(
+      reinterpret_cast<const __nv_bfloat16*>(x), d, wg, bias, E, Ep, k, fb_list, fb_count,
+      fb_logits, a.gcoef, force, idx, w, counts, stats);
+  INFMOE_LAUNCH_CHECK();
+  if (approx_out)  // every token's L~ is in fb_logits (Ep-strided)
+    INFMOE_CUDA(cudaMemcpy2DAsync(approx_out, size_t(E) * 4, fb_logits, size_t(Ep) * 4,
+                                  size_t(E) * 4, size_t(N), cudaMemcpyDeviceToDevice, s));
+  if (stats_out)
+    INFMOE_CUDA(cudaMemcpyAsync(stats_out, stats, 32, cudaMemcpyDeviceToDevice, s));
+}
+
 template <typename T, int EB>
 void softmax_go(const void* x, int64_t N, int d, const float* wg, const float* bias, int E, int k,
                 int32_t* idx, float* w, int32_t* counts, cudaStream_t s) {
@@ -755,9 +1455,20 @@ void softmax_launch(const void* x, int64_t N, int d, const float* wg, const floa
 
 }  // namespace
 
+size_t gate_softmax_ws_bytes(int dtype, int64_t N, int d, int E, int k) {
+  if (!tc_gate_applies(dtype, std::max<int64_t>(N, 1), d, E, k)) return 0;
+  return tc_gate_layout(N, d, (E + 31) / 32 * 32).total;
+}
+
+void gate_softmax_prepare(const float* wg, int d, int E, void* ws, cudaStream_t stream) {
+  require(ws != nullptr && wg != nullptr, "softmax gate prepare: NULL pointer");
+  tc_gate_prepare(wg, E, d, static_cast<uint8_t*>(ws), stream);
+}
+
 void launch_gate_softmax(const void* x, int dtype, int64_t N, int d, const float* wg,
                          const float* bias, int E, int k, int32_t* topk_idx, float* topk_w,
-                         int32_t* counts, cudaStream_t stream) {
+                         int32_t* counts, cudaStream_t stream, void* ws, size_t ws_bytes,
+                         bool ws_prepared, float* approx_logits, unsigned long long* tc_stats) {
   require(E >= 1 && E <= 128, "softmax gate: n_experts must be in [1, 128]");
   require(k >= 1 && k <= 8 && k <= E, "softmax gate: top_k must be in [1, min(8, E)]");
   require(d >= 1, "softmax gate: d_model must be >= 1");
@@ -766,6 +1477,19 @@ void launch_gate_softmax(const void* x, int dtype, int64_t N, int d, const float
           "softmax gate: x and gate weights must be 16-byte aligned");
   INFMOE_CUDA(cudaMemsetAsync(counts, 0, sizeof(int32_t) * size_t(E), stream));
   if (N == 0) return;
+  const size_t need = gate_softmax_ws_bytes(dtype, N, d, E, k);
+  if (need) {  // tensor-core logits + certified exact selection
+    require(reinterpret_cast<uintptr_t>(x) % 16 == 0, "softmax gate: x must be 16-byte aligned");
+    uint8_t* w = static_cast<uint8_t*>(ws);
+    const bool own = w == nullptr || ws_bytes < need;
+    if (own) INFMOE_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&w), need, stream));
+    if (own || !ws_prepared) tc_gate_prepare(wg, E, d, w, stream);
+    tc_gate_go(x, N, d, wg, bias, E, k, topk_idx, topk_w, counts, w, approx_logits, tc_stats,
+               stream);
+    if (own) INFMOE_CUDA(cudaFreeAsync(w, stream));
+    return;
+  }
+  if (tc_stats) INFMOE_CUDA(cudaMemsetAsync(tc_stats, 0xff, 32, stream));  // not on this path
   if (dtype == kDtypeBf16)
     softmax_launch<__nv_bfloat16>(x, N, d, wg, bias, E, k, topk_idx, topk_w, counts, stream);
   else

@@ -17,9 +17,24 @@ void launch_set_flag(int32_t* flag, cudaStream_t s);
 // N1a: logits by a sequential fmaf chain per (token, expert), top-k by strict
 // argmax (ties -> lower index), softmax weights.  counts must be zeroed by the
 // launcher (it is: the launcher issues the memset).
+// For bf16 x and top_k >= 2 (E <= 128, d % 64 == 0) the logits come from
+// tcgen05 and only the candidates the error bound cannot exclude are re-run
+// through the exact chain (gate.cu, "N1a on tensor cores"): same indices and
+// counts.  It needs gate_softmax_ws_bytes() of device workspace (0 = the
+// CUDA-core path); a NULL or short ws is allocated stream-ordered.  A caller
+// with fixed gate weights runs gate_softmax_prepare(wg) into ws once and
+// passes ws_prepared = true (the bf16 split of W_g lives in ws).
+// approx_logits [N, E] / tc_stats {certified tokens, fallback tokens, exact
+// chains, full-exact tokens} (device, optional) are test hooks; tc_stats is
+// set to all-ones on the CUDA-core path.
+size_t gate_softmax_ws_bytes(int dtype, int64_t N, int d, int E, int k);
+void gate_softmax_prepare(const float* wg, int d, int E, void* ws, cudaStream_t stream);
 void launch_gate_softmax(const void* x, int dtype, int64_t N, int d, const float* wg,
                          const float* bias, int E, int k, int32_t* topk_idx, float* topk_w,
-                         int32_t* counts, cudaStream_t stream);
+                         int32_t* counts, cudaStream_t stream, void* ws = nullptr,
+                         size_t ws_bytes = 0, bool ws_prepared = false,
+                         float* approx_logits = nullptr,
+                         unsigned long long* tc_stats = nullptr);
 // N1b: LSH sign-bit code over the fp64 promotion of x (gating.hpp:61-104).
 void launch_gate_lsh(const void* x, int dtype, int64_t N, int d, const double* proj, int bits,
                      int E, uint32_t* codes, int32_t* topk_idx, float* topk_w, int32_t* counts,

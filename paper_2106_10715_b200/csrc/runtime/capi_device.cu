@@ -56,6 +56,18 @@ int infmoe_gate_softmax_topk(const void* x, int32_t dtype, int64_t N, int32_t d,
   });
 }
 
+int infmoe_gate_softmax_debug(const void* x, int32_t dtype, int64_t N, int32_t d,
+                              const float* wg, const float* bias, int32_t E, int32_t k,
+                              int32_t* topk_idx, float* topk_w, int32_t* counts,
+                              float* approx_logits, uint64_t* stats, void* stream) {
+  return guarded([&] {
+    require(x && wg && topk_idx && topk_w && counts, "gate: NULL pointer");
+    launch_gate_softmax(x, dtype, N, d, wg, bias, E, k, topk_idx, topk_w, counts,
+                        as_stream(stream), nullptr, 0, false, approx_logits,
+                        reinterpret_cast<unsigned long long*>(stats));
+  });
+}
+
 int infmoe_gate_lsh(const void* x, int32_t dtype, int64_t N, int32_t d, const double* proj,
                     int32_t bits, int32_t E, uint32_t* codes, int32_t* topk_idx, float* topk_w,
                     int32_t* counts, void* stream) {

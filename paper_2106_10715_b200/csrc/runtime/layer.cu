@@ -94,6 +94,10 @@ Layer::Layer(const infmoe_layer_desc& d) : desc(d) {
   perm = dalloc<int32_t>(size_t(A), owned);
   inv = dalloc<int32_t>(size_t(A), owned);
   dws = dalloc<uint8_t>(dispatch_workspace_bytes(A, d.n_experts), owned);
+  if (d.gate_kind != INFMOE_GATE_LSH) {  // the tensor-core softmax gate's workspace (or 0)
+    gws_bytes = gate_softmax_ws_bytes(d.dtype, d.max_tokens, d.d_model, d.n_experts, d.top_k);
+    if (gws_bytes) gws = dalloc<uint8_t>(gws_bytes, owned);
+  }
   done_ctr = dalloc<int32_t>(size_t(d.n_experts) + 1, owned);  // + the tile-claim counter
   xp = dalloc<uint8_t>(size_t(A) * d.d_model * esz, owned);
   yp = dalloc<uint8_t>(size_t(A) * d.d_model * esz, owned);
@@ -132,6 +136,10 @@ Layer::Layer(const infmoe_layer_desc& d) : desc(d) {
     const size_t n = size_t(d.n_experts) * d.d_model;
     gate_w = dalloc<float>(n, owned);
     INFMOE_CUDA(cudaMemcpy(gate_w, d.gate_weight, n * sizeof(float), cudaMemcpyHostToDevice));
+    if (gws) {  // the tensor-core gate's bf16 split of W_g, once
+      gate_softmax_prepare(gate_w, d.d_model, d.n_experts, gws, nullptr);
+      INFMOE_CUDA(cudaDeviceSynchronize());
+    }
     if (d.gate_bias) {
       gate_b = dalloc<float>(size_t(d.n_experts), owned);
       INFMOE_CUDA(cudaMemcpy(gate_b, d.gate_bias, sizeof(float) * d.n_experts,
@@ -180,6 +188,7 @@ Layer::Layer(const infmoe_layer_desc& d) : desc(d) {
     require(d.prefetch_depth >= 0, "layer: prefetch_depth must be >= 0");
     INFMOE_CUDA(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
     INFMOE_CUDA(cudaEventCreateWithFlags(&last_load, cudaEventDisableTiming));
+    INFMOE_CUDA(cudaEventCreateWithFlags(&in_half, cudaEventDisableTiming));
     const size_t E = size_t(n_local);
     for (auto* v : {&load_done, &compute_done}) {
       v->resize(E);
@@ -335,6 +344,7 @@ Layer::~Layer() {
     for (cudaEvent_t e : *v) cudaEventDestroy(e);
   if (t_start) cudaEventDestroy(t_start);
   if (last_load) cudaEventDestroy(last_load);
+  if (in_half) cudaEventDestroy(in_half);
   if (t_pin0) cudaEventDestroy(t_pin0);
   if (t_pin1) cudaEventDestroy(t_pin1);
   if (pin_in) cudaFree(pin_in);
@@ -365,7 +375,7 @@ void Layer::route(const void* x, int64_t N, cudaStream_t s, const int32_t* given
                     counts, s);
   } else {
     launch_gate_softmax(x, desc.dtype, N, desc.d_model, gate_w, gate_b, E, k, idx, wts, counts,
-                        s);
+                        s, gws, gws_bytes, /*ws_prepared=*/true);
   }
   launch_dispatch(idx, N * k, E, offsets, perm, inv, dws, s);
   if (given_idx) launch_counts_from_offsets(offsets, E, counts, s);
@@ -537,14 +547,27 @@ void Layer::compute_offloaded(const Rows& r, bool timed, infmoe_forward_out* out
   for (int j = 0; j < E; ++j) {
     const int e = members[size_t(pl.order[size_t(j)])];
     const int slot = slot_of(j);
+    const bool split_last = pack && j == E - 1 && j >= pf_reused && r.counts[e] > 0;
+    bool w_in_decoded = false;
     if (j < pf_reused) {  // streamed in by the previous layer: no copy
       INFMOE_CUDA(cudaStreamWaitEvent(s, load_done[size_t(j)], 0));
     } else {
     if (j >= n_rot)
       INFMOE_CUDA(cudaStreamWaitEvent(copy_stream, compute_done[size_t(j - n_rot)], 0));
     if (timed) INFMOE_CUDA(cudaEventRecord(t_load0[size_t(j)], copy_stream));
-    if (pack) {  // packed codec: one copy of the expert's pack pair into its staging buffer
-      // (one 108 MB copy ran at 55.00 GB/s, two half copies at 54.82)
+    if (pack && split_last) {
+      // the layer's LAST expert: its W_in pack is copied first and decoded
+      // while the W_out pack is still on the link, so only one decode stays in
+      // the layer's tail (elsewhere one copy per expert: one 108 MB copy ran at
+      // 55.00 GB/s, two half copies at 54.82)
+      const uint64_t a = pack->in_size[size_t(e)];
+      INFMOE_CUDA(cudaMemcpyAsync(stage_of(slot), pack->host + pack->off[size_t(e)], a,
+                                  cudaMemcpyHostToDevice, copy_stream));
+      INFMOE_CUDA(cudaEventRecord(in_half, copy_stream));
+      INFMOE_CUDA(cudaMemcpyAsync(stage_of(slot) + a, pack->host + pack->off[size_t(e)] + a,
+                                  pack->size[size_t(e)] - a, cudaMemcpyHostToDevice,
+                                  copy_stream));
+    } else if (pack) {  // packed codec: one copy of the expert's pack pair into its staging buffer
       INFMOE_CUDA(cudaMemcpyAsync(stage_of(slot), pack->host + pack->off[size_t(e)],
                                   pack->size[size_t(e)], cudaMemcpyHostToDevice, copy_stream));
     } else {
@@ -565,6 +588,15 @@ void Layer::compute_offloaded(const Rows& r, bool timed, infmoe_forward_out* out
     if (timed) INFMOE_CUDA(cudaEventRecord(t_load1[size_t(j)], copy_stream));
     INFMOE_CUDA(cudaEventRecord(load_done[size_t(j)], copy_stream));
 
+    if (pack && split_last) {  // W_in decode overlaps the W_out copy (part of the load)
+      INFMOE_CUDA(cudaStreamWaitEvent(s, in_half, 0));
+      auto* w1 = reinterpret_cast<uint16_t*>(slot_in + size_t(slot) * expert_in_bytes);
+      if (pack->codec_id == INFMOE_CODEC_EXPH)
+        codec::launch_exph_unpack(stage_of(slot), pack->lay_in[size_t(e)], w1, s);
+      else
+        codec::launch_exp4_unpack(stage_of(slot), uint64_t(desc.d_ff) * desc.d_model, w1, s);
+      w_in_decoded = true;
+    }
     INFMOE_CUDA(cudaStreamWaitEvent(s, load_done[size_t(j)], 0));
     }
     const int32_t ex = e, sl = slot;
@@ -580,10 +612,10 @@ void Layer::compute_offloaded(const Rows& r, bool timed, infmoe_forward_out* out
         const uint8_t* p1 = stage_of(slot);
         const uint8_t* p2 = p1 + pack->in_size[size_t(e)];
         if (pack->codec_id == INFMOE_CODEC_EXPH) {
-          codec::launch_exph_unpack(p1, pack->lay_in[size_t(e)], w1, s);
+          if (!w_in_decoded) codec::launch_exph_unpack(p1, pack->lay_in[size_t(e)], w1, s);
           codec::launch_exph_unpack(p2, pack->lay_out[size_t(e)], w2, s);
         } else {
-          codec::launch_exp4_unpack(p1, elems, w1, s);
+          if (!w_in_decoded) codec::launch_exp4_unpack(p1, elems, w1, s);
           codec::launch_exp4_unpack(p2, elems, w2, s);
         }
         e0 = nullptr;

@@ -110,6 +110,8 @@ struct Layer {
   int32_t* perm = nullptr;
   int32_t* inv = nullptr;
   uint8_t* dws = nullptr;
+  uint8_t* gws = nullptr;  // softmax gate workspace (tensor-core path), gws_bytes
+  size_t gws_bytes = 0;
   uint8_t* xp = nullptr;
   uint8_t* hbuf = nullptr;
   uint8_t* yp = nullptr;
@@ -135,6 +137,7 @@ struct Layer {
   std::vector<Prefetched> pf;
   int pf_reused = 0;
   cudaEvent_t last_load = nullptr;
+  cudaEvent_t in_half = nullptr;  // the last expert's W_in pack has landed
   void prefetch(cudaEvent_t after_loads, cudaEvent_t after_computes);
   std::vector<int> predicted_order(std::vector<int>* members) const;
   uint8_t* slot_in = nullptr;

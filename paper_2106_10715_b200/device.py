@@ -69,7 +69,10 @@ def set_flag(flag, stream=None) -> None:
     _check(_lib.infmoe_debug_set_flag(_p(flag), s))
 
 
-def gate_softmax_topk(x, wg, k: int, bias=None):
+def gate_softmax_topk(x, wg, k: int, bias=None, debug: bool = False):
+    """N1a gate.  debug=True also returns the tensor-core path's approximate
+    logits [N, E] and its counters {certified, fallback, candidates, full_exact}
+    (None on the CUDA-core path)."""
     torch = _torch()
     _need_cuda(x, wg, bias)
     N, d = x.shape
@@ -77,9 +80,20 @@ def gate_softmax_topk(x, wg, k: int, bias=None):
     idx = torch.empty((N, k), dtype=torch.int32, device=x.device)
     w = torch.empty((N, k), dtype=torch.float32, device=x.device)
     counts = torch.empty(E, dtype=torch.int32, device=x.device)
-    _check(_lib.infmoe_gate_softmax_topk(_p(x), _dtype_code(x), N, d, _p(wg), _p(bias), E, k,
-                                         _p(idx), _p(w), _p(counts), _stream_ptr()))
-    return idx, w, counts
+    if not debug:
+        _check(_lib.infmoe_gate_softmax_topk(_p(x), _dtype_code(x), N, d, _p(wg), _p(bias), E,
+                                             k, _p(idx), _p(w), _p(counts), _stream_ptr()))
+        return idx, w, counts
+    approx = torch.empty((N, E), dtype=torch.float32, device=x.device)
+    stats = torch.zeros(4, dtype=torch.int64, device=x.device)
+    _check(_lib.infmoe_gate_softmax_debug(_p(x), _dtype_code(x), N, d, _p(wg), _p(bias), E, k,
+                                          _p(idx), _p(w), _p(counts), _p(approx), _p(stats),
+                                          _stream_ptr()))
+    st = stats.cpu().tolist()
+    if st[0] == -1:
+        return idx, w, counts, None, None
+    return idx, w, counts, approx, {"certified": st[0], "fallback": st[1],
+                                    "candidates": st[2], "full_exact": st[3]}
 
 
 def gate_lsh(x, proj, n_experts: int):
