@@ -491,7 +491,9 @@ def measure_c5(torch, im, dv, dev, local, stream, peaks, h2d_peak, reps: int = 3
         return float(np.median(ts))
 
     wg_dev, b_dev = torch.from_numpy(gw).to(dev), torch.from_numpy(bias).to(dev)
-    t_gate = timed(lambda: dv.gate_softmax_topk(x, wg_dev, k, bias=b_dev))
+    gws = dv.GateWorkspace(wg_dev, N, k)  # as a layer holds it: W_g split once
+    t_gate = timed(lambda: dv.gate_softmax_topk(x, wg_dev, k, bias=b_dev, workspace=gws))
+    gstats = dv.gate_softmax_topk(x, wg_dev, k, bias=b_dev, debug=True)[4]
     t_disp = timed(lambda: dv.dispatch(idx, E))
     t_gath = timed(lambda: dv.gather_rows_by_token(x, inv, k))  # the layer's k > 1 path
     t_comb = timed(lambda: dv.combine(xp, inv, w, N, k))
@@ -505,7 +507,12 @@ def measure_c5(torch, im, dv, dev, local, stream, peaks, h2d_peak, reps: int = 3
           "ncu": "profiles/r02_dm_ncu_summary.txt (cold-cache, serialised launches)",
           "gate_softmax_topk": {"us": t_gate * 1e6, "gbs": gate_b / t_gate / 1e9,
                                 "frac": gate_b / t_gate / 1e9 / hbm,
-                                "bytes": gate_b},
+                                "bytes": gate_b,
+                                "path": "tcgen05 logits (W_g = hi + mid + lo bf16) + certified "
+                                        "top-k, exact fmaf chains for the uncertified tokens",
+                                "certified_tokens": gstats["certified"] if gstats else None,
+                                "fallback_tokens": gstats["fallback"] if gstats else None,
+                                "exact_chains": gstats["candidates"] if gstats else None},
           "dispatch_counting_sort": {"us": t_disp * 1e6, "assignments": N * k},
           "gather_rows": {"us": t_gath * 1e6, "gbs": gath_b / t_gath / 1e9,
                           "frac": gath_b / t_gath / 1e9 / hbm, "bytes": gath_b,

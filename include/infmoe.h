@@ -235,6 +235,19 @@ int infmoe_debug_set_flag(int32_t* flag, void* stream);
 int infmoe_gate_softmax_topk(const void* x, int32_t dtype, int64_t N, int32_t d,
                              const float* wg, const float* bias, int32_t E, int32_t k,
                              int32_t* topk_idx, float* topk_w, int32_t* counts, void* stream);
+/* The same gate with caller-owned workspace, for fixed gate weights: the
+ * tensor-core path (bf16 x, 2 <= k <= 8, E <= 128, d % 64 == 0) keeps W_g's
+ * bf16 split there.  ws_bytes() is 0 when the call takes the CUDA-core path
+ * (ws may then be NULL); prepare(wg) fills ws once (stream-ordered), after
+ * which topk_ws() runs without re-splitting W_g.  Results equal
+ * infmoe_gate_softmax_topk's. */
+size_t infmoe_gate_softmax_ws_bytes(int32_t dtype, int64_t N, int32_t d, int32_t E, int32_t k);
+int infmoe_gate_softmax_prepare(const float* wg, int32_t d, int32_t E, void* ws,
+                                size_t ws_bytes, void* stream);
+int infmoe_gate_softmax_topk_ws(const void* x, int32_t dtype, int64_t N, int32_t d,
+                                const float* wg, const float* bias, int32_t E, int32_t k,
+                                int32_t* topk_idx, float* topk_w, int32_t* counts, void* ws,
+                                size_t ws_bytes, void* stream);
 /* Test hook of the same gate: also returns the tensor-core path's approximate
  * logits (approx_logits[N,E] f32 device, may be NULL) and its counters
  * (stats[4] u64 device: tokens certified from the tensor-core logits, tokens

@@ -182,6 +182,11 @@ _lib.infmoe_debug_occupy_sms.argtypes = [_i32, _i32, _vp, _u64, _vp, _vp]
 _lib.infmoe_debug_set_flag.argtypes = [_vp, _vp]
 _lib.infmoe_gate_softmax_topk.argtypes = [_vp, _i32, C.c_int64, _i32, _vp, _vp, _i32, _i32,
                                           _vp, _vp, _vp, _vp]
+_lib.infmoe_gate_softmax_ws_bytes.argtypes = [_i32, C.c_int64, _i32, _i32, _i32]
+_lib.infmoe_gate_softmax_ws_bytes.restype = C.c_size_t
+_lib.infmoe_gate_softmax_prepare.argtypes = [_vp, _i32, _i32, _vp, C.c_size_t, _vp]
+_lib.infmoe_gate_softmax_topk_ws.argtypes = [_vp, _i32, C.c_int64, _i32, _vp, _vp, _i32, _i32,
+                                             _vp, _vp, _vp, _vp, C.c_size_t, _vp]
 _lib.infmoe_gate_softmax_debug.argtypes = [_vp, _i32, C.c_int64, _i32, _vp, _vp, _i32, _i32,
                                            _vp, _vp, _vp, _vp, _vp, _vp]
 _lib.infmoe_gate_lsh.argtypes = [_vp, _i32, C.c_int64, _i32, _vp, _i32, _i32, _vp, _vp, _vp,

@@ -56,6 +56,35 @@ int infmoe_gate_softmax_topk(const void* x, int32_t dtype, int64_t N, int32_t d,
   });
 }
 
+size_t infmoe_gate_softmax_ws_bytes(int32_t dtype, int64_t N, int32_t d, int32_t E, int32_t k) {
+  size_t r = 0;
+  guarded([&] { r = gate_softmax_ws_bytes(dtype, N, d, E, k); });
+  return r;
+}
+
+int infmoe_gate_softmax_prepare(const float* wg, int32_t d, int32_t E, void* ws,
+                                size_t ws_bytes, void* stream) {
+  return guarded([&] {
+    require(wg && ws, "gate prepare: NULL pointer");
+    require(ws_bytes >= gate_softmax_ws_bytes(kDtypeBf16, 1, d, E, 2),
+            "gate prepare: workspace too small");
+    gate_softmax_prepare(wg, d, E, ws, as_stream(stream));
+  });
+}
+
+int infmoe_gate_softmax_topk_ws(const void* x, int32_t dtype, int64_t N, int32_t d,
+                                const float* wg, const float* bias, int32_t E, int32_t k,
+                                int32_t* topk_idx, float* topk_w, int32_t* counts, void* ws,
+                                size_t ws_bytes, void* stream) {
+  return guarded([&] {
+    require(x && wg && topk_idx && topk_w && counts, "gate: NULL pointer");
+    const size_t need = gate_softmax_ws_bytes(dtype, N, d, E, k);
+    require(need == 0 || (ws && ws_bytes >= need), "gate: workspace too small");
+    launch_gate_softmax(x, dtype, N, d, wg, bias, E, k, topk_idx, topk_w, counts,
+                        as_stream(stream), ws, ws_bytes, /*ws_prepared=*/true);
+  });
+}
+
 int infmoe_gate_softmax_debug(const void* x, int32_t dtype, int64_t N, int32_t d,
                               const float* wg, const float* bias, int32_t E, int32_t k,
                               int32_t* topk_idx, float* topk_w, int32_t* counts,

@@ -136,9 +136,13 @@ Layer::Layer(const infmoe_layer_desc& d) : desc(d) {
     const size_t n = size_t(d.n_experts) * d.d_model;
     gate_w = dalloc<float>(n, owned);
     INFMOE_CUDA(cudaMemcpy(gate_w, d.gate_weight, n * sizeof(float), cudaMemcpyHostToDevice));
-    if (gws) {  // the tensor-core gate's bf16 split of W_g, once
-      gate_softmax_prepare(gate_w, d.d_model, d.n_experts, gws, nullptr);
-      INFMOE_CUDA(cudaDeviceSynchronize());
+    if (gws) {  // the tensor-core gate's bf16 split of W_g, once, on a private stream (a
+                // device-wide sync could wait behind another EP rank's spinning barrier)
+      cudaStream_t ps;
+      INFMOE_CUDA(cudaStreamCreateWithFlags(&ps, cudaStreamNonBlocking));
+      gate_softmax_prepare(gate_w, d.d_model, d.n_experts, gws, ps);
+      INFMOE_CUDA(cudaStreamSynchronize(ps));
+      INFMOE_CUDA(cudaStreamDestroy(ps));
     }
     if (d.gate_bias) {
       gate_b = dalloc<float>(size_t(d.n_experts), owned);

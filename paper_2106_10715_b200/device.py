@@ -69,7 +69,25 @@ def set_flag(flag, stream=None) -> None:
     _check(_lib.infmoe_debug_set_flag(_p(flag), s))
 
 
-def gate_softmax_topk(x, wg, k: int, bias=None, debug: bool = False):
+class GateWorkspace:
+    """Device workspace of the softmax gate for fixed gate weights wg [E, d]
+    (infmoe_gate_softmax_ws_bytes / _prepare): W_g's bf16 split is made once;
+    None-sized (nbytes == 0) when the calls take the CUDA-core path."""
+
+    def __init__(self, wg, max_tokens: int, k: int, dtype=None):
+        torch = _torch()
+        _need_cuda(wg)
+        E, d = wg.shape
+        code = _dtype_code(torch.empty(0, dtype=dtype or torch.bfloat16))
+        self.nbytes = int(_lib.infmoe_gate_softmax_ws_bytes(code, max_tokens, d, E, k))
+        self.buf = torch.empty(max(self.nbytes, 1), dtype=torch.uint8, device=wg.device)
+        self.wg = wg
+        if self.nbytes:
+            _check(_lib.infmoe_gate_softmax_prepare(_p(wg), d, E, _p(self.buf), self.nbytes,
+                                                    _stream_ptr()))
+
+
+def gate_softmax_topk(x, wg, k: int, bias=None, debug: bool = False, workspace=None):
     """N1a gate.  debug=True also returns the tensor-core path's approximate
     logits [N, E] and its counters {certified, fallback, candidates, full_exact}
     (None on the CUDA-core path)."""
@@ -80,6 +98,12 @@ def gate_softmax_topk(x, wg, k: int, bias=None, debug: bool = False):
     idx = torch.empty((N, k), dtype=torch.int32, device=x.device)
     w = torch.empty((N, k), dtype=torch.float32, device=x.device)
     counts = torch.empty(E, dtype=torch.int32, device=x.device)
+    if workspace is not None and not debug:
+        _check(_lib.infmoe_gate_softmax_topk_ws(_p(x), _dtype_code(x), N, d, _p(wg), _p(bias),
+                                                E, k, _p(idx), _p(w), _p(counts),
+                                                _p(workspace.buf), workspace.nbytes,
+                                                _stream_ptr()))
+        return idx, w, counts
     if not debug:
         _check(_lib.infmoe_gate_softmax_topk(_p(x), _dtype_code(x), N, d, _p(wg), _p(bias), E,
                                              k, _p(idx), _p(w), _p(counts), _stream_ptr()))

@@ -155,28 +155,51 @@ def test_tc_gate_force_exact_and_cuda_core_path_agree(cuda):
     assert np.array_equal(cc[0].cpu().numpy(), tc[0].cpu().numpy())
 
 
+def test_tc_gate_workspace_api(cuda):
+    """infmoe_gate_softmax_ws_bytes / _prepare / _topk_ws: W_g split once, same
+    results as the one-shot call; 0 bytes (CUDA-core path) for top-1."""
+    N, d, E, k = 700, 1024, 48, 2
+    xb, xf, wg, bias = _inputs(31, N, d, E, 0.7)
+    x = torch.from_numpy(xb.view(np.int16).reshape(N, d)).to(cuda).view(torch.bfloat16)
+    g, b = torch.from_numpy(wg).to(cuda), torch.from_numpy(bias).to(cuda)
+    ws = dv.GateWorkspace(g, N, k)
+    assert ws.nbytes > 0
+    ref = _oracle(xf, wg, bias, k)
+    for n in (N, 300):  # fewer tokens than the workspace was sized for
+        got = dv.gate_softmax_topk(x[:n], g, k, b, workspace=ws)
+        r = _oracle(xf[:n], wg, bias, k)
+        _check(got, r)
+    assert dv.GateWorkspace(g, N, 1).nbytes == 0
+    got1 = dv.gate_softmax_topk(x, g, 1, b, workspace=dv.GateWorkspace(g, N, 1))
+    _check(got1, _oracle(xf, wg, bias, 1))
+    del ref
+
+
 def test_tc_gate_faster_than_cuda_core_at_c5(cuda):
     N, d, E, k = 16384, 4096, 64, 2
     xb, _, wg, bias = _inputs(29, N, d, E, 0.6258)
     x = torch.from_numpy(xb.view(np.int16).reshape(N, d)).to(cuda).view(torch.bfloat16)
     g, b = torch.from_numpy(wg).to(cuda), torch.from_numpy(bias).to(cuda)
+    ws = dv.GateWorkspace(g, N, k)
 
-    def timed():
+    def timed(**kw):
         for _ in range(3):
-            dv.gate_softmax_topk(x, g, k, b)
+            dv.gate_softmax_topk(x, g, k, b, **kw)
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
         for _ in range(10):
-            dv.gate_softmax_topk(x, g, k, b)
+            dv.gate_softmax_topk(x, g, k, b, **kw)
         e.record()
         torch.cuda.synchronize()
         return s.elapsed_time(e) / 10
 
+    t_ws = timed(workspace=ws)
     t_tc = timed()
     try:
         os.environ["INFMOE_GATE_TC"] = "0"
         t_cc = timed()
     finally:
         del os.environ["INFMOE_GATE_TC"]
-    print(f"C5 gate: tensor-core {t_tc * 1e3:.1f} us, CUDA-core {t_cc * 1e3:.1f} us")
-    assert t_tc < 0.5 * t_cc
+    print(f"C5 gate: tensor-core {t_ws * 1e3:.1f} us with a prepared workspace, "
+          f"{t_tc * 1e3:.1f} us one-shot, CUDA-core {t_cc * 1e3:.1f} us")
+    assert t_ws < 0.3 * t_cc and t_tc < 0.5 * t_cc
