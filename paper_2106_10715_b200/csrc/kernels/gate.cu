@@ -756,8 +756,8 @@ void lsh_mma_go(const void* x, int64_t N, int d, const double* proj, int bits, i
 //     the exact chain would pick the same experts in the same order: the
 //     token is CERTIFIED and its picks, softmax weights (from L~, renormalised
 //     over the picks) and counts are written right there.
-//  2. gate_tc_fallback_kernel (one warp per uncertified token, listed by
-//     step 1): every expert whose upper bound reaches the k-th largest lower
+//  2. gate_tc_fallback_kernel (one CTA per uncertified token, listed by
+//     step 1; the candidates' chains spread over its warps): every expert whose upper bound reaches the k-th largest lower
 //     bound is a candidate and gets its exact logit by the CUDA-core gate's
 //     fmaf chain and butterfly; top-k over those (ties and NaN -> lower
 //     index).  A token with a non-finite value or more than kTcCandMax
@@ -779,8 +779,8 @@ constexpr int kTcMaxStages = 8;
 constexpr int kTcParts = 3;     // hi, mid, lo
 constexpr int kTcKMax = 8;
 constexpr int kTcCandMax = 24;
-constexpr int kTcSelWarps = 4;  // tokens per fallback CTA
-constexpr int kTcMaxD = 16384;  // the fallback stages d bf16 per warp in shared memory
+constexpr int kTcSelWarps = 4;  // warps per fallback CTA (one token)
+constexpr int kTcMaxD = 16384;  // the fallback stages the d bf16 of a row in shared memory
 constexpr int kTcTmemCols = 512;
 constexpr int kTcSplitSeg = 16; // column segments per expert row in the split
 
@@ -1145,7 +1145,10 @@ __device__ __forceinline__ float exact_logit(const __nv_bfloat16* xs,
   return bias ? __fadd_rn(acc, bias[e]) : acc;
 }
 
-// persistent over the uncertified tokens listed by gate_tc_kernel
+// one CTA (kTcSelWarps warps) per uncertified token listed by gate_tc_kernel,
+// persistent over the list: the warps stage the x row in shared memory
+// together, each derives the same candidate set, and candidate i's exact chain
+// runs on warp i % kTcSelWarps; warp 0 then picks the top-k.
 __global__ void __launch_bounds__(kTcSelWarps * 32) gate_tc_fallback_kernel(
     const __nv_bfloat16* __restrict__ x, int d, const float* __restrict__ wg,
     const float* __restrict__ bias, int E, int Ep, int k, const int32_t* __restrict__ fb_list,
@@ -1154,48 +1157,41 @@ __global__ void __launch_bounds__(kTcSelWarps * 32) gate_tc_fallback_kernel(
     float* __restrict__ topk_w, int32_t* __restrict__ counts,
     unsigned long long* __restrict__ stats) {
   constexpr int SQ = 4;  // experts per lane (E <= 128)
+  constexpr int W = kTcSelWarps;
   extern __shared__ __align__(16) uint8_t sel_smem[];
   __shared__ int hist[128];
+  __shared__ float ss_w[W];
+  __shared__ float ex_s[128];
   const int64_t n_fb = *fb_count;
-  if (int64_t(blockIdx.x) * kTcSelWarps >= n_fb) return;
+  if (int64_t(blockIdx.x) >= n_fb) return;
   for (int i = threadIdx.x; i < E; i += blockDim.x) hist[i] = 0;
-  __syncthreads();
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  __nv_bfloat16* xs = reinterpret_cast<__nv_bfloat16*>(sel_smem) + size_t(warp) * d;
-  const int64_t stride = int64_t(gridDim.x) * kTcSelWarps;
+  __nv_bfloat16* xs = reinterpret_cast<__nv_bfloat16*>(sel_smem);
   unsigned long long n_cand = 0, n_full = 0, n_tok = 0;
-  for (int64_t it = int64_t(blockIdx.x) * kTcSelWarps + warp; it < n_fb; it += stride) {
+  for (int64_t it = blockIdx.x; it < n_fb; it += gridDim.x) {
     const int64_t tok = fb_list[it];
     const __nv_bfloat16* xr = x + tok * d;
+    __syncthreads();  // the previous token is done with xs / ex_s
+    // the row in 16-byte slices: slice j -> lane j % 32 of warp (j / 32) % W
     float ss = 0.0f;
-    constexpr int G = 8;  // 16-byte slices in flight per lane
-    __syncwarp();
-    for (int cb = 0; cb * 256 < d; cb += G) {
-      uint4 raw[G];
+    for (int c = (warp * 32 + lane) * 8; c < d; c += W * 256) {
+      const uint4 raw = __ldg(reinterpret_cast<const uint4*>(xr + c));
+      *reinterpret_cast<uint4*>(xs + c) = raw;
+      const uint32_t wds[4] = {raw.x, raw.y, raw.z, raw.w};
 #pragma unroll
-      for (int j = 0; j < G; ++j) {
-        const int c = (cb + j) * 256 + lane * 8;
-        if (c < d) raw[j] = __ldg(reinterpret_cast<const uint4*>(xr + c));
-      }
-#pragma unroll
-      for (int j = 0; j < G; ++j) {
-        const int c = (cb + j) * 256 + lane * 8;
-        if (c < d) {
-          *reinterpret_cast<uint4*>(xs + c) = raw[j];
-          const uint32_t wds[4] = {raw[j].x, raw[j].y, raw[j].z, raw[j].w};
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const float p = __uint_as_float(wds[i] << 16),
-                        q = __uint_as_float(wds[i] & 0xffff0000u);
-            ss = fmaf(p, p, ss);
-            ss = fmaf(q, q, ss);
-          }
-        }
+      for (int i = 0; i < 4; ++i) {
+        const float p = __uint_as_float(wds[i] << 16), q = __uint_as_float(wds[i] & 0xffff0000u);
+        ss = fmaf(p, p, ss);
+        ss = fmaf(q, q, ss);
       }
     }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
-    __syncwarp();
+    if (lane == 0) ss_w[warp] = ss;
+    __syncthreads();
+    ss = 0.0f;
+#pragma unroll
+    for (int w = 0; w < W; ++w) ss += ss_w[w];
     const float nx = __fmul_ru(__fsqrt_ru(ss), 1.001f);
     float lo_b[SQ], hi_b[SQ];
     bool live[SQ];
@@ -1249,56 +1245,63 @@ __global__ void __launch_bounds__(kTcSelWarps * 32) gate_tc_fallback_kernel(
 #pragma unroll
       for (int q = 0; q < SQ; ++q) cand[q] = live[q];
     }
-    float ex[SQ];
+    // candidate i (ascending expert index) -> warp i % W
+    int rank = 0;
 #pragma unroll
     for (int q = 0; q < SQ; ++q) {
-      ex[q] = 0.0f;
       unsigned m = __ballot_sync(0xffffffffu, cand[q]);
       while (m) {
         const int b = __ffs(m) - 1;
         m &= m - 1;
-        const int e = b + 32 * q;
-        const float L = exact_logit(xs, wg + size_t(e) * d, d, lane, bias, e);
-        if (lane == b) ex[q] = L;
+        if (rank++ % W == warp) {
+          const int e = b + 32 * q;
+          const float L = exact_logit(xs, wg + size_t(e) * d, d, lane, bias, e);
+          if (lane == 0) ex_s[e] = L;
+        }
       }
     }
-    // top-k over the exact candidate logits (ties and NaN -> lower index)
-    float mx = -INFINITY;
+    __syncthreads();
+    if (warp == 0) {  // top-k over the exact candidate logits (ties and NaN -> lower index)
+      float ex[SQ];
 #pragma unroll
-    for (int q = 0; q < SQ; ++q)
-      if (cand[q] && !isnan(ex[q])) mx = fmaxf(mx, ex[q]);
-    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    float psum = 0.0f, pk_mine = 0.0f;
-    int ik_mine = 0;
-    for (int j = 0; j < k; ++j) {
-      Cand best{0.0f, -1};
-#pragma unroll
-      for (int q = 0; q < SQ; ++q) {
-        Cand c{ex[q], cand[q] ? lane + 32 * q : -1};
-        if (better(c, best)) best = c;
-      }
-      for (int o = 16; o; o >>= 1) {
-        Cand other{__shfl_xor_sync(0xffffffffu, best.v, o),
-                   __shfl_xor_sync(0xffffffffu, best.i, o)};
-        if (better(other, best)) best = other;
-      }
-      const float pj = expf(best.v - mx);
-      psum += pj;
-      if (lane == j) { pk_mine = pj; ik_mine = best.i; }
+      for (int q = 0; q < SQ; ++q) ex[q] = cand[q] ? ex_s[lane + 32 * q] : 0.0f;
+      float mx = -INFINITY;
 #pragma unroll
       for (int q = 0; q < SQ; ++q)
-        if (lane + 32 * q == best.i) cand[q] = false;
-    }
-    if (lane < k) {
-      topk_idx[tok * k + lane] = ik_mine;
-      topk_w[tok * k + lane] = pk_mine / psum;
-      atomicAdd(&hist[ik_mine], 1);
+        if (cand[q] && !isnan(ex[q])) mx = fmaxf(mx, ex[q]);
+      for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      float psum = 0.0f, pk_mine = 0.0f;
+      int ik_mine = 0;
+      for (int j = 0; j < k; ++j) {
+        Cand best{0.0f, -1};
+#pragma unroll
+        for (int q = 0; q < SQ; ++q) {
+          Cand c{ex[q], cand[q] ? lane + 32 * q : -1};
+          if (better(c, best)) best = c;
+        }
+        for (int o = 16; o; o >>= 1) {
+          Cand other{__shfl_xor_sync(0xffffffffu, best.v, o),
+                     __shfl_xor_sync(0xffffffffu, best.i, o)};
+          if (better(other, best)) best = other;
+        }
+        const float pj = expf(best.v - mx);
+        psum += pj;
+        if (lane == j) { pk_mine = pj; ik_mine = best.i; }
+#pragma unroll
+        for (int q = 0; q < SQ; ++q)
+          if (lane + 32 * q == best.i) cand[q] = false;
+      }
+      if (lane < k) {
+        topk_idx[tok * k + lane] = ik_mine;
+        topk_w[tok * k + lane] = pk_mine / psum;
+        atomicAdd(&hist[ik_mine], 1);
+      }
     }
     n_cand += full ? unsigned(E) : unsigned(nc);
     n_full += full ? 1u : 0u;
     n_tok += 1;
   }
-  if (stats && lane == 0 && n_tok) {
+  if (stats && threadIdx.x == 0 && n_tok) {
     atomicAdd(&stats[1], n_tok);
     atomicAdd(&stats[2], n_cand);
     if (n_full) atomicAdd(&stats[3], n_full);
@@ -1412,13 +1415,12 @@ void tc_gate_go(const void* x, int64_t N, int d, const float* wg, const float* b
   INFMOE_CUDA(cudaLaunchKernel(kern, dim3(unsigned(grid)), dim3(kTcThreads), kargs, smem, s));
   INFMOE_LAUNCH_CHECK();
 
-  const size_t sel_smem = size_t(kTcSelWarps) * d * 2;
+  const size_t sel_smem = size_t(d) * 2;  // one x row per CTA
   ensure_dyn_smem(reinterpret_cast<const void*>(gate_tc_fallback_kernel), sel_smem);
   int per_sm = 0;
   INFMOE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
       &per_sm, gate_tc_fallback_kernel, kTcSelWarps * 32, sel_smem));
-  const int64_t fb_grid = std::min<int64_t>((N + kTcSelWarps - 1) / kTcSelWarps,
-                                            int64_t(std::max(per_sm, 1)) * device_sm_count());
+  const int64_t fb_grid = std::min<int64_t>(N, int64_t(std::max(per_sm, 1)) * device_sm_count());
   gate_tc_fallback_kernel<<<unsigned(fb_grid), kTcSelWarps * 32, sel_smem, s>>>(
       reinterpret_cast<const __nv_bfloat16*>(x), d, wg, bias, E, Ep, k, fb_list, fb_count,
       fb_logits, a.gcoef, force, idx, w, counts, stats);

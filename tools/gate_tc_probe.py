@@ -20,11 +20,12 @@ wg = np.ascontiguousarray((im.gaussian_stream(im.derive_seed(seed, 1), d * E) /
 bias = (-0.6258 * np.log(np.arange(1, E + 1))).astype(np.float32)
 x = torch.from_numpy(xb.view(np.int16).reshape(N, d)).cuda().view(torch.bfloat16)
 g, b = torch.from_numpy(wg).cuda(), torch.from_numpy(bias).cuda()
+ws = dv.GateWorkspace(g, N, k)  # as a layer holds it
 out = dv.gate_softmax_topk(x, g, k, b, debug=True)
 print("gate stats", out[4], "exact chains per fallback token",
       out[4]["candidates"] / max(out[4]["fallback"], 1))
 for _ in range(3):
-    dv.gate_softmax_topk(x, g, k, b)
+    dv.gate_softmax_topk(x, g, k, b, workspace=ws)
 os.environ["INFMOE_GATE_TC"] = "0"
 for _ in range(2):
     dv.gate_softmax_topk(x, g, k, b)
