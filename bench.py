@@ -605,6 +605,10 @@ def main() -> None:
     ap.add_argument("--pin-frac", type=float, default=0.5,
                     help="hot-expert pinning line (SURVEY 8(f)-4, not reference-faithful): "
                          "fraction of each layer's experts kept on the device (0 skips it)")
+    ap.add_argument("--pack-cache", default=None,
+                    help="directory of h2d-codec packs (infmoe_set_pack_cache_dir): packs are "
+                         "read from it instead of encoded when their content matches, and "
+                         "written to it after encoding (default: encode, no files)")
     ap.add_argument("--h2d-codec", default="exph", choices=["exph", "exp4", "raw"],
                     help="exph (default) / exp4: the headline streams lossless packs (Huffman-"
                          "coded or 4-bit exponents, ~10.7 / 12 bits per weight, decoded on the "
@@ -753,6 +757,8 @@ def main() -> None:
     exp_layers = []
     pack_s = 0.0
     if args.h2d_codec != "raw":
+        if args.pack_cache:
+            im.set_pack_cache_dir(args.pack_cache)
         t0 = time.perf_counter()
         for l in range(L):
             wi, wo = w_host[l % n_sets]
@@ -1206,7 +1212,8 @@ def main() -> None:
             "link_idle_ms_per_layer": link_idle_ms(ex_infos[-1], t_ex),
             "bit_identical_to_raw_stream": bool(torch.equal(y_ex.view(torch.int16),
                                                             y_off.view(torch.int16))),
-            "pack_seconds_host_once": pack_s}
+            "pack_seconds_host_once": pack_s,
+            "pack_source": exp_layers[0].pack_source()}
         line["clocks"] = ex_clocks.summary()
         line["gpu_launches"] = line["gpu_launches"] + 2 * L * El  # two decodes per expert
         line["speedup_vs_raw_stream"] = t_in / t_ex

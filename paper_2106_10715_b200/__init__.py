@@ -182,6 +182,8 @@ _lib.infmoe_debug_occupy_sms.argtypes = [_i32, _i32, _vp, _u64, _vp, _vp]
 _lib.infmoe_debug_set_flag.argtypes = [_vp, _vp]
 _lib.infmoe_gate_softmax_topk.argtypes = [_vp, _i32, C.c_int64, _i32, _vp, _vp, _i32, _i32,
                                           _vp, _vp, _vp, _vp]
+_lib.infmoe_layer_pack_source.argtypes = [_vp, _vp]
+_lib.infmoe_set_pack_cache_dir.argtypes = [C.c_char_p]
 _lib.infmoe_gate_softmax_ws_bytes.argtypes = [_i32, C.c_int64, _i32, _i32, _i32]
 _lib.infmoe_gate_softmax_ws_bytes.restype = C.c_size_t
 _lib.infmoe_gate_softmax_prepare.argtypes = [_vp, _i32, _i32, _vp, C.c_size_t, _vp]
@@ -307,6 +309,14 @@ def gaussian_fill_typed(dtype: str, seeds, scales, n_each: int, outs, threads: i
     code = {"bf16": DTYPE_BF16, "f32": DTYPE_F32}[dtype]
     _check(_lib.infmoe_gaussian_fill_typed(code, sd.size, _ptr(sd), _ptr(sc), n_each,
                                            _ptr(addr), threads))
+
+
+def set_pack_cache_dir(path) -> None:
+    """Process-wide directory of h2d-codec packs (infmoe_set_pack_cache_dir);
+    None disables.  Codec layers read their pack from it instead of encoding
+    when a file for the same host-weight content exists, and write it after
+    encoding."""
+    _check(_lib.infmoe_set_pack_cache_dir(None if path is None else str(path).encode()))
 
 
 def gaussian_bf16(seed: int, n: int, scale: float = 1.0) -> np.ndarray:

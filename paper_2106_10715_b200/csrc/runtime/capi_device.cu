@@ -403,6 +403,17 @@ int infmoe_codec_roundtrip_host(int32_t codec_id, const uint16_t* in, uint64_t n
   });
 }
 
+int infmoe_layer_pack_source(infmoe_layer* layer, int32_t* source) {
+  return guarded([&] {
+    require(layer && layer->impl && source, "pack_source: NULL argument");
+    *source = layer->impl->pack_source();
+  });
+}
+
+int infmoe_set_pack_cache_dir(const char* dir) {
+  return guarded([&] { HostPack::set_cache_dir(dir); });
+}
+
 int infmoe_layer_h2d_bytes(infmoe_layer* layer, uint64_t* packed, uint64_t* raw) {
   return guarded([&] {
     require(layer && layer->impl, "h2d_bytes: NULL layer");

@@ -22,6 +22,7 @@
 // owner runs its local experts (resident or offloaded), and the reverse
 // all-to-allv brings the results home for the combine.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <string>
 #include <cstring>
@@ -1095,6 +1096,122 @@ static uint64_t host_digest(const void* w_in, const void* w_out, uint64_t bytes_
   return h;
 }
 
+// ---- on-disk pack cache ----------------------------------------------------
+// <dir>/<digest>-<codec>-<experts>x<elems>.infmoe-pack:
+//   "INFMOEPK" | u32 version | u32 codec | u64 experts | u64 elems | u64 digest |
+//   u64 total | u64 max_size | u64 raw_bytes | u64 pack checksum |
+//   per expert {off, size, in_size} | exph: per expert {lay_in, lay_out} |
+//   the pack bytes.  A file whose header or checksum does not match is ignored
+//   (and replaced by the next encode).
+namespace {
+std::string g_pack_dir = [] {
+  const char* e = std::getenv("INFMOE_PACK_CACHE_DIR");
+  return std::string(e ? e : "");
+}();
+constexpr char kPackMagic[8] = {'I', 'N', 'F', 'M', 'O', 'E', 'P', 'K'};
+constexpr uint32_t kPackVersion = 1;
+
+uint64_t pack_checksum(const uint8_t* p, uint64_t bytes) {
+  // both halves (and an odd last byte)
+  return host_digest(p, p + bytes / 2, bytes / 2) ^ dev_mix64(bytes + (bytes & 1 ? p[bytes - 1] : 0));
+}
+
+std::string pack_path(uint64_t digest, int codec_id, int n_experts, uint64_t elems) {
+  char name[128];
+  std::snprintf(name, sizeof(name), "%016llx-%d-%dx%llu.infmoe-pack",
+                static_cast<unsigned long long>(digest), codec_id, n_experts,
+                static_cast<unsigned long long>(elems));
+  return g_pack_dir + "/" + name;
+}
+
+struct PackHeader {
+  char magic[8];
+  uint32_t version, codec;
+  uint64_t experts, elems, digest, total, max_size, raw_bytes, checksum;
+};
+
+bool pack_load(const std::string& path, HostPack& p, int n_experts, uint64_t elems) {
+  FILE* f = std::fopen(path.c_str(), "rb");
+  if (!f) return false;
+  PackHeader h;
+  bool ok = std::fread(&h, sizeof(h), 1, f) == 1 && std::memcmp(h.magic, kPackMagic, 8) == 0 &&
+            h.version == kPackVersion && int(h.codec) == p.codec_id &&
+            h.experts == uint64_t(n_experts) && h.elems == elems && h.digest == p.digest;
+  const size_t ne = size_t(n_experts);
+  if (ok) {
+    p.off.resize(ne);
+    p.size.resize(ne);
+    p.in_size.resize(ne);
+    for (size_t e = 0; e < ne && ok; ++e) {
+      uint64_t v[3];
+      ok = std::fread(v, sizeof(v), 1, f) == 1;
+      p.off[e] = v[0];
+      p.size[e] = v[1];
+      p.in_size[e] = v[2];
+    }
+  }
+  if (ok && p.codec_id == INFMOE_CODEC_EXPH) {
+    p.lay_in.resize(ne);
+    p.lay_out.resize(ne);
+    for (size_t e = 0; e < ne && ok; ++e)
+      ok = std::fread(&p.lay_in[e], sizeof(codec::ExphLayout), 1, f) == 1 &&
+           std::fread(&p.lay_out[e], sizeof(codec::ExphLayout), 1, f) == 1;
+  }
+  if (ok) {
+    p.total = h.total;
+    p.max_size = h.max_size;
+    p.raw_bytes = h.raw_bytes;
+    INFMOE_CUDA(cudaMallocHost(&p.host, p.total));
+    ok = std::fread(p.host, 1, p.total, f) == p.total && pack_checksum(p.host, p.total) == h.checksum;
+    for (size_t e = 0; e < ne && ok; ++e) ok = p.off[e] + p.size[e] <= p.total;
+    if (!ok) {
+      cudaFreeHost(p.host);
+      p.host = nullptr;
+    }
+  }
+  std::fclose(f);
+  if (!ok) {
+    p.off.clear(); p.size.clear(); p.in_size.clear(); p.lay_in.clear(); p.lay_out.clear();
+    p.total = p.max_size = p.raw_bytes = 0;
+  }
+  return ok;
+}
+
+void pack_save(const std::string& path, const HostPack& p, int n_experts, uint64_t elems) {
+  const std::string tmp = path + ".tmp." + std::to_string(::getpid());
+  FILE* f = std::fopen(tmp.c_str(), "wb");
+  if (!f) return;  // an unwritable cache directory only costs the next re-encode
+  PackHeader h;
+  std::memcpy(h.magic, kPackMagic, 8);
+  h.version = kPackVersion;
+  h.codec = uint32_t(p.codec_id);
+  h.experts = uint64_t(n_experts);
+  h.elems = elems;
+  h.digest = p.digest;
+  h.total = p.total;
+  h.max_size = p.max_size;
+  h.raw_bytes = p.raw_bytes;
+  h.checksum = pack_checksum(p.host, p.total);
+  bool ok = std::fwrite(&h, sizeof(h), 1, f) == 1;
+  for (int e = 0; e < n_experts && ok; ++e) {
+    const uint64_t v[3] = {p.off[size_t(e)], p.size[size_t(e)], p.in_size[size_t(e)]};
+    ok = std::fwrite(v, sizeof(v), 1, f) == 1;
+  }
+  if (p.codec_id == INFMOE_CODEC_EXPH)
+    for (int e = 0; e < n_experts && ok; ++e)
+      ok = std::fwrite(&p.lay_in[size_t(e)], sizeof(codec::ExphLayout), 1, f) == 1 &&
+           std::fwrite(&p.lay_out[size_t(e)], sizeof(codec::ExphLayout), 1, f) == 1;
+  ok = ok && std::fwrite(p.host, 1, p.total, f) == p.total;
+  ok = (std::fclose(f) == 0) && ok;
+  if (!ok || std::rename(tmp.c_str(), path.c_str()) != 0) std::remove(tmp.c_str());
+}
+}  // namespace
+
+void HostPack::set_cache_dir(const char* dir) {
+  std::lock_guard<std::mutex> lock(g_pack_mu);
+  g_pack_dir = dir ? dir : "";
+}
+
 std::shared_ptr<HostPack> HostPack::acquire(const void* w_in, const void* w_out, int n_experts,
                                             uint64_t matrix_elems, int codec_id, bool fresh) {
   std::lock_guard<std::mutex> lock(g_pack_mu);
@@ -1107,6 +1224,13 @@ std::shared_ptr<HostPack> HostPack::acquire(const void* w_in, const void* w_out,
   auto p = std::make_shared<HostPack>();
   p->codec_id = codec_id;
   p->digest = digest;
+  const std::string path =
+      g_pack_dir.empty() ? std::string() : pack_path(digest, codec_id, n_experts, matrix_elems);
+  if (!path.empty() && pack_load(path, *p, n_experts, matrix_elems)) {
+    p->source = 2;
+    g_packs[key] = p;
+    return p;
+  }
   const auto* in = static_cast<const uint16_t*>(w_in);
   const auto* out = static_cast<const uint16_t*>(w_out);
   const bool h = codec_id == INFMOE_CODEC_EXPH;
@@ -1145,6 +1269,7 @@ std::shared_ptr<HostPack> HostPack::acquire(const void* w_in, const void* w_out,
       codec::exp4_fill(m2, p4[size_t(2 * e + 1)], dst + p->in_size[size_t(e)]);
     }
   }
+  if (!path.empty()) pack_save(path, *p, n_experts, matrix_elems);
   g_packs[key] = p;
   return p;
 }

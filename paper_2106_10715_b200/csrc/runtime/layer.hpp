@@ -36,8 +36,13 @@ struct HostPack {
   int codec_id = 0;
   uint64_t max_size = 0, total = 0, raw_bytes = 0;
   uint64_t digest = 0;              // content digest of the host weights packed
+  int source = 1;                   // 1 encoded in this process, 2 read from the pack cache
   // the pack of (w_in, w_out): a live cached pack of the same buffers and the
   // same content digest is shared, unless `fresh` (always re-pack)
+  // packs are also kept on disk when a pack cache directory is set
+  // (infmoe_set_pack_cache_dir / INFMOE_PACK_CACHE_DIR): one file per content
+  // digest, read back instead of re-encoding, verified by its own checksum
+  static void set_cache_dir(const char* dir);
   static std::shared_ptr<HostPack> acquire(const void* w_in, const void* w_out, int n_experts,
                                            uint64_t matrix_elems, int codec_id, bool fresh);
   ~HostPack();
@@ -65,6 +70,7 @@ struct Layer {
   int n_pinned_experts() const { return n_pinned; }
   // continuous_load_stream: the layer forwarded after this one
   void set_next(Layer* nxt);
+  int pack_source() const { return pack ? pack->source : 0; }
   void h2d_bytes(uint64_t* packed, uint64_t* raw) const {
     const uint64_t r = uint64_t(n_local) * 2 * expert_in_bytes;
     if (raw) *raw = r;

@@ -360,6 +360,13 @@ class MoELayer:
         _check(_lib.infmoe_layer_h2d_bytes(self._h, C.byref(pk), C.byref(raw)))
         return pk.value
 
+    def pack_source(self) -> str:
+        """Where the h2d-codec pack came from: "none" (raw stream), "encoded" or
+        "cache" (read from the pack cache directory, set_pack_cache_dir)."""
+        v = C.c_int32(0)
+        _check(_lib.infmoe_layer_pack_source(self._h, C.byref(v)))
+        return {0: "none", 1: "encoded", 2: "cache"}[v.value]
+
     def pin_hottest(self, n: int) -> list:
         """Cross-batch cache policy: pin the n local experts with the highest
         running load estimate (EMA of routed rows, decay 0.5).  Returns them."""

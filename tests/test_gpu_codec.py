@@ -144,3 +144,54 @@ def test_codec_layer_from_pageable_weights(cuda):
     assert not wi.is_pinned()
     raw.close()
     ex.close()
+
+
+@pytest.mark.parametrize("codec", ["exp4", "exph"])
+def test_pack_cache_dir(cuda, tmp_path, codec):
+    """set_pack_cache_dir: the first codec layer encodes and writes one file per
+    host-weight content; a later layer on the same content reads it back (no
+    encode) with output bit-identical to the raw stream; a damaged file or new
+    content is never used -- it is re-encoded (and the file replaced)."""
+    N, d, f, E, K = 256, 256, 512, 4, 1
+    t = lambda b, sh: torch.from_numpy(b.view(np.int16).reshape(sh)).view(torch.bfloat16)
+    x = t(fill_bf16(51, N * d, 1.7320508), (N, d)).to(cuda)
+    wi = t(fill_bf16(52, E * f * d, 1.7320508 / 16), (E, f, d)).pin_memory()
+    wo = t(fill_bf16(53, E * d * f, 1.534 * 1.7320508 / np.sqrt(f)), (E, d, f)).pin_memory()
+    kw = dict(gate="lsh", lsh_seed=5, lsh_bits=2, max_tokens=N, offloaded=True, K=K)
+    raw = dv.MoELayer(d, f, E, 1, wi, wo, **kw)
+    y_raw, _ = raw.forward(x)
+    im.set_pack_cache_dir(tmp_path)
+    try:
+        a = dv.MoELayer(d, f, E, 1, wi, wo, h2d_codec=codec, **kw)
+        assert a.pack_source() == "encoded"
+        files = sorted(tmp_path.glob("*.infmoe-pack"))
+        assert len(files) == 1 and not list(tmp_path.glob("*.tmp.*"))
+        a.close()
+        b = dv.MoELayer(d, f, E, 1, wi, wo, h2d_codec=codec, **kw)
+        assert b.pack_source() == "cache"
+        y_b, _ = b.forward(x)
+        torch.cuda.synchronize()
+        assert torch.equal(y_b.view(torch.int16), y_raw.view(torch.int16))
+        assert b.packed_bytes() < 2 * E * d * f * 2
+        b.close()
+        # flip one byte of the pack area: the checksum rejects the file
+        blob = bytearray(files[0].read_bytes())
+        blob[-100] ^= 0x5A
+        files[0].write_bytes(bytes(blob))
+        c = dv.MoELayer(d, f, E, 1, wi, wo, h2d_codec=codec, **kw)
+        assert c.pack_source() == "encoded"
+        y_c, _ = c.forward(x)
+        torch.cuda.synchronize()
+        assert torch.equal(y_c.view(torch.int16), y_raw.view(torch.int16))
+        c.close()
+        assert files[0].read_bytes() != bytes(blob)  # replaced by the fresh encode
+        # new content -> a second file, encoded
+        wi.copy_(t(fill_bf16(54, E * f * d, 1.7320508 / 16), (E, f, d)))
+        e2 = dv.MoELayer(d, f, E, 1, wi, wo, h2d_codec=codec, **kw)
+        assert e2.pack_source() == "encoded"
+        assert len(list(tmp_path.glob("*.infmoe-pack"))) == 2
+        e2.close()
+    finally:
+        im.set_pack_cache_dir(None)
+    assert raw.pack_source() == "none"
+    raw.close()
