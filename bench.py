@@ -1210,6 +1210,10 @@ def main() -> None:
             "measured_over_simulated": t_ex / (sim_eff.makespan * 1e3),
             "replay_check_violations": audit_ex,
             "link_idle_ms_per_layer": link_idle_ms(ex_infos[-1], t_ex),
+            # the copies' own rate in the timeline step (pack bytes / summed load
+            # durations): separates a slower link from idle gaps between copies
+            "load_lane_gbs": link_bytes / max(1e-12, sum(
+                e[4] - e[3] for i in ex_infos[-1] for e in i["events"] if e[0] == 0)) / 1e9,
             "bit_identical_to_raw_stream": bool(torch.equal(y_ex.view(torch.int16),
                                                             y_off.view(torch.int16))),
             "pack_seconds_host_once": pack_s,
