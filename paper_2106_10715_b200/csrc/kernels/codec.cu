@@ -6,7 +6,9 @@
 #include "codec.cuh"
 
 #include <algorithm>
+#include <cstring>
 #include <atomic>
+#include <iterator>
 #include <queue>
 #include <thread>
 
@@ -152,62 +154,59 @@ void launch_exp4_unpack(const uint8_t* pack, uint64_t n, uint16_t* out, cudaStre
 // ------------------------------------------------------------------ exph --
 namespace {
 
+// (dist, m2) symbol of a bf16 value against its base
 inline uint32_t exph_sym(uint16_t v, uint32_t base) {
   const uint32_t d = base - ((v >> 7) & 0xFFu);
-  return d >= uint32_t(kExphEsc) ? uint32_t(kExphEsc) : d;
+  return ((d >= uint32_t(kExphEsc) ? uint32_t(kExphEsc) : d) << 2) | ((v >> 5) & 3u);
 }
+inline bool exph_is_esc(uint32_t sym) { return (sym >> 2) == uint32_t(kExphEsc); }
 
-// Huffman code lengths for <= 32 symbols, limited to kExphMaxLen bits (longer
-// codes are clamped and the Kraft sum restored by lengthening the longest
-// codes below the limit); canonical codes assigned by (length, symbol)
+// Optimal code lengths for kExphSyms symbols under the kExphMaxLen-bit limit
+// (package-merge: the L-1 rounds of pairing the cheapest entries; a symbol's
+// length is the number of chosen entries that contain it).  Canonical codes
+// are then assigned by (length, symbol).
 void huffman_lengths(const uint64_t* freq, uint8_t* len) {
-  struct Node { uint64_t f; int id; };
-  auto cmp = [](const Node& a, const Node& b) { return a.f != b.f ? a.f > b.f : a.id > b.id; };
-  std::priority_queue<Node, std::vector<Node>, decltype(cmp)> q(cmp);
-  std::vector<int> parent(64, -1);
-  int next = 32, used = 0;
-  for (int i = 0; i < 32; ++i) {
+  constexpr int S = kExphSyms;
+  struct Entry {
+    uint64_t w;
+    std::vector<uint16_t> syms;  // symbols (with multiplicity) inside this entry
+  };
+  std::vector<Entry> items;
+  for (int i = 0; i < S; ++i) {
     len[i] = 0;
-    if (freq[i]) { q.push({freq[i], i}); ++used; }
+    if (freq[i]) items.push_back({freq[i], {uint16_t(i)}});
   }
-  if (used == 0) return;
-  if (used == 1) { len[q.top().id] = 1; return; }
-  while (q.size() > 1) {
-    Node a = q.top(); q.pop();
-    Node b = q.top(); q.pop();
-    parent[size_t(a.id)] = next;
-    parent[size_t(b.id)] = next;
-    q.push({a.f + b.f, next++});
-  }
-  for (int i = 0; i < 32; ++i) {
-    if (!freq[i]) continue;
-    int d = 0;
-    for (int j = i; parent[size_t(j)] >= 0; j = parent[size_t(j)]) ++d;
-    len[i] = uint8_t(d);
-  }
-  int64_t kraft = 0;
-  const int64_t one = int64_t(1) << kExphMaxLen;
-  for (int i = 0; i < 32; ++i)
-    if (len[i]) {
-      if (len[i] > kExphMaxLen) len[i] = kExphMaxLen;
-      kraft += one >> len[i];
+  const size_t n = items.size();
+  if (n == 0) return;
+  if (n == 1) { len[items[0].syms[0]] = 1; return; }
+  // ascending weight, ties by the lowest symbol inside (deterministic)
+  auto less = [](const Entry& x, const Entry& y) {
+    return x.w != y.w ? x.w < y.w : x.syms.front() < y.syms.front();
+  };
+  std::stable_sort(items.begin(), items.end(), less);
+  std::vector<Entry> list = items;
+  for (int round = 1; round < kExphMaxLen; ++round) {
+    std::vector<Entry> merged;
+    for (size_t j = 0; j + 1 < list.size(); j += 2) {
+      Entry e{list[j].w + list[j + 1].w, list[j].syms};
+      e.syms.insert(e.syms.end(), list[j + 1].syms.begin(), list[j + 1].syms.end());
+      merged.push_back(std::move(e));
     }
-  while (kraft > one) {  // lengthen the longest code still below the limit
-    int best = -1;
-    for (int i = 0; i < 32; ++i)
-      if (len[i] && len[i] < kExphMaxLen && (best < 0 || len[i] > len[best] ||
-                                             (len[i] == len[best] && freq[i] < freq[best])))
-        best = i;
-    kraft -= one >> (len[best] + 1);
-    ++len[best];
+    std::vector<Entry> next;
+    next.reserve(items.size() + merged.size());
+    std::merge(items.begin(), items.end(), merged.begin(), merged.end(),
+               std::back_inserter(next), less);
+    list = std::move(next);
   }
+  for (size_t j = 0; j < 2 * n - 2; ++j)
+    for (uint16_t sym : list[j].syms) ++len[sym];
 }
 
 void canonical_codes(const uint8_t* len, uint32_t* code) {
   uint32_t c = 0;
   int prev = 0;
   for (int l = 1; l <= kExphMaxLen; ++l) {
-    for (int s = 0; s < 32; ++s)
+    for (int s = 0; s < kExphSyms; ++s)
       if (len[s] == l) {
         c <<= (l - prev);
         prev = l;
@@ -216,13 +215,22 @@ void canonical_codes(const uint8_t* len, uint32_t* code) {
   }
 }
 
+// bits [bit, bit + 5) of the 192-bit little-endian residual record (A, B, C)
+__device__ __forceinline__ uint32_t rec5(uint64_t A, uint64_t B, uint64_t C, int bit) {
+  if (bit + 5 <= 64) return uint32_t(A >> bit) & 31u;
+  if (bit < 64) return uint32_t((A >> bit) | (B << (64 - bit))) & 31u;
+  if (bit + 5 <= 128) return uint32_t(B >> (bit - 64)) & 31u;
+  if (bit < 128) return uint32_t((B >> (bit - 64)) | (C << (128 - bit))) & 31u;
+  return uint32_t(C >> (bit - 128)) & 31u;
+}
+
 // One warp decodes 32 consecutive chunks, one per lane (Huffman codes are
-// sequential within a chunk).  The sign/mantissa bytes are stored
-// lane-interleaved per 16-value group (exph_sm_offset), so each group load is
-// one contiguous 512-byte warp access; each half of a lane's 256 output bytes
-// is staged in shared memory (16-byte slots XOR-swizzled by row) and written
-// back as full 128-byte lines.  Only the bitstream refills stay per lane (one
-// word ahead).
+// sequential within a chunk).  The 6-bit residuals are stored as 24-byte
+// records per 32 values, lane-interleaved (exph_res_offset), so each record
+// load is one contiguous 768-byte warp access; each quarter of a lane's 512
+// output bytes is staged in shared memory (16-byte slots XOR-swizzled by row)
+// and written back as full 128-byte lines.  Only the bitstream refills stay
+// per lane (one word ahead).
 constexpr int kExphWarps = 8;
 __global__ void __launch_bounds__(kExphWarps * 32) exph_unpack_kernel(const uint8_t* __restrict__ pack,
                                                                       ExphLayout L,
@@ -259,65 +267,76 @@ __global__ void __launch_bounds__(kExphWarps * 32) exph_unpack_kernel(const uint
         nw = __ldg(++wp);
         return w;
       };
+      auto refill = [&]() {
+        if (nbits < 32) {
+          buf |= uint64_t(take()) << (32 - nbits);
+          nbits += 32;
+        }
+      };
+      // exponent << 7 | m2 << 5 of one value from its LUT entry (escape: the raw
+      // exponent follows the code)
       auto one = [&](uint32_t ent) -> uint32_t {
-        const uint32_t sym = (ent >> 4) & 31u, ln = ent & 15u;
+        const uint32_t sym = (ent >> 4) & 127u, ln = ent & 15u;
         buf <<= ln;
         nbits -= int(ln);
-        if (sym == uint32_t(kExphEsc)) {
-          const uint32_t e = uint32_t(buf >> 56);
+        uint32_t e;
+        if ((sym >> 2) == uint32_t(kExphEsc)) {
+          e = uint32_t(buf >> 56);
           buf <<= 8;
           nbits -= 8;
-          return e;
+        } else {
+          e = (base - (sym >> 2)) & 0xFFu;
         }
-        return (base - sym) & 0xFFu;
+        return (e << 7) | ((sym & 3u) << 5);
       };
-      const uint8_t* smg = pack + c0 * kExphChunk + uint64_t(lane) * 16;
-      const uint64_t qstride = uint64_t(nch) * 16;
-      uint4 s_next = __ldg(reinterpret_cast<const uint4*>(smg));
+      const uint64_t* rec = reinterpret_cast<const uint64_t*>(
+          pack + c0 * (kExphChunk / 32) * kExphRec + uint64_t(lane) * kExphRec);
+      const uint64_t qstride = uint64_t(nch) * kExphRec / 8;  // in uint64
+      uint64_t nA = __ldg(rec), nB = __ldg(rec + 1), nC = __ldg(rec + 2);
 #pragma unroll 1
-      for (int q = 0; q < kExphChunk / 16; ++q) {
-        const uint4 s4 = s_next;
-        if (q + 1 < kExphChunk / 16)
-          s_next = __ldg(reinterpret_cast<const uint4*>(smg + uint64_t(q + 1) * qstride));
-        const uint32_t sw[4] = {s4.x, s4.y, s4.z, s4.w};
-        uint32_t r[8];
+      for (int q = 0; q < kExphChunk / 32; ++q) {
+        const uint64_t A = nA, B = nB, C = nC;
+        if (q + 1 < kExphChunk / 32) {
+          const uint64_t* r2 = rec + uint64_t(q + 1) * qstride;
+          nA = __ldg(r2);
+          nB = __ldg(r2 + 1);
+          nC = __ldg(r2 + 2);
+        }
+        uint32_t r[16];
 #pragma unroll
-        for (int jp = 0; jp < 8; ++jp) {  // values in pairs: one table lookup per pair
-          if (nbits < 32) {
-            buf |= uint64_t(take()) << (32 - nbits);
-            nbits += 32;
-          }
+        for (int jp = 0; jp < 16; ++jp) {  // values in pairs: one table lookup per pair
+          refill();
           const uint32_t ent = lut[uint32_t(buf >> (64 - kExphMaxLen))];
-          uint32_t e0, e1;
-          if (ent & (1u << 19)) {  // both codes inside the 12-bit window
-            const uint32_t ln = (ent >> 14) & 31u;
+          uint32_t h0, h1;  // exponent << 7 | m2 << 5
+          if (ent & (1u << 23)) {  // both codes inside the 12-bit window, no escape
+            const uint32_t ln = (ent >> 18) & 31u;
             buf <<= ln;
             nbits -= int(ln);
-            e0 = (base - ((ent >> 4) & 31u)) & 0xFFu;
-            e1 = (base - ((ent >> 9) & 31u)) & 0xFFu;
+            const uint32_t s0 = (ent >> 4) & 127u, s1 = (ent >> 11) & 127u;
+            h0 = (((base - (s0 >> 2)) & 0xFFu) << 7) | ((s0 & 3u) << 5);
+            h1 = (((base - (s1 >> 2)) & 0xFFu) << 7) | ((s1 & 3u) << 5);
           } else {  // a long code or an escape: the two values one at a time
-            e0 = one(ent);
-            if (nbits < 32) {
-              buf |= uint64_t(take()) << (32 - nbits);
-              nbits += 32;
-            }
-            e1 = one(lut[uint32_t(buf >> (64 - kExphMaxLen))]);
+            h0 = one(ent);
+            refill();
+            h1 = one(lut[uint32_t(buf >> (64 - kExphMaxLen))]);
           }
-          const uint32_t s0 = (sw[jp / 2] >> (16 * (jp % 2))) & 0xFFu;
-          const uint32_t s1 = (sw[jp / 2] >> (16 * (jp % 2) + 8)) & 0xFFu;
-          r[jp] = (((s0 & 0x80u) << 8) | (e0 << 7) | (s0 & 0x7Fu)) |
-                  ((((s1 & 0x80u) << 8) | (e1 << 7) | (s1 & 0x7Fu)) << 16);
+          const int i0 = 2 * jp, i1 = 2 * jp + 1;
+          const uint32_t v0b = ((uint32_t(A >> i0) & 1u) << 15) | h0 | rec5(A, B, C, 32 + 5 * i0);
+          const uint32_t v1b = ((uint32_t(A >> i1) & 1u) << 15) | h1 | rec5(A, B, C, 32 + 5 * i1);
+          r[jp] = v0b | (v1b << 16);
         }
-        // row = lane (the current half of its chunk: 8 16-byte slots), swizzled
-        const int sl = 2 * (q % 4);
-        st[lane * 8 + (sl ^ (lane & 7))] = make_uint4(r[0], r[1], r[2], r[3]);
-        st[lane * 8 + ((sl + 1) ^ (lane & 7))] = make_uint4(r[4], r[5], r[6], r[7]);
-        if (q % 4 == 3) {  // flush this half: 4 full 128-byte lines per warp store
+        // row = lane (the current quarter of its chunk: 8 16-byte slots), swizzled
+        const int sl = 4 * (q % 2);
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+          st[lane * 8 + ((sl + t) ^ (lane & 7))] =
+              make_uint4(r[4 * t], r[4 * t + 1], r[4 * t + 2], r[4 * t + 3]);
+        if (q % 2 == 1) {  // flush this quarter: full 128-byte lines per warp store
           __syncwarp(active);
           uint4* dst = reinterpret_cast<uint4*>(out + c0 * kExphChunk);
           for (int u = lane; u < nch * 8; u += nch) {
             const int row = u / 8, slot = u % 8;
-            dst[row * (kExphChunk / 8) + (q / 4) * 8 + slot] = st[row * 8 + (slot ^ (row & 7))];
+            dst[row * (kExphChunk / 8) + (q / 2) * 8 + slot] = st[row * 8 + (slot ^ (row & 7))];
           }
           __syncwarp(active);
         }
@@ -331,6 +350,7 @@ __global__ void __launch_bounds__(kExphWarps * 32) exph_unpack_kernel(const uint
 
 ExphPlan exph_plan(const uint16_t* in, uint64_t n) {
   require(n > 0 && n % kExphChunk == 0, "exph: value count must be a positive multiple of 256");
+  constexpr int S = kExphSyms;
   ExphPlan p;
   ExphLayout& L = p.L;
   L.n = n;
@@ -355,8 +375,8 @@ ExphPlan exph_plan(const uint16_t* in, uint64_t n) {
     p.base[b] = uint8_t(mx);
   });
   const uint32_t gmax = *std::max_element(p.base.begin(), p.base.end());
-  // histograms of the distance symbols against both choices of base
-  std::vector<std::vector<uint64_t>> hb(hw, std::vector<uint64_t>(32, 0)), hg = hb;
+  // histograms of the symbols against both choices of base
+  std::vector<std::vector<uint64_t>> hb(hw, std::vector<uint64_t>(S, 0)), hg = hb;
   run([&](unsigned t, uint64_t b) {
     const uint64_t v0 = b * kExp4Block, v1 = std::min(n, v0 + kExp4Block);
     for (uint64_t i = v0; i < v1; ++i) {
@@ -365,29 +385,29 @@ ExphPlan exph_plan(const uint16_t* in, uint64_t n) {
     }
   });
   // One base for the whole matrix codes the distance with the exponent's own
-  // entropy (i.i.d. weights: 2.55 bits for Gaussian bf16), block bases add the
-  // spread of the block maxima (2.62); blocks help when the magnitude drifts
-  // along the matrix.  The encoder keeps whichever costs fewer bits; the pack
-  // format (a base per block) and the decoder are the same either way.
-  uint64_t fb[32] = {}, fg[32] = {};
+  // entropy (i.i.d. weights), block bases add the spread of the block maxima;
+  // blocks help when the magnitude drifts along the matrix.  The encoder keeps
+  // whichever costs fewer bits; the pack format (a base per block) and the
+  // decoder are the same either way.
+  uint64_t fb[S] = {}, fg[S] = {};
   for (unsigned t = 0; t < hw; ++t)
-    for (int i = 0; i < 32; ++i) {
+    for (int i = 0; i < S; ++i) {
       fb[i] += hb[t][size_t(i)];
       fg[i] += hg[t][size_t(i)];
     }
-  uint8_t lb[32], lg[32];
+  uint8_t lb[S], lg[S];
   huffman_lengths(fb, lb);
   huffman_lengths(fg, lg);
   auto cost = [](const uint64_t* f, const uint8_t* l) {
     uint64_t bits = 0;
-    for (int i = 0; i < 32; ++i) bits += f[i] * (l[i] + (i == kExphEsc ? 8u : 0u));
+    for (int i = 0; i < S; ++i) bits += f[i] * (l[i] + (exph_is_esc(uint32_t(i)) ? 8u : 0u));
     return bits;
   };
   if (cost(fg, lg) < cost(fb, lb)) {
     std::fill(p.base.begin(), p.base.end(), uint8_t(gmax));
-    std::copy(lg, lg + 32, p.len);
+    std::copy(lg, lg + S, p.len);
   } else {
-    std::copy(lb, lb + 32, p.len);
+    std::copy(lb, lb + S, p.len);
   }
   canonical_codes(p.len, p.code);
   std::vector<uint32_t> cb(L.nchunks, 0);
@@ -396,7 +416,7 @@ ExphPlan exph_plan(const uint16_t* in, uint64_t n) {
     const uint32_t base = p.base[c * kExphChunk / kExp4Block];
     for (uint64_t i = c * kExphChunk; i < (c + 1) * kExphChunk; ++i) {
       const uint32_t sym = exph_sym(in[i], base);
-      bits += p.len[sym] + (sym == uint32_t(kExphEsc) ? 8u : 0u);
+      bits += p.len[sym] + (exph_is_esc(sym) ? 8u : 0u);
     }
     cb[c] = bits;
   });
@@ -408,7 +428,7 @@ ExphPlan exph_plan(const uint16_t* in, uint64_t n) {
   }
   require(total < (uint64_t(1) << 32) - 64, "exph: bitstream exceeds 2^32 bits");
   p.chunk_bit[L.nchunks] = uint32_t(total);
-  L.off_bits = align16(n);
+  L.off_bits = align16(n / 32 * kExphRec);
   L.off_group = align16(L.off_bits + (total + 31) / 32 * 4 + 32);  // reader runs 32 B ahead
   L.off_chunk = align16(L.off_group + 4 * L.ngroups);
   L.off_base = align16(L.off_chunk + 2 * L.nchunks);
@@ -422,7 +442,7 @@ void exph_fill(const uint16_t* in, const ExphPlan& p, uint8_t* out) {
   std::fill(out, out + L.bytes, uint8_t(0));
   auto* words = reinterpret_cast<uint32_t*>(out + L.off_bits);
   parallel_blocks(L.nchunks, [&](uint64_t c) {
-    // the chunk's bits go to a local buffer (<= 128 x 20 bits); only its first
+    // the chunk's bits go to a local buffer (<= 256 x 20 bits); only its first
     // and last words can be shared with the neighbouring chunks
     const uint32_t base = p.base[c * kExphChunk / kExp4Block];
     const uint64_t start = p.chunk_bit[c];
@@ -438,13 +458,21 @@ void exph_fill(const uint16_t* in, const ExphPlan& p, uint8_t* out) {
         nb -= take;
       }
     };
-    for (uint64_t i = c * kExphChunk; i < (c + 1) * kExphChunk; ++i) {
-      const uint16_t v = in[i];
-      const uint32_t k = uint32_t(i - c * kExphChunk);
-      out[exph_sm_offset(c, k / 16, L.nchunks) + k % 16] = uint8_t(((v >> 8) & 0x80u) | (v & 0x7Fu));
-      const uint32_t sym = exph_sym(v, base);
-      put(p.code[sym], p.len[sym]);
-      if (sym == uint32_t(kExphEsc)) put((v >> 7) & 0xFFu, 8);
+    for (uint32_t q = 0; q < kExphChunk / 32; ++q) {
+      // residual record: u32 signs | 32 x 5 low mantissa bits, little-endian
+      uint64_t rec[3] = {0, 0, 0};
+      for (uint32_t j = 0; j < 32; ++j) {
+        const uint16_t v = in[c * kExphChunk + q * 32 + j];
+        rec[0] |= uint64_t((v >> 15) & 1u) << j;
+        const uint32_t bit = 32 + 5 * j;
+        const uint64_t m5 = v & 31u;
+        rec[bit / 64] |= m5 << (bit % 64);
+        if (bit % 64 > 59) rec[bit / 64 + 1] |= m5 >> (64 - bit % 64);
+        const uint32_t sym = exph_sym(v, base);
+        put(p.code[sym], p.len[sym]);
+        if (exph_is_esc(sym)) put((v >> 7) & 0xFFu, 8);
+      }
+      std::memcpy(out + exph_res_offset(c, q, L.nchunks), rec, kExphRec);
     }
     if (pos == (start & 31)) return;  // empty chunk (cannot happen: lengths >= 1)
     const uint64_t w0 = start >> 5;
@@ -463,10 +491,11 @@ void exph_fill(const uint16_t* in, const ExphPlan& p, uint8_t* out) {
     cb[c] = uint16_t(p.chunk_bit[c] - p.chunk_bit[c - c % kExphGroup]);
   }
   std::copy(p.base.begin(), p.base.end(), out + L.off_base);
-  // LUT entry per 12-bit window: len0 | sym0 << 4 | sym1 << 9 | (len0 + len1) << 14 |
-  // two << 19; "two" when a second non-escape code also fits inside the window
+  // LUT entry per 12-bit window: len0 | sym0 << 4 | sym1 << 11 | (len0 + len1) << 18 |
+  // two << 23; "two" when a second code also fits inside the window and neither
+  // of the two escapes
   std::vector<uint32_t> one(1u << kExphMaxLen, 0);
-  for (int sym = 0; sym < 32; ++sym) {
+  for (int sym = 0; sym < kExphSyms; ++sym) {
     const uint32_t l = p.len[sym];
     if (!l) continue;
     const uint32_t first = p.code[sym] << (kExphMaxLen - l);
@@ -476,12 +505,12 @@ void exph_fill(const uint16_t* in, const ExphPlan& p, uint8_t* out) {
   const uint32_t mask = (1u << kExphMaxLen) - 1;
   for (uint32_t w = 0; w <= mask; ++w) {
     uint32_t ent = one[w];
-    const uint32_t l0 = ent & 15u, s0 = (ent >> 4) & 31u;
-    if (l0 && l0 < uint32_t(kExphMaxLen) && s0 != uint32_t(kExphEsc)) {
+    const uint32_t l0 = ent & 15u, s0 = (ent >> 4) & 127u;
+    if (l0 && l0 < uint32_t(kExphMaxLen) && !exph_is_esc(s0)) {
       const uint32_t e1 = one[(w << l0) & mask];
-      const uint32_t l1 = e1 & 15u, s1 = (e1 >> 4) & 31u;
-      if (l1 && l0 + l1 <= uint32_t(kExphMaxLen) && s1 != uint32_t(kExphEsc))
-        ent |= (s1 << 9) | ((l0 + l1) << 14) | (1u << 19);
+      const uint32_t l1 = e1 & 15u, s1 = (e1 >> 4) & 127u;
+      if (l1 && l0 + l1 <= uint32_t(kExphMaxLen) && !exph_is_esc(s1))
+        ent |= (s1 << 11) | ((l0 + l1) << 18) | (1u << 23);
     }
     lut[w] = ent;
   }
@@ -496,20 +525,27 @@ void exph_unpack_host(const uint8_t* pack, const ExphLayout& L, uint16_t* out) {
   for (uint64_t c = 0; c < L.nchunks; ++c) {
     uint64_t q = uint64_t(gbit[c / kExphGroup]) + cbit[c];
     const uint32_t base = pack[L.off_base + c * kExphChunk / kExp4Block];
-    for (uint64_t i = c * kExphChunk; i < (c + 1) * kExphChunk; ++i) {
-      uint32_t peek = 0;
-      for (int k = 0; k < kExphMaxLen; ++k) peek = (peek << 1) | bit(q + k);
-      const uint32_t sym = (lut[peek] >> 4) & 31u, ln = lut[peek] & 15u;
-      q += ln;
-      uint32_t e = (base - sym) & 0xFFu;
-      if (sym == uint32_t(kExphEsc)) {
-        e = 0;
-        for (int k = 0; k < 8; ++k) e = (e << 1) | bit(q + k);
-        q += 8;
+    for (uint32_t g = 0; g < kExphChunk / 32; ++g) {
+      uint64_t rec[3];
+      std::memcpy(rec, pack + exph_res_offset(c, g, L.nchunks), kExphRec);
+      for (uint32_t j = 0; j < 32; ++j) {
+        uint32_t peek = 0;
+        for (int k = 0; k < kExphMaxLen; ++k) peek = (peek << 1) | bit(q + k);
+        const uint32_t sym = (lut[peek] >> 4) & 127u, ln = lut[peek] & 15u;
+        q += ln;
+        uint32_t e = (base - (sym >> 2)) & 0xFFu;
+        if (exph_is_esc(sym)) {
+          e = 0;
+          for (int k = 0; k < 8; ++k) e = (e << 1) | bit(q + k);
+          q += 8;
+        }
+        const uint32_t b = 32 + 5 * j;
+        uint64_t m5 = rec[b / 64] >> (b % 64);
+        if (b % 64 > 59) m5 |= rec[b / 64 + 1] << (64 - b % 64);
+        const uint32_t sign = uint32_t(rec[0] >> j) & 1u;
+        out[c * kExphChunk + g * 32 + j] =
+            uint16_t((sign << 15) | (e << 7) | ((sym & 3u) << 5) | uint32_t(m5 & 31u));
       }
-      const uint32_t k = uint32_t(i - c * kExphChunk);
-      const uint32_t smb = pack[exph_sm_offset(c, k / 16, L.nchunks) + k % 16];
-      out[i] = uint16_t(((smb & 0x80u) << 8) | (e << 7) | (smb & 0x7Fu));
     }
   }
 }

@@ -67,37 +67,43 @@ void exp4_unpack_host(const uint8_t* pack, uint64_t n, uint16_t* out);
 void launch_exp4_unpack(const uint8_t* pack, uint64_t n, uint16_t* out, cudaStream_t s);
 
 // ------------------------------------------------------------------ exph --
-// Entropy-coded exponents ("exph"): the same sign/mantissa bytes, and per value
-// a canonical Huffman code (<= 12 bits, one code table per matrix) of
+// Entropy-coded exponents ("exph"): per value a canonical Huffman code (<= 12
+// bits, one code table per matrix) of the symbol (dist, m2): dist =
 // min(base - exponent, 31) against the per-block base (the encoder may give
-// every block the matrix's base when that codes shorter); symbol 31 is
-// followed by the raw 8-bit exponent.  Codes are concatenated MSB-first per
-// 256-value chunk; a chunk's starting bit is a uint32 per group of 8 chunks
-// plus a uint16 offset inside the group (0.078 bits per value), so one GPU
-// thread decodes one chunk through a 4096-entry lookup table in shared memory.
-// ~10.7 bits per value for Gaussian bf16 weights (entropy 10.46).
+// every block the matrix's base when that codes shorter), m2 the top two
+// mantissa bits -- a Gaussian weight's mantissa is not uniform inside its
+// binade, so coding them jointly with the exponent saves ~0.07 bits per value;
+// dist 31 escapes: the raw 8-bit exponent follows the code.  The sign and the
+// low five mantissa bits (6 bits) are stored raw.  Codes are concatenated
+// MSB-first per 256-value chunk; a chunk's starting bit is a uint32 per group
+// of 8 chunks plus a uint16 offset inside the group (0.078 bits per value), so
+// one GPU thread decodes one chunk through a 4096-entry lookup table in shared
+// memory.  ~10.6 bits per value for Gaussian bf16 weights (entropy 10.46).
 //
-// Layout: [0, n) sign/mantissa (lane-interleaved, exph_sm_offset) | [off_bits) bitstream (uint32 words, + 8 B
-// slack) | [off_group) uint32 start bit per group | [off_chunk) uint16 offset
-// per chunk | [off_base) base per block | [off_lut) uint32 LUT[4096] = len0 |
-// sym0 << 4 | sym1 << 9 | (len0 + len1) << 14 | two << 19 (the decoder takes two
-// values per lookup when both codes fit in the 12-bit window)
+// Layout: [0, 3n/4) raw 6-bit residuals (exph_res_offset) | [off_bits)
+// bitstream (uint32 words, + 32 B slack) | [off_group) uint32 start bit per
+// group | [off_chunk) uint16 offset per chunk | [off_base) base per block |
+// [off_lut) uint32 LUT[4096] = len0 | sym0 << 4 | sym1 << 11 | (len0 + len1) << 18 |
+// two << 23 (the decoder takes two values per lookup when both codes fit in the
+// 12-bit window and neither escapes)
 constexpr int kExphChunk = 256;
 constexpr int kExphWarpChunks = 32;  // chunks decoded together by one warp (one per lane)
+constexpr int kExphSyms = 128;       // (dist, m2)
+constexpr int kExphRec = 24;         // residual record of 32 values: u32 signs | 5 x u32 (32 x 5 bits)
 
-// byte offset of the 16 sign/mantissa bytes of chunk c's 16-value group q: the
-// chunks of a warp group are interleaved per 16-byte group, so one warp-wide
-// load of group q reads contiguous memory
-__host__ __device__ inline uint64_t exph_sm_offset(uint64_t c, uint32_t q, uint64_t nchunks) {
+// byte offset of the residual record of chunk c's 32-value group q: the chunks
+// of a warp group are interleaved per record, so one warp-wide load of group q
+// reads contiguous memory
+__host__ __device__ inline uint64_t exph_res_offset(uint64_t c, uint32_t q, uint64_t nchunks) {
   const uint64_t g = c / kExphWarpChunks, lane = c % kExphWarpChunks;
   const uint64_t first = g * kExphWarpChunks;
   const uint64_t nch = (nchunks - first) < uint64_t(kExphWarpChunks) ? (nchunks - first)
                                                                       : uint64_t(kExphWarpChunks);
-  return first * kExphChunk + uint64_t(q) * nch * 16 + lane * 16;
+  return first * (kExphChunk / 32) * kExphRec + uint64_t(q) * nch * kExphRec + lane * kExphRec;
 }
 constexpr int kExphGroup = 8;  // chunks per group (8 x 256 x 20 bits < 2^16: uint16 offsets)
 constexpr int kExphMaxLen = 12;
-constexpr int kExphEsc = 31;
+constexpr int kExphEsc = 31;   // dist of the escape symbols (sym >> 2 == 31)
 
 struct ExphLayout {
   uint64_t n = 0, nblocks = 0, nchunks = 0, ngroups = 0;
@@ -106,8 +112,8 @@ struct ExphLayout {
 struct ExphPlan {
   ExphLayout L;
   std::vector<uint8_t> base;
-  uint8_t len[32] = {};
-  uint32_t code[32] = {};
+  uint8_t len[kExphSyms] = {};
+  uint32_t code[kExphSyms] = {};
   std::vector<uint32_t> chunk_bit;  // [nchunks + 1]
 };
 ExphPlan exph_plan(const uint16_t* in, uint64_t n);

@@ -29,9 +29,10 @@ def test_host_roundtrip_rejects_bad_sizes():
 
 
 def test_exph_length_limit_fibonacci_histogram():
-    """Fibonacci symbol counts give the deepest Huffman tree (a 30-bit code
-    for 31 symbols); the encoder must clamp to 12 bits and keep the code
-    prefix-free, so the round trip stays exact."""
+    """Exponent distances with Fibonacci counts (each spread over the four top
+    mantissa pairs) give a Huffman tree far deeper than 12 bits; the encoder's
+    length-limited code (package-merge) must stay prefix-free and complete, so
+    the round trip is exact."""
     rng = np.random.default_rng(5)
     fib = [1, 1]
     while len(fib) < 31:
@@ -44,3 +45,15 @@ def test_exph_length_limit_fibonacci_histogram():
         (rng.integers(0, 2, n, dtype=np.uint16) << 15)
     out, nb = im.codec_roundtrip_host(a, "exph")
     assert np.array_equal(out, a)
+
+
+def test_exph_gaussian_weights_bits():
+    """SURVEY 8(d) weights (GaussianStream x d^-1/2, bf16): the (dist, m2) code
+    with package-merge lengths takes 10.61 bits per value (the exponent-only
+    code: 10.67; i.i.d. entropy of the bf16 values: 10.46)."""
+    n = 10240 * 4096  # one expert matrix (the per-matrix tables amortised as in use)
+    w = im.gaussian_bf16(im.derive_seed(20261018, 1000), n, 4096 ** -0.5)
+    out, nb = im.codec_roundtrip_host(w, "exph")
+    assert np.array_equal(out, w)
+    bits = 8.0 * nb / n
+    assert 10.5 < bits < 10.62, bits
