@@ -1187,12 +1187,13 @@ def main() -> None:
                     "sign/mantissa byte and a 4-bit exponent code per value against a "
                     "per-32768-value base, exceptions listed -- decoded on the GPU before "
                     "each expert's FFN; outputs bit-identical to the raw stream)",
-            "exph": "exph (lossless: the same bf16 weights packed once on the host -- a "
-                    "sign/mantissa byte and a canonical Huffman code (<= 12 bits, one table "
-                    "per matrix) of the exponent's distance to a per-32768-value or matrix-wide "
-                    "base (whichever codes shorter), 256-value chunks with recorded start bits "
-                    "-- decoded on the GPU before each expert's FFN, the last expert's W_in "
-                    "while its W_out is on the link; outputs bit-identical to the raw stream)"}
+            "exph": "exph (lossless: the same bf16 weights packed once on the host -- per "
+                    "value a canonical Huffman code (<= 12 bits, one table per matrix) of "
+                    "(exponent distance to a per-32768-value or matrix-wide base, top two "
+                    "mantissa bits) plus the raw sign and low five mantissa bits, 256-value "
+                    "chunks with recorded start bits, 256-byte aligned pack parts -- decoded "
+                    "on the GPU before each expert's FFN, the last expert's W_in while its "
+                    "W_out is on the link; outputs bit-identical to the raw stream)"}
         line["h2d"] = {
             "codec": codec_desc[args.h2d_codec],
             "achieved_gbs": link_bytes / (t_ex * 1e-3) / 1e9, "peak_gbs": h2d_peak,

@@ -357,11 +357,13 @@ typedef struct {
    * pinned exp4 packs -- 12 bits per value, exponents coded against a per-block
    * base -- shared by every layer on the same host weights; each load copies
    * the pack and a decoder kernel restores the bf16 slot bit for bit before the
-   * FFN).  INFMOE_CODEC_EXPH codes the exponent's distance to its block base
-   * with a per-matrix canonical Huffman code (<= 12 bits) instead: 256-value
-   * chunks with recorded start bits, decoded one warp per 32 chunks (one lane
-   * per chunk) through a shared-memory table, sign/mantissa bytes
-   * lane-interleaved; ~10.3-10.7 bits per value (uniform / Gaussian weights).
+   * FFN).  INFMOE_CODEC_EXPH instead codes each value's (exponent distance
+   * to its block or matrix base, top two mantissa bits) with a per-matrix
+   * canonical Huffman code (<= 12 bits, length-limited optimally) and stores
+   * the sign and low five mantissa bits raw: 256-value chunks with recorded
+   * start bits, decoded one warp per 32 chunks (one lane per chunk) through a
+   * shared-memory table; ~10.1-10.9 bits per value (uniform .. Laplace
+   * weights; 10.61 on Gaussian).
    * Packs are SNAPSHOTS of the host weights taken at create and at every
    * infmoe_layer_set_host_weights call (which always re-packs); layers created
    * on the same host buffers share one pack only while its content digest
