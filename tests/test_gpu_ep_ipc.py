@@ -1,11 +1,11 @@
-"""The PEER expert-parallel transport across PROCESSES: two ranks are two
+"""The PEER expert-parallel transport across PROCESSES: P = 2 or 4 ranks are P
 processes on one GPU, so every peer buffer (received rows, return addresses,
 results, counts, barrier flags) is a real CUDA-IPC mapping (cudaIpcGetMemHandle
 / cudaIpcOpenMemHandle in Layer::peer_setup), exchanged through the
 process-shared stand-in collectives of tests/loopback_nccl/ipc_nccl.cpp (host
 barriers in /dev/shm: no kernel waits on another process's kernel; the layer's
-barriers use its NCCL path, INFMOE_EP_BARRIER=nccl).  The two halves of the
-output must equal the one-GPU layer on the whole batch bit for bit."""
+barriers use its NCCL path, INFMOE_EP_BARRIER=nccl).  The ranks' slices of
+the output must equal the one-GPU layer on the whole batch bit for bit."""
 import os
 import subprocess
 import sys
@@ -24,7 +24,7 @@ import paper_2106_10715_b200 as im
 from paper_2106_10715_b200 import device as dv
 cuda = torch.device("cuda:0")
 k, gate, offloaded = {k}, "{gate}", {offloaded}
-N, d, f, E, P = 768, 256, 384, 8, 2
+N, d, f, E, P = 768, 256, 384, 8, {P}
 g = torch.Generator().manual_seed(3)
 x = torch.randn(N, d, generator=g).to(torch.bfloat16).to(cuda)
 wi = (torch.randn(E, f, d, generator=g) / d ** 0.5).to(torch.bfloat16)
@@ -72,15 +72,17 @@ def ipc_lib(tmp_path_factory):
     return so
 
 
-@pytest.mark.parametrize("k,gate,offloaded", [(1, "lsh", False), (2, "softmax", False),
-                                              (1, "lsh", True)])
-def test_peer_transport_across_processes(ipc_lib, tmp_path, k, gate, offloaded):
+@pytest.mark.parametrize("P,k,gate,offloaded", [(2, 1, "lsh", False), (2, 2, "softmax", False),
+                                                (2, 1, "lsh", True), (4, 2, "softmax", False),
+                                                (4, 1, "lsh", True)])
+def test_peer_transport_across_processes(ipc_lib, tmp_path, P, k, gate, offloaded):
     uid = os.urandom(128).hex()
     env = dict(os.environ, INFMOE_NCCL_LIB=str(ipc_lib), INFMOE_EP_BARRIER="nccl")
-    code = RANK.format(root=ROOT, k=k, gate=gate, offloaded=offloaded, uid=uid, out=tmp_path)
+    code = RANK.format(root=ROOT, P=P, k=k, gate=gate, offloaded=offloaded, uid=uid,
+                       out=tmp_path)
     procs = [subprocess.Popen([sys.executable, "-c", code, str(r)], env=env,
                               stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)
-             for r in range(2)]
+             for r in range(P)]
     outs = []
     for p in procs:
         try:
@@ -91,7 +93,7 @@ def test_peer_transport_across_processes(ipc_lib, tmp_path, k, gate, offloaded):
             raise
     for p, (o, e) in zip(procs, outs):
         assert p.returncode == 0 and "rank ok" in o, o[-2000:] + e[-4000:]
-    r = subprocess.run([sys.executable, "-c", REF.format(root=ROOT, k=k, gate=gate,
+    r = subprocess.run([sys.executable, "-c", REF.format(root=ROOT, P=P, k=k, gate=gate,
                                                          offloaded=offloaded, out=tmp_path)],
                        capture_output=True, text=True, timeout=240)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
