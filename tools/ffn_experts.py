@@ -4,6 +4,7 @@ rows each (the per-rank shape of the C4 expert-parallel stack at P = 8 / 4 / 2
 back-to-back launches after an L2 flush) and algorithmic HBM GB/s (weights
 once + x_perm + H write/read + y) against MEASURED_PEAKS.json (dev tool)."""
 import json
+import os
 import sys
 from pathlib import Path
 
@@ -21,21 +22,22 @@ peak = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"] \
     if (ROOT / "MEASURED_PEAKS.json").exists() else 6549.1
 flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 g = torch.Generator(device="cpu").manual_seed(1)
-for E in (4, 8, 16, 32):
+for E in [int(v) for v in sys.argv[1:]] or (4, 8, 16, 32):
     counts = [rows + (e % 3) * 7 - 7 for e in range(E)]
     R = sum(counts)
     offs = torch.tensor(np.concatenate([[0], np.cumsum(counts)]), dtype=torch.int32, device=dev)
     x = torch.randn(R, d, generator=g).to(torch.bfloat16).to(dev)
     wi = (torch.randn(E, f, d, generator=g) / d ** 0.5).to(torch.bfloat16).to(dev)
     wo = (torch.randn(E, d, f, generator=g) / f ** 0.5).to(torch.bfloat16).to(dev)
+    kw = {}
     for _ in range(3):
-        dv.expert_ffn_fused(x, offs, wi, wo)
+        dv.expert_ffn_fused(x, offs, wi, wo, **kw)
     ts = []
     for _ in range(20):
         flush.zero_()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        dv.expert_ffn_fused(x, offs, wi, wo)
+        dv.expert_ffn_fused(x, offs, wi, wo, **kw)
         b.record()
         b.synchronize()
         ts.append(a.elapsed_time(b) * 1e-3)
