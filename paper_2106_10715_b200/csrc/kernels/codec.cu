@@ -215,34 +215,43 @@ void canonical_codes(const uint8_t* len, uint32_t* code) {
   }
 }
 
-// bits [bit, bit + 5) of the 192-bit little-endian residual record (A, B, C)
-__device__ __forceinline__ uint32_t rec5(uint64_t A, uint64_t B, uint64_t C, int bit) {
-  if (bit + 5 <= 64) return uint32_t(A >> bit) & 31u;
-  if (bit < 64) return uint32_t((A >> bit) | (B << (64 - bit))) & 31u;
-  if (bit + 5 <= 128) return uint32_t(B >> (bit - 64)) & 31u;
-  if (bit < 128) return uint32_t((B >> (bit - 64)) | (C << (128 - bit))) & 31u;
-  return uint32_t(C >> (bit - 128)) & 31u;
+// bits [bit, bit + 12) of the 192-bit little-endian residual record (A, B, C)
+__device__ __forceinline__ uint32_t rec12(uint64_t A, uint64_t B, uint64_t C, int bit) {
+  if (bit + 12 <= 64) return uint32_t(A >> bit) & 0xFFFu;
+  if (bit < 64) return uint32_t((A >> bit) | (B << (64 - bit))) & 0xFFFu;
+  if (bit + 12 <= 128) return uint32_t(B >> (bit - 64)) & 0xFFFu;
+  if (bit < 128) return uint32_t((B >> (bit - 64)) | (C << (128 - bit))) & 0xFFFu;
+  return uint32_t(C >> (bit - 128)) & 0xFFFu;
+}
+
+// a pair field s1 | m5_1 | s0 | m5_0 spread onto two bf16 values' sign and low
+// mantissa bits
+__device__ __forceinline__ uint32_t pair_resid(uint32_t f) {
+  return (f & 0x1Fu) | ((f << 10) & 0x1F8000u) | ((f << 20) & 0x80000000u);
 }
 
 // One warp decodes 32 consecutive chunks, one per lane (Huffman codes are
-// sequential within a chunk).  The 6-bit residuals are stored as 24-byte
-// records per 32 values, lane-interleaved (exph_res_offset), so each record
-// load is one contiguous 768-byte warp access; each quarter of a lane's 512
-// output bytes is staged in shared memory (16-byte slots XOR-swizzled by row)
-// and written back as full 128-byte lines.  Only the bitstream refills stay
+// sequential within a chunk).  The residuals are stored as 24-byte records per
+// 32 values, lane-interleaved (exph_res_offset), so each record load is one
+// contiguous 768-byte warp access.  A table lookup yields, for two short codes,
+// both values' exponent and top mantissa bits as 16-bit offsets from the
+// block base (one packed add); a 12-bit pair field then supplies both values'
+// signs and low mantissa bits.  Each group's 64 output bytes per lane are
+// staged in shared memory (16-byte slots XOR-swizzled by row) and written
+// back row by row as whole 32-byte sectors.  Only the bitstream refills stay
 // per lane (one word ahead).
 constexpr int kExphWarps = 8;
 __global__ void __launch_bounds__(kExphWarps * 32) exph_unpack_kernel(const uint8_t* __restrict__ pack,
                                                                       ExphLayout L,
                                                                       uint16_t* __restrict__ out) {
-  __shared__ uint32_t lut[1 << kExphMaxLen];
-  extern __shared__ uint4 stage[];  // [kExphWarps][kExphWarpChunks * 8]: 4 KB per warp
+  __shared__ uint2 lut[1 << kExphMaxLen];
+  extern __shared__ uint4 stage[];  // [kExphWarps][kExphWarpChunks * 4]: 2 KB per warp
   const auto* glut = reinterpret_cast<const uint4*>(pack + L.off_lut);
-  for (int i = threadIdx.x; i < (1 << kExphMaxLen) / 4; i += blockDim.x)
+  for (int i = threadIdx.x; i < (1 << kExphMaxLen) / 2; i += blockDim.x)
     reinterpret_cast<uint4*>(lut)[i] = __ldg(glut + i);
   __syncthreads();
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  uint4* st = stage + warp * (kExphWarpChunks * 8);
+  uint4* st = stage + warp * (kExphWarpChunks * 4);
   const auto* bw = reinterpret_cast<const uint32_t*>(pack + L.off_bits);
   const auto* gbit = reinterpret_cast<const uint32_t*>(pack + L.off_group);
   const auto* cbit = reinterpret_cast<const uint16_t*>(pack + L.off_chunk);
@@ -255,39 +264,35 @@ __global__ void __launch_bounds__(kExphWarps * 32) exph_unpack_kernel(const uint
     if (lane < nch) {
       const uint64_t c = c0 + lane;
       const uint64_t v0 = c * kExphChunk;
-      const uint32_t base = pack[L.off_base + v0 / kExp4Block];
+      // table offsets carry a +4096 bias (positive halves: no carry between them)
+      const uint32_t base7 = uint32_t(pack[L.off_base + v0 / kExp4Block]) << 7;
+      const uint32_t base7b = base7 - kExphOffBias;  // mod 2^32
+      const uint32_t base7x2b = (base7 | (base7 << 16)) - (kExphOffBias | (kExphOffBias << 16));
       const uint32_t p = __ldg(gbit + c / kExphGroup) + __ldg(cbit + c);
       const uint32_t* wp = bw + (p >> 5);
       uint64_t buf = ((uint64_t(__ldg(wp)) << 32) | __ldg(wp + 1)) << (p & 31);
       int nbits = 64 - int(p & 31);
       wp += 2;
       uint32_t nw = __ldg(wp);
-      auto take = [&]() -> uint32_t {
-        const uint32_t w = nw;
-        nw = __ldg(++wp);
-        return w;
-      };
       auto refill = [&]() {
         if (nbits < 32) {
-          buf |= uint64_t(take()) << (32 - nbits);
+          buf |= uint64_t(nw) << (32 - nbits);
           nbits += 32;
+          nw = __ldg(++wp);
         }
       };
-      // exponent << 7 | m2 << 5 of one value from its LUT entry (escape: the raw
-      // exponent follows the code)
-      auto one = [&](uint32_t ent) -> uint32_t {
-        const uint32_t sym = (ent >> 4) & 127u, ln = ent & 15u;
+      // exponent << 7 | m2 << 5 of one value (escape: the raw exponent follows)
+      auto one = [&](uint2 ent) -> uint32_t {
+        const uint32_t sym = (ent.x >> 4) & 127u, ln = ent.x & 15u;
         buf <<= ln;
         nbits -= int(ln);
-        uint32_t e;
         if ((sym >> 2) == uint32_t(kExphEsc)) {
-          e = uint32_t(buf >> 56);
+          const uint32_t e = uint32_t(buf >> 56);
           buf <<= 8;
           nbits -= 8;
-        } else {
-          e = (base - (sym >> 2)) & 0xFFu;
+          return (e << 7) | ((sym & 3u) << 5);
         }
-        return (e << 7) | ((sym & 3u) << 5);
+        return (base7b + (ent.y & 0xFFFFu)) & 0xFFFFu;
       };
       const uint64_t* rec = reinterpret_cast<const uint64_t*>(
           pack + c0 * (kExphChunk / 32) * kExphRec + uint64_t(lane) * kExphRec);
@@ -306,40 +311,33 @@ __global__ void __launch_bounds__(kExphWarps * 32) exph_unpack_kernel(const uint
 #pragma unroll
         for (int jp = 0; jp < 16; ++jp) {  // values in pairs: one table lookup per pair
           refill();
-          const uint32_t ent = lut[uint32_t(buf >> (64 - kExphMaxLen))];
-          uint32_t h0, h1;  // exponent << 7 | m2 << 5
-          if (ent & (1u << 23)) {  // both codes inside the 12-bit window, no escape
-            const uint32_t ln = (ent >> 18) & 31u;
+          const uint2 ent = lut[uint32_t(buf >> (64 - kExphMaxLen))];
+          uint32_t hp;  // both values' exponent and top mantissa bits
+          if (ent.x & (1u << 16)) {
+            const uint32_t ln = (ent.x >> 11) & 31u;
             buf <<= ln;
             nbits -= int(ln);
-            const uint32_t s0 = (ent >> 4) & 127u, s1 = (ent >> 11) & 127u;
-            h0 = (((base - (s0 >> 2)) & 0xFFu) << 7) | ((s0 & 3u) << 5);
-            h1 = (((base - (s1 >> 2)) & 0xFFu) << 7) | ((s1 & 3u) << 5);
+            hp = base7x2b + ent.y;  // each half ends in [0, 2^15): exact per half
           } else {  // a long code or an escape: the two values one at a time
-            h0 = one(ent);
+            const uint32_t h0 = one(ent);
             refill();
-            h1 = one(lut[uint32_t(buf >> (64 - kExphMaxLen))]);
+            hp = h0 | (one(lut[uint32_t(buf >> (64 - kExphMaxLen))]) << 16);
           }
-          const int i0 = 2 * jp, i1 = 2 * jp + 1;
-          const uint32_t v0b = ((uint32_t(A >> i0) & 1u) << 15) | h0 | rec5(A, B, C, 32 + 5 * i0);
-          const uint32_t v1b = ((uint32_t(A >> i1) & 1u) << 15) | h1 | rec5(A, B, C, 32 + 5 * i1);
-          r[jp] = v0b | (v1b << 16);
+          r[jp] = hp | pair_resid(rec12(A, B, C, 12 * jp));
         }
-        // row = lane (the current quarter of its chunk: 8 16-byte slots), swizzled
-        const int sl = 4 * (q % 2);
+        // row = lane (this group's 64 output bytes: 4 16-byte slots), swizzled;
+        // the warp then stores every row's 64 bytes (two full 32-byte sectors)
 #pragma unroll
         for (int t = 0; t < 4; ++t)
-          st[lane * 8 + ((sl + t) ^ (lane & 7))] =
+          st[lane * 4 + (t ^ (lane & 3))] =
               make_uint4(r[4 * t], r[4 * t + 1], r[4 * t + 2], r[4 * t + 3]);
-        if (q % 2 == 1) {  // flush this quarter: full 128-byte lines per warp store
-          __syncwarp(active);
-          uint4* dst = reinterpret_cast<uint4*>(out + c0 * kExphChunk);
-          for (int u = lane; u < nch * 8; u += nch) {
-            const int row = u / 8, slot = u % 8;
-            dst[row * (kExphChunk / 8) + (q / 2) * 8 + slot] = st[row * 8 + (slot ^ (row & 7))];
-          }
-          __syncwarp(active);
+        __syncwarp(active);
+        uint4* dst = reinterpret_cast<uint4*>(out + c0 * kExphChunk);
+        for (int u = lane; u < nch * 4; u += nch) {
+          const int row = u / 4, slot = u % 4;
+          dst[row * (kExphChunk / 8) + q * 4 + slot] = st[row * 4 + (slot ^ (row & 3))];
         }
+        __syncwarp(active);
       }
     }
     __syncwarp();  // every lane is done with st before the next group reuses it
@@ -433,7 +431,7 @@ ExphPlan exph_plan(const uint16_t* in, uint64_t n) {
   L.off_chunk = align16(L.off_group + 4 * L.ngroups);
   L.off_base = align16(L.off_chunk + 2 * L.nchunks);
   L.off_lut = align16(L.off_base + L.nblocks);
-  L.bytes = align16(L.off_lut + 4 * (1 << kExphMaxLen));
+  L.bytes = align16(L.off_lut + 8 * (1 << kExphMaxLen));
   return p;
 }
 
@@ -459,15 +457,14 @@ void exph_fill(const uint16_t* in, const ExphPlan& p, uint8_t* out) {
       }
     };
     for (uint32_t q = 0; q < kExphChunk / 32; ++q) {
-      // residual record: u32 signs | 32 x 5 low mantissa bits, little-endian
+      // residual record: 16 pair fields s1 | m5_1 | s0 | m5_0 of 12 bits, little-endian
       uint64_t rec[3] = {0, 0, 0};
       for (uint32_t j = 0; j < 32; ++j) {
         const uint16_t v = in[c * kExphChunk + q * 32 + j];
-        rec[0] |= uint64_t((v >> 15) & 1u) << j;
-        const uint32_t bit = 32 + 5 * j;
-        const uint64_t m5 = v & 31u;
-        rec[bit / 64] |= m5 << (bit % 64);
-        if (bit % 64 > 59) rec[bit / 64 + 1] |= m5 >> (64 - bit % 64);
+        const uint64_t six = ((v >> 10) & 0x20u) | (v & 31u);  // sign << 5 | m5
+        const uint32_t bit = 12 * (j / 2) + 6 * (j % 2);
+        rec[bit / 64] |= six << (bit % 64);
+        if (bit % 64 > 58) rec[bit / 64 + 1] |= six >> (64 - bit % 64);
         const uint32_t sym = exph_sym(v, base);
         put(p.code[sym], p.len[sym]);
         if (exph_is_esc(sym)) put((v >> 7) & 0xFFu, 8);
@@ -491,9 +488,9 @@ void exph_fill(const uint16_t* in, const ExphPlan& p, uint8_t* out) {
     cb[c] = uint16_t(p.chunk_bit[c] - p.chunk_bit[c - c % kExphGroup]);
   }
   std::copy(p.base.begin(), p.base.end(), out + L.off_base);
-  // LUT entry per 12-bit window: len0 | sym0 << 4 | sym1 << 11 | (len0 + len1) << 18 |
-  // two << 23; "two" when a second code also fits inside the window and neither
-  // of the two escapes
+  // LUT entry per 12-bit window (uint2): .x = len0 | sym0 << 4 | (len0 + len1) << 11 |
+  // two << 16, .y = off(sym0) | off(sym1) << 16, off = (m2 << 5) - (dist << 7) + 4096;
+  // "two" when a second code also fits inside the window and neither escapes
   std::vector<uint32_t> one(1u << kExphMaxLen, 0);
   for (int sym = 0; sym < kExphSyms; ++sym) {
     const uint32_t l = p.len[sym];
@@ -501,18 +498,25 @@ void exph_fill(const uint16_t* in, const ExphPlan& p, uint8_t* out) {
     const uint32_t first = p.code[sym] << (kExphMaxLen - l);
     for (uint32_t s = 0; s < (1u << (kExphMaxLen - l)); ++s) one[first | s] = (uint32_t(sym) << 4) | l;
   }
+  auto off = [](uint32_t sym) {  // biased: >= 256 for every non-escape symbol
+    return (((sym & 3u) << 5) - ((sym >> 2) << 7) + uint32_t(kExphOffBias)) & 0xFFFFu;
+  };
   auto* lut = reinterpret_cast<uint32_t*>(out + L.off_lut);
   const uint32_t mask = (1u << kExphMaxLen) - 1;
   for (uint32_t w = 0; w <= mask; ++w) {
-    uint32_t ent = one[w];
-    const uint32_t l0 = ent & 15u, s0 = (ent >> 4) & 127u;
+    const uint32_t e0 = one[w];
+    const uint32_t l0 = e0 & 15u, s0 = (e0 >> 4) & 127u;
+    uint32_t x = e0, y = l0 ? off(s0) : 0u;
     if (l0 && l0 < uint32_t(kExphMaxLen) && !exph_is_esc(s0)) {
       const uint32_t e1 = one[(w << l0) & mask];
       const uint32_t l1 = e1 & 15u, s1 = (e1 >> 4) & 127u;
-      if (l1 && l0 + l1 <= uint32_t(kExphMaxLen) && !exph_is_esc(s1))
-        ent |= (s1 << 11) | ((l0 + l1) << 18) | (1u << 23);
+      if (l1 && l0 + l1 <= uint32_t(kExphMaxLen) && !exph_is_esc(s1)) {
+        x |= ((l0 + l1) << 11) | (1u << 16);
+        y |= off(s1) << 16;
+      }
     }
-    lut[w] = ent;
+    lut[2 * w] = x;
+    lut[2 * w + 1] = y;
   }
 }
 
@@ -531,7 +535,7 @@ void exph_unpack_host(const uint8_t* pack, const ExphLayout& L, uint16_t* out) {
       for (uint32_t j = 0; j < 32; ++j) {
         uint32_t peek = 0;
         for (int k = 0; k < kExphMaxLen; ++k) peek = (peek << 1) | bit(q + k);
-        const uint32_t sym = (lut[peek] >> 4) & 127u, ln = lut[peek] & 15u;
+        const uint32_t sym = (lut[2 * peek] >> 4) & 127u, ln = lut[2 * peek] & 15u;
         q += ln;
         uint32_t e = (base - (sym >> 2)) & 0xFFu;
         if (exph_is_esc(sym)) {
@@ -539,12 +543,11 @@ void exph_unpack_host(const uint8_t* pack, const ExphLayout& L, uint16_t* out) {
           for (int k = 0; k < 8; ++k) e = (e << 1) | bit(q + k);
           q += 8;
         }
-        const uint32_t b = 32 + 5 * j;
-        uint64_t m5 = rec[b / 64] >> (b % 64);
-        if (b % 64 > 59) m5 |= rec[b / 64 + 1] << (64 - b % 64);
-        const uint32_t sign = uint32_t(rec[0] >> j) & 1u;
-        out[c * kExphChunk + g * 32 + j] =
-            uint16_t((sign << 15) | (e << 7) | ((sym & 3u) << 5) | uint32_t(m5 & 31u));
+        const uint32_t b = 12 * (j / 2) + 6 * (j % 2);
+        uint64_t six = rec[b / 64] >> (b % 64);
+        if (b % 64 > 58) six |= rec[b / 64 + 1] << (64 - b % 64);
+        out[c * kExphChunk + g * 32 + j] = uint16_t(((six & 0x20u) << 10) | (e << 7) |
+                                                    ((sym & 3u) << 5) | uint32_t(six & 31u));
       }
     }
   }
@@ -553,8 +556,8 @@ void exph_unpack_host(const uint8_t* pack, const ExphLayout& L, uint16_t* out) {
 void launch_exph_unpack(const uint8_t* pack, const ExphLayout& L, uint16_t* out, cudaStream_t s) {
   const uint64_t groups = (L.nchunks + kExphWarpChunks - 1) / kExphWarpChunks;
   const uint64_t want = (groups + kExphWarps - 1) / kExphWarps;
-  const uint64_t cap = uint64_t(device_sm_count()) * 4;  // 4 CTAs (48 KB smem each) per SM
-  constexpr int kStage = kExphWarps * kExphWarpChunks * 8 * 16;
+  const uint64_t cap = uint64_t(device_sm_count()) * 4;  // 4 CTAs (32 KB LUT + 16 KB staging) per SM
+  constexpr int kStage = kExphWarps * kExphWarpChunks * 4 * 16;
   ensure_dyn_smem(reinterpret_cast<const void*>(exph_unpack_kernel), size_t(kStage));
   exph_unpack_kernel<<<unsigned(std::max<uint64_t>(std::min(want, cap), 1)), kExphWarps * 32,
                        kStage, s>>>(pack, L, out);

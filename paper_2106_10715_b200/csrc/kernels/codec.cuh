@@ -74,22 +74,26 @@ void launch_exp4_unpack(const uint8_t* pack, uint64_t n, uint16_t* out, cudaStre
 // mantissa bits -- a Gaussian weight's mantissa is not uniform inside its
 // binade, so coding them jointly with the exponent saves ~0.07 bits per value;
 // dist 31 escapes: the raw 8-bit exponent follows the code.  The sign and the
-// low five mantissa bits (6 bits) are stored raw.  Codes are concatenated
+// low five mantissa bits (6 bits) are stored raw, two values per 12-bit field.  Codes are concatenated
 // MSB-first per 256-value chunk; a chunk's starting bit is a uint32 per group
 // of 8 chunks plus a uint16 offset inside the group (0.078 bits per value), so
 // one GPU thread decodes one chunk through a 4096-entry lookup table in shared
 // memory.  ~10.6 bits per value for Gaussian bf16 weights (entropy 10.46).
 //
-// Layout: [0, 3n/4) raw 6-bit residuals (exph_res_offset) | [off_bits)
-// bitstream (uint32 words, + 32 B slack) | [off_group) uint32 start bit per
-// group | [off_chunk) uint16 offset per chunk | [off_base) base per block |
-// [off_lut) uint32 LUT[4096] = len0 | sym0 << 4 | sym1 << 11 | (len0 + len1) << 18 |
-// two << 23 (the decoder takes two values per lookup when both codes fit in the
-// 12-bit window and neither escapes)
+// Layout: [0, 3n/4) raw residuals (exph_res_offset; per 32 values 16 pair
+// fields of 12 bits = s1 << 11 | m5_1 << 6 | s0 << 5 | m5_0, little-endian) |
+// [off_bits) bitstream (uint32 words, + 32 B slack) | [off_group) uint32 start
+// bit per group | [off_chunk) uint16 offset per chunk | [off_base) base per
+// block | [off_lut) uint2 LUT[4096]: .x = len0 | sym0 << 4 | (len0 + len1) << 11 |
+// two << 16, .y = off0 | off1 << 16 with off = (m2 << 5) - (dist << 7) + 4096, so
+// (base << 7) - 4096 + off is a value's exponent and top mantissa bits (positive
+// 16-bit halves: one 32-bit add decodes a pair); "two" when both
+// codes fit in the 12-bit window and neither escapes (one packed add then
+// yields both values)
 constexpr int kExphChunk = 256;
 constexpr int kExphWarpChunks = 32;  // chunks decoded together by one warp (one per lane)
 constexpr int kExphSyms = 128;       // (dist, m2)
-constexpr int kExphRec = 24;         // residual record of 32 values: u32 signs | 5 x u32 (32 x 5 bits)
+constexpr int kExphRec = 24;         // residual record of 32 values: 16 pair fields of 12 bits
 
 // byte offset of the residual record of chunk c's 32-value group q: the chunks
 // of a warp group are interleaved per record, so one warp-wide load of group q
@@ -104,6 +108,7 @@ __host__ __device__ inline uint64_t exph_res_offset(uint64_t c, uint32_t q, uint
 constexpr int kExphGroup = 8;  // chunks per group (8 x 256 x 20 bits < 2^16: uint16 offsets)
 constexpr int kExphMaxLen = 12;
 constexpr int kExphEsc = 31;   // dist of the escape symbols (sym >> 2 == 31)
+constexpr uint32_t kExphOffBias = 4096;  // keeps the table's exponent offsets positive
 
 struct ExphLayout {
   uint64_t n = 0, nblocks = 0, nchunks = 0, ngroups = 0;

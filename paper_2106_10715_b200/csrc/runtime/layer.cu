@@ -1109,7 +1109,7 @@ std::string g_pack_dir = [] {
   return std::string(e ? e : "");
 }();
 constexpr char kPackMagic[8] = {'I', 'N', 'F', 'M', 'O', 'E', 'P', 'K'};
-constexpr uint32_t kPackVersion = 3;  // 2: 256-byte aligned pack parts; 3: exph (dist, m2) symbols
+constexpr uint32_t kPackVersion = 4;  // 2: 256-byte aligned pack parts; 3: exph (dist, m2) symbols; 4: pair residuals, 64-bit LUT
 
 uint64_t pack_checksum(const uint8_t* p, uint64_t bytes) {
   // both halves (and an odd last byte)
