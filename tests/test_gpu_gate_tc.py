@@ -61,6 +61,7 @@ def _check(got, ref):
     (1000, 4096, 32, 2, 0.0),
     (129, 1024, 5, 2, 1.0),        # E = 5 (Ep = 32), one token past a 128-row tile
     (300, 512, 100, 8, 0.8),       # E = 100 (Ep = 128), k = 8
+    (513, 768, 80, 3, 0.5),        # E = 80 (Ep = 96: 4 hi segments of 96 TMEM columns)
     (1, 64, 8, 3, 0.0),            # one token, one K-block
 ])
 def test_tc_gate_matches_oracle(cuda, N, d, E, k, bias_c):
