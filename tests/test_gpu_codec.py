@@ -195,3 +195,43 @@ def test_pack_cache_dir(cuda, tmp_path, codec):
         im.set_pack_cache_dir(None)
     assert raw.pack_source() == "none"
     raw.close()
+
+
+def _fuzz_case(rng):
+    n = 256 * int(rng.integers(1, 2400))
+    kind = rng.choice(["gauss", "laplace", "uniform", "outliers", "drift", "special", "runs"])
+    sig = float(10.0 ** rng.uniform(-5, 1))
+    if kind == "gauss":
+        x = rng.normal(0, sig, n)
+    elif kind == "laplace":
+        x = rng.laplace(0, sig, n)
+    elif kind == "uniform":
+        x = rng.uniform(-sig, sig, n)
+    elif kind == "outliers":
+        x = rng.normal(0, sig, n)
+        m = rng.random(n) < 0.02
+        x[m] *= 10.0 ** rng.uniform(1, 6, m.sum())
+    elif kind == "drift":  # magnitude drifting along the matrix: block bases differ
+        x = rng.normal(0, 1, n) * np.exp(np.linspace(-12, 12, n))
+    elif kind == "special":  # subnormals, zeros, +-inf, NaN sprinkled into normal data
+        x = rng.normal(0, sig, n)
+        idx = rng.integers(0, n, max(1, n // 50))
+        x[idx] = rng.choice([0.0, -0.0, np.inf, -np.inf, np.nan, 1e-39, -3e-40, 1e38], idx.size)
+    else:  # long runs of one value
+        x = np.repeat(rng.normal(0, sig, n // 256 + 1), 256)[:n]
+    u = x.astype(np.float32).view(np.uint32)
+    return kind, ((u + 0x7FFF + ((u >> 16) & 1)) >> 16).astype(np.uint16)
+
+
+def test_roundtrip_fuzz(cuda):
+    """40 random inputs (distribution, scale, size, NaN / Inf / subnormals, drift
+    of the block maxima, constant runs): the GPU decoders and the host reference
+    decoder restore every bit pattern."""
+    rng = np.random.default_rng(20261019)
+    for _ in range(40):
+        kind, a = _fuzz_case(rng)
+        for codec in ("exph", "exp4"):
+            out, _ = dv.codec_roundtrip(a, codec)
+            assert np.array_equal(out, a), (kind, codec, a.size)
+        out, _ = im.codec_roundtrip_host(a, "exph")
+        assert np.array_equal(out, a), (kind, "host", a.size)

@@ -347,3 +347,49 @@ def test_forward_routing_outputs(cuda, gate, k, offloaded):
     assert torch.equal(info["offsets"], offs.view(-1))
     assert np.array_equal(info["counts"], cnt.cpu().numpy())
     lay.close()
+
+
+def test_layer_fuzz_vs_oracle(cuda):
+    """30 random small layers (d, f, E, top-k, gate, token count, residency, K,
+    host-link codec): counts equal the oracle gate's, the output is within the
+    bf16 tolerance of the fp64 oracle chain, and an offloaded layer equals the
+    resident one bit for bit."""
+    rng = np.random.default_rng(20261019)
+    for case in range(30):
+        d = int(rng.choice([128, 256, 384, 512]))
+        f = int(rng.choice([256, 384, 512, 768]))
+        E = int(rng.integers(2, 17))
+        gate = str(rng.choice(["lsh", "softmax"]))
+        k = 1 if gate == "lsh" else int(rng.integers(1, min(4, E) + 1))
+        bits = max(1, int(np.ceil(np.log2(E))))
+        N = int(rng.integers(1, 401))
+        seed = 1000 + case
+        (xb, wib, wob), (x, wi, wo) = _setup(cuda, N, d, f, E, seed=seed)
+        gw = (rng.standard_normal((E, d)) / np.sqrt(d)).astype(np.float32)
+        kw = dict(gate=gate, gate_weight=gw, lsh_seed=seed, lsh_bits=bits, max_tokens=N)
+        res = dv.MoELayer(d, f, E, k, wi.to(cuda), wo.to(cuda), **kw)
+        y, info = res.forward(x)
+        K = int(rng.integers(1, E + 1))
+        codec = str(rng.choice(["raw", "exph"]))
+        off = dv.MoELayer(d, f, E, k, wi.pin_memory(), wo.pin_memory(), offloaded=True, K=K,
+                          h2d_codec=codec, **kw)
+        y_off, _ = off.forward(x)
+        torch.cuda.synchronize()
+        what = (case, d, f, E, k, gate, N, K, codec)
+        assert torch.equal(y.view(torch.int16), y_off.view(torch.int16)), what
+        xf = bf16_bits_to_f32(xb).reshape(N, d)
+        idx = np.zeros((N, k), np.int32)
+        w = np.zeros((N, k), np.float32)
+        cnt = np.zeros(E, np.int32)
+        if gate == "lsh":
+            proj = im.gating_projection(seed, bits, d)
+            O.or_gate_lsh(ptr(xf), N, d, ptr(np.ascontiguousarray(proj)), bits, E, ptr(idx),
+                          ptr(w), ptr(cnt))
+        else:
+            O.or_gate_softmax(ptr(xf), N, d, ptr(gw), None, E, k, ptr(idx), ptr(w), ptr(cnt))
+        assert np.array_equal(info["counts"], cnt), what
+        ref = _oracle_layer(xb, wib, wob, N, d, f, E, k, idx, w)
+        err = np.abs(y.float().cpu().numpy() - ref)
+        assert np.all(err <= ATOL + RTOL * np.abs(ref)), (what, float(err.max()))
+        res.close()
+        off.close()
