@@ -1101,8 +1101,9 @@ static uint64_t host_digest(const void* w_in, const void* w_out, uint64_t bytes_
 //   "INFMOEPK" | u32 version | u32 codec | u64 experts | u64 elems | u64 digest |
 //   u64 total | u64 max_size | u64 raw_bytes | u64 pack checksum |
 //   per expert {off, size, in_size} | exph: per expert {lay_in, lay_out} |
-//   the pack bytes.  A file whose header or checksum does not match is ignored
-//   (and replaced by the next encode).
+//   the pack bytes.  The checksum covers the tables and the pack bytes; a file
+//   whose header, tables or checksum do not match is ignored (and replaced by
+//   the next encode).
 namespace {
 std::string g_pack_dir = [] {
   const char* e = std::getenv("INFMOE_PACK_CACHE_DIR");
@@ -1114,6 +1115,43 @@ constexpr uint32_t kPackVersion = 4;  // 2: 256-byte aligned pack parts; 3: exph
 uint64_t pack_checksum(const uint8_t* p, uint64_t bytes) {
   // both halves (and an odd last byte)
   return host_digest(p, p + bytes / 2, bytes / 2) ^ dev_mix64(bytes + (bytes & 1 ? p[bytes - 1] : 0));
+}
+
+// digest of the per-expert tables (offsets, sizes, exph layouts) and the header
+// sizes: the file's checksum covers them together with the pack bytes
+uint64_t tables_digest(const HostPack& p) {
+  uint64_t h = dev_mix64(p.total ^ (p.max_size << 1) ^ (p.raw_bytes << 2));
+  auto mix = [&](const void* q, size_t bytes) {
+    const auto* b = static_cast<const uint8_t*>(q);
+    for (size_t i = 0; i < bytes; i += 8) {
+      uint64_t w = 0;
+      std::memcpy(&w, b + i, std::min<size_t>(8, bytes - i));
+      h = dev_mix64(h ^ w);
+    }
+  };
+  mix(p.off.data(), p.off.size() * 8);
+  mix(p.size.data(), p.size.size() * 8);
+  mix(p.in_size.data(), p.in_size.size() * 8);
+  mix(p.lay_in.data(), p.lay_in.size() * sizeof(codec::ExphLayout));
+  mix(p.lay_out.data(), p.lay_out.size() * sizeof(codec::ExphLayout));
+  return h;
+}
+
+// the tables describe parts that lie inside the pack and layouts that fit their
+// parts (a damaged file is rejected before any decode could read past a part)
+bool tables_sane(const HostPack& p, uint64_t elems) {
+  for (size_t e = 0; e < p.off.size(); ++e) {
+    if (p.in_size[e] > p.size[e] || p.off[e] + p.size[e] > p.total || p.size[e] > p.max_size)
+      return false;
+    if (p.codec_id == INFMOE_CODEC_EXPH) {
+      const codec::ExphLayout& a = p.lay_in[e];
+      const codec::ExphLayout& b = p.lay_out[e];
+      if (a.n != elems || b.n != elems || a.bytes > p.in_size[e] ||
+          b.bytes > p.size[e] - p.in_size[e])
+        return false;
+    }
+  }
+  return true;
 }
 
 std::string pack_path(uint64_t digest, int codec_id, int n_experts, uint64_t elems) {
@@ -1161,9 +1199,12 @@ bool pack_load(const std::string& path, HostPack& p, int n_experts, uint64_t ele
     p.total = h.total;
     p.max_size = h.max_size;
     p.raw_bytes = h.raw_bytes;
+    ok = tables_sane(p, elems);
+  }
+  if (ok) {
     INFMOE_CUDA(cudaMallocHost(&p.host, p.total));
-    ok = std::fread(p.host, 1, p.total, f) == p.total && pack_checksum(p.host, p.total) == h.checksum;
-    for (size_t e = 0; e < ne && ok; ++e) ok = p.off[e] + p.size[e] <= p.total;
+    ok = std::fread(p.host, 1, p.total, f) == p.total &&
+         (pack_checksum(p.host, p.total) ^ tables_digest(p)) == h.checksum;
     if (!ok) {
       cudaFreeHost(p.host);
       p.host = nullptr;
@@ -1191,7 +1232,7 @@ void pack_save(const std::string& path, const HostPack& p, int n_experts, uint64
   h.total = p.total;
   h.max_size = p.max_size;
   h.raw_bytes = p.raw_bytes;
-  h.checksum = pack_checksum(p.host, p.total);
+  h.checksum = pack_checksum(p.host, p.total) ^ tables_digest(p);
   bool ok = std::fwrite(&h, sizeof(h), 1, f) == 1;
   for (int e = 0; e < n_experts && ok; ++e) {
     const uint64_t v[3] = {p.off[size_t(e)], p.size[size_t(e)], p.in_size[size_t(e)]};

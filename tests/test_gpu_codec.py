@@ -185,6 +185,16 @@ def test_pack_cache_dir(cuda, tmp_path, codec):
         assert torch.equal(y_c.view(torch.int16), y_raw.view(torch.int16))
         c.close()
         assert files[0].read_bytes() != bytes(blob)  # replaced by the fresh encode
+        # a damaged table (expert 0's size, right after the 72-byte header) too
+        blob = bytearray(files[0].read_bytes())
+        blob[72 + 8] ^= 0x01
+        files[0].write_bytes(bytes(blob))
+        c2 = dv.MoELayer(d, f, E, 1, wi, wo, h2d_codec=codec, **kw)
+        assert c2.pack_source() == "encoded"
+        y_c2, _ = c2.forward(x)
+        torch.cuda.synchronize()
+        assert torch.equal(y_c2.view(torch.int16), y_raw.view(torch.int16))
+        c2.close()
         # new content -> a second file, encoded
         wi.copy_(t(fill_bf16(54, E * f * d, 1.7320508 / 16), (E, f, d)))
         e2 = dv.MoELayer(d, f, E, 1, wi, wo, h2d_codec=codec, **kw)
