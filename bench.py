@@ -1103,7 +1103,7 @@ def main() -> None:
 
     hbm_peak = float(peaks["hbm_gbs"])
     traffic = None  # DRAM bytes per launch of the same kernel from the committed ncu capture
-    tp = ROOT / "profiles" / "r01_ffn_traffic.json"
+    tp = ROOT / "profiles" / "r02_ffn_traffic.json"
     if tp.exists():
         traffic = json.loads(tp.read_text()).get("traffic_bytes_per_launch")
     ffn_gbs = ffn_bytes / ffn_secs / 1e9 if ffn_secs else 0.0
@@ -1134,7 +1134,7 @@ def main() -> None:
                                "all local experts in one launch",
                      "bound": "hbm", "achieved": rg_gbs, "peak": hbm_peak, "unit": "GB/s",
                      "frac": rg_gbs / hbm_peak, "traffic": traffic,
-                     "traffic_src": "profiles/r01_ffn_traffic.json (ncu dram__bytes_read+write)",
+                     "traffic_src": "profiles/r02_ffn_traffic.json (ncu dram__bytes_read+write)",
                      "bytes_per_launch": rg_bytes / max(1, len(rinfos)),
                      "launches_timed": len(rinfos), "peak_src": peaks["_src"],
                      "timing": "per-launch CUDA events in a 24-layer resident pass that reads "
