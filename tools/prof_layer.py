@@ -21,12 +21,18 @@ ap.add_argument("--skew", type=float, default=0.0, help="softmax logit bias -ske
 a = ap.parse_args()
 d, f, E, N = 4096, 10240, a.E, a.N
 dev = torch.device("cuda:0")
-wi = torch.empty((E, f, d), dtype=torch.bfloat16, device=dev)
-wo = torch.empty((E, d, f), dtype=torch.bfloat16, device=dev)
-x = torch.empty((N, d), dtype=torch.bfloat16, device=dev)
-dv.fill_uniform(wi, 1, 3 ** 0.5 / d ** 0.5)
-dv.fill_uniform(wo, 2, 1.534 * 3 ** 0.5 / f ** 0.5)
-dv.fill_uniform(x, 3, 3 ** 0.5)
+# SURVEY 8(d) inputs, as bench.py: GaussianStream weights x d^-1/2 / f^-1/2,
+# gaussian_tokens x, all rounded to bf16 on the host
+S = 20261018
+wi = torch.empty((E, f, d), dtype=torch.bfloat16, pin_memory=True)
+wo = torch.empty((E, d, f), dtype=torch.bfloat16, pin_memory=True)
+x = torch.empty((N, d), dtype=torch.bfloat16, pin_memory=True)
+im.gaussian_fill_typed("bf16", [im.derive_seed(S, 1000 + 2 * e) for e in range(E)] +
+                       [im.derive_seed(S, 1001 + 2 * e) for e in range(E)],
+                       [d ** -0.5] * E + [f ** -0.5] * E, f * d,
+                       [wi[e].data_ptr() for e in range(E)] + [wo[e].data_ptr() for e in range(E)])
+im.gaussian_fill_typed("bf16", [im.derive_seed(S, 0)], [1.0], N * d, [x.data_ptr()])
+wi, wo, x = wi.to(dev), wo.to(dev), x.to(dev)
 gw = torch.randn(E, d).numpy() / d ** 0.5
 bias = -a.skew * torch.log(torch.arange(1, E + 1, dtype=torch.float32)).numpy()
 layer = dv.MoELayer(d, f, E, a.k, wi, wo, gate=a.gate, gate_weight=gw, gate_bias=bias, lsh_seed=7,
