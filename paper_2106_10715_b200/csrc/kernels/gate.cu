@@ -757,10 +757,10 @@ void lsh_mma_go(const void* x, int64_t N, int d, const double* proj, int bits, i
 //     token is CERTIFIED and its picks, softmax weights (from L~, renormalised
 //     over the picks) and counts are written right there.
 //  2. gate_tc_fallback_kernel (one CTA per uncertified token, listed by
-//     step 1; the candidates' chains spread over its warps): every expert whose upper bound reaches the k-th largest lower
-//     bound is a candidate and gets its exact logit by the CUDA-core gate's
-//     fmaf chain and butterfly; top-k over those (ties and NaN -> lower
-//     index).  A token with a non-finite value or more than kTcCandMax
+//     step 1; the candidates' chains spread over its warps): every expert
+//     whose upper bound reaches the k-th largest lower bound is a candidate
+//     and gets its exact logit by the CUDA-core gate's fmaf chain and
+//     butterfly; top-k over those (ties and NaN -> lower index).  A token with a non-finite value or more than kTcCandMax
 //     candidates takes every expert through the exact chain.
 // So indices and counts equal the exact gate's by construction; the weights
 // carry the tensor-core logits' error (observed <= 1.5e-7 ||x|| ||w||).
